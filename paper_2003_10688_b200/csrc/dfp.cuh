@@ -1,0 +1,161 @@
+// Fused DFP (depth-first parallelism) kernels for sm_100a.
+//
+// The reference lowers each fused unit to a KernelIR loop nest whose body is an expression tree,
+// with producers inlined depth-first (proj/src/dfp_lower.cpp:392-796) and interprets it per
+// output element (proj/src/dfp_interp.cpp:40-164). Here a unit compiles (module.cpp) to one of a
+// few hand-written kernel families over NHWC tensors, each parameterised by small per-channel
+// "programs": straight-line, vectorised (16 bytes = 8 bf16 / 4 f32 channels per thread) register
+// code evaluated at a pixel. The loop nest becomes the grid; the expression tree becomes the
+// program; reductions (pool windows, global average, per-channel statistics) are explicit.
+#pragma once
+
+#include "common.cuh"
+
+namespace solb200 {
+
+constexpr int DFP_MAX_INS = 24;
+constexpr int DFP_MAX_IN = 8;
+constexpr int DFP_MAX_P = 16;
+constexpr int DFP_MAX_CAT = 40;
+
+enum PwOp : uint8_t {
+    PW_LD = 0,     // r[dst] = input[a] at the current pixel
+    PW_AFF,        // r[dst] = r[dst] * P[arg][c] + P[arg+1][c]
+    PW_AXPBY,      // r[dst] = r[dst] * P[arg][c] + r[b] * P[arg+1][c] + P[arg+2][c]
+    PW_RELU,       // r[dst] = max(r[dst], 0)
+    PW_RELU6,      // r[dst] = min(max(r[dst], 0), 6)
+    PW_ADD,        // r[dst] = r[a] + r[b]
+    PW_MASK,       // r[dst] = r[a] * (r[b] > 0)
+    PW_MASK6,      // r[dst] = r[a] * (r[b] > 0 && r[b] < 6)
+    PW_MOV,        // r[dst] = r[a]
+    PW_SCALE,      // r[dst] = r[dst] * imm
+    PW_PARAM,      // r[dst] = P[arg][c]
+};
+
+struct PwInstr {
+    uint8_t op = 0, dst = 0, a = 0, b = 0;
+    int16_t arg = 0;
+    int16_t pad = 0;
+    float imm = 0.f;
+};
+
+struct Program {
+    int n = 0;
+    PwInstr ins[DFP_MAX_INS];
+};
+
+enum InKind : int {
+    IN_PIX = 0,    // NHWC tensor on the program's grid: ptr + pixel*ld + coff + c
+    IN_NC = 1,     // [N, C] tensor broadcast over pixels: ptr + n*ld + c
+    IN_CAT = 2,    // concat over channel segments (cat_* fields)
+};
+
+enum Family : int {
+    FAM_POINTWISE = 0,  // out[p, c] = post(p, c)
+    FAM_POOL,           // out[o, c] = post(reduce_{window(o)} pre(i, c))          (Max/AvgPool2d)
+    FAM_GAP,            // out[n, c] = post(mean_{h,w} pre((n,h,w), c))             (GlobalAvgPool)
+    FAM_DWCONV,         // out[o, c] = post(sum_{window} pre(i, c) * w[kh,kw,c] (+b)) (depthwise Conv2d)
+    FAM_CHAN_REDUCE,    // S1[c] = sum_p pre.r0, S2[c] = sum_p pre.r0 * pre.r1      (BN statistics / grads)
+    FAM_MAXPOOL_BACK,   // dx[i, c] = post(sum_{o: argmax(o)==i} pre(o, c))         (MaxPool2dBack)
+    FAM_AVGPOOL_BACK,   // dx[i, c] = post(sum_{o: i in window(o)} pre(o, c) / cnt(o))
+};
+
+struct DfpArgs {
+    int family = FAM_POINTWISE;
+    int dtype = DT_BF16;
+    // source grid (where `pre` runs) and output grid (where `post` runs); NHWC
+    int N = 0, H = 1, W = 1, C = 0;
+    int OH = 1, OW = 1;
+    int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
+    float min_init = 0.f;
+    int count_padding = 0;
+    // inputs
+    int n_in = 0;
+    const void* in[DFP_MAX_IN] = {};
+    int in_kind[DFP_MAX_IN] = {};
+    int in_ld[DFP_MAX_IN] = {};
+    int in_coff[DFP_MAX_IN] = {};
+    int in_f32[DFP_MAX_IN] = {};   // input stored as f32 even in a bf16 plan
+    int n_cat = 0;
+    const void* cat_ptr[DFP_MAX_CAT] = {};
+    int cat_off[DFP_MAX_CAT + 1] = {};
+    // per-channel f32 parameter arrays
+    const float* P[DFP_MAX_P] = {};
+    // extra operands
+    const float* dw_w = nullptr;   // FAM_DWCONV: [kh][kw][C] f32
+    const float* dw_b = nullptr;
+    int pool_x = -1;               // FAM_MAXPOOL_BACK: input slot holding the forward pool input
+    int pool_max = 1;              // FAM_POOL: 1 = max, 0 = average
+    Program pre, post;
+    // outputs
+    void* out = nullptr;
+    int out_ld = 0, out_coff = 0;
+    int out_f32 = 0;               // output stored as f32 even in a bf16 plan
+    float* partial = nullptr;      // FAM_CHAN_REDUCE: [blocks][C][2]
+    int reduce_blocks = 0;
+};
+
+void dfp_launch(const DfpArgs& a, cudaStream_t s);
+int dfp_reduce_blocks(int64_t pixels, int C);  // partial blocks used by FAM_CHAN_REDUCE
+
+// Small fixed-function kernels (rows of [N, C], BN finalisation, SGD, layout conversion).
+void softmax_rows(int dtype, const void* x, void* y, int rows, int cols, int ld, cudaStream_t s);
+// loss = -sum(t * log(p)) / rows  (reference.cpp CrossEntropyLoss); writes one f32
+void ce_loss(int dtype, const void* p, const void* t, float* loss, int rows, int cols, int ld, cudaStream_t s);
+// dx = (p - t) / rows (SoftmaxCeBack) or -t / (p * rows) (CeBack)
+void ce_back(int dtype, int fused_softmax, const void* p, const void* t, void* dx, int rows, int cols, int ld,
+             cudaStream_t s);
+// dx = y * (delta - sum_c delta*y)  (SoftmaxBack)
+void softmax_back(int dtype, const void* delta, const void* y, void* dx, int rows, int cols, int ld, cudaStream_t s);
+
+// Per-channel finalisation of FAM_CHAN_REDUCE partials (in f64).
+enum FinalizeMode : int {
+    FIN_BN_STATS = 0,   // mean/var from shifted sums -> stats[2C] = (mean, rstd),
+                        // coef[2C] = (gamma*rstd, beta - mean*gamma*rstd); optional running update
+    FIN_SUMS = 1,       // out0[c] = S1, out1[c] = S2 (f32)
+    FIN_BN_BACK = 2,    // dbeta = S1, dgamma = S2 (over xhat); coef[3C] for dx = dy*A + x*B + Cc
+};
+struct FinalizeArgs {
+    int mode = FIN_BN_STATS;
+    int C = 0;
+    int blocks = 0;
+    const float* partial = nullptr;
+    double count = 1.0;
+    float eps = 1e-5f;
+    float momentum = 0.1f;
+    const float* shift = nullptr;  // per-channel shift used by the stats reduction (FIN_BN_STATS)
+    const float* gamma = nullptr;
+    const float* beta = nullptr;
+    const float* stats = nullptr;  // (mean, rstd) for FIN_BN_BACK
+    float* running_mean = nullptr;
+    float* running_var = nullptr;
+    float* stats_out = nullptr;
+    float* coef = nullptr;
+    float* out0 = nullptr;
+    float* out1 = nullptr;
+};
+void dfp_finalize(const FinalizeArgs& a, cudaStream_t s);
+
+// BN inference coefficients: coef = (gamma/sqrt(var+eps), beta - mean*gamma/sqrt(var+eps)).
+void bn_infer_coef(const float* gamma, const float* beta, const float* mean, const float* var, float eps,
+                   float* coef, int C, cudaStream_t s);
+// Shift vector for shifted-sum statistics: shift[c] = x[0, c] (first pixel).
+void bn_shift(int dtype, const void* x, int ld, int C, float* shift, cudaStream_t s);
+
+// w -= lr * g over n f32 elements (SgdUpdate, reference.cpp:580-584); optional bf16 mirror.
+void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror_bf16, cudaStream_t s);
+
+// Layout/dtype conversion between canonical NCHW f32 (host-facing) and NHWC plan storage.
+// c_pad >= C channels; padded channels are zero.
+void nchw_to_nhwc(const float* src, void* dst, int dtype, int N, int C, int H, int W, int c_pad,
+                  cudaStream_t s);
+void nhwc_to_nchw(const void* src, float* dst, int dtype, int N, int C, int H, int W, int ld,
+                  cudaStream_t s);
+// Flatten in canonical (reference) order: out[n, c*H*W + h*W + w] = x[n, h, w, c]
+// (dfp_lower.cpp:1098-1112; reference.cpp:245-254) and its inverse (FlattenBack).
+void flatten_nhwc(int dtype, const void* x, void* y, int N, int C, int H, int W, int inverse,
+                  cudaStream_t s);
+// dtype cast (f32 <-> bf16) of n elements.
+void cast_copy(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, cudaStream_t s);
+
+}  // namespace solb200

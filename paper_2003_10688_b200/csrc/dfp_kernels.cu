@@ -1,0 +1,811 @@
+// Fused DFP kernel families (see dfp.cuh). All kernels are HBM-bound: 16-byte vector access
+// along the contiguous channel dimension, grids sized in multiples of the SM count, no shared
+// memory except for the per-channel reductions.
+#include "dfp.cuh"
+
+#include <algorithm>
+
+namespace solb200 {
+namespace {
+
+constexpr int NREG = 4;
+constexpr int THREADS = 256;
+
+template <typename T> constexpr int VEC = 16 / sizeof(T);
+
+// ---------------------------------------------------------------------------------------------
+// program interpreter (uniform control flow; register file indexed by unrolled selects)
+// ---------------------------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ void load_in(const DfpArgs& a, int slot, int64_t pix, int n, int c,
+                                        float* v) {
+    const int kind = a.in_kind[slot];
+    const T* base;
+    if (kind == IN_PIX) {
+        base = static_cast<const T*>(a.in[slot]) + pix * a.in_ld[slot] + a.in_coff[slot] + c;
+    } else if (kind == IN_NC) {
+        base = static_cast<const T*>(a.in[slot]) + static_cast<int64_t>(n) * a.in_ld[slot] + c;
+    } else {
+        int s = 0;
+        while (s + 1 < a.n_cat && c >= a.cat_off[s + 1]) ++s;
+        const int cs = a.cat_off[s + 1] - a.cat_off[s];
+        base = static_cast<const T*>(a.cat_ptr[s]) + pix * cs + (c - a.cat_off[s]);
+    }
+    load16(base, v);
+}
+
+template <typename T>
+__device__ __forceinline__ void run_prog(const Program& pg, const DfpArgs& a, int64_t pix, int n,
+                                         int c, float (&r)[NREG][VEC<T>]) {
+    constexpr int V = VEC<T>;
+    for (int k = 0; k < pg.n; ++k) {
+        const PwInstr ins = pg.ins[k];
+        switch (ins.op) {
+            case PW_LD: {
+                float t[V];
+                load_in<T>(a, ins.a, pix, n, c, t);
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) r[d][i] = t[i];
+                    }
+                break;
+            }
+            case PW_AFF: {
+                const float* s0 = a.P[ins.arg] + c;
+                const float* s1 = a.P[ins.arg + 1] + c;
+                float m[V], b[V];
+#pragma unroll
+                for (int i = 0; i < V; i += 4) {
+                    float4 x = __ldg(reinterpret_cast<const float4*>(s0 + i));
+                    float4 y = __ldg(reinterpret_cast<const float4*>(s1 + i));
+                    m[i] = x.x; m[i + 1] = x.y; m[i + 2] = x.z; m[i + 3] = x.w;
+                    b[i] = y.x; b[i + 1] = y.y; b[i + 2] = y.z; b[i + 3] = y.w;
+                }
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) r[d][i] = fmaf(r[d][i], m[i], b[i]);
+                    }
+                break;
+            }
+            case PW_PARAM: {
+                const float* s0 = a.P[ins.arg] + c;
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) r[d][i] = __ldg(s0 + i);
+                    }
+                break;
+            }
+            case PW_AXPBY: {
+                float tb[V];
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.b == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) tb[i] = r[d][i];
+                    }
+                const float* s0 = a.P[ins.arg] + c;
+                const float* s1 = a.P[ins.arg + 1] + c;
+                const float* s2 = a.P[ins.arg + 2] + c;
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i)
+                            r[d][i] = fmaf(r[d][i], __ldg(s0 + i), fmaf(tb[i], __ldg(s1 + i), __ldg(s2 + i)));
+                    }
+                break;
+            }
+            case PW_RELU:
+            case PW_RELU6:
+            case PW_SCALE: {
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) {
+                            float x = r[d][i];
+                            if (ins.op == PW_SCALE) x *= ins.imm;
+                            else {
+                                x = x > 0.f ? x : 0.f;
+                                if (ins.op == PW_RELU6) x = x < 6.f ? x : 6.f;
+                            }
+                            r[d][i] = x;
+                        }
+                    }
+                break;
+            }
+            case PW_ADD:
+            case PW_MASK:
+            case PW_MASK6:
+            case PW_MOV: {
+                float ta[V], tb[V];
+#pragma unroll
+                for (int d = 0; d < NREG; ++d) {
+                    if (ins.a == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) ta[i] = r[d][i];
+                    }
+                    if (ins.b == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) tb[i] = r[d][i];
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (ins.op == PW_ADD) ta[i] = ta[i] + tb[i];
+                    else if (ins.op == PW_MASK) ta[i] = tb[i] > 0.f ? ta[i] : 0.f;
+                    else if (ins.op == PW_MASK6) ta[i] = (tb[i] > 0.f && tb[i] < 6.f) ? ta[i] : 0.f;
+                }
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i) r[d][i] = ta[i];
+                    }
+                break;
+            }
+            default:
+                break;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_out(const DfpArgs& a, int64_t pix, int c, const float* v) {
+    T* o = static_cast<T*>(a.out) + pix * a.out_ld + a.out_coff + c;
+    store16(o, v);
+}
+
+inline unsigned grid_for(int64_t work, int per_block) {
+    const int64_t blocks = ceil_div(work, per_block);
+    const int64_t cap = static_cast<int64_t>(num_sms()) * 16;
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min(blocks, cap)));
+}
+
+// ---------------------------------------------------------------------------------------------
+// FAM_POINTWISE
+// ---------------------------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(THREADS) pointwise_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t hw = static_cast<int64_t>(a.OH) * a.OW;
+    const int64_t total = static_cast<int64_t>(a.N) * hw * cv;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t pix = v / cv;
+        const int c = static_cast<int>(v - pix * cv) * V;
+        const int n = static_cast<int>(pix / hw);
+        float r[NREG][V];
+        run_prog<T>(a.post, a, pix, n, c, r);
+        store_out<T>(a, pix, c, r[0]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// FAM_POOL (max / avg window reduce over pre-program values)
+// ---------------------------------------------------------------------------------------------
+
+template <typename T, bool IS_MAX>
+__global__ void __launch_bounds__(THREADS) pool_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t opix = v / cv;
+        const int c = static_cast<int>(v - opix * cv) * V;
+        const int ow = static_cast<int>(opix % a.OW);
+        const int oh = static_cast<int>((opix / a.OW) % a.OH);
+        const int n = static_cast<int>(opix / (static_cast<int64_t>(a.OW) * a.OH));
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = IS_MAX ? a.min_init : 0.f;
+        int cnt = 0;
+        for (int kh = 0; kh < a.kh; ++kh) {
+            const int ih = oh * a.sh - a.ph + kh;
+            if (ih < 0 || ih >= a.H) continue;
+            for (int kw = 0; kw < a.kw; ++kw) {
+                const int iw = ow * a.sw - a.pw + kw;
+                if (iw < 0 || iw >= a.W) continue;
+                const int64_t ipix = (static_cast<int64_t>(n) * a.H + ih) * a.W + iw;
+                float r[NREG][V];
+                run_prog<T>(a.pre, a, ipix, n, c, r);
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] = IS_MAX ? fmaxf(acc[i], r[0][i]) : acc[i] + r[0][i];
+                ++cnt;
+            }
+        }
+        float r[NREG][V];
+        const float div = IS_MAX ? 1.f : static_cast<float>(a.count_padding ? a.kh * a.kw : cnt);
+#pragma unroll
+        for (int i = 0; i < V; ++i) r[0][i] = IS_MAX ? acc[i] : acc[i] / div;
+        run_prog<T>(a.post, a, opix, n, c, r);
+        store_out<T>(a, opix, c, r[0]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// FAM_GAP
+// ---------------------------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(THREADS) gap_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * cv;
+    const int hw = a.H * a.W;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int n = static_cast<int>(v / cv);
+        const int c = static_cast<int>(v - static_cast<int64_t>(n) * cv) * V;
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        for (int p = 0; p < hw; ++p) {
+            float r[NREG][V];
+            run_prog<T>(a.pre, a, static_cast<int64_t>(n) * hw + p, n, c, r);
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] += r[0][i];
+        }
+        float r[NREG][V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) r[0][i] = acc[i] / static_cast<float>(hw);
+        run_prog<T>(a.post, a, n, n, c, r);
+        store_out<T>(a, n, c, r[0]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// FAM_DWCONV (depthwise conv as weighted pooling, dfp_lower.cpp:519-540)
+// ---------------------------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t opix = v / cv;
+        const int c = static_cast<int>(v - opix * cv) * V;
+        const int ow = static_cast<int>(opix % a.OW);
+        const int oh = static_cast<int>((opix / a.OW) % a.OH);
+        const int n = static_cast<int>(opix / (static_cast<int64_t>(a.OW) * a.OH));
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = a.dw_b ? __ldg(a.dw_b + c + i) : 0.f;
+        for (int kh = 0; kh < a.kh; ++kh) {
+            const int ih = oh * a.sh - a.ph + kh;
+            if (ih < 0 || ih >= a.H) continue;
+            for (int kw = 0; kw < a.kw; ++kw) {
+                const int iw = ow * a.sw - a.pw + kw;
+                if (iw < 0 || iw >= a.W) continue;
+                const int64_t ipix = (static_cast<int64_t>(n) * a.H + ih) * a.W + iw;
+                float r[NREG][V];
+                run_prog<T>(a.pre, a, ipix, n, c, r);
+                const float* wv = a.dw_w + (kh * a.kw + kw) * a.C + c;
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] = fmaf(r[0][i], __ldg(wv + i), acc[i]);
+            }
+        }
+        float r[NREG][V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) r[0][i] = acc[i];
+        run_prog<T>(a.post, a, opix, n, c, r);
+        store_out<T>(a, opix, c, r[0]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// FAM_CHAN_REDUCE: per-channel S1 = sum r0, S2 = sum r0*r1 over all pixels of the source grid
+// ---------------------------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    __shared__ float red[THREADS * V * 2];
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int tid = threadIdx.x;
+    const int row = tid / cvb;
+    const int cvi = tid - row * cvb;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const int64_t hw = static_cast<int64_t>(a.H) * a.W;
+    const int64_t P = static_cast<int64_t>(a.N) * hw;
+    const int64_t per = ceil_div(P, gridDim.x);
+    const int64_t p0 = blockIdx.x * per;
+    const int64_t p1 = min(P, p0 + per);
+    float s1[V], s2[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    const bool active = row < rows && (blockIdx.y * cvb + cvi) < cv_total;
+    if (active) {
+        for (int64_t p = p0 + row; p < p1; p += rows) {
+            float r[NREG][V];
+            run_prog<T>(a.pre, a, p, static_cast<int>(p / hw), c, r);
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                s1[i] += r[0][i];
+                s2[i] = fmaf(r[0][i], r[1][i], s2[i]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        red[(tid * V + i) * 2] = s1[i];
+        red[(tid * V + i) * 2 + 1] = s2[i];
+    }
+    __syncthreads();
+    if (row == 0 && active) {
+        for (int rr = 1; rr < rows; ++rr) {
+            const int t2 = rr * cvb + cvi;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                s1[i] += red[(t2 * V + i) * 2];
+                s2[i] += red[(t2 * V + i) * 2 + 1];
+            }
+        }
+        float* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * a.C + c) * 2;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            dst[2 * i] = s1[i];
+            dst[2 * i + 1] = s2[i];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// FAM_MAXPOOL_BACK / FAM_AVGPOOL_BACK: gather formulation (deterministic, no atomics).
+// Grid = dx pixels (H, W); windows = delta pixels (OH, OW).
+// MaxPool routing: first max in (kh, kw) scan order, only when max > min_init
+// (reference.cpp:294-327; dfp_lower.cpp:546-610).
+// ---------------------------------------------------------------------------------------------
+
+template <typename T, bool IS_MAX>
+__global__ void __launch_bounds__(THREADS) pool_back_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.H * a.W * cv;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t ipix = v / cv;
+        const int c = static_cast<int>(v - ipix * cv) * V;
+        const int iw = static_cast<int>(ipix % a.W);
+        const int ih = static_cast<int>((ipix / a.W) % a.H);
+        const int n = static_cast<int>(ipix / (static_cast<int64_t>(a.W) * a.H));
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        const int oh_lo = max(0, (ih + a.ph - a.kh + a.sh) / a.sh);
+        const int oh_hi = min(a.OH - 1, (ih + a.ph) / a.sh);
+        const int ow_lo = max(0, (iw + a.pw - a.kw + a.sw) / a.sw);
+        const int ow_hi = min(a.OW - 1, (iw + a.pw) / a.sw);
+        for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+            const int dkh = ih - (oh * a.sh - a.ph);
+            if (dkh < 0 || dkh >= a.kh) continue;
+            for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+                const int dkw = iw - (ow * a.sw - a.pw);
+                if (dkw < 0 || dkw >= a.kw) continue;
+                const int64_t opix = (static_cast<int64_t>(n) * a.OH + oh) * a.OW + ow;
+                float take[V];
+                if (IS_MAX) {
+                    float best[V];
+                    int bidx[V];
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        best[i] = -INFINITY;
+                        bidx[i] = -1;
+                    }
+                    for (int kh = 0; kh < a.kh; ++kh) {
+                        const int hh = oh * a.sh - a.ph + kh;
+                        if (hh < 0 || hh >= a.H) continue;
+                        for (int kw = 0; kw < a.kw; ++kw) {
+                            const int ww = ow * a.sw - a.pw + kw;
+                            if (ww < 0 || ww >= a.W) continue;
+                            float xv[V];
+                            load_in<T>(a, a.pool_x, (static_cast<int64_t>(n) * a.H + hh) * a.W + ww, n, c, xv);
+#pragma unroll
+                            for (int i = 0; i < V; ++i)
+                                if (xv[i] > best[i]) {
+                                    best[i] = xv[i];
+                                    bidx[i] = kh * a.kw + kw;
+                                }
+                        }
+                    }
+                    const int me = dkh * a.kw + dkw;
+#pragma unroll
+                    for (int i = 0; i < V; ++i) take[i] = (bidx[i] == me && best[i] > a.min_init) ? 1.f : 0.f;
+                } else {
+                    int cnt = a.kh * a.kw;
+                    if (!a.count_padding) {
+                        cnt = 0;
+                        for (int kh = 0; kh < a.kh; ++kh) {
+                            const int hh = oh * a.sh - a.ph + kh;
+                            if (hh < 0 || hh >= a.H) continue;
+                            for (int kw = 0; kw < a.kw; ++kw) {
+                                const int ww = ow * a.sw - a.pw + kw;
+                                if (ww >= 0 && ww < a.W) ++cnt;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < V; ++i) take[i] = 1.f / static_cast<float>(cnt);
+                }
+                float r[NREG][V];
+                run_prog<T>(a.pre, a, opix, n, c, r);
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] = fmaf(r[0][i], take[i], acc[i]);
+            }
+        }
+        float r[NREG][V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) r[0][i] = acc[i];
+        run_prog<T>(a.post, a, ipix, n, c, r);
+        store_out<T>(a, ipix, c, r[0]);
+    }
+}
+
+template <typename T>
+void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
+    constexpr int V = VEC<T>;
+    if (a.C % V != 0) throw std::invalid_argument("dfp: channel count must be a multiple of 16 bytes");
+    switch (a.family) {
+        case FAM_POINTWISE: {
+            const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+            pointwise_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            break;
+        }
+        case FAM_POOL: {
+            const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+            if (a.pre.n == 0) throw std::invalid_argument("dfp: pool without source program");
+            if (a.pool_max) pool_kernel<T, true><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            else pool_kernel<T, false><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            break;
+        }
+        case FAM_GAP: {
+            const int64_t work = static_cast<int64_t>(a.N) * (a.C / V);
+            gap_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            break;
+        }
+        case FAM_DWCONV: {
+            const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+            dwconv_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            break;
+        }
+        case FAM_CHAN_REDUCE: {
+            const int cv_total = a.C / V;
+            const int cvb = std::min(cv_total, THREADS);
+            dim3 grid(static_cast<unsigned>(a.reduce_blocks), static_cast<unsigned>(ceil_div(cv_total, cvb)));
+            chan_reduce_kernel<T><<<grid, THREADS, 0, s>>>(a);
+            break;
+        }
+        case FAM_MAXPOOL_BACK: {
+            const int64_t work = static_cast<int64_t>(a.N) * a.H * a.W * (a.C / V);
+            pool_back_kernel<T, true><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            break;
+        }
+        case FAM_AVGPOOL_BACK: {
+            const int64_t work = static_cast<int64_t>(a.N) * a.H * a.W * (a.C / V);
+            pool_back_kernel<T, false><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            break;
+        }
+        default:
+            throw std::invalid_argument("dfp: unknown family");
+    }
+    SOL_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------------------
+// row kernels over [rows, cols] (Softmax / CrossEntropyLoss and their backward)
+// ---------------------------------------------------------------------------------------------
+
+template <typename T>
+__global__ void softmax_kernel(const T* __restrict__ x, T* __restrict__ y, int rows, int cols, int ld) {
+    const int warps = blockDim.x / 32;
+    const int row = blockIdx.x * warps + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const T* xr = x + static_cast<int64_t>(row) * ld;
+    float mx = -INFINITY;
+    for (int c = lane; c < cols; c += 32) mx = fmaxf(mx, to_f32(xr[c]));
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int c = lane; c < cols; c += 32) sum += expf(to_f32(xr[c]) - mx);
+    sum = warp_sum(sum);
+    const float inv = 1.f / sum;
+    for (int c = lane; c < ld; c += 32)
+        y[static_cast<int64_t>(row) * ld + c] = from_f32<T>(c < cols ? expf(to_f32(xr[c]) - mx) * inv : 0.f);
+}
+
+template <typename T>
+__global__ void ce_loss_kernel(const T* __restrict__ p, const T* __restrict__ t, float* loss, int rows,
+                               int cols, int ld) {
+    __shared__ double part[32];
+    double acc = 0.0;
+    const int64_t n = static_cast<int64_t>(rows) * cols;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const int64_t i = (k / cols) * ld + (k % cols);
+        const float tv = to_f32(t[i]);
+        acc -= static_cast<double>(tv) * log(static_cast<double>(to_f32(p[i])));
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) s += part[w];
+        *loss = static_cast<float>(s / rows);
+    }
+}
+
+template <typename T>
+__global__ void ce_back_kernel(const T* __restrict__ p, const T* __restrict__ t, T* __restrict__ dx,
+                               int64_t n, int rows, int fused, int cols, int ld) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % ld);
+        float v = 0.f;
+        if (c < cols) {
+            const float pv = to_f32(p[i]), tv = to_f32(t[i]);
+            v = fused ? (pv - tv) / rows : -tv / (pv * rows);
+        }
+        dx[i] = from_f32<T>(v);
+    }
+}
+
+template <typename T>
+__global__ void softmax_back_kernel(const T* __restrict__ d, const T* __restrict__ y, T* __restrict__ dx,
+                                    int rows, int cols, int ld) {
+    const int warps = blockDim.x / 32;
+    const int row = blockIdx.x * warps + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t base = static_cast<int64_t>(row) * ld;
+    float dot = 0.f;
+    for (int c = lane; c < cols; c += 32) dot += to_f32(d[base + c]) * to_f32(y[base + c]);
+    dot = warp_sum(dot);
+    for (int c = lane; c < ld; c += 32)
+        dx[base + c] = from_f32<T>(c < cols ? to_f32(y[base + c]) * (to_f32(d[base + c]) - dot) : 0.f);
+}
+
+// ---------------------------------------------------------------------------------------------
+// finalisation of per-channel partial sums (f64)
+// ---------------------------------------------------------------------------------------------
+
+__global__ void finalize_kernel(const FinalizeArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.C) return;
+    double s1 = 0.0, s2 = 0.0;
+    for (int b = 0; b < a.blocks; ++b) {
+        s1 += a.partial[(static_cast<int64_t>(b) * a.C + c) * 2];
+        s2 += a.partial[(static_cast<int64_t>(b) * a.C + c) * 2 + 1];
+    }
+    const double m = a.count;
+    if (a.mode == FIN_BN_STATS) {
+        // sums over (x - shift): mean = shift + s1/m, var = s2/m - (s1/m)^2 (biased)
+        const double d = s1 / m;
+        double var = s2 / m - d * d;
+        if (var < 0) var = 0;
+        const double mean = static_cast<double>(a.shift[c]) + d;
+        const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
+        if (a.stats_out) {
+            a.stats_out[c] = static_cast<float>(mean);
+            a.stats_out[a.C + c] = static_cast<float>(rstd);
+        }
+        if (a.coef) {
+            const double g = a.gamma[c], bt = a.beta[c];
+            a.coef[c] = static_cast<float>(g * rstd);
+            a.coef[a.C + c] = static_cast<float>(bt - mean * g * rstd);
+        }
+        if (a.running_mean) {
+            const double unbias = m > 1 ? m / (m - 1) : 1.0;
+            const double mom = a.momentum;
+            a.running_mean[c] = static_cast<float>((1 - mom) * a.running_mean[c] + mom * mean);
+            a.running_var[c] = static_cast<float>((1 - mom) * a.running_var[c] + mom * var * unbias);
+        }
+    } else if (a.mode == FIN_SUMS) {
+        if (a.out0) a.out0[c] = static_cast<float>(s1);
+        if (a.out1) a.out1[c] = static_cast<float>(s2);
+    } else {
+        // s1 = sum dy (dbeta), s2 = sum dy * xhat (dgamma); dx = g*r*(dy - s1/m - xhat*s2/m)
+        if (a.out0) a.out0[c] = static_cast<float>(s1);
+        if (a.out1) a.out1[c] = static_cast<float>(s2);
+        if (a.coef) {
+            const double g = a.gamma[c];
+            const double mean = a.stats[c], rstd = a.stats[a.C + c];
+            const double gr = g * rstd;
+            // dx = dy * gr + x * (-gr*rstd*s2/m) + (-gr*s1/m + gr*mean*rstd*s2/m)
+            a.coef[c] = static_cast<float>(gr);
+            a.coef[a.C + c] = static_cast<float>(-gr * rstd * s2 / m);
+            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m + gr * mean * rstd * s2 / m);
+        }
+    }
+}
+
+__global__ void bn_infer_coef_kernel(const float* g, const float* b, const float* mu, const float* var,
+                                     float eps, float* coef, int C) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const double rstd = 1.0 / sqrt(static_cast<double>(var[c]) + eps);
+    coef[c] = static_cast<float>(g[c] * rstd);
+    coef[C + c] = static_cast<float>(b[c] - mu[c] * g[c] * rstd);
+}
+
+template <typename T>
+__global__ void bn_shift_kernel(const T* x, int ld, int C, float* shift) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < C) shift[c] = to_f32(x[c]);
+    (void)ld;
+}
+
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, int64_t n, float lr,
+                           __nv_bfloat16* mirror) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float v = w[i] - lr * g[i];
+        w[i] = v;
+        if (mirror) mirror[i] = __float2bfloat16_rn(v);
+    }
+}
+
+// per image: in [R][C] (row stride ld_in) -> out [C][R_out] (row stride ld_out); r >= R is zero
+template <typename TI, typename TO>
+__global__ void transpose_kernel(const TI* __restrict__ in, TO* __restrict__ out, int R, int C,
+                                 int ld_in, int r_out, int ld_out) {
+    __shared__ float tile[32][33];
+    const int n = blockIdx.z;
+    const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const TI* src = in + static_cast<int64_t>(n) * R * ld_in;
+    TO* dst = out + static_cast<int64_t>(n) * C * ld_out;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < R && c < C) ? to_f32(src[static_cast<int64_t>(r) * ld_in + c]) : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (c < C && r < r_out) dst[static_cast<int64_t>(c) * ld_out + r] = from_f32<TO>(tile[threadIdx.x][i]);
+    }
+}
+
+template <typename TI, typename TO>
+__global__ void cast_kernel(const TI* __restrict__ in, TO* __restrict__ out, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = from_f32<TO>(to_f32(in[i]));
+}
+
+template <typename TI, typename TO>
+void transpose(const void* in, void* out, int N, int R, int C, int ld_in, int r_out, int ld_out,
+               cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(ceil_div(r_out, 32)), static_cast<unsigned>(ceil_div(C, 32)),
+              static_cast<unsigned>(N));
+    transpose_kernel<TI, TO><<<grid, dim3(32, 8), 0, s>>>(static_cast<const TI*>(in), static_cast<TO*>(out), R,
+                                                          C, ld_in, r_out, ld_out);
+    SOL_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+int dfp_reduce_blocks(int64_t pixels, int C) {
+    (void)C;
+    // ~256 pixels per thread row keeps f32 partial sums short; cap at a few waves
+    const int64_t want = ceil_div(pixels, 2048);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4 * num_sms())));
+}
+
+void dfp_launch(const DfpArgs& a, cudaStream_t s) {
+    if (a.dtype == DT_BF16) dfp_launch_t<__nv_bfloat16>(a, s);
+    else dfp_launch_t<float>(a, s);
+}
+
+void softmax_rows(int dtype, const void* x, void* y, int rows, int cols, int ld, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(ceil_div(rows, 8));
+    if (dtype == DT_BF16)
+        softmax_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), rows, cols, ld);
+    else
+        softmax_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(x), static_cast<float*>(y), rows, cols, ld);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void ce_loss(int dtype, const void* p, const void* t, float* loss, int rows, int cols, int ld, cudaStream_t s) {
+    if (dtype == DT_BF16)
+        ce_loss_kernel<<<1, 1024, 0, s>>>(static_cast<const __nv_bfloat16*>(p), static_cast<const __nv_bfloat16*>(t), loss, rows, cols, ld);
+    else
+        ce_loss_kernel<<<1, 1024, 0, s>>>(static_cast<const float*>(p), static_cast<const float*>(t), loss, rows, cols, ld);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void ce_back(int dtype, int fused, const void* p, const void* t, void* dx, int rows, int cols, int ld, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(rows) * ld;
+    const unsigned grid = grid_for(n, 256);
+    if (dtype == DT_BF16)
+        ce_back_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(p), static_cast<const __nv_bfloat16*>(t),
+                                           static_cast<__nv_bfloat16*>(dx), n, rows, fused, cols, ld);
+    else
+        ce_back_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(p), static_cast<const float*>(t),
+                                           static_cast<float*>(dx), n, rows, fused, cols, ld);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void softmax_back(int dtype, const void* d, const void* y, void* dx, int rows, int cols, int ld, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(ceil_div(rows, 8));
+    if (dtype == DT_BF16)
+        softmax_back_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(d), static_cast<const __nv_bfloat16*>(y),
+                                                static_cast<__nv_bfloat16*>(dx), rows, cols, ld);
+    else
+        softmax_back_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(d), static_cast<const float*>(y),
+                                                static_cast<float*>(dx), rows, cols, ld);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void dfp_finalize(const FinalizeArgs& a, cudaStream_t s) {
+    finalize_kernel<<<static_cast<unsigned>(ceil_div(a.C, 128)), 128, 0, s>>>(a);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void bn_infer_coef(const float* g, const float* b, const float* mu, const float* var, float eps, float* coef,
+                   int C, cudaStream_t s) {
+    bn_infer_coef_kernel<<<static_cast<unsigned>(ceil_div(C, 128)), 128, 0, s>>>(g, b, mu, var, eps, coef, C);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void bn_shift(int dtype, const void* x, int ld, int C, float* shift, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(ceil_div(C, 128));
+    if (dtype == DT_BF16) bn_shift_kernel<<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(x), ld, C, shift);
+    else bn_shift_kernel<<<grid, 128, 0, s>>>(static_cast<const float*>(x), ld, C, shift);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror, cudaStream_t s) {
+    sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, g, n, lr, static_cast<__nv_bfloat16*>(mirror));
+    SOL_CUDA(cudaGetLastError());
+}
+
+void nchw_to_nhwc(const float* src, void* dst, int dtype, int N, int C, int H, int W, int c_pad, cudaStream_t s) {
+    const int hw = H * W;
+    if (dtype == DT_BF16) transpose<float, __nv_bfloat16>(src, dst, N, C, hw, hw, c_pad, c_pad, s);
+    else transpose<float, float>(src, dst, N, C, hw, hw, c_pad, c_pad, s);
+}
+
+void nhwc_to_nchw(const void* src, float* dst, int dtype, int N, int C, int H, int W, int ld, cudaStream_t s) {
+    const int hw = H * W;
+    if (dtype == DT_BF16) transpose<__nv_bfloat16, float>(src, dst, N, hw, C, ld, hw, hw, s);
+    else transpose<float, float>(src, dst, N, hw, C, ld, hw, hw, s);
+}
+
+void flatten_nhwc(int dtype, const void* x, void* y, int N, int C, int H, int W, int inverse, cudaStream_t s) {
+    const int hw = H * W;
+    if (!inverse) {
+        if (dtype == DT_BF16) transpose<__nv_bfloat16, __nv_bfloat16>(x, y, N, hw, C, C, hw, hw, s);
+        else transpose<float, float>(x, y, N, hw, C, C, hw, hw, s);
+    } else {
+        if (dtype == DT_BF16) transpose<__nv_bfloat16, __nv_bfloat16>(x, y, N, C, hw, hw, C, C, s);
+        else transpose<float, float>(x, y, N, C, hw, hw, C, C, s);
+    }
+}
+
+void cast_copy(const void* src, int sd, void* dst, int dd, int64_t n, cudaStream_t s) {
+    const unsigned grid = grid_for(n, 256);
+    if (sd == DT_F32 && dd == DT_BF16)
+        cast_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(src), static_cast<__nv_bfloat16*>(dst), n);
+    else if (sd == DT_BF16 && dd == DT_F32)
+        cast_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src), static_cast<float*>(dst), n);
+    else if (sd == DT_F32 && dd == DT_F32)
+        cast_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(src), static_cast<float*>(dst), n);
+    else
+        cast_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src), static_cast<__nv_bfloat16*>(dst), n);
+    SOL_CUDA(cudaGetLastError());
+}
+
+}  // namespace solb200

@@ -1,0 +1,641 @@
+// tcgen05 / TMEM implicit-GEMM kernels for sm_100a. See igemm.cuh for the semantics.
+//
+// Structure (one output tile per CTA, 128 threads = 4 warps):
+//   * all 4 warps gather A (im2col / transposed-conv gather) and B (packed weights) tiles with
+//     16-byte cp.async into a STAGES-deep ring of 128B-swizzled shared-memory tiles
+//     (zero-fill implements conv padding, stride holes and ragged edges);
+//   * one elected thread issues tcgen05.mma (M=128, N=BN, K=16 bf16 / K=8 tf32) reading both
+//     operands through UMMA shared-memory descriptors, accumulating in TMEM; tcgen05.commit
+//     arrives on the stage's mbarrier, which is what releases the slot for the next gather;
+//   * the epilogue moves TMEM -> registers with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31,
+//     i.e. output rows), adds the bias and stores NHWC rows.
+#include "igemm.cuh"
+
+#include <algorithm>
+#include <mutex>
+
+namespace solb200 {
+namespace {
+
+constexpr int BM = 128;
+constexpr int ROWB = 128;  // bytes per swizzle row
+constexpr int THREADS = 128;
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+// ---------------------------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(addr),
+        "r"(parity));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+}
+
+template <uint32_t COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t slot_addr) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(slot_addr),
+                 "n"(COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+template <uint32_t COLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(COLS));
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), sm_100 version 1.
+// K-major:  LBO unused (16 B), SBO = 1024 B between 8-row core-matrix groups.
+// MN-major: LBO = stride between 64-element MN blocks, SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
+    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: f32 accumulate, A/B format (1 = bf16, 2 = tf32), majors, N, M.
+__host__ __device__ constexpr uint32_t make_idesc(int ab_fmt, int n, int m, int a_mn, int b_mn) {
+    return (1u << 4) | (static_cast<uint32_t>(ab_fmt) << 7) | (static_cast<uint32_t>(ab_fmt) << 10) |
+           (static_cast<uint32_t>(a_mn) << 15) | (static_cast<uint32_t>(b_mn) << 16) |
+           (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+template <typename T>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                    uint32_t accum);
+template <>
+__device__ __forceinline__ void mma<__nv_bfloat16>(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                   uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+template <>
+__device__ __forceinline__ void mma<float>(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar_addr) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+        mbar_addr));
+}
+
+// 32 lanes x 32 bits, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+        "[%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+}
+
+template <typename T> struct AbFmt;
+template <> struct AbFmt<__nv_bfloat16> { static constexpr int v = 1; };
+template <> struct AbFmt<float> { static constexpr int v = 2; };
+
+template <int STAGE_BYTES>
+constexpr int stages_for() {
+    return std::min(8, (SMEM_BUDGET - 2048) / STAGE_BYTES);
+}
+
+template <int BN>
+constexpr uint32_t tmem_cols() {
+    return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+}
+
+// Epilogue store of 16 consecutive fp32 accumulators of one row.
+// Columns in [nout, ld) are row padding and are written as zeros.
+template <typename TO>
+__device__ __forceinline__ void store_row16(TO* out, int n, int nout, int ld, const float* f) {
+    if (n + 16 <= nout && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        constexpr int V = 16 / sizeof(TO);
+#pragma unroll
+        for (int q = 0; q < 16; q += V) store16(out + q, f + q);
+    } else {
+        for (int q = 0; q < 16 && n + q < ld; ++q) out[q] = from_f32<TO>(n + q < nout ? f[q] : 0.f);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// fprop / dgrad: A K-major gathered rows, B K-major packed weights
+// ---------------------------------------------------------------------------------------------
+
+template <typename T, typename TO, int BN, int MODE>
+__global__ void __launch_bounds__(THREADS, 1) igemm_kernel(IgemmArgs a) {
+    constexpr int VEC = 16 / sizeof(T);
+    constexpr int BK = ROWB / sizeof(T);
+    constexpr int A_BYTES = BM * ROWB;
+    constexpr int B_BYTES = BN * ROWB;
+    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    constexpr int STAGES = stages_for<STAGE_BYTES>();
+    constexpr uint32_t TCOLS = tmem_cols<BN>();
+    constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
+    constexpr int KSTEP_BYTES = 32;  // K=16 bf16 / K=8 tf32 per MMA instruction
+    static_assert(BN % 16 == 0 && BN <= 256, "bad BN");
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * BN;
+    const int num_kb = a.K_pad / BK;
+    const int M = a.N * a.OH * a.OW;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&mbar[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+
+    // Per-thread gather rows: chunk j of rows rbase + 16*i.
+    const int j = tid & 7;
+    const int rbase = tid >> 3;
+    int rn[8], rh[8], rw[8];
+    const int ohw = a.OH * a.OW;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int m = m0 + rbase + 16 * i;
+        if (m < M) {
+            const int n = m / ohw;
+            const int rem = m - n * ohw;
+            const int oh = rem / a.OW;
+            const int ow = rem - oh * a.OW;
+            rn[i] = n;
+            if (MODE == IG_FPROP) {
+                rh[i] = oh * a.sh - a.ph;
+                rw[i] = ow * a.sw - a.pw;
+            } else {
+                rh[i] = oh + a.ph;
+                rw[i] = ow + a.pw;
+            }
+        } else {
+            rn[i] = -1;
+            rh[i] = rw[i] = 0;
+        }
+    }
+    const T* src = static_cast<const T*>(a.src);
+    const T* wt = static_cast<const T*>(a.wt);
+    const int ntaps = a.kh * a.kw;
+
+    auto load_stage = [&](int slot, int kb) {
+        uint8_t* sa = smem + slot * STAGE_BYTES;
+        uint8_t* sb = sa + A_BYTES;
+        const int k = kb * BK + j * VEC;
+        const int tap = k / a.SC;
+        const int c = k - tap * a.SC;
+        const int dkh = tap / a.kw;
+        const int dkw = tap - dkh * a.kw;
+        const bool tap_ok = tap < ntaps;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int r = rbase + 16 * i;
+            bool ok = tap_ok && rn[i] >= 0;
+            int hh, ww;
+            if (MODE == IG_FPROP) {
+                hh = rh[i] + dkh;
+                ww = rw[i] + dkw;
+            } else {
+                const int nh = rh[i] - dkh, nw = rw[i] - dkw;
+                ok = ok && nh >= 0 && nw >= 0 && (nh % a.sh) == 0 && (nw % a.sw) == 0;
+                hh = nh / a.sh;
+                ww = nw / a.sw;
+            }
+            ok = ok && hh >= 0 && hh < a.SH && ww >= 0 && ww < a.SW;
+            const T* g = ok ? src + ((static_cast<int64_t>(rn[i]) * a.SH + hh) * a.SW + ww) * a.SC + c : src;
+            cp_async16(smem_u32(sa + r * ROWB + ((j ^ (r & 7)) << 4)), g, ok);
+        }
+#pragma unroll
+        for (int i = 0; i < BN / 16; ++i) {
+            const int r = rbase + 16 * i;
+            const int row = n0 + r;
+            const bool ok = row < a.Nout;
+            const T* g = ok ? wt + static_cast<int64_t>(row) * a.K_pad + kb * BK + j * VEC : wt;
+            cp_async16(smem_u32(sb + r * ROWB + ((j ^ (r & 7)) << 4)), g, ok);
+        }
+    };
+
+    // prologue
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < num_kb) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    for (int kb = 0; kb < num_kb; ++kb) {
+        const int nk = kb + STAGES - 1;
+        if (nk < num_kb) {
+            const int ns = nk % STAGES;
+            if (kb >= 1) mbar_wait(smem_u32(&mbar[ns]), ((kb - 1) / STAGES) & 1);  // MMA(kb-1) freed it
+            load_stage(ns, nk);
+        }
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const int slot = kb % STAGES;
+            const uint32_t a_addr = smem_u32(smem + slot * STAGE_BYTES);
+            const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < ROWB / KSTEP_BYTES; ++k) {
+                const uint64_t ad = sw128_desc(a_addr + k * KSTEP_BYTES, 16, 1024);
+                const uint64_t bd = sw128_desc(b_addr + k * KSTEP_BYTES, 16, 1024);
+                mma<T>(tmem_d, ad, bd, IDESC, (kb | k) != 0);
+            }
+            mma_commit(smem_u32(&mbar[slot]));
+        }
+    }
+    {
+        const int last = num_kb - 1;
+        mbar_wait(smem_u32(&mbar[last % STAGES]), (last / STAGES) & 1);
+    }
+    tc_fence_after();
+
+    // epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
+    const int row = warp * 32 + lane;
+    const int m = m0 + row;
+    TO* out = static_cast<TO*>(a.out);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem_d + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+        const int n = n0 + c0;
+        if (m < M && n < a.ldo) {
+            float f[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                float x = __uint_as_float(v[q]);
+                if (a.bias != nullptr && n + q < a.Nout) x += __ldg(a.bias + n + q);
+                if (a.relu) x = fmaxf(x, 0.0f);
+                f[q] = x;
+            }
+            store_row16<TO>(out + static_cast<int64_t>(m) * a.ldo + n, n, a.Nout, a.ldo, f);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<TCOLS>(tmem_d);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// wgrad: D[Cout][Ncol] += dy^T[Cout][P] * Xcol^T[P][Ncol]; both operands MN-major in smem.
+// Tile layout per operand: [mn-block of 64 elems][k-group of 8 pixels][8 rows][128 B]
+//   -> LBO (mn-block stride) = (BK/8)*1024 B, SBO (k-group stride) = 1024 B.
+// Split-K over pixel ranges; partial tiles go to a workspace reduced by wgrad_reduce_kernel.
+// ---------------------------------------------------------------------------------------------
+
+template <typename T, int BN>
+__global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_per_split, int ncol) {
+    constexpr int VEC = 16 / sizeof(T);
+    constexpr int EPB = ROWB / sizeof(T);  // elements per 128B (MN block width)
+    constexpr int BK = 64;                 // pixels per k-block (8 k-groups)
+    constexpr int A_BLOCKS = BM / EPB;
+    constexpr int B_BLOCKS = BN / EPB;
+    constexpr int A_BYTES = A_BLOCKS * BK * ROWB;
+    constexpr int B_BYTES = B_BLOCKS * BK * ROWB;
+    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    constexpr int STAGES = stages_for<STAGE_BYTES>();
+    constexpr uint32_t TCOLS = tmem_cols<BN>();
+    constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 1, 1);
+    constexpr int KPER_MMA = 32 / sizeof(T);  // 16 bf16 / 8 tf32 pixels per instruction
+    constexpr uint32_t LBO = (BK / 8) * 1024;
+    static_assert(BN % EPB == 0, "BN must be a multiple of the 128B MN block");
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int m0 = blockIdx.x * BM;   // Cout block
+    const int n0 = blockIdx.y * BN;   // (tap, ci) block
+    const int split = blockIdx.z;
+    const int P = a.N * a.OH * a.OW;
+    const int total_kb = (P + BK - 1) / BK;
+    const int kb_begin = split * kb_per_split;
+    const int kb_end = min(total_kb, kb_begin + kb_per_split);
+    const int num_kb = max(0, kb_end - kb_begin);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&mbar[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+
+    const T* dy = static_cast<const T*>(a.dy);
+    const T* x = static_cast<const T*>(a.x);
+    const int j = tid & 7;
+    const int rbase = tid >> 3;  // pixel row within k-block: rbase + 16*i, i < 4
+    const int ohw = a.OH * a.OW;
+    const int ntaps = a.kh * a.kw;
+
+    auto load_stage = [&](int slot, int kb) {
+        uint8_t* sa = smem + slot * STAGE_BYTES;
+        uint8_t* sb = sa + A_BYTES;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = rbase + 16 * i;           // pixel within k-block
+            const int p = kb * BK + r;
+            const bool pv = p < P;
+            int n = 0, oh = 0, ow = 0;
+            if (pv) {
+                n = p / ohw;
+                const int rem = p - n * ohw;
+                oh = rem / a.OW;
+                ow = rem - oh * a.OW;
+            }
+            const int kg = r >> 3, rr = r & 7;
+            // A: dy[p][m0 + blk*EPB + j*VEC]
+#pragma unroll
+            for (int blk = 0; blk < A_BLOCKS; ++blk) {
+                const int co = m0 + blk * EPB + j * VEC;
+                const bool ok = pv && co < a.Cout;
+                const T* g = ok ? dy + static_cast<int64_t>(p) * a.ld_dy + co : dy;
+                cp_async16(smem_u32(sa + (blk * (BK / 8) + kg) * 1024 + rr * ROWB + ((j ^ rr) << 4)), g, ok);
+            }
+            // B: x gathered at pixel p for column n0 + blk*EPB + j*VEC = (tap, ci)
+#pragma unroll
+            for (int blk = 0; blk < B_BLOCKS; ++blk) {
+                const int col = n0 + blk * EPB + j * VEC;
+                const int tap = col / a.SC;
+                const int ci = col - tap * a.SC;
+                const int dkh = tap / a.kw, dkw = tap - (tap / a.kw) * a.kw;
+                const int hh = oh * a.sh - a.ph + dkh, ww = ow * a.sw - a.pw + dkw;
+                const bool ok = pv && col < ncol && tap < ntaps && hh >= 0 && hh < a.SH && ww >= 0 && ww < a.SW;
+                const T* g = ok ? x + ((static_cast<int64_t>(n) * a.SH + hh) * a.SW + ww) * a.SC + ci : x;
+                cp_async16(smem_u32(sb + (blk * (BK / 8) + kg) * 1024 + rr * ROWB + ((j ^ rr) << 4)), g, ok);
+            }
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < num_kb) load_stage(s, kb_begin + s);
+        cp_async_commit();
+    }
+    for (int kb = 0; kb < num_kb; ++kb) {
+        const int nk = kb + STAGES - 1;
+        if (nk < num_kb) {
+            const int ns = nk % STAGES;
+            if (kb >= 1) mbar_wait(smem_u32(&mbar[ns]), ((kb - 1) / STAGES) & 1);
+            load_stage(ns, kb_begin + nk);
+        }
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const int slot = kb % STAGES;
+            const uint32_t a_addr = smem_u32(smem + slot * STAGE_BYTES);
+            const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / KPER_MMA; ++k) {
+                // K advance: KPER_MMA pixels = KPER_MMA/8 k-groups of 1024 B
+                const uint32_t koff = (k * KPER_MMA / 8) * 1024;
+                const uint64_t ad = sw128_desc(a_addr + koff, LBO, 1024);
+                const uint64_t bd = sw128_desc(b_addr + koff, LBO, 1024);
+                mma<T>(tmem_d, ad, bd, IDESC, (kb | k) != 0);
+            }
+            mma_commit(smem_u32(&mbar[slot]));
+        }
+    }
+    if (num_kb > 0) {
+        const int last = num_kb - 1;
+        mbar_wait(smem_u32(&mbar[last % STAGES]), (last / STAGES) & 1);
+    }
+    tc_fence_after();
+
+    const int row = warp * 32 + lane;
+    const int co = m0 + row;
+    float* dst = a.workspace ? a.workspace + static_cast<int64_t>(split) * a.Cout * ncol : a.dw;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem_d + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+        const int n = n0 + c0;
+        if (co < a.Cout && n < ncol) {
+            float f[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) f[q] = num_kb > 0 ? __uint_as_float(v[q]) : 0.0f;
+            store_row16<float>(dst + static_cast<int64_t>(co) * ncol + n, n, ncol, ncol, f);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<TCOLS>(tmem_d);
+    }
+}
+
+__global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dw, int64_t n,
+                                    int splits) {
+    const int64_t i4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (i4 >= n) return;
+    if (i4 + 4 <= n) {
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int s = 0; s < splits; ++s) {
+            float4 v = __ldg(reinterpret_cast<const float4*>(ws + s * n + i4));
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(dw + i4) = acc;
+    } else {
+        for (int64_t i = i4; i < n; ++i) {
+            float acc = 0.f;
+            for (int s = 0; s < splits; ++s) acc += ws[s * n + i];
+            dw[i] = acc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host dispatch
+// ---------------------------------------------------------------------------------------------
+
+template <typename T, typename TO, int BN, int MODE>
+void launch_igemm_t(const IgemmArgs& a, cudaStream_t s) {
+    constexpr int STAGE_BYTES = BM * ROWB + BN * ROWB;
+    constexpr int STAGES = stages_for<STAGE_BYTES>();
+    constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + STAGES * 8 + 16;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        SOL_CUDA(cudaFuncSetAttribute(igemm_kernel<T, TO, BN, MODE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    });
+    const int M = a.N * a.OH * a.OW;
+    dim3 grid(static_cast<unsigned>(ceil_div(M, BM)), static_cast<unsigned>(ceil_div(a.Nout, BN)));
+    igemm_kernel<T, TO, BN, MODE><<<grid, THREADS, SMEM, s>>>(a);
+    SOL_CUDA(cudaGetLastError());
+}
+
+template <typename T, typename TO, int MODE>
+void dispatch_bn(const IgemmArgs& a, cudaStream_t s) {
+    switch (igemm_block_n(a.Nout)) {
+        case 16: return launch_igemm_t<T, TO, 16, MODE>(a, s);
+        case 32: return launch_igemm_t<T, TO, 32, MODE>(a, s);
+        case 64: return launch_igemm_t<T, TO, 64, MODE>(a, s);
+        case 128: return launch_igemm_t<T, TO, 128, MODE>(a, s);
+        default: return launch_igemm_t<T, TO, 256, MODE>(a, s);
+    }
+}
+
+template <typename T, int BN>
+void launch_wgrad_t(const WgradArgs& a, int ncol, int splits, int kb_per_split, cudaStream_t s) {
+    constexpr int EPB = ROWB / sizeof(T);
+    constexpr int STAGE_BYTES = (BM / EPB) * 64 * ROWB + (BN / EPB) * 64 * ROWB;
+    constexpr int STAGES = stages_for<STAGE_BYTES>();
+    constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + STAGES * 8 + 16;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        SOL_CUDA(cudaFuncSetAttribute(wgrad_kernel<T, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    });
+    dim3 grid(static_cast<unsigned>(ceil_div(a.Cout, BM)), static_cast<unsigned>(ceil_div(ncol, BN)),
+              static_cast<unsigned>(splits));
+    wgrad_kernel<T, BN><<<grid, THREADS, SMEM, s>>>(a, kb_per_split, ncol);
+    SOL_CUDA(cudaGetLastError());
+}
+
+struct WgradPlan {
+    int ncol, bn, splits, kb_per_split;
+};
+
+WgradPlan plan_wgrad(const WgradArgs& a) {
+    WgradPlan p;
+    p.ncol = a.kh * a.kw * a.SC;
+    const int epb = a.dtype == DT_BF16 ? 64 : 32;
+    p.bn = p.ncol <= epb ? epb : (p.ncol <= 2 * epb ? 2 * epb : 256);
+    if (a.dtype == DT_F32 && p.bn > 128) p.bn = 128;
+    const int tiles = static_cast<int>(ceil_div(a.Cout, BM) * ceil_div(p.ncol, p.bn));
+    const int total_kb = static_cast<int>(ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, 64));
+    int splits = std::max(1, std::min(total_kb, (2 * num_sms() + tiles - 1) / tiles));
+    p.kb_per_split = static_cast<int>(ceil_div(total_kb, splits));
+    p.splits = static_cast<int>(ceil_div(total_kb, p.kb_per_split));
+    return p;
+}
+
+}  // namespace
+
+int igemm_block_n(int nout) {
+    if (nout <= 16) return 16;
+    if (nout <= 32) return 32;
+    if (nout <= 64) return 64;
+    if (nout <= 128) return 128;
+    return 256;
+}
+
+void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
+    const int vec = a.dtype == DT_BF16 ? 8 : 4;
+    const int bk = a.dtype == DT_BF16 ? 64 : 32;
+    if (a.SC % vec != 0) throw std::invalid_argument("igemm: channel count must be a multiple of 16 bytes");
+    if (a.K_pad % bk != 0) throw std::invalid_argument("igemm: K_pad must be a multiple of the k-block");
+    if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
+    if (a.dtype == DT_BF16) {
+        if (a.out_dtype == DT_BF16) {
+            if (a.mode == IG_FPROP) dispatch_bn<__nv_bfloat16, __nv_bfloat16, IG_FPROP>(a, s);
+            else dispatch_bn<__nv_bfloat16, __nv_bfloat16, IG_DGRAD>(a, s);
+        } else {
+            if (a.mode == IG_FPROP) dispatch_bn<__nv_bfloat16, float, IG_FPROP>(a, s);
+            else dispatch_bn<__nv_bfloat16, float, IG_DGRAD>(a, s);
+        }
+    } else {
+        if (a.out_dtype != DT_F32) throw std::invalid_argument("igemm: tf32 path writes f32");
+        if (a.mode == IG_FPROP) dispatch_bn<float, float, IG_FPROP>(a, s);
+        else dispatch_bn<float, float, IG_DGRAD>(a, s);
+    }
+}
+
+size_t wgrad_workspace_floats(const WgradArgs& a) {
+    WgradPlan p = plan_wgrad(a);
+    return p.splits > 1 ? static_cast<size_t>(p.splits) * a.Cout * p.ncol : 0;
+}
+
+void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
+    WgradArgs a = a_in;
+    const int vec = a.dtype == DT_BF16 ? 8 : 4;
+    if (a.SC % vec != 0 || a.ld_dy % vec != 0)
+        throw std::invalid_argument("wgrad: channel counts must be multiples of 16 bytes");
+    WgradPlan p = plan_wgrad(a);
+    if (p.splits <= 1) a.workspace = nullptr;
+    else if (a.workspace == nullptr) throw std::invalid_argument("wgrad: workspace required");
+    if (a.dtype == DT_BF16) {
+        switch (p.bn) {
+            case 64: launch_wgrad_t<__nv_bfloat16, 64>(a, p.ncol, p.splits, p.kb_per_split, s); break;
+            case 128: launch_wgrad_t<__nv_bfloat16, 128>(a, p.ncol, p.splits, p.kb_per_split, s); break;
+            default: launch_wgrad_t<__nv_bfloat16, 256>(a, p.ncol, p.splits, p.kb_per_split, s); break;
+        }
+    } else {
+        switch (p.bn) {
+            case 32: launch_wgrad_t<float, 32>(a, p.ncol, p.splits, p.kb_per_split, s); break;
+            case 64: launch_wgrad_t<float, 64>(a, p.ncol, p.splits, p.kb_per_split, s); break;
+            default: launch_wgrad_t<float, 128>(a, p.ncol, p.splits, p.kb_per_split, s); break;
+        }
+    }
+    if (p.splits > 1) {
+        const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
+        const int threads = 256;
+        wgrad_reduce_kernel<<<static_cast<unsigned>(ceil_div(ceil_div(n, 4), threads)), threads, 0, s>>>(
+            a.workspace, a.dw, n, p.splits);
+        SOL_CUDA(cudaGetLastError());
+    }
+}
+
+}  // namespace solb200

@@ -1,0 +1,59 @@
+// tcgen05/TMEM implicit-GEMM for Conv2d / Linear (fprop, dgrad) and the wgrad GEMM, sm_100a.
+//
+// Semantics follow the reference's heavy-layer providers and oracle:
+//   fprop   y[n,oh,ow,co] = b[co] + sum_{kh,kw,ci} x[n, oh*sh-ph+kh, ow*sw-pw+kw, ci] W[co,ci,kh,kw]
+//           (proj/src/reference.cpp:138-161; dnn_providers.cpp:104-183)
+//   dgrad   dx[n,ih,iw,ci] = sum_{kh,kw,co} dy[n,(ih+ph-kh)/sh,(iw+pw-kw)/sw,co] W[co,ci,kh,kw]
+//           over exactly divisible, in-range positions (reference.cpp:482-506; dnn_providers.cpp:185-215)
+//   wgrad   dW[co,(kh,kw,ci)] = sum_{n,oh,ow} dy[n,oh,ow,co] x[n,oh*sh-ph+kh,ow*sw-pw+kw,ci]
+//           (reference.cpp:507-533; dnn_providers.cpp:217-241)
+// Layout: activations NHWC (ActLayout::ChannelsLast), weights packed K-major [rows][K_pad].
+#pragma once
+
+#include "common.cuh"
+
+namespace solb200 {
+
+enum IgemmMode : int {
+    IG_FPROP = 0,   // A = im2col(x) gathered K-major; B = W packed [Cout][kh][kw][Cin_pad]
+    IG_DGRAD = 1,   // A = transposed-conv gather of dy; B = W packed [Cin][kh][kw][Cout_pad]
+};
+
+struct IgemmArgs {
+    int mode = IG_FPROP;
+    int dtype = DT_BF16;       // element type of A/B (bf16 -> kind::f16, f32 -> kind::tf32)
+    int out_dtype = DT_BF16;   // element type of the output
+    const void* src = nullptr; // gathered operand source, NHWC [N, SH, SW, SC]
+    const void* wt = nullptr;  // packed B, [n_rows][K_pad]
+    const float* bias = nullptr;
+    void* out = nullptr;       // [M][ldo]
+    int N = 0, SH = 0, SW = 0, SC = 0;
+    int OH = 0, OW = 0;
+    int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
+    int Nout = 0;              // GEMM N
+    int K_pad = 0;             // padded reduction extent of the packed operand
+    int ldo = 0;
+    int relu = 0;              // fused epilogue ReLU (unused by the reference path)
+};
+
+// Launches on `stream`. Throws on unsupported shapes (no fallback path exists).
+void igemm_launch(const IgemmArgs& a, cudaStream_t stream);
+
+// Tile configuration chosen for a GEMM (exposed for the roofline/bench bookkeeping).
+int igemm_block_n(int nout);
+
+// wgrad: dW[Cout][K_pad] (f32) = dy^T x im2col(x), both operands MN-major.
+struct WgradArgs {
+    int dtype = DT_BF16;
+    const void* dy = nullptr;  // [N, OH, OW, Cout] (Cout padded/strided by ld_dy)
+    const void* x = nullptr;   // [N, SH, SW, SC]
+    float* dw = nullptr;       // [Cout][kh*kw*SC] f32 (packed order kh, kw, ci)
+    int N = 0, SH = 0, SW = 0, SC = 0, OH = 0, OW = 0, Cout = 0;
+    int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
+    int ld_dy = 0;
+    float* workspace = nullptr;  // split-K partials (size from wgrad_workspace_floats)
+};
+void wgrad_launch(const WgradArgs& a, cudaStream_t stream);
+size_t wgrad_workspace_floats(const WgradArgs& a);
+
+}  // namespace solb200

@@ -1,0 +1,1148 @@
+// Unit compiler: sol_unit_desc (ops + attrs + boundary bindings, i.e. an ExecUnit with its
+// KernelIR bindings) -> one hand-written kernel family. There is no generic fallback: a unit whose
+// op signature no family covers fails at compile time with SOL_E_UNSUPPORTED, mirroring the
+// reference's "unknown op -> hard error" policy (dfp_lower.cpp UnsupportedInGroupError).
+//
+// Op semantics followed (reference = /root/reference/proj):
+//   BatchNorm2d inference  dfp_lower.cpp:454-472 / reference.cpp:216-237 (gamma*(x-mu)*rstd+beta)
+//   BatchNorm2d training   bn_batch_stats dfp_lower.cpp:362-390 (biased batch variance)
+//   ReLU / Add / Copy      dfp_lower.cpp:399-404
+//   Max/AvgPool2d          dfp_lower.cpp:406-434 (min_init, count_padding)
+//   GlobalAvgPool          dfp_lower.cpp:436-452
+//   depthwise Conv2d       dfp_lower.cpp:519-540 (groups == Cin == Cout)
+//   backward units         dfp_lower.cpp:542-753, :800-868; reference.cpp:294-584
+#include "module.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "dfp.cuh"
+#include "igemm.cuh"
+#include "pack.cuh"
+
+namespace solb200 {
+
+Module::~Module() {
+    for (void* p : owned_) cudaFree(p);
+}
+
+void* Module::dev_alloc(size_t bytes) {
+    void* p = nullptr;
+    SOL_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    SOL_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    owned_.push_back(p);
+    return p;
+}
+
+namespace {
+
+struct Geo {
+    int64_t N = 1, C = 1, H = 1, W = 1, ld = 1;
+    int rank = 0;
+    int64_t numel() const { return N * C * H * W; }
+    int64_t pixels() const { return N * H * W; }
+};
+
+Geo geo_of_dims(int rank, const int64_t* d, int64_t ld) {
+    Geo g;
+    g.rank = rank;
+    if (rank == 4) {
+        g.N = d[0]; g.C = d[1]; g.H = d[2]; g.W = d[3];
+    } else if (rank == 2) {
+        g.N = d[0]; g.C = d[1];
+    } else if (rank == 1) {
+        g.C = d[0];
+    } else if (rank == 3) {
+        g.C = d[0] * d[1] * d[2];
+    }
+    g.ld = ld > 0 ? ld : g.C;
+    return g;
+}
+
+Geo geo_b(const sol_binding& b) { return geo_of_dims(b.rank, b.dims, b.ld); }
+
+int64_t param_numel(const sol_binding& b) {
+    int64_t n = 1;
+    for (int i = 0; i < b.rank; ++i) n *= b.dims[i];
+    return n;
+}
+
+size_t elem_size(int dtype) { return dtype == DT_BF16 ? 2 : 4; }
+
+bool is_heavy_op(int op) {
+    return op == SOL_OP_CONV2D || op == SOL_OP_LINEAR || op == SOL_OP_CONV2DBACKX ||
+           op == SOL_OP_CONV2DBACKW || op == SOL_OP_LINEARBACKX || op == SOL_OP_LINEARBACKW;
+}
+
+bool is_depthwise(const sol_unit_op& o, int64_t cin) {
+    return o.op == SOL_OP_CONV2D && o.attrs.groups > 1 && o.attrs.groups == o.attrs.out_channels &&
+           o.attrs.groups == cin;
+}
+
+[[noreturn]] void unsupported(const std::string& what) { throw UnsupportedError(what); }
+
+// bytes an activation binding occupies in plan storage
+size_t binding_bytes(const sol_binding& b) {
+    if (b.is_param) return static_cast<size_t>(param_numel(b)) * 4;
+    if (b.rank == 0) return elem_size(b.dtype);
+    Geo g = geo_b(b);
+    return static_cast<size_t>(g.pixels() * g.ld) * elem_size(b.dtype);
+}
+
+void fill_arg_bytes(Module& m, const sol_unit_desc& d) {
+    m.arg_bytes.clear();
+    for (int i = 0; i < d.n_bindings; ++i) m.arg_bytes.push_back(binding_bytes(d.bindings[i]));
+    m.arg_bytes.push_back(binding_bytes(d.output));
+    m.n_args = d.n_bindings + 1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// heavy layers: tcgen05 implicit GEMM (KernelProvider::execute replacement, dnn.hpp:61-63)
+// ---------------------------------------------------------------------------------------------
+
+class HeavyModule : public Module {
+public:
+    explicit HeavyModule(const sol_unit_desc& d) : dtype_(d.dtype) {
+        const sol_unit_op& o = d.ops[0];
+        op_ = o.op;
+        const sol_attrs& a = o.attrs;
+        kh_ = static_cast<int>(a.kh ? a.kh : 1);
+        kw_ = static_cast<int>(a.kw ? a.kw : 1);
+        sh_ = static_cast<int>(a.sh ? a.sh : 1);
+        sw_ = static_cast<int>(a.sw ? a.sw : 1);
+        ph_ = static_cast<int>(a.ph);
+        pw_ = static_cast<int>(a.pw);
+        if (op_ == SOL_OP_LINEAR || op_ == SOL_OP_LINEARBACKX || op_ == SOL_OP_LINEARBACKW) {
+            kh_ = kw_ = sh_ = sw_ = 1;
+            ph_ = pw_ = 0;
+        }
+        if (a.groups > 1 && (op_ == SOL_OP_CONV2D || op_ == SOL_OP_CONV2DBACKX || op_ == SOL_OP_CONV2DBACKW))
+            unsupported("grouped (non-depthwise) convolution has no B200 provider");
+        const int bk = dtype_ == DT_BF16 ? 64 : 32;
+        in_ = geo_b(d.bindings[o.inputs[0]]);
+        out_ = geo_b(d.output);
+        fill_arg_bytes(*this, d);
+        switch (op_) {
+            case SOL_OP_CONV2D:
+            case SOL_OP_LINEAR: {
+                family = op_ == SOL_OP_CONV2D ? "conv_fprop_tcgen05" : "linear_tcgen05";
+                w_idx_ = o.params[0];
+                b_idx_ = (a.has_bias && o.n_params > 1) ? o.params[1] : -1;
+                cin_ = in_.C;
+                cout_ = out_.C;
+                kpad_ = static_cast<int>(round_up(static_cast<int64_t>(kh_) * kw_ * in_.ld, bk));
+                packed_ = dev_alloc(static_cast<size_t>(cout_) * kpad_ * elem_size(dtype_));
+                algo_flops = 2.0 * out_.pixels() * cout_ * kh_ * kw_ * cin_;
+                algo_bytes = (in_.pixels() * in_.ld + out_.pixels() * out_.ld) * double(elem_size(dtype_)) +
+                             double(cout_) * cin_ * kh_ * kw_ * elem_size(dtype_);
+                launches = 2;
+                break;
+            }
+            case SOL_OP_CONV2DBACKX:
+            case SOL_OP_LINEARBACKX: {
+                family = op_ == SOL_OP_CONV2DBACKX ? "conv_dgrad_tcgen05" : "linear_dgrad_tcgen05";
+                w_idx_ = o.params[0];
+                // in_ = delta (Cout), out_ = dx (Cin)
+                cin_ = out_.C;
+                cout_ = in_.C;
+                kpad_ = static_cast<int>(round_up(static_cast<int64_t>(kh_) * kw_ * in_.ld, bk));
+                packed_ = dev_alloc(static_cast<size_t>(cin_) * kpad_ * elem_size(dtype_));
+                algo_flops = 2.0 * in_.pixels() * cout_ * kh_ * kw_ * cin_;
+                algo_bytes = (in_.pixels() * in_.ld + out_.pixels() * out_.ld) * double(elem_size(dtype_)) +
+                             double(cout_) * cin_ * kh_ * kw_ * elem_size(dtype_);
+                launches = 2;
+                break;
+            }
+            case SOL_OP_CONV2DBACKW:
+            case SOL_OP_LINEARBACKW: {
+                family = op_ == SOL_OP_CONV2DBACKW ? "conv_wgrad_tcgen05" : "linear_wgrad_tcgen05";
+                // inputs: delta, x ; output dW canonical f32
+                x_ = geo_b(d.bindings[o.inputs[1]]);
+                cout_ = in_.C;
+                cin_ = x_.C;
+                WgradArgs w = wargs(nullptr, nullptr, nullptr, nullptr);
+                ws_floats_ = wgrad_workspace_floats(w);
+                packed_floats_ = static_cast<size_t>(cout_) * kh_ * kw_ * x_.ld;
+                algo_flops = 2.0 * in_.pixels() * cout_ * kh_ * kw_ * cin_;
+                algo_bytes = (in_.pixels() * in_.ld + x_.pixels() * x_.ld) * double(elem_size(dtype_)) +
+                             double(cout_) * cin_ * kh_ * kw_ * 4.0;
+                launches = ws_floats_ ? 3 : 2;
+                break;
+            }
+            default:
+                unsupported("not a heavy op");
+        }
+    }
+
+    size_t scratch_bytes() const override {
+        return op_ == SOL_OP_CONV2DBACKW || op_ == SOL_OP_LINEARBACKW ? (packed_floats_ + ws_floats_) * 4 + 256 : 0;
+    }
+
+    WgradArgs wargs(const void* dy, const void* x, float* dw, float* ws) const {
+        WgradArgs w;
+        w.dtype = dtype_;
+        w.dy = dy;
+        w.x = x;
+        w.dw = dw;
+        w.workspace = ws;
+        w.N = static_cast<int>(x_.N);
+        w.SH = static_cast<int>(x_.H);
+        w.SW = static_cast<int>(x_.W);
+        w.SC = static_cast<int>(x_.ld);
+        w.OH = static_cast<int>(in_.H);
+        w.OW = static_cast<int>(in_.W);
+        w.Cout = static_cast<int>(cout_);
+        w.kh = kh_; w.kw = kw_; w.sh = sh_; w.sw = sw_; w.ph = ph_; w.pw = pw_;
+        w.ld_dy = static_cast<int>(in_.ld);
+        return w;
+    }
+
+    void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) override {
+        if (nargs != n_args) throw std::invalid_argument("heavy module: wrong argument count");
+        void* out = args[nargs - 1];
+        switch (op_) {
+            case SOL_OP_CONV2D:
+            case SOL_OP_LINEAR: {
+                if (!(frozen && packed_valid_)) {
+                    pack_conv_weight(static_cast<const float*>(args[w_idx_]), packed_, dtype_, static_cast<int>(cout_),
+                                     static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), kpad_, s);
+                    packed_valid_ = true;
+                }
+                IgemmArgs g;
+                g.mode = IG_FPROP;
+                g.dtype = dtype_;
+                g.out_dtype = dtype_;
+                g.src = args[0];
+                g.wt = packed_;
+                g.bias = b_idx_ >= 0 ? static_cast<const float*>(args[b_idx_]) : nullptr;
+                g.out = out;
+                g.N = static_cast<int>(in_.N);
+                g.SH = static_cast<int>(in_.H);
+                g.SW = static_cast<int>(in_.W);
+                g.SC = static_cast<int>(in_.ld);
+                g.OH = static_cast<int>(out_.H);
+                g.OW = static_cast<int>(out_.W);
+                g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
+                g.Nout = static_cast<int>(cout_);
+                g.K_pad = kpad_;
+                g.ldo = static_cast<int>(out_.ld);
+                igemm_launch(g, s);
+                break;
+            }
+            case SOL_OP_CONV2DBACKX:
+            case SOL_OP_LINEARBACKX: {
+                if (!(frozen && packed_valid_)) {
+                    pack_conv_weight_t(static_cast<const float*>(args[w_idx_]), packed_, dtype_,
+                                       static_cast<int>(cout_), static_cast<int>(cin_), kh_, kw_,
+                                       static_cast<int>(in_.ld), kpad_, s);
+                    packed_valid_ = true;
+                }
+                IgemmArgs g;
+                g.mode = (sh_ == 1 && sw_ == 1 && ph_ == 0 && pw_ == 0 && kh_ == 1 && kw_ == 1) ? IG_FPROP : IG_DGRAD;
+                g.dtype = dtype_;
+                g.out_dtype = dtype_;
+                g.src = args[0];
+                g.wt = packed_;
+                g.out = out;
+                g.N = static_cast<int>(in_.N);
+                g.SH = static_cast<int>(in_.H);
+                g.SW = static_cast<int>(in_.W);
+                g.SC = static_cast<int>(in_.ld);
+                g.OH = static_cast<int>(out_.H);
+                g.OW = static_cast<int>(out_.W);
+                g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
+                g.Nout = static_cast<int>(cin_);
+                g.K_pad = kpad_;
+                g.ldo = static_cast<int>(out_.ld);
+                igemm_launch(g, s);
+                break;
+            }
+            default: {
+                float* packed = static_cast<float*>(scratch);
+                float* ws = ws_floats_ ? packed + round_up(static_cast<int64_t>(packed_floats_), 64) : nullptr;
+                WgradArgs w = wargs(args[0], args[1], packed, ws);
+                wgrad_launch(w, s);
+                unpack_conv_grad(packed, static_cast<float*>(out), static_cast<int>(cout_), static_cast<int>(cin_),
+                                 kh_, kw_, static_cast<int>(x_.ld), s);
+                break;
+            }
+        }
+    }
+
+private:
+    int dtype_;
+    int op_;
+    int kh_, kw_, sh_, sw_, ph_, pw_;
+    Geo in_, out_, x_;
+    int64_t cin_ = 0, cout_ = 0;
+    int kpad_ = 0;
+    int w_idx_ = -1, b_idx_ = -1;
+    void* packed_ = nullptr;
+    bool packed_valid_ = false;
+    size_t ws_floats_ = 0, packed_floats_ = 0;
+};
+
+// ---------------------------------------------------------------------------------------------
+// row kernels: Softmax / CrossEntropyLoss / SoftmaxCeBack / CeBack / SoftmaxBack
+// ---------------------------------------------------------------------------------------------
+
+class RowModule : public Module {
+public:
+    explicit RowModule(const sol_unit_desc& d) : dtype_(d.dtype), op_(d.ops[0].op) {
+        fill_arg_bytes(*this, d);
+        const Geo g = geo_b(d.bindings[d.ops[0].inputs[0]]);
+        if (g.H != 1 || g.W != 1) unsupported("row ops over pixel dims are not supported");
+        rows_ = static_cast<int>(g.N);
+        cols_ = static_cast<int>(g.C);
+        ld_ = static_cast<int>(g.ld);
+        if (op_ == SOL_OP_CROSSENTROPYLOSS || op_ == SOL_OP_SOFTMAXCEBACK || op_ == SOL_OP_CEBACK ||
+            op_ == SOL_OP_SOFTMAXBACK) {
+            const Geo t = geo_b(d.bindings[d.ops[0].inputs[1]]);
+            if (t.ld != g.ld) throw ShapeError("row op operands differ in row stride");
+        }
+        family = op_ == SOL_OP_SOFTMAX ? "softmax_rows" : op_ == SOL_OP_CROSSENTROPYLOSS ? "ce_loss" : "ce_back";
+        algo_bytes = double(rows_) * ld_ * elem_size(dtype_) * (op_ == SOL_OP_SOFTMAX ? 2 : 3);
+    }
+    void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
+        if (nargs != n_args) throw std::invalid_argument("row module: wrong argument count");
+        switch (op_) {
+            case SOL_OP_SOFTMAX: softmax_rows(dtype_, args[0], args[1], rows_, cols_, ld_, s); break;
+            case SOL_OP_CROSSENTROPYLOSS:
+                ce_loss(dtype_, args[0], args[1], static_cast<float*>(args[2]), rows_, cols_, ld_, s);
+                break;
+            case SOL_OP_SOFTMAXCEBACK: ce_back(dtype_, 1, args[0], args[1], args[2], rows_, cols_, ld_, s); break;
+            case SOL_OP_CEBACK: ce_back(dtype_, 0, args[0], args[1], args[2], rows_, cols_, ld_, s); break;
+            case SOL_OP_SOFTMAXBACK: softmax_back(dtype_, args[0], args[1], args[2], rows_, cols_, ld_, s); break;
+            default: unsupported("row op");
+        }
+    }
+
+private:
+    int dtype_, op_;
+    int rows_, cols_, ld_;
+};
+
+// Flatten / FlattenBack in the reference's canonical order (dfp_lower.cpp:1098-1112).
+class FlattenModule : public Module {
+public:
+    explicit FlattenModule(const sol_unit_desc& d) : dtype_(d.dtype), inverse_(d.ops[0].op == SOL_OP_FLATTENBACK) {
+        fill_arg_bytes(*this, d);
+        family = inverse_ ? "flatten_back" : "flatten";
+        img_ = inverse_ ? geo_b(d.output) : geo_b(d.bindings[d.ops[0].inputs[0]]);
+        const Geo flat = inverse_ ? geo_b(d.bindings[d.ops[0].inputs[0]]) : geo_b(d.output);
+        if (img_.ld != img_.C || flat.ld != flat.C) unsupported("flatten over padded channel storage");
+        algo_bytes = 2.0 * img_.numel() * elem_size(dtype_);
+    }
+    void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
+        if (nargs != n_args) throw std::invalid_argument("flatten: wrong argument count");
+        flatten_nhwc(dtype_, args[0], args[1], static_cast<int>(img_.N), static_cast<int>(img_.C),
+                     static_cast<int>(img_.H), static_cast<int>(img_.W), inverse_, s);
+    }
+
+private:
+    int dtype_;
+    int inverse_;
+    Geo img_;
+};
+
+// Reorder steps at the plan boundary (fe::Step::Kind::Reorder): canonical f32 host layout
+// (NCHW / NC, the reference's meta_nchw order, tensor.cpp:141-151) <-> NHWC plan storage.
+class ReorderModule : public Module {
+public:
+    explicit ReorderModule(const sol_unit_desc& d) : dtype_(d.dtype), inbound_(d.ops[0].op == SOL_OP_REORDER_IN) {
+        fill_arg_bytes(*this, d);
+        family = inbound_ ? "reorder_in" : "reorder_out";
+        stored_ = inbound_ ? geo_b(d.output) : geo_b(d.bindings[0]);
+        algo_bytes = stored_.numel() * (4.0 + elem_size(dtype_));
+    }
+    void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
+        if (nargs != n_args) throw std::invalid_argument("reorder: wrong argument count");
+        const Geo& g = stored_;
+        if (g.rank == 0) {
+            cast_copy(args[0], inbound_ ? DT_F32 : dtype_, args[1], inbound_ ? dtype_ : DT_F32, 1, s);
+        } else if (inbound_) {
+            nchw_to_nhwc(static_cast<const float*>(args[0]), args[1], dtype_, static_cast<int>(g.N),
+                         static_cast<int>(g.C), static_cast<int>(g.H), static_cast<int>(g.W), static_cast<int>(g.ld), s);
+        } else {
+            nhwc_to_nchw(args[0], static_cast<float*>(args[1]), dtype_, static_cast<int>(g.N), static_cast<int>(g.C),
+                         static_cast<int>(g.H), static_cast<int>(g.W), static_cast<int>(g.ld), s);
+        }
+    }
+
+private:
+    int dtype_;
+    bool inbound_;
+    Geo stored_;
+};
+
+// SgdUpdate: theta' = theta - lr * g (dfp_lower.cpp:780-783; reference.cpp:580-584). f32 master.
+class SgdModule : public Module {
+public:
+    explicit SgdModule(const sol_unit_desc& d) {
+        fill_arg_bytes(*this, d);
+        family = "sgd_update";
+        lr_ = d.ops[0].attrs.lr;
+        n_ = param_numel(d.bindings[d.ops[0].inputs[0]]);
+        algo_bytes = 12.0 * n_;
+    }
+    void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
+        if (nargs != n_args) throw std::invalid_argument("sgd: wrong argument count");
+        float* w = static_cast<float*>(args[0]);
+        float* o = static_cast<float*>(args[2]);
+        if (o != w) SOL_CUDA(cudaMemcpyAsync(o, w, n_ * 4, cudaMemcpyDeviceToDevice, s));
+        sgd_update(o, static_cast<const float*>(args[1]), n_, lr_, nullptr, s);
+    }
+
+private:
+    float lr_;
+    int64_t n_;
+};
+
+// ---------------------------------------------------------------------------------------------
+// per-channel reductions: BatchNormBack{X,Gamma,Beta} (training), Conv2dBackB, LinearBackB
+// ---------------------------------------------------------------------------------------------
+
+Program prog_load(int slot) {
+    Program p;
+    p.n = 1;
+    p.ins[0].op = PW_LD;
+    p.ins[0].dst = 0;
+    p.ins[0].a = static_cast<uint8_t>(slot);
+    return p;
+}
+
+void push(Program& p, PwOp op, int dst, int a = 0, int b = 0, int arg = 0, float imm = 0.f) {
+    if (p.n >= DFP_MAX_INS) unsupported("fused unit too long for one program");
+    PwInstr& i = p.ins[p.n++];
+    i.op = op;
+    i.dst = static_cast<uint8_t>(dst);
+    i.a = static_cast<uint8_t>(a);
+    i.b = static_cast<uint8_t>(b);
+    i.arg = static_cast<int16_t>(arg);
+    i.imm = imm;
+}
+
+class ReduceModule : public Module {
+public:
+    explicit ReduceModule(const sol_unit_desc& d) : dtype_(d.dtype) {
+        fill_arg_bytes(*this, d);
+        const sol_unit_op& o = d.ops[0];
+        op_ = o.op;
+        training_ = o.attrs.training != 0;
+        eps_ = o.attrs.eps;
+        delta_ = geo_b(d.bindings[o.inputs[0]]);
+        C_ = static_cast<int>(delta_.C);
+        if (delta_.ld != delta_.C) unsupported("reduction over padded channel storage");
+        blocks_ = dfp_reduce_blocks(delta_.pixels(), C_);
+        const bool needs_x = op_ == SOL_OP_BATCHNORMBACKX || op_ == SOL_OP_BATCHNORMBACKGAMMA;
+        if (needs_x && !training_) unsupported("BatchNorm backward in inference mode");
+        if (needs_x) {
+            x_idx_ = o.inputs[1];
+            ones_ = static_cast<float*>(dev_alloc(C_ * 4));
+            std::vector<float> ones(C_, 1.f);
+            SOL_CUDA(cudaMemcpy(ones_, ones.data(), C_ * 4, cudaMemcpyHostToDevice));
+            zeros_ = static_cast<float*>(dev_alloc(C_ * 4));
+            shift_ = static_cast<float*>(dev_alloc(C_ * 4));
+            stats_ = static_cast<float*>(dev_alloc(2 * C_ * 4));
+            xhat_ = static_cast<float*>(dev_alloc(2 * C_ * 4));
+            coef_ = static_cast<float*>(dev_alloc(3 * C_ * 4));
+            gamma_idx_ = o.n_params > 0 ? o.params[0] : -1;
+        }
+        switch (op_) {
+            case SOL_OP_BATCHNORMBACKX: family = "bn_back_x"; launches = 7; break;
+            case SOL_OP_BATCHNORMBACKGAMMA: family = "bn_back_gamma"; launches = 6; break;
+            case SOL_OP_BATCHNORMBACKBETA: family = "bn_back_beta"; launches = 2; break;
+            default: family = "bias_grad"; launches = 2; break;
+        }
+        const double es = double(elem_size(dtype_));
+        algo_bytes = delta_.numel() * es * (needs_x ? 2 : 1) + (op_ == SOL_OP_BATCHNORMBACKX ? delta_.numel() * es : 0);
+    }
+    size_t scratch_bytes() const override { return static_cast<size_t>(blocks_) * C_ * 2 * 4 + 256; }
+
+    DfpArgs base(void* const* args, float* partial) const {
+        DfpArgs a;
+        a.family = FAM_CHAN_REDUCE;
+        a.dtype = dtype_;
+        a.N = static_cast<int>(delta_.N);
+        a.H = static_cast<int>(delta_.H);
+        a.W = static_cast<int>(delta_.W);
+        a.C = C_;
+        a.n_in = 2;
+        a.in[0] = args[0];
+        a.in_kind[0] = IN_PIX;
+        a.in_ld[0] = C_;
+        if (x_idx_ >= 0) {
+            a.in[1] = args[x_idx_];
+            a.in_kind[1] = IN_PIX;
+            a.in_ld[1] = C_;
+        }
+        a.partial = partial;
+        a.reduce_blocks = blocks_;
+        return a;
+    }
+
+    // x statistics -> xhat coefficients (rstd, -mean*rstd) and (mean, rstd)
+    void x_stats(void* const* args, float* partial, cudaStream_t s) {
+        bn_shift(dtype_, args[x_idx_], C_, C_, shift_, s);
+        DfpArgs a = base(args, partial);
+        a.P[0] = shift_;
+        push(a.pre, PW_LD, 0, 1);                  // r0 = x
+        push(a.pre, PW_PARAM, 1, 0, 0, 0);         // r1 = shift
+        push(a.pre, PW_SCALE, 1, 0, 0, 0, -1.f);   // r1 = -shift
+        push(a.pre, PW_ADD, 0, 0, 1);              // r0 = x - shift
+        push(a.pre, PW_MOV, 1, 0);                 // r1 = r0
+        dfp_launch(a, s);
+        FinalizeArgs f;
+        f.mode = FIN_BN_STATS;
+        f.C = C_;
+        f.blocks = blocks_;
+        f.partial = partial;
+        f.count = static_cast<double>(delta_.pixels());
+        f.eps = eps_;
+        f.shift = shift_;
+        f.gamma = ones_;
+        f.beta = zeros_;
+        f.stats_out = stats_;
+        f.coef = xhat_;  // (rstd, -mean*rstd)
+        dfp_finalize(f, s);
+    }
+
+    void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool) override {
+        if (nargs != n_args) throw std::invalid_argument("reduce module: wrong argument count");
+        float* partial = static_cast<float*>(scratch);
+        float* out = static_cast<float*>(args[nargs - 1]);
+        if (op_ == SOL_OP_BATCHNORMBACKBETA || op_ == SOL_OP_CONV2DBACKB || op_ == SOL_OP_LINEARBACKB) {
+            DfpArgs a = base(args, partial);
+            a.pre = prog_load(0);
+            push(a.pre, PW_MOV, 1, 0);
+            dfp_launch(a, s);
+            FinalizeArgs f;
+            f.mode = FIN_SUMS;
+            f.C = C_;
+            f.blocks = blocks_;
+            f.partial = partial;
+            f.out0 = out;
+            dfp_finalize(f, s);
+            return;
+        }
+        x_stats(args, partial, s);
+        // S1 = sum delta, S2 = sum delta * xhat
+        DfpArgs a = base(args, partial);
+        a.P[0] = xhat_;
+        a.P[1] = xhat_ + C_;
+        a.pre = Program();
+        push(a.pre, PW_LD, 0, 0);      // r0 = delta
+        push(a.pre, PW_LD, 1, 1);      // r1 = x
+        push(a.pre, PW_AFF, 1, 0, 0, 0);  // r1 = xhat
+        dfp_launch(a, s);
+        FinalizeArgs f;
+        f.mode = FIN_BN_BACK;
+        f.C = C_;
+        f.blocks = blocks_;
+        f.partial = partial;
+        f.count = static_cast<double>(delta_.pixels());
+        f.stats = stats_;
+        if (op_ == SOL_OP_BATCHNORMBACKGAMMA) {
+            f.out1 = out;
+            dfp_finalize(f, s);
+            return;
+        }
+        f.gamma = static_cast<const float*>(args[gamma_idx_]);
+        f.coef = coef_;
+        dfp_finalize(f, s);
+        // dx = delta*A + x*B + Cc
+        DfpArgs p;
+        p.family = FAM_POINTWISE;
+        p.dtype = dtype_;
+        p.N = static_cast<int>(delta_.N);
+        p.H = p.OH = static_cast<int>(delta_.H);
+        p.W = p.OW = static_cast<int>(delta_.W);
+        p.C = C_;
+        p.n_in = 2;
+        p.in[0] = args[0];
+        p.in_ld[0] = C_;
+        p.in[1] = args[x_idx_];
+        p.in_ld[1] = C_;
+        p.P[0] = coef_;
+        p.P[1] = coef_ + C_;
+        p.P[2] = coef_ + 2 * C_;
+        push(p.post, PW_LD, 0, 0);
+        push(p.post, PW_LD, 1, 1);
+        push(p.post, PW_AXPBY, 0, 0, 1, 0);
+        p.out = out;
+        p.out_ld = C_;
+        dfp_launch(p, s);
+    }
+
+private:
+    int dtype_;
+    int op_;
+    bool training_ = false;
+    float eps_ = 1e-5f;
+    Geo delta_;
+    int C_ = 0;
+    int blocks_ = 1;
+    int x_idx_ = -1, gamma_idx_ = -1;
+    float *ones_ = nullptr, *zeros_ = nullptr, *shift_ = nullptr, *stats_ = nullptr, *xhat_ = nullptr,
+          *coef_ = nullptr;
+};
+
+// ---------------------------------------------------------------------------------------------
+// DFP fused groups: pointwise / pool / gap / depthwise / pool-backward families
+// ---------------------------------------------------------------------------------------------
+
+class DfpModule : public Module {
+public:
+    explicit DfpModule(const sol_unit_desc& d);
+    void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) override;
+    size_t scratch_bytes() const override { return stats_scratch_; }
+
+private:
+    struct SlotSrc {
+        int binding;
+    };
+    struct BnPrep {
+        bool training;
+        int x_binding;      // training: the BN input (boundary binding)
+        int g, b, m, v;     // param bindings
+        float eps;
+        int C;
+        float* coef;        // [2C] -> P[pidx], P[pidx+1]
+        float* shift;
+        float* stats;
+        int64_t pixels;
+        int x_ld;
+        int xN, xH, xW;
+    };
+    struct DwPrep {
+        int w, bias;
+        int C, kh, kw;
+        float* packed;
+    };
+
+    // program building
+    int key_op(int k) const { return k; }
+    int key_b(int b) const { return 1000 + b; }
+    int reg_get(int ref);
+    int reg_take(int ref);
+    void consume(int ref);
+    int alloc_reg();
+    int emit_value(int key);
+    int slot_for(int binding, int kind, int coff);
+    void count_uses(int key, const std::set<int>& members, bool root);
+
+    const sol_unit_desc& d_;  // valid during construction only
+    DfpArgs tmpl_;
+    std::vector<int> slot_binding_;
+    std::vector<int> cat_bindings_;
+    std::vector<BnPrep> bn_;
+    std::vector<DwPrep> dw_;
+    std::map<int, int> bn_of_op_;  // op index -> bn_ index
+    int dtype_;
+    int anchor_ = -1;
+    size_t stats_scratch_ = 0;
+    bool coef_ready_ = false;
+    float* ones_ = nullptr;
+    float* zeros_ = nullptr;
+
+    // builder state
+    Program* prog_ = nullptr;
+    std::map<int, int> uses_, reg_of_;
+    unsigned free_regs_ = 0xF;
+    std::set<int> prog_members_;
+};
+
+int DfpModule::alloc_reg() {
+    for (int r = 0; r < 4; ++r)
+        if (free_regs_ & (1u << r)) {
+            free_regs_ &= ~(1u << r);
+            return r;
+        }
+    unsupported("fused unit needs more than 4 live values");
+}
+
+void DfpModule::consume(int key) {
+    auto it = uses_.find(key);
+    if (it == uses_.end()) return;
+    if (--it->second == 0) {
+        auto r = reg_of_.find(key);
+        if (r != reg_of_.end()) {
+            free_regs_ |= 1u << r->second;
+            reg_of_.erase(r);
+        }
+    }
+}
+
+int DfpModule::reg_get(int key) {
+    auto it = reg_of_.find(key);
+    if (it != reg_of_.end()) return it->second;
+    const int r = emit_value(key);
+    reg_of_[key] = r;
+    return r;
+}
+
+int DfpModule::reg_take(int key) {
+    const int r = reg_get(key);
+    if (uses_[key] > 1) {
+        const int r2 = alloc_reg();
+        push(*prog_, PW_MOV, r2, r);
+        consume(key);
+        return r2;
+    }
+    // last use: steal the register
+    uses_[key] = 0;
+    reg_of_.erase(key);
+    return r;
+}
+
+int DfpModule::slot_for(int binding, int kind, int coff) {
+    for (size_t i = 0; i < slot_binding_.size(); ++i)
+        if (slot_binding_[i] == binding && tmpl_.in_kind[i] == kind && tmpl_.in_coff[i] == coff)
+            return static_cast<int>(i);
+    const int s = static_cast<int>(slot_binding_.size());
+    if (s >= DFP_MAX_IN) unsupported("too many unit inputs");
+    slot_binding_.push_back(binding);
+    tmpl_.in_kind[s] = kind;
+    tmpl_.in_coff[s] = coff;
+    tmpl_.in_ld[s] = static_cast<int>(geo_b(d_.bindings[binding]).ld);
+    tmpl_.n_in = s + 1;
+    return s;
+}
+
+void DfpModule::count_uses(int key, const std::set<int>& members, bool root) {
+    uses_[key] += 1;
+    if (key >= 1000 || key == 2000) return;
+    if (!members.count(key)) unsupported("fused value used on two pixel grids");
+    if (uses_[key] > 1 && !root) return;  // already expanded
+    const sol_unit_op& o = d_.ops[key];
+    const int ni = (o.op == SOL_OP_CONCAT) ? 0 : o.n_inputs;
+    for (int i = 0; i < ni; ++i) {
+        if (key == anchor_) break;
+        const int r = o.inputs[i];
+        count_uses(r >= 0 ? key_b(r) : key_op(-r - 1), members, false);
+    }
+}
+
+// Emits code for value `key` into a fresh register; returns the register.
+int DfpModule::emit_value(int key) {
+    Program& p = *prog_;
+    if (key == 2000) unsupported("anchor value requested outside the post program");
+    if (key >= 1000) {
+        const int b = key - 1000;
+        const int r = alloc_reg();
+        const int slot = slot_for(b, IN_PIX, 0);
+        push(p, PW_LD, r, slot);
+        return r;
+    }
+    if (key == anchor_) {
+        // anchor result is preloaded in r0 by the family kernel
+        free_regs_ &= ~1u;
+        return 0;
+    }
+    const sol_unit_op& o = d_.ops[key];
+    auto in_key = [&](int i) {
+        const int r = o.inputs[i];
+        return r >= 0 ? key_b(r) : key_op(-r - 1);
+    };
+    switch (o.op) {
+        case SOL_OP_RELU:
+        case SOL_OP_RELU6:
+        case SOL_OP_COPY: {
+            const int r = reg_take(in_key(0));
+            if (o.op != SOL_OP_COPY) push(p, o.op == SOL_OP_RELU ? PW_RELU : PW_RELU6, r);
+            return r;
+        }
+        case SOL_OP_BATCHNORM2D: {
+            const int r = reg_take(in_key(0));
+            const int bi = bn_of_op_.at(key);
+            push(p, PW_AFF, r, 0, 0, 2 * bi);
+            return r;
+        }
+        case SOL_OP_ADD: {
+            const int ra = reg_take(in_key(0));
+            const int rb = reg_get(in_key(1));
+            push(p, PW_ADD, ra, ra, rb);
+            consume(in_key(1));
+            return ra;
+        }
+        case SOL_OP_RELUBACK:
+        case SOL_OP_RELU6BACK: {
+            const int ra = reg_take(in_key(0));
+            const int rb = reg_get(in_key(1));
+            push(p, o.op == SOL_OP_RELUBACK ? PW_MASK : PW_MASK6, ra, ra, rb);
+            consume(in_key(1));
+            return ra;
+        }
+        case SOL_OP_CONCAT: {
+            if (!cat_bindings_.empty()) unsupported("more than one Concat in a unit");
+            int off = 0;
+            tmpl_.cat_off[0] = 0;
+            for (int i = 0; i < o.n_inputs; ++i) {
+                if (o.inputs[i] < 0) unsupported("Concat of a fused intermediate");
+                if (o.n_inputs > DFP_MAX_CAT) unsupported("Concat arity");
+                const Geo g = geo_b(d_.bindings[o.inputs[i]]);
+                if (g.ld != g.C) unsupported("Concat over padded storage");
+                cat_bindings_.push_back(o.inputs[i]);
+                off += static_cast<int>(g.C);
+                tmpl_.cat_off[i + 1] = off;
+            }
+            tmpl_.n_cat = o.n_inputs;
+            const int s = static_cast<int>(slot_binding_.size());
+            slot_binding_.push_back(-1);
+            tmpl_.in_kind[s] = IN_CAT;
+            tmpl_.n_in = s + 1;
+            const int r = alloc_reg();
+            push(p, PW_LD, r, s);
+            return r;
+        }
+        case SOL_OP_CONCATBACK: {
+            if (o.inputs[0] < 0) unsupported("ConcatBack of a fused intermediate");
+            const int r = alloc_reg();
+            push(p, PW_LD, r, slot_for(o.inputs[0], IN_PIX, static_cast<int>(o.attrs.offset)));
+            return r;
+        }
+        case SOL_OP_GLOBALAVGPOOLBACK: {
+            if (o.inputs[0] < 0) unsupported("GlobalAvgPoolBack of a fused intermediate");
+            const int r = alloc_reg();
+            push(p, PW_LD, r, slot_for(o.inputs[0], IN_NC, 0));
+            const double hw = static_cast<double>(o.saved_dims[2] * o.saved_dims[3]);
+            push(p, PW_SCALE, r, 0, 0, 0, static_cast<float>(1.0 / hw));
+            return r;
+        }
+        default:
+            unsupported(std::string("op ") + std::to_string(o.op) + " cannot be fused into a DFP kernel");
+    }
+}
+
+DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
+    fill_arg_bytes(*this, d);
+    tmpl_.dtype = dtype_;
+    const int n = d.n_ops;
+    // anchor
+    for (int k = 0; k < n; ++k) {
+        const sol_unit_op& o = d.ops[k];
+        bool anchor = o.op == SOL_OP_MAXPOOL2D || o.op == SOL_OP_AVGPOOL2D || o.op == SOL_OP_GLOBALAVGPOOL ||
+                      o.op == SOL_OP_MAXPOOL2DBACK || o.op == SOL_OP_AVGPOOL2DBACK || o.op == SOL_OP_CONV2D;
+        if (anchor) {
+            if (anchor_ >= 0) unsupported("unit has two window/global reductions");
+            anchor_ = k;
+        }
+    }
+    // geometry helpers
+    auto geo_ref = [&](int r) -> Geo {
+        if (r >= 0) return geo_b(d.bindings[r]);
+        const sol_unit_op& o = d.ops[-r - 1];
+        return geo_of_dims(o.out_rank, o.out_dims, 0);
+    };
+    const Geo out = geo_b(d.output);
+    // BN preps (one param pair per BatchNorm2d op)
+    for (int k = 0; k < n; ++k) {
+        const sol_unit_op& o = d.ops[k];
+        if (o.op != SOL_OP_BATCHNORM2D) continue;
+        BnPrep b{};
+        b.training = o.attrs.training != 0;
+        b.g = o.params[0];
+        b.b = o.params[1];
+        b.m = o.n_params > 2 ? o.params[2] : -1;
+        b.v = o.n_params > 3 ? o.params[3] : -1;
+        b.eps = o.attrs.eps;
+        const Geo xg = geo_ref(o.inputs[0]);
+        b.C = static_cast<int>(xg.C);
+        b.coef = static_cast<float*>(dev_alloc(2 * b.C * 4));
+        if (b.training) {
+            if (o.inputs[0] < 0) unsupported("training BatchNorm2d over a fused intermediate");
+            b.x_binding = o.inputs[0];
+            b.shift = static_cast<float*>(dev_alloc(b.C * 4));
+            b.stats = static_cast<float*>(dev_alloc(2 * b.C * 4));
+            b.pixels = xg.pixels();
+            b.x_ld = static_cast<int>(xg.ld);
+            b.xN = static_cast<int>(xg.N);
+            b.xH = static_cast<int>(xg.H);
+            b.xW = static_cast<int>(xg.W);
+            if (xg.ld != xg.C) unsupported("training BatchNorm2d over padded storage");
+            stats_scratch_ = std::max(stats_scratch_,
+                                      static_cast<size_t>(dfp_reduce_blocks(b.pixels, b.C)) * b.C * 2 * 4 + 256);
+        }
+        bn_of_op_[k] = static_cast<int>(bn_.size());
+        if (2 * static_cast<int>(bn_.size()) + 1 >= DFP_MAX_P) unsupported("too many BatchNorms in one unit");
+        bn_.push_back(b);
+    }
+    if (std::any_of(bn_.begin(), bn_.end(), [](const BnPrep& b) { return b.training; })) {
+        int cmax = 0;
+        for (auto& b : bn_) cmax = std::max(cmax, b.C);
+        ones_ = static_cast<float*>(dev_alloc(cmax * 4));
+        std::vector<float> ones(cmax, 1.f);
+        SOL_CUDA(cudaMemcpy(ones_, ones.data(), cmax * 4, cudaMemcpyHostToDevice));
+        zeros_ = static_cast<float*>(dev_alloc(cmax * 4));
+    }
+
+    // member sets: pre = ancestors of the anchor's primary input; post = everything else
+    std::set<int> pre, post;
+    if (anchor_ >= 0) {
+        std::vector<int> stack;
+        const int r0 = d.ops[anchor_].inputs[0];
+        if (r0 < 0) stack.push_back(-r0 - 1);
+        while (!stack.empty()) {
+            int k = stack.back();
+            stack.pop_back();
+            if (!pre.insert(k).second) continue;
+            const sol_unit_op& o = d.ops[k];
+            for (int i = 0; i < o.n_inputs; ++i)
+                if (o.inputs[i] < 0) stack.push_back(-o.inputs[i] - 1);
+        }
+    }
+    for (int k = 0; k < n; ++k)
+        if (!pre.count(k) && k != anchor_) post.insert(k);
+
+    const int root = n - 1;  // unit output = last member
+    // anchor-specific family + geometry
+    if (anchor_ < 0) {
+        tmpl_.family = FAM_POINTWISE;
+        tmpl_.N = static_cast<int>(out.N);
+        tmpl_.H = tmpl_.OH = static_cast<int>(out.H);
+        tmpl_.W = tmpl_.OW = static_cast<int>(out.W);
+        tmpl_.C = static_cast<int>(out.C);
+        family = "dfp_pointwise";
+    } else {
+        const sol_unit_op& a = d.ops[anchor_];
+        const Geo src = geo_ref(a.inputs[0]);
+        const Geo aout = geo_of_dims(a.out_rank, a.out_dims, 0);
+        tmpl_.N = static_cast<int>(src.N);
+        tmpl_.C = static_cast<int>(src.C);
+        tmpl_.kh = static_cast<int>(a.attrs.kh);
+        tmpl_.kw = static_cast<int>(a.attrs.kw);
+        tmpl_.sh = static_cast<int>(a.attrs.sh);
+        tmpl_.sw = static_cast<int>(a.attrs.sw);
+        tmpl_.ph = static_cast<int>(a.attrs.ph);
+        tmpl_.pw = static_cast<int>(a.attrs.pw);
+        tmpl_.min_init = a.attrs.min_init;
+        tmpl_.count_padding = a.attrs.count_padding;
+        switch (a.op) {
+            case SOL_OP_MAXPOOL2D:
+            case SOL_OP_AVGPOOL2D:
+                tmpl_.family = FAM_POOL;
+                tmpl_.pool_max = a.op == SOL_OP_MAXPOOL2D;
+                tmpl_.H = static_cast<int>(src.H);
+                tmpl_.W = static_cast<int>(src.W);
+                tmpl_.OH = static_cast<int>(aout.H);
+                tmpl_.OW = static_cast<int>(aout.W);
+                family = a.op == SOL_OP_MAXPOOL2D ? "dfp_maxpool" : "dfp_avgpool";
+                break;
+            case SOL_OP_GLOBALAVGPOOL:
+                tmpl_.family = FAM_GAP;
+                tmpl_.H = static_cast<int>(src.H);
+                tmpl_.W = static_cast<int>(src.W);
+                family = "dfp_gap";
+                break;
+            case SOL_OP_CONV2D: {
+                if (!is_depthwise(a, src.C)) unsupported("non-depthwise Conv2d inside a DFP group");
+                tmpl_.family = FAM_DWCONV;
+                tmpl_.H = static_cast<int>(src.H);
+                tmpl_.W = static_cast<int>(src.W);
+                tmpl_.OH = static_cast<int>(aout.H);
+                tmpl_.OW = static_cast<int>(aout.W);
+                DwPrep w{};
+                w.w = a.params[0];
+                w.bias = (a.attrs.has_bias && a.n_params > 1) ? a.params[1] : -1;
+                w.C = static_cast<int>(src.C);
+                w.kh = tmpl_.kh;
+                w.kw = tmpl_.kw;
+                w.packed = static_cast<float*>(dev_alloc(static_cast<size_t>(w.C) * w.kh * w.kw * 4));
+                dw_.push_back(w);
+                family = "dfp_dwconv";
+                algo_flops = 2.0 * aout.pixels() * w.C * w.kh * w.kw;
+                break;
+            }
+            case SOL_OP_MAXPOOL2DBACK:
+            case SOL_OP_AVGPOOL2DBACK: {
+                // grid = dx (anchor output), windows = delta (anchor input 0)
+                tmpl_.family = a.op == SOL_OP_MAXPOOL2DBACK ? FAM_MAXPOOL_BACK : FAM_AVGPOOL_BACK;
+                tmpl_.H = static_cast<int>(aout.H);
+                tmpl_.W = static_cast<int>(aout.W);
+                tmpl_.OH = static_cast<int>(src.H);
+                tmpl_.OW = static_cast<int>(src.W);
+                if (a.op == SOL_OP_MAXPOOL2DBACK) {
+                    if (a.inputs[1] < 0) unsupported("MaxPool2dBack over a fused forward input");
+                    tmpl_.pool_x = slot_for(a.inputs[1], IN_PIX, 0);
+                }
+                family = a.op == SOL_OP_MAXPOOL2DBACK ? "dfp_maxpool_back" : "dfp_avgpool_back";
+                break;
+            }
+        }
+    }
+
+    // pre program (anchor input at source pixels)
+    if (anchor_ >= 0) {
+        prog_ = &tmpl_.pre;
+        uses_.clear();
+        reg_of_.clear();
+        free_regs_ = 0xF;
+        const int r0 = d.ops[anchor_].inputs[0];
+        const int key0 = r0 >= 0 ? key_b(r0) : key_op(-r0 - 1);
+        count_uses(key0, pre, true);
+        const int r = reg_get(key0);
+        if (r != 0) push(tmpl_.pre, PW_MOV, 0, r);
+    }
+    // post program (output pixels; r0 holds the anchor result)
+    {
+        prog_ = &tmpl_.post;
+        uses_.clear();
+        reg_of_.clear();
+        free_regs_ = 0xF;
+        std::set<int> members = post;
+        if (anchor_ >= 0) {
+            members.insert(anchor_);
+            free_regs_ &= ~1u;
+            reg_of_[key_op(anchor_)] = 0;
+        }
+        count_uses(key_op(root), members, true);
+        const int r = reg_get(key_op(root));
+        if (r != 0) push(tmpl_.post, PW_MOV, 0, r);
+    }
+    tmpl_.out_ld = static_cast<int>(out.ld);
+    if (tmpl_.family == FAM_POINTWISE || tmpl_.family == FAM_GAP) {
+        if (out.C != tmpl_.C && tmpl_.family == FAM_POINTWISE) tmpl_.C = static_cast<int>(out.C);
+    }
+    // parameter arrays: BN coefficient pairs at P[2i], P[2i+1]
+    for (size_t i = 0; i < bn_.size(); ++i) {
+        tmpl_.P[2 * i] = bn_[i].coef;
+        tmpl_.P[2 * i + 1] = bn_[i].coef + bn_[i].C;
+    }
+    // algorithmic bytes: external activation inputs + output
+    double bytes = binding_bytes(d.output);
+    for (int i = 0; i < d.n_bindings; ++i)
+        if (!d.bindings[i].is_param) bytes += binding_bytes(d.bindings[i]);
+    algo_bytes = bytes;
+    launches = 1;
+    for (auto& b : bn_) launches += b.training ? 3 : 1;
+    launches += static_cast<int>(dw_.size());
+}
+
+void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) {
+    if (nargs != n_args) throw std::invalid_argument("dfp module: wrong argument count");
+    // BN coefficients (inference: from running stats; training: from batch statistics)
+    for (auto& b : bn_) {
+        if (!b.training) {
+            if (!(frozen && coef_ready_))
+                bn_infer_coef(static_cast<const float*>(args[b.g]), static_cast<const float*>(args[b.b]),
+                              static_cast<const float*>(args[b.m]), static_cast<const float*>(args[b.v]), b.eps,
+                              b.coef, b.C, s);
+            continue;
+        }
+        float* partial = static_cast<float*>(scratch);
+        bn_shift(dtype_, args[b.x_binding], b.x_ld, b.C, b.shift, s);
+        DfpArgs a;
+        a.family = FAM_CHAN_REDUCE;
+        a.dtype = dtype_;
+        a.N = b.xN;
+        a.H = b.xH;
+        a.W = b.xW;
+        a.C = b.C;
+        a.n_in = 1;
+        a.in[0] = args[b.x_binding];
+        a.in_ld[0] = b.x_ld;
+        a.P[0] = b.shift;
+        push(a.pre, PW_LD, 0, 0);                 // r0 = x
+        push(a.pre, PW_PARAM, 1, 0, 0, 0);        // r1 = shift
+        push(a.pre, PW_SCALE, 1, 0, 0, 0, -1.f);  // r1 = -shift
+        push(a.pre, PW_ADD, 0, 0, 1);             // r0 = x - shift
+        push(a.pre, PW_MOV, 1, 0);                // r1 = r0
+        a.partial = partial;
+        a.reduce_blocks = dfp_reduce_blocks(b.pixels, b.C);
+        dfp_launch(a, s);
+        FinalizeArgs f;
+        f.mode = FIN_BN_STATS;
+        f.C = b.C;
+        f.blocks = a.reduce_blocks;
+        f.partial = partial;
+        f.count = static_cast<double>(b.pixels);
+        f.eps = b.eps;
+        f.shift = b.shift;
+        f.gamma = static_cast<const float*>(args[b.g]);
+        f.beta = static_cast<const float*>(args[b.b]);
+        f.stats_out = b.stats;
+        f.coef = b.coef;
+        dfp_finalize(f, s);
+    }
+    for (auto& w : dw_) {
+        if (!(frozen && coef_ready_))
+            pack_dw_weight(static_cast<const float*>(args[w.w]), w.packed, w.C, w.kh, w.kw, s);
+    }
+    coef_ready_ = true;
+    DfpArgs a = tmpl_;
+    for (size_t i = 0; i < slot_binding_.size(); ++i)
+        if (slot_binding_[i] >= 0) a.in[i] = args[slot_binding_[i]];
+    for (size_t i = 0; i < cat_bindings_.size(); ++i) a.cat_ptr[i] = args[cat_bindings_[i]];
+    if (!dw_.empty()) {
+        a.dw_w = dw_[0].packed;
+        a.dw_b = dw_[0].bias >= 0 ? static_cast<const float*>(args[dw_[0].bias]) : nullptr;
+    }
+    a.out = args[nargs - 1];
+    dfp_launch(a, s);
+}
+
+}  // namespace
+
+std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
+    if (d.n_ops <= 0 || d.ops == nullptr) throw std::invalid_argument("empty unit");
+    if (d.dtype != DT_F32 && d.dtype != DT_BF16) throw std::invalid_argument("unit dtype");
+    for (int k = 0; k < d.n_ops; ++k) {
+        const sol_unit_op& o = d.ops[k];
+        if (o.n_inputs > SOL_MAX_OP_IN) throw std::invalid_argument("op arity");
+        for (int i = 0; i < o.n_inputs; ++i) {
+            const int r = o.inputs[i];
+            if (r >= d.n_bindings || (r < 0 && -r - 1 >= k)) throw std::invalid_argument("bad operand ref");
+        }
+    }
+    const sol_unit_op& o0 = d.ops[0];
+    if (d.n_ops == 1) {
+        const int op = o0.op;
+        if (is_heavy_op(op)) {
+            if (op == SOL_OP_CONV2D) {
+                const Geo g = geo_b(d.bindings[o0.inputs[0]]);
+                if (!is_depthwise(o0, g.C)) return std::make_unique<HeavyModule>(d);
+            } else {
+                return std::make_unique<HeavyModule>(d);
+            }
+        }
+        switch (op) {
+            case SOL_OP_SOFTMAX:
+            case SOL_OP_CROSSENTROPYLOSS:
+            case SOL_OP_SOFTMAXCEBACK:
+            case SOL_OP_CEBACK:
+            case SOL_OP_SOFTMAXBACK:
+                return std::make_unique<RowModule>(d);
+            case SOL_OP_FLATTEN:
+            case SOL_OP_FLATTENBACK:
+                return std::make_unique<FlattenModule>(d);
+            case SOL_OP_SGDUPDATE:
+                return std::make_unique<SgdModule>(d);
+            case SOL_OP_REORDER_IN:
+            case SOL_OP_REORDER_OUT:
+                return std::make_unique<ReorderModule>(d);
+            case SOL_OP_BATCHNORMBACKX:
+            case SOL_OP_BATCHNORMBACKGAMMA:
+            case SOL_OP_BATCHNORMBACKBETA:
+            case SOL_OP_CONV2DBACKB:
+            case SOL_OP_LINEARBACKB:
+                return std::make_unique<ReduceModule>(d);
+            default:
+                break;
+        }
+    }
+    for (int k = 0; k < d.n_ops; ++k) {
+        const int op = d.ops[k].op;
+        const bool single_only = (is_heavy_op(op) && !(op == SOL_OP_CONV2D)) || op == SOL_OP_SOFTMAX ||
+                                 op == SOL_OP_CROSSENTROPYLOSS || op == SOL_OP_SOFTMAXCEBACK || op == SOL_OP_CEBACK ||
+                                 op == SOL_OP_SOFTMAXBACK || op == SOL_OP_FLATTEN || op == SOL_OP_FLATTENBACK ||
+                                 op == SOL_OP_SGDUPDATE || op == SOL_OP_BATCHNORMBACKX ||
+                                 op == SOL_OP_BATCHNORMBACKGAMMA || op == SOL_OP_BATCHNORMBACKBETA ||
+                                 op == SOL_OP_CONV2DBACKB || op == SOL_OP_LINEARBACKB;
+        if (single_only) unsupported("op " + std::to_string(op) + " must form its own unit on B200");
+    }
+    return std::make_unique<DfpModule>(d);
+}
+
+}  // namespace solb200

@@ -1,0 +1,43 @@
+// Execution-unit modules: a compiled ExecUnit (dfp::ExecUnit, include/sol/dfp.hpp:21-28) bound
+// to one hand-written sm_100a kernel family (DFP groups) or tcgen05 provider (heavy nodes).
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/solb200.h"
+#include "common.cuh"
+
+namespace solb200 {
+
+struct UnsupportedError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ShapeError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+class Module {
+public:
+    virtual ~Module();
+    // args: bindings in order, then the output (device pointers)
+    virtual void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) = 0;
+    virtual size_t scratch_bytes() const { return 0; }
+
+    std::string family;
+    int n_args = 0;
+    int launches = 1;
+    double algo_bytes = 0.0;
+    double algo_flops = 0.0;
+    std::vector<size_t> arg_bytes;  // minimum bytes each arg must span (queue bounds checks)
+
+protected:
+    // module-owned device constants / caches (freed with the module)
+    void* dev_alloc(size_t bytes);
+    std::vector<void*> owned_;
+};
+
+std::unique_ptr<Module> compile_unit(const sol_unit_desc& d);
+
+}  // namespace solb200

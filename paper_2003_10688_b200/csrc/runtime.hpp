@@ -1,0 +1,155 @@
+// Device runtime: stream-ordered arena, the CommandQueue mirror (rt::CommandQueue,
+// include/sol/runtime.hpp:95-145) and execution plans (fe::DevicePlan, frontend.hpp:52-61).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "module.hpp"
+
+namespace solb200 {
+
+// First-fit sub-allocator over one device slab. Allocation and free are host-side bookkeeping
+// only: every consumer is ordered on the owning stream, so a freed block may be handed out again
+// immediately (the cudaMallocAsync contract) and nothing ever blocks the launch stream.
+class Arena {
+public:
+    Arena() = default;
+    ~Arena();
+    void init(size_t bytes);
+    // returns offset or -1 when full
+    int64_t alloc(size_t bytes);
+    void free(int64_t off);
+    uint8_t* base() const { return base_; }
+    size_t capacity() const { return cap_; }
+    size_t in_use() const { return used_; }
+
+private:
+    uint8_t* base_ = nullptr;
+    size_t cap_ = 0, used_ = 0;
+    std::map<int64_t, size_t> free_;   // offset -> size
+    std::map<int64_t, size_t> live_;   // offset -> size
+};
+
+struct QueueErr {
+    int code;
+    std::string msg;
+};
+
+class Queue {
+public:
+    Queue(int device, size_t arena_bytes, bool coalesce);
+    ~Queue();
+
+    uint64_t malloc_async(uint64_t bytes);
+    void free_async(uint64_t vptr);
+    void memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes);
+    void memcpy_d2h(void* dst, uint64_t src, uint64_t bytes);
+    void launch(Module* m, const uint64_t* args, int nargs);
+    void barrier();
+    int synchronize(std::string* msg);
+    sol_transfer_stats stats() const { return stats_; }
+    cudaStream_t stream() const { return stream_; }
+
+private:
+    struct Alloc {
+        int64_t off;
+        uint64_t bytes;
+    };
+    // resolves to a device pointer; on failure records the deferred error and returns nullptr
+    uint8_t* resolve(uint64_t vptr, uint64_t bytes);
+    bool failed() const { return err_.code != 0; }
+    void defer(int code, const std::string& msg);
+    void close_copy_run();
+    void* staging(size_t bytes);
+    void mark_start();
+
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    Arena arena_;
+    bool coalesce_;
+    std::map<uint32_t, Alloc> allocs_;
+    std::map<uint32_t, bool> freed_;
+    uint64_t next_ref_ = 1;
+    QueueErr err_{0, ""};
+    sol_transfer_stats stats_{};
+    // open H2D copy run (coalescing): payload staged in pinned memory
+    struct PendingCopy {
+        uint8_t* dst;
+        uint64_t off;
+        uint64_t bytes;
+    };
+    std::vector<PendingCopy> run_;
+    std::vector<uint8_t> run_payload_;
+    // pinned staging buffers released at synchronize
+    std::vector<void*> pinned_live_;
+    struct D2H {
+        void* user;
+        void* pinned;
+        uint64_t bytes;
+    };
+    std::vector<D2H> d2h_;
+    int64_t scratch_off_ = -1;
+    size_t scratch_bytes_ = 0;
+    cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
+    bool timing_ = false;
+};
+
+class Plan {
+public:
+    explicit Plan(int device);
+    ~Plan();
+    int add_buffer(uint64_t bytes, bool persistent);
+    void add_step(std::unique_ptr<Module> m, const int32_t* ids, int n);
+    void add_allreduce(int id, uint64_t count, int dtype, float scale);
+    void finalize();
+    void* buffer_ptr(int id) const;
+    void set_frozen(bool f) { frozen_ = f; }
+    void run(bool use_graph);
+    void sync();
+    cudaStream_t stream() const { return stream_; }
+    void profile(double* times_us, int n);
+    int num_steps() const { return static_cast<int>(steps_.size()); }
+    const Module* step_module(int i) const { return steps_[i].module.get(); }
+    uint64_t arena_bytes() const { return total_; }
+    void set_comm(const uint8_t id[128], int rank, int nranks);
+    void h2d(int id, const void* src, uint64_t bytes);
+    void d2h(void* dst, int id, uint64_t bytes);
+    void event_record(int slot);
+    float event_elapsed(int a, int b);
+
+private:
+    struct Buf {
+        uint64_t bytes;
+        bool persistent;
+        int first = -1, last = -1;
+        uint64_t off = 0;
+    };
+    struct Step {
+        std::unique_ptr<Module> module;
+        std::vector<int> ids;
+        // all-reduce step
+        int ar_id = -1;
+        uint64_t ar_count = 0;
+        int ar_dtype = 0;
+        float ar_scale = 1.f;
+    };
+    void run_step(Step& s, cudaStream_t st);
+    void run_steps(cudaStream_t st);
+
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    std::vector<Buf> bufs_;
+    std::vector<Step> steps_;
+    uint8_t* base_ = nullptr;
+    uint64_t total_ = 0, scratch_off_ = 0, scratch_bytes_ = 0;
+    bool finalized_ = false, frozen_ = false;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    void* comm_ = nullptr;  // ncclComm_t
+    int nranks_ = 1;
+    cudaEvent_t events_[16] = {};
+};
+
+}  // namespace solb200
