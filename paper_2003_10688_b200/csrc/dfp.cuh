@@ -30,6 +30,8 @@ enum PwOp : uint8_t {
     PW_MOV,        // r[dst] = r[a]
     PW_SCALE,      // r[dst] = r[dst] * imm
     PW_PARAM,      // r[dst] = P[arg][c]
+    PW_BN,         // r[dst] = ((r[dst] - P[arg][c]) - P[arg+1][c]) * P[arg+2][c] + P[arg+3][c]
+                   //   (BatchNorm apply; the mean is split hi+lo so x - mean keeps f64-grade accuracy)
 };
 
 struct PwInstr {
@@ -48,6 +50,7 @@ enum InKind : int {
     IN_PIX = 0,    // NHWC tensor on the program's grid: ptr + pixel*ld + coff + c
     IN_NC = 1,     // [N, C] tensor broadcast over pixels: ptr + n*ld + c
     IN_CAT = 2,    // concat over channel segments (cat_* fields)
+    IN_FLAT = 3,   // canonical-order flattened [N, C*HW] read at pixel p, channel c (FlattenBack)
 };
 
 enum Family : int {
@@ -76,6 +79,7 @@ struct DfpArgs {
     int in_ld[DFP_MAX_IN] = {};
     int in_coff[DFP_MAX_IN] = {};
     int in_f32[DFP_MAX_IN] = {};   // input stored as f32 even in a bf16 plan
+    int in_hw[DFP_MAX_IN] = {};    // IN_FLAT: H*W of the unflattened tensor
     int n_cat = 0;
     const void* cat_ptr[DFP_MAX_CAT] = {};
     int cat_off[DFP_MAX_CAT + 1] = {};
@@ -91,7 +95,7 @@ struct DfpArgs {
     void* out = nullptr;
     int out_ld = 0, out_coff = 0;
     int out_f32 = 0;               // output stored as f32 even in a bf16 plan
-    float* partial = nullptr;      // FAM_CHAN_REDUCE: [blocks][C][2]
+    double* partial = nullptr;     // FAM_CHAN_REDUCE: [blocks][C][2] (f64)
     int reduce_blocks = 0;
 };
 
@@ -111,15 +115,16 @@ void softmax_back(int dtype, const void* delta, const void* y, void* dx, int row
 // Per-channel finalisation of FAM_CHAN_REDUCE partials (in f64).
 enum FinalizeMode : int {
     FIN_BN_STATS = 0,   // mean/var from shifted sums -> stats[2C] = (mean, rstd),
-                        // coef[2C] = (gamma*rstd, beta - mean*gamma*rstd); optional running update
+                        // coef[4C] = (mean_hi, mean_lo, gamma*rstd, beta) for PW_BN; optional running update
     FIN_SUMS = 1,       // out0[c] = S1, out1[c] = S2 (f32)
     FIN_BN_BACK = 2,    // dbeta = S1, dgamma = S2 (over xhat); coef[3C] for dx = dy*A + x*B + Cc
 };
 struct FinalizeArgs {
     int mode = FIN_BN_STATS;
     int C = 0;
+    int Cstride = 0;               // channel stride of the partial sums (>= C; 0 = C)
     int blocks = 0;
-    const float* partial = nullptr;
+    const double* partial = nullptr;
     double count = 1.0;
     float eps = 1e-5f;
     float momentum = 0.1f;
@@ -136,7 +141,7 @@ struct FinalizeArgs {
 };
 void dfp_finalize(const FinalizeArgs& a, cudaStream_t s);
 
-// BN inference coefficients: coef = (gamma/sqrt(var+eps), beta - mean*gamma/sqrt(var+eps)).
+// BN inference coefficients for PW_BN: coef[4C] = (mean, 0, gamma/sqrt(var+eps), beta).
 void bn_infer_coef(const float* gamma, const float* beta, const float* mean, const float* var, float eps,
                    float* coef, int C, cudaStream_t s);
 // Shift vector for shifted-sum statistics: shift[c] = x[0, c] (first pixel).

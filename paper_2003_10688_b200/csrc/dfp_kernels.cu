@@ -26,6 +26,13 @@ __device__ __forceinline__ void load_in(const DfpArgs& a, int slot, int64_t pix,
         base = static_cast<const T*>(a.in[slot]) + pix * a.in_ld[slot] + a.in_coff[slot] + c;
     } else if (kind == IN_NC) {
         base = static_cast<const T*>(a.in[slot]) + static_cast<int64_t>(n) * a.in_ld[slot] + c;
+    } else if (kind == IN_FLAT) {
+        const int hw = a.in_hw[slot];
+        const T* b = static_cast<const T*>(a.in[slot]) + static_cast<int64_t>(n) * a.in_ld[slot] +
+                     static_cast<int64_t>(c) * hw + (pix - static_cast<int64_t>(n) * hw);
+#pragma unroll
+        for (int i = 0; i < 16 / static_cast<int>(sizeof(T)); ++i) v[i] = to_f32(b[static_cast<int64_t>(i) * hw]);
+        return;
     } else {
         int s = 0;
         while (s + 1 < a.n_cat && c >= a.cat_off[s + 1]) ++s;
@@ -79,6 +86,20 @@ __device__ __forceinline__ void run_prog(const Program& pg, const DfpArgs& a, in
                     if (ins.dst == d) {
 #pragma unroll
                         for (int i = 0; i < V; ++i) r[d][i] = __ldg(s0 + i);
+                    }
+                break;
+            }
+            case PW_BN: {
+                const float* mh = a.P[ins.arg] + c;
+                const float* ml = a.P[ins.arg + 1] + c;
+                const float* sc = a.P[ins.arg + 2] + c;
+                const float* bt = a.P[ins.arg + 3] + c;
+#pragma unroll
+                for (int d = 0; d < NREG; ++d)
+                    if (ins.dst == d) {
+#pragma unroll
+                        for (int i = 0; i < V; ++i)
+                            r[d][i] = fmaf((r[d][i] - __ldg(mh + i)) - __ldg(ml + i), __ldg(sc + i), __ldg(bt + i));
                     }
                 break;
             }
@@ -312,7 +333,7 @@ __global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__
 template <typename T>
 __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_constant__ DfpArgs a) {
     constexpr int V = VEC<T>;
-    __shared__ float red[THREADS * V * 2];
+    __shared__ double red[THREADS * V * 2];
     const int cv_total = a.C / V;
     const int cvb = min(cv_total, THREADS);
     const int rows = THREADS / cvb;
@@ -325,9 +346,9 @@ __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_const
     const int64_t per = ceil_div(P, gridDim.x);
     const int64_t p0 = blockIdx.x * per;
     const int64_t p1 = min(P, p0 + per);
-    float s1[V], s2[V];
+    double s1[V], s2[V];  // f64 accumulation: memory-bound, and var = E[d^2] - E[d]^2 needs it
 #pragma unroll
-    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.f;
+    for (int i = 0; i < V; ++i) s1[i] = s2[i] = 0.0;
     const bool active = row < rows && (blockIdx.y * cvb + cvi) < cv_total;
     if (active) {
         for (int64_t p = p0 + row; p < p1; p += rows) {
@@ -335,8 +356,8 @@ __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_const
             run_prog<T>(a.pre, a, p, static_cast<int>(p / hw), c, r);
 #pragma unroll
             for (int i = 0; i < V; ++i) {
-                s1[i] += r[0][i];
-                s2[i] = fmaf(r[0][i], r[1][i], s2[i]);
+                s1[i] += static_cast<double>(r[0][i]);
+                s2[i] = fma(static_cast<double>(r[0][i]), static_cast<double>(r[1][i]), s2[i]);
             }
         }
     }
@@ -355,7 +376,7 @@ __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_const
                 s2[i] += red[(t2 * V + i) * 2 + 1];
             }
         }
-        float* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * a.C + c) * 2;
+        double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * a.C + c) * 2;
 #pragma unroll
         for (int i = 0; i < V; ++i) {
             dst[2 * i] = s1[i];
@@ -536,7 +557,7 @@ __global__ void ce_loss_kernel(const T* __restrict__ p, const T* __restrict__ t,
     for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
         const int64_t i = (k / cols) * ld + (k % cols);
         const float tv = to_f32(t[i]);
-        acc -= static_cast<double>(tv) * log(static_cast<double>(to_f32(p[i])));
+        if (tv != 0.f) acc -= static_cast<double>(tv) * log(static_cast<double>(to_f32(p[i])));  // 0*log 0 = 0
     }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = acc;
@@ -585,10 +606,11 @@ __global__ void softmax_back_kernel(const T* __restrict__ d, const T* __restrict
 __global__ void finalize_kernel(const FinalizeArgs a) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= a.C) return;
+    const int cs = a.Cstride > 0 ? a.Cstride : a.C;
     double s1 = 0.0, s2 = 0.0;
     for (int b = 0; b < a.blocks; ++b) {
-        s1 += a.partial[(static_cast<int64_t>(b) * a.C + c) * 2];
-        s2 += a.partial[(static_cast<int64_t>(b) * a.C + c) * 2 + 1];
+        s1 += a.partial[(static_cast<int64_t>(b) * cs + c) * 2];
+        s2 += a.partial[(static_cast<int64_t>(b) * cs + c) * 2 + 1];
     }
     const double m = a.count;
     if (a.mode == FIN_BN_STATS) {
@@ -603,9 +625,11 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
             a.stats_out[a.C + c] = static_cast<float>(rstd);
         }
         if (a.coef) {
-            const double g = a.gamma[c], bt = a.beta[c];
-            a.coef[c] = static_cast<float>(g * rstd);
-            a.coef[a.C + c] = static_cast<float>(bt - mean * g * rstd);
+            const float hi = static_cast<float>(mean);
+            a.coef[c] = hi;
+            a.coef[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
+            a.coef[2 * a.C + c] = static_cast<float>(static_cast<double>(a.gamma[c]) * rstd);
+            a.coef[3 * a.C + c] = a.beta[c];
         }
         if (a.running_mean) {
             const double unbias = m > 1 ? m / (m - 1) : 1.0;
@@ -637,8 +661,10 @@ __global__ void bn_infer_coef_kernel(const float* g, const float* b, const float
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
     const double rstd = 1.0 / sqrt(static_cast<double>(var[c]) + eps);
-    coef[c] = static_cast<float>(g[c] * rstd);
-    coef[C + c] = static_cast<float>(b[c] - mu[c] * g[c] * rstd);
+    coef[c] = mu[c];
+    coef[C + c] = 0.f;
+    coef[2 * C + c] = static_cast<float>(g[c] * rstd);
+    coef[3 * C + c] = b[c];
 }
 
 template <typename T>

@@ -76,13 +76,15 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), sm_100 version 1.
 // K-major:  LBO unused (16 B), SBO = 1024 B between 8-row core-matrix groups.
 // MN-major: LBO = stride between 64-element MN blocks, SBO = stride between 8-row K groups.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// Layout type 2 = SWIZZLE_128B; 1 = SWIZZLE_128B_BASE32B (32-byte swizzle atoms, used for the
+// MN-major 32-bit (tf32) operands of wgrad).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
     d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
     d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
     d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
-    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    d |= static_cast<uint64_t>(layout) << 61;
     return d;
 }
 
@@ -351,7 +353,12 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
     constexpr uint32_t TCOLS = tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 1, 1);
     constexpr int KPER_MMA = 32 / sizeof(T);  // 16 bf16 / 8 tf32 pixels per instruction
-    constexpr uint32_t LBO = (BK / 8) * 1024;
+    // bf16: 128B-swizzle atoms of 8 K-rows (1024 B); tf32: 128B_BASE32B atoms of 4 K-rows (512 B)
+    constexpr bool B32 = sizeof(T) == 4;
+    constexpr int GR = B32 ? 4 : 8;
+    constexpr int AT = GR * ROWB;
+    constexpr uint32_t LAYOUT = B32 ? 1 : 2;
+    constexpr uint32_t LBO = (BK / GR) * AT;
     static_assert(BN % EPB == 0, "BN must be a multiple of the 128B MN block");
 
     extern __shared__ uint8_t smem_raw[];
@@ -402,14 +409,15 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
                 oh = rem / a.OW;
                 ow = rem - oh * a.OW;
             }
-            const int kg = r >> 3, rr = r & 7;
+            const int kg = r / GR, rr = r % GR;
+            const int jp = B32 ? ((((j >> 1) ^ (r & 3)) << 1) | (j & 1)) : (j ^ (r & 7));
             // A: dy[p][m0 + blk*EPB + j*VEC]
 #pragma unroll
             for (int blk = 0; blk < A_BLOCKS; ++blk) {
                 const int co = m0 + blk * EPB + j * VEC;
                 const bool ok = pv && co < a.Cout;
                 const T* g = ok ? dy + static_cast<int64_t>(p) * a.ld_dy + co : dy;
-                cp_async16(smem_u32(sa + (blk * (BK / 8) + kg) * 1024 + rr * ROWB + ((j ^ rr) << 4)), g, ok);
+                cp_async16(smem_u32(sa + (blk * (BK / GR) + kg) * AT + rr * ROWB + (jp << 4)), g, ok);
             }
             // B: x gathered at pixel p for column n0 + blk*EPB + j*VEC = (tap, ci)
 #pragma unroll
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
                 const int hh = oh * a.sh - a.ph + dkh, ww = ow * a.sw - a.pw + dkw;
                 const bool ok = pv && col < ncol && tap < ntaps && hh >= 0 && hh < a.SH && ww >= 0 && ww < a.SW;
                 const T* g = ok ? x + ((static_cast<int64_t>(n) * a.SH + hh) * a.SW + ww) * a.SC + ci : x;
-                cp_async16(smem_u32(sb + (blk * (BK / 8) + kg) * 1024 + rr * ROWB + ((j ^ rr) << 4)), g, ok);
+                cp_async16(smem_u32(sb + (blk * (BK / GR) + kg) * AT + rr * ROWB + (jp << 4)), g, ok);
             }
         }
     };
@@ -450,9 +458,9 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
 #pragma unroll
             for (int k = 0; k < BK / KPER_MMA; ++k) {
                 // K advance: KPER_MMA pixels = KPER_MMA/8 k-groups of 1024 B
-                const uint32_t koff = (k * KPER_MMA / 8) * 1024;
-                const uint64_t ad = sw128_desc(a_addr + koff, LBO, 1024);
-                const uint64_t bd = sw128_desc(b_addr + koff, LBO, 1024);
+                const uint32_t koff = (k * KPER_MMA / GR) * AT;
+                const uint64_t ad = sw128_desc(a_addr + koff, LBO, AT, LAYOUT);
+                const uint64_t bd = sw128_desc(b_addr + koff, LBO, AT, LAYOUT);
                 mma<T>(tmem_d, ad, bd, IDESC, (kb | k) != 0);
             }
             mma_commit(smem_u32(&mbar[slot]));

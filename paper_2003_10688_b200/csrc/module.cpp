@@ -433,11 +433,12 @@ public:
         training_ = o.attrs.training != 0;
         eps_ = o.attrs.eps;
         delta_ = geo_b(d.bindings[o.inputs[0]]);
-        C_ = static_cast<int>(delta_.C);
-        if (delta_.ld != delta_.C) unsupported("reduction over padded channel storage");
+        C_ = static_cast<int>(delta_.ld);       // reduce over the stored (padded) width
+        Creal_ = static_cast<int>(delta_.C);
         blocks_ = dfp_reduce_blocks(delta_.pixels(), C_);
         const bool needs_x = op_ == SOL_OP_BATCHNORMBACKX || op_ == SOL_OP_BATCHNORMBACKGAMMA;
         if (needs_x && !training_) unsupported("BatchNorm backward in inference mode");
+        if (needs_x && C_ != Creal_) unsupported("BatchNorm backward over padded channel storage");
         if (needs_x) {
             x_idx_ = o.inputs[1];
             ones_ = static_cast<float*>(dev_alloc(C_ * 4));
@@ -446,7 +447,7 @@ public:
             zeros_ = static_cast<float*>(dev_alloc(C_ * 4));
             shift_ = static_cast<float*>(dev_alloc(C_ * 4));
             stats_ = static_cast<float*>(dev_alloc(2 * C_ * 4));
-            xhat_ = static_cast<float*>(dev_alloc(2 * C_ * 4));
+            xhat_ = static_cast<float*>(dev_alloc(4 * C_ * 4));
             coef_ = static_cast<float*>(dev_alloc(3 * C_ * 4));
             gamma_idx_ = o.n_params > 0 ? o.params[0] : -1;
         }
@@ -459,9 +460,9 @@ public:
         const double es = double(elem_size(dtype_));
         algo_bytes = delta_.numel() * es * (needs_x ? 2 : 1) + (op_ == SOL_OP_BATCHNORMBACKX ? delta_.numel() * es : 0);
     }
-    size_t scratch_bytes() const override { return static_cast<size_t>(blocks_) * C_ * 2 * 4 + 256; }
+    size_t scratch_bytes() const override { return static_cast<size_t>(blocks_) * C_ * 2 * 8 + 256; }
 
-    DfpArgs base(void* const* args, float* partial) const {
+    DfpArgs base(void* const* args, double* partial) const {
         DfpArgs a;
         a.family = FAM_CHAN_REDUCE;
         a.dtype = dtype_;
@@ -484,7 +485,7 @@ public:
     }
 
     // x statistics -> xhat coefficients (rstd, -mean*rstd) and (mean, rstd)
-    void x_stats(void* const* args, float* partial, cudaStream_t s) {
+    void x_stats(void* const* args, double* partial, cudaStream_t s) {
         bn_shift(dtype_, args[x_idx_], C_, C_, shift_, s);
         DfpArgs a = base(args, partial);
         a.P[0] = shift_;
@@ -505,13 +506,13 @@ public:
         f.gamma = ones_;
         f.beta = zeros_;
         f.stats_out = stats_;
-        f.coef = xhat_;  // (rstd, -mean*rstd)
+        f.coef = xhat_;  // (mean, rstd, 0): PW_BN gives xhat
         dfp_finalize(f, s);
     }
 
     void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool) override {
         if (nargs != n_args) throw std::invalid_argument("reduce module: wrong argument count");
-        float* partial = static_cast<float*>(scratch);
+        double* partial = static_cast<double*>(scratch);
         float* out = static_cast<float*>(args[nargs - 1]);
         if (op_ == SOL_OP_BATCHNORMBACKBETA || op_ == SOL_OP_CONV2DBACKB || op_ == SOL_OP_LINEARBACKB) {
             DfpArgs a = base(args, partial);
@@ -520,7 +521,8 @@ public:
             dfp_launch(a, s);
             FinalizeArgs f;
             f.mode = FIN_SUMS;
-            f.C = C_;
+            f.C = Creal_;
+            f.Cstride = C_;
             f.blocks = blocks_;
             f.partial = partial;
             f.out0 = out;
@@ -532,10 +534,12 @@ public:
         DfpArgs a = base(args, partial);
         a.P[0] = xhat_;
         a.P[1] = xhat_ + C_;
+        a.P[2] = xhat_ + 2 * C_;
+        a.P[3] = xhat_ + 3 * C_;
         a.pre = Program();
         push(a.pre, PW_LD, 0, 0);      // r0 = delta
         push(a.pre, PW_LD, 1, 1);      // r1 = x
-        push(a.pre, PW_AFF, 1, 0, 0, 0);  // r1 = xhat
+        push(a.pre, PW_BN, 1, 0, 0, 0);   // r1 = xhat = (x - mean) * rstd
         dfp_launch(a, s);
         FinalizeArgs f;
         f.mode = FIN_BN_BACK;
@@ -582,7 +586,7 @@ private:
     bool training_ = false;
     float eps_ = 1e-5f;
     Geo delta_;
-    int C_ = 0;
+    int C_ = 0, Creal_ = 0;
     int blocks_ = 1;
     int x_idx_ = -1, gamma_idx_ = -1;
     float *ones_ = nullptr, *zeros_ = nullptr, *shift_ = nullptr, *stats_ = nullptr, *xhat_ = nullptr,
@@ -609,7 +613,7 @@ private:
         int g, b, m, v;     // param bindings
         float eps;
         int C;
-        float* coef;        // [2C] -> P[pidx], P[pidx+1]
+        float* coef;        // [3C] (mean, scale, beta) -> P[3i], P[3i+1], P[3i+2]
         float* shift;
         float* stats;
         int64_t pixels;
@@ -757,7 +761,7 @@ int DfpModule::emit_value(int key) {
         case SOL_OP_BATCHNORM2D: {
             const int r = reg_take(in_key(0));
             const int bi = bn_of_op_.at(key);
-            push(p, PW_AFF, r, 0, 0, 2 * bi);
+            push(p, PW_BN, r, 0, 0, 4 * bi);
             return r;
         }
         case SOL_OP_ADD: {
@@ -801,6 +805,14 @@ int DfpModule::emit_value(int key) {
             if (o.inputs[0] < 0) unsupported("ConcatBack of a fused intermediate");
             const int r = alloc_reg();
             push(p, PW_LD, r, slot_for(o.inputs[0], IN_PIX, static_cast<int>(o.attrs.offset)));
+            return r;
+        }
+        case SOL_OP_FLATTENBACK: {
+            if (o.inputs[0] < 0) unsupported("FlattenBack of a fused intermediate");
+            const int r = alloc_reg();
+            const int s = slot_for(o.inputs[0], IN_FLAT, 0);
+            tmpl_.in_hw[s] = static_cast<int>(o.saved_dims[2] * o.saved_dims[3]);
+            push(p, PW_LD, r, s);
             return r;
         }
         case SOL_OP_GLOBALAVGPOOLBACK: {
@@ -850,7 +862,7 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
         b.eps = o.attrs.eps;
         const Geo xg = geo_ref(o.inputs[0]);
         b.C = static_cast<int>(xg.C);
-        b.coef = static_cast<float*>(dev_alloc(2 * b.C * 4));
+        b.coef = static_cast<float*>(dev_alloc(4 * b.C * 4));
         if (b.training) {
             if (o.inputs[0] < 0) unsupported("training BatchNorm2d over a fused intermediate");
             b.x_binding = o.inputs[0];
@@ -863,10 +875,10 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
             b.xW = static_cast<int>(xg.W);
             if (xg.ld != xg.C) unsupported("training BatchNorm2d over padded storage");
             stats_scratch_ = std::max(stats_scratch_,
-                                      static_cast<size_t>(dfp_reduce_blocks(b.pixels, b.C)) * b.C * 2 * 4 + 256);
+                                      static_cast<size_t>(dfp_reduce_blocks(b.pixels, b.C)) * b.C * 2 * 8 + 256);
         }
         bn_of_op_[k] = static_cast<int>(bn_.size());
-        if (2 * static_cast<int>(bn_.size()) + 1 >= DFP_MAX_P) unsupported("too many BatchNorms in one unit");
+        if (4 * static_cast<int>(bn_.size()) + 3 >= DFP_MAX_P) unsupported("too many BatchNorms in one unit");
         bn_.push_back(b);
     }
     if (std::any_of(bn_.begin(), bn_.end(), [](const BnPrep& b) { return b.training; })) {
@@ -1005,10 +1017,9 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
     if (tmpl_.family == FAM_POINTWISE || tmpl_.family == FAM_GAP) {
         if (out.C != tmpl_.C && tmpl_.family == FAM_POINTWISE) tmpl_.C = static_cast<int>(out.C);
     }
-    // parameter arrays: BN coefficient pairs at P[2i], P[2i+1]
+    // parameter arrays: BN coefficient triples at P[3i..3i+2]
     for (size_t i = 0; i < bn_.size(); ++i) {
-        tmpl_.P[2 * i] = bn_[i].coef;
-        tmpl_.P[2 * i + 1] = bn_[i].coef + bn_[i].C;
+        for (int k = 0; k < 4; ++k) tmpl_.P[4 * i + k] = bn_[i].coef + k * bn_[i].C;
     }
     // algorithmic bytes: external activation inputs + output
     double bytes = binding_bytes(d.output);
@@ -1031,7 +1042,7 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
                               b.coef, b.C, s);
             continue;
         }
-        float* partial = static_cast<float*>(scratch);
+        double* partial = static_cast<double*>(scratch);
         bn_shift(dtype_, args[b.x_binding], b.x_ld, b.C, b.shift, s);
         DfpArgs a;
         a.family = FAM_CHAN_REDUCE;
@@ -1136,7 +1147,7 @@ std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
         const int op = d.ops[k].op;
         const bool single_only = (is_heavy_op(op) && !(op == SOL_OP_CONV2D)) || op == SOL_OP_SOFTMAX ||
                                  op == SOL_OP_CROSSENTROPYLOSS || op == SOL_OP_SOFTMAXCEBACK || op == SOL_OP_CEBACK ||
-                                 op == SOL_OP_SOFTMAXBACK || op == SOL_OP_FLATTEN || op == SOL_OP_FLATTENBACK ||
+                                 op == SOL_OP_SOFTMAXBACK || op == SOL_OP_FLATTEN ||
                                  op == SOL_OP_SGDUPDATE || op == SOL_OP_BATCHNORMBACKX ||
                                  op == SOL_OP_BATCHNORMBACKGAMMA || op == SOL_OP_BATCHNORMBACKBETA ||
                                  op == SOL_OP_CONV2DBACKB || op == SOL_OP_LINEARBACKB;

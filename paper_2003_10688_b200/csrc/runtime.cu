@@ -453,12 +453,17 @@ void Plan::run(bool use_graph) {
     SOL_CUDA(cudaSetDevice(device_));
     if (!use_graph) {
         run_steps(stream_);
+        has_run_ = true;
+        return;
+    }
+    if (!has_run_) {
+        // the first execution is always eager: kernel attributes and frozen-parameter caches are
+        // set up outside stream capture (each call is exactly one pass of the plan)
+        run_steps(stream_);
+        has_run_ = true;
         return;
     }
     if (!graph_exec_) {
-        // one eager pass first: kernel attributes and frozen-parameter caches are set up outside capture
-        run_steps(stream_);
-        SOL_CUDA(cudaStreamSynchronize(stream_));
         cudaGraph_t g;
         SOL_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
         try {

@@ -145,7 +145,7 @@ private:
     std::vector<Step> steps_;
     uint8_t* base_ = nullptr;
     uint64_t total_ = 0, scratch_off_ = 0, scratch_bytes_ = 0;
-    bool finalized_ = false, frozen_ = false;
+    bool finalized_ = false, frozen_ = false, has_run_ = false;
     cudaGraphExec_t graph_exec_ = nullptr;
     void* comm_ = nullptr;  // ncclComm_t
     int nranks_ = 1;

@@ -58,6 +58,7 @@ def _dims(meta: Meta, arr):
 
 def binding_for(meta: Meta, dtype: int, is_param: bool, f32: bool = False) -> L.Binding:
     b = L.Binding()
+    is_param = is_param or meta.kind == "plain"   # plain f32 tensors: params and their gradients
     b.is_param = int(is_param)
     b.dtype = L.DT_F32 if (is_param or f32) else dtype
     b.rank = _dims(meta, b.dims)

@@ -1,0 +1,331 @@
+"""Network API over the B200 backend: optimize() -> OptimizedModel.predict / train_step.
+
+This is the frontend the reference declares but does not implement
+(include/sol/frontend.hpp:104-174: fe::optimize, OptimizedModel::predict, train_step(batch, lr,
+TrainMode::Native), load_state, DevicePlan/Step). The compile pipeline follows the declared one
+(frontend.hpp:167-172): infer_shapes -> [build_training_graph] -> run_pipeline -> partition ->
+per-unit module compile -> plan (buffers + steps) -> layouts. The plan executes in C++
+(libsolb200.so: arena placement by liveness, one CUDA stream, optional CUDA-graph replay, NCCL
+all-reduce of gradients for batch-sharded data parallelism) — Python only compiles.
+
+Activations live in NHWC (ActLayout::ChannelsLast) in the plan dtype (bf16, or f32 with TF32
+tensor-core GEMMs); parameters are f32 master copies in the reference's canonical layouts.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import _lib as L
+from .autodiff import build_training_graph
+from .dfp import (DTYPES, ELEM, create_module, is_f32_tensor, reorder_module, sgd_module, storage_bytes)
+from .graph import Meta, ModelGraph, infer_shapes
+from .partition import ExecUnit, partition
+from .passes import run_pipeline
+
+
+@dataclass
+class OptimizeOptions:
+    """Mirror of fe::OptimizeOptions (frontend.hpp:27-36) plus the B200 knobs."""
+    batch: int = 1
+    dtype: str = "bf16"        # "bf16" or "f32" (TF32 tensor cores, f32 storage)
+    train: bool = False        # compile forward+backward+SGD (TrainMode::Native)
+    lr: float = 0.1
+    use_graph: bool = True     # replay the plan as one CUDA graph
+    device: int = 0
+    world_size: int = 1        # batch-sharded data parallelism (one process per GPU)
+    rank: int = 0
+    nccl_id: Optional[bytes] = None
+    passes: bool = True        # reference rewrite pipeline (passes.cpp:168-178)
+    keep_all: bool = False     # debug: every unit output persistent (no arena reuse)
+
+
+@dataclass
+class StepInfo:
+    kind: str          # "unit" | "reorder" | "sgd" | "allreduce"
+    family: str
+    output: str
+    algo_bytes: float = 0.0
+    algo_flops: float = 0.0
+    launches: int = 1
+    node_ids: List[str] = field(default_factory=list)
+
+
+class PinnedBuffer:
+    """Page-locked host memory (cudaMallocHost through the C ABI) viewed as a numpy array."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        L.check(L.lib().sol_b200_host_alloc(max(nbytes, 16), C.byref(self.ptr)))
+        self.nbytes = nbytes
+        buf = (C.c_uint8 * max(nbytes, 16)).from_address(self.ptr.value)
+        self.u8 = np.frombuffer(buf, dtype=np.uint8)
+
+    def view(self, dtype, shape):
+        n = int(np.prod(shape)) if shape else 1
+        return self.u8[: n * np.dtype(dtype).itemsize].view(dtype).reshape(shape)
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                L.lib().sol_b200_host_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+class OptimizedModel:
+    def __init__(self, g: ModelGraph, options: OptimizeOptions):
+        t0 = time.perf_counter()
+        self.options = options
+        self.dtype = DTYPES[options.dtype]
+        gi = infer_shapes(g, options.batch)
+        self.param_grads = []
+        if options.train:
+            tg = build_training_graph(gi)
+            cg = infer_shapes(tg.graph, options.batch)
+            self.loss_name = tg.loss
+            self.param_grads = list(tg.param_grads)
+        else:
+            cg = gi
+            self.loss_name = None
+        if options.passes:
+            cg = run_pipeline(cg)
+        self.graph = cg
+        self.units: List[ExecUnit] = partition(cg)
+        self.params: Dict[str, np.ndarray] = {k: np.asarray(v, np.float32).copy() for k, v in g.params.items()}
+        self._build_plan()
+        self.compile_ms = (time.perf_counter() - t0) * 1e3
+
+    # ------------------------------------------------------------------------------------------
+    def _build_plan(self):
+        o = self.options
+        lib = L.lib()
+        self.plan = C.c_void_p()
+        L.check(lib.sol_b200_plan_create(o.device, C.byref(self.plan)))
+        g = self.graph
+        self.buf: Dict[str, int] = {}
+        self.steps: List[StepInfo] = []
+        self._step_ids: List[List[int]] = []
+
+        def add_buf(nbytes, persistent):
+            i = C.c_int32()
+            L.check(lib.sol_b200_plan_add_buffer(self.plan, int(nbytes), int(persistent), C.byref(i)))
+            return i.value
+
+        def add_step(mod, ids, info: StepInfo):
+            arr = (C.c_int32 * len(ids))(*ids)
+            L.check(lib.sol_b200_plan_add_step(self.plan, mod.handle, arr, len(ids)))
+            info.family = mod.family
+            info.algo_bytes, info.algo_flops, info.launches = mod.algo_bytes, mod.algo_flops, mod.launches
+            self.steps.append(info)
+
+        # parameters: persistent f32 master copies
+        for name, arr in self.params.items():
+            self.buf[name] = add_buf(arr.nbytes, True)
+        outputs = set(g.outputs)
+        # graph inputs: canonical f32 staging buffer + NHWC plan buffer + reorder step
+        self.inputs: Dict[str, Meta] = {}
+        self.in_canon: Dict[str, int] = {}
+        for gi in g.graph_inputs:
+            self.inputs[gi.name] = gi.meta
+            self.in_canon[gi.name] = add_buf(4 * gi.meta.numel, True)
+            self.buf[gi.name] = add_buf(storage_bytes(gi.meta, self.dtype), True)
+            add_step(reorder_module(gi.meta, self.dtype, True), [self.in_canon[gi.name], self.buf[gi.name]],
+                     StepInfo("reorder", "", gi.name))
+        # unit outputs
+        self.modules = []
+        for u in self.units:
+            meta = g.meta_of(u.output)
+            f32 = is_f32_tensor(g, u.output)
+            self.buf[u.output] = add_buf(storage_bytes(meta, self.dtype, f32),
+                                         u.output in outputs or o.keep_all)
+            mod = create_module(g, u, self.dtype)
+            ids = [self.buf[n] for n in list(u.inputs) + list(u.params)] + [self.buf[u.output]]
+            add_step(mod, ids, StepInfo("unit", "", u.output, node_ids=list(u.node_ids)))
+        # graph outputs: canonical f32 copies for the host
+        self.out_canon: Dict[str, int] = {}
+        for name in g.outputs:
+            meta = g.meta_of(name)
+            if is_f32_tensor(g, name):
+                self.out_canon[name] = self.buf[name]   # already canonical f32 (loss / gradients)
+                continue
+            self.out_canon[name] = add_buf(4 * meta.numel, True)
+            add_step(reorder_module(meta, self.dtype, False), [self.buf[name], self.out_canon[name]],
+                     StepInfo("reorder", "", name))
+        # native training: all-reduce gradients across ranks, then SGD on the device
+        if o.train:
+            for pname, gname in self.param_grads:
+                if o.world_size > 1:
+                    L.check(lib.sol_b200_plan_add_allreduce(self.plan, self.buf[gname], self.params[pname].size,
+                                                            L.DT_F32, 1.0 / o.world_size))
+                    self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname,
+                                               algo_bytes=4.0 * self.params[pname].size))
+            for pname, gname in self.param_grads:
+                mod = sgd_module(self.params[pname].shape, o.lr, self.dtype)
+                add_step(mod, [self.buf[pname], self.buf[gname], self.buf[pname]], StepInfo("sgd", "", pname))
+        if o.world_size > 1:
+            if o.nccl_id is None:
+                raise ValueError("world_size > 1 needs the rank-0 NCCL unique id")
+            idb = (C.c_uint8 * 128)(*o.nccl_id)
+            L.check(lib.sol_b200_plan_set_comm(self.plan, idb, o.rank, o.world_size))
+        L.check(lib.sol_b200_plan_finalize(self.plan))
+        self._upload_params()
+        self._ran = False
+        self.stream = C.c_void_p()
+        L.check(lib.sol_b200_plan_stream(self.plan, C.byref(self.stream)))
+        # pinned staging for the host interface
+        self.pin_in = {n: PinnedBuffer(4 * m.numel) for n, m in self.inputs.items()}
+        self.pin_out = {n: PinnedBuffer(4 * g.meta_of(n).numel) for n in g.outputs}
+
+    def _upload_params(self):
+        lib = L.lib()
+        for name, arr in self.params.items():
+            pb = PinnedBuffer(arr.nbytes)
+            pb.view(np.float32, arr.shape)[...] = arr
+            L.check(lib.sol_b200_plan_h2d(self.plan, self.buf[name], pb.ptr, arr.nbytes))
+            L.check(lib.sol_b200_plan_sync(self.plan))
+        L.check(lib.sol_b200_plan_set_frozen(self.plan, 0))
+        self._frozen = False
+
+    # ------------------------------------------------------------------------------------------
+    def load_state(self, params: Dict[str, np.ndarray]):
+        """Replaces the master parameters (frontend.hpp:115); device caches are rebuilt."""
+        for k, v in params.items():
+            if k not in self.params or self.params[k].shape != np.shape(v):
+                raise ValueError(f"parameter {k} mismatch")
+            self.params[k] = np.asarray(v, np.float32).copy()
+        self._upload_params()
+        self._ran = False
+
+    def host_params(self) -> Dict[str, np.ndarray]:
+        """Pulls device parameters back (frontend.hpp:127-128: sync_host_params)."""
+        lib = L.lib()
+        out = {}
+        for name, arr in self.params.items():
+            pb = PinnedBuffer(arr.nbytes)
+            L.check(lib.sol_b200_plan_d2h(self.plan, pb.ptr, self.buf[name], arr.nbytes))
+            L.check(lib.sol_b200_plan_sync(self.plan))
+            out[name] = pb.view(np.float32, arr.shape).copy()
+        return out
+
+    def set_inputs(self, inputs: Dict[str, np.ndarray]):
+        lib = L.lib()
+        for name, meta in self.inputs.items():
+            if name not in inputs:
+                raise KeyError(f"missing graph input '{name}'")
+            a = np.asarray(inputs[name], np.float32)
+            if a.size != meta.numel:
+                raise ValueError(f"input '{name}' size mismatch")
+            self.pin_in[name].view(np.float32, meta.shape)[...] = a.reshape(meta.shape)
+        for name, meta in self.inputs.items():
+            L.check(lib.sol_b200_plan_h2d(self.plan, self.in_canon[name], self.pin_in[name].ptr, 4 * meta.numel))
+
+    def run(self):
+        """One pass of the plan on its stream (no host synchronisation)."""
+        lib = L.lib()
+        use_graph = self.options.use_graph
+        if not self._ran:
+            # first run eagerly (module caches + kernel attributes), then freeze for inference
+            L.check(lib.sol_b200_plan_run(self.plan, 0))
+            self._ran = True
+            if not self.options.train:
+                L.check(lib.sol_b200_plan_set_frozen(self.plan, 1))
+            return
+        L.check(lib.sol_b200_plan_run(self.plan, int(use_graph)))
+
+    def fetch_outputs(self, names=None) -> Dict[str, np.ndarray]:
+        lib = L.lib()
+        names = list(self.graph.outputs) if names is None else names
+        for n in names:
+            meta = self.graph.meta_of(n)
+            L.check(lib.sol_b200_plan_d2h(self.plan, self.pin_out[n].ptr, self.out_canon[n], 4 * meta.numel))
+        L.check(lib.sol_b200_plan_sync(self.plan))
+        return {n: self.pin_out[n].view(np.float32, self.graph.meta_of(n).shape).copy() for n in names}
+
+    def predict(self, inputs: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
+        """fe::OptimizedModel::predict (frontend.hpp:119): host in, host out, canonical layouts."""
+        self.set_inputs(inputs)
+        self.run()
+        return self.fetch_outputs()
+
+    def train_step(self, batch: Dict[str, np.ndarray]) -> float:
+        """fe::OptimizedModel::train_step(batch, lr, TrainMode::Native): forward, backward,
+        gradient all-reduce (DP) and SGD on the device; returns the loss."""
+        if not self.options.train:
+            raise RuntimeError("model was not compiled for training")
+        self.set_inputs(batch)
+        self.run()
+        return float(self.fetch_outputs([self.loss_name])[self.loss_name].reshape(()))
+
+    def gradients(self) -> Dict[str, np.ndarray]:
+        """Parameter gradients of the last step (canonical f32)."""
+        lib = L.lib()
+        out = {}
+        for pname, gname in self.param_grads:
+            shape = self.params[pname].shape
+            pb = PinnedBuffer(4 * int(np.prod(shape)))
+            L.check(lib.sol_b200_plan_d2h(self.plan, pb.ptr, self.buf[gname], 4 * int(np.prod(shape))))
+            L.check(lib.sol_b200_plan_sync(self.plan))
+            out[pname] = pb.view(np.float32, shape).copy()
+        return out
+
+    def read_tensor(self, name: str) -> np.ndarray:
+        """Debug/parity access to any plan buffer still live (persistent or final values)."""
+        lib = L.lib()
+        meta = self.graph.meta_of(name) if name not in self.params else Meta("plain", self.params[name].shape)
+        f32 = name in self.params or is_f32_tensor(self.graph, name)
+        nbytes = storage_bytes(meta, self.dtype, f32)
+        pb = PinnedBuffer(nbytes)
+        L.check(lib.sol_b200_plan_d2h(self.plan, pb.ptr, self.buf[name], nbytes))
+        L.check(lib.sol_b200_plan_sync(self.plan))
+        return pb.u8[:nbytes].copy()
+
+    # ------------------------------------------------------------------------------------------
+    def profile(self) -> List[float]:
+        """Per-step device times (us), CUDA events around every step (eager, no graph)."""
+        lib = L.lib()
+        n = C.c_int32()
+        L.check(lib.sol_b200_plan_num_steps(self.plan, C.byref(n)))
+        arr = (C.c_double * n.value)()
+        L.check(lib.sol_b200_plan_profile(self.plan, arr, n.value))
+        return list(arr)
+
+    def event(self, slot: int):
+        L.check(L.lib().sol_b200_plan_event_record(self.plan, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        L.check(L.lib().sol_b200_plan_event_elapsed(self.plan, a, b, C.byref(ms)))
+        return ms.value
+
+    def sync(self):
+        L.check(L.lib().sol_b200_plan_sync(self.plan))
+
+    def arena_bytes(self) -> int:
+        v = C.c_uint64()
+        L.check(L.lib().sol_b200_plan_arena_bytes(self.plan, C.byref(v)))
+        return v.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "plan", None):
+                L.lib().sol_b200_plan_destroy(self.plan)
+                self.plan = None
+        except Exception:
+            pass
+
+
+def optimize(g: ModelGraph, options: OptimizeOptions) -> OptimizedModel:
+    """fe::optimize_graph (frontend.hpp:173-174)."""
+    return OptimizedModel(g, options)
+
+
+def nccl_unique_id() -> bytes:
+    arr = (C.c_uint8 * 128)()
+    L.check(L.lib().sol_b200_nccl_unique_id(arr))
+    return bytes(arr)

@@ -106,9 +106,7 @@ def test_conv_dgrad(gpu, case, dt):
     assert err <= 1e-2, err
 
 
-@pytest.mark.parametrize("dt", [1, pytest.param(0, marks=pytest.mark.xfail(
-    reason="TF32 MN-major operands need the SWIZZLE_128B_BASE32B atom; f32 wgrad not wired yet", strict=False))],
-    ids=["bf16", "tf32"])
+@pytest.mark.parametrize("dt", [1, 0], ids=["bf16", "tf32"])
 @pytest.mark.parametrize("case", [c for c in CASES if c[4] % 8 == 0])
 def test_conv_wgrad(gpu, case, dt):
     import torch

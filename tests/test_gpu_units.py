@@ -1,0 +1,106 @@
+"""Per-unit parity of every fused DFP kernel and tcgen05 provider against the oracle, on
+oracle-supplied unit inputs (proj/tests/test_dfp.cpp:26-45, :223-270; test_autodiff.cpp:355-385).
+
+Bars: f32 plans (fp32 DFP arithmetic) oracle_err <= 1e-5 for fused non-GEMM units — the
+reference's own kernel bar; bit-exact for pure movement (Flatten, Concat); TF32 / bf16 GEMM
+units and every bf16 unit <= 1e-2 against the oracle run on bf16-rounded unit inputs."""
+import numpy as np
+import pytest
+
+from oracle import sol_oracle as O
+from tests.gpu_util import quant, run_unit
+
+pytestmark = pytest.mark.gpu
+
+MOVEMENT = {"flatten", "flatten_back"}
+
+
+def tf32(a):
+    """TF32 operand rounding of the tcgen05 kind::tf32 path (low 13 mantissa bits dropped)."""
+    a = np.ascontiguousarray(np.asarray(a, np.float32))
+    return (a.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+def _graphs():
+    from paper_2003_10688_b200 import models
+    return {
+        "small_cnn": lambda tr: models.small_cnn(train=tr, hw=16),
+        "resnet18": lambda tr: models.resnet(18, hw=32, classes=16, width=16, train=tr),
+        "resnet50": lambda tr: models.resnet(50, hw=64, classes=16, width=16, train=tr),
+        "densenet": lambda tr: models.densenet121(hw=32, classes=16, growth=8, blocks=(2, 3), init=16, train=tr),
+        "mobilenet": lambda tr: models.mobilenet_v2(hw=32, classes=16, width_mult=0.5, train=tr),
+    }
+
+
+def _inputs(g, batch, seed=0):
+    rng = np.random.default_rng(seed)
+    ins = {}
+    for gi in g.graph_inputs:
+        if gi.name == "t":
+            t = np.zeros(gi.meta.shape, np.float32)
+            t[np.arange(batch), np.arange(batch) % gi.meta.shape[1]] = 1.0
+            ins["t"] = t
+        else:
+            ins[gi.name] = rng.uniform(-1, 1, gi.meta.shape).astype(np.float32)
+    return ins
+
+
+def _compile(name, train, batch):
+    from paper_2003_10688_b200 import autodiff, graph, partition, passes
+    g = _graphs()[name](train)
+    gi = graph.infer_shapes(g, batch)
+    if train:
+        gi = graph.infer_shapes(autodiff.build_training_graph(gi).graph, batch)
+    gp = passes.run_pipeline(gi)
+    return gp, partition.partition(gp)
+
+
+def _check_units(gp, units, env, dtype, gpu, only_dfp=False):
+    worst = {}
+    for u in units:
+        if only_dfp and u.kind != "dfp":
+            continue
+        # oracle output of this unit from (dtype-rounded) oracle inputs
+        heavy = u.kind == "dnn"
+        sub = {}
+        for nm in u.inputs:
+            sub[nm] = quant(env[nm], dtype) if dtype == 1 else env[nm]
+            if heavy and dtype == 0:
+                sub[nm] = tf32(sub[nm])
+        params = {k: np.asarray(v, np.float64) for k, v in gp.params.items()}
+        if heavy:
+            # the tensor cores read W in the operand precision
+            for pn in u.params:
+                if gp.params[pn].ndim >= 2:
+                    params[pn] = (tf32 if dtype == 0 else (lambda a: quant(a, 1)))(gp.params[pn]).astype(np.float64)
+        local = dict(sub)
+        for nid in u.node_ids:
+            n = gp.find_node(nid)
+            local[nid] = O.eval_node(n, [local[i] for i in n.inputs], params)
+        want = np.asarray(local[u.output], np.float32)
+        fam, got = run_unit(gp, u, env, dtype, gpu)
+        err = O.oracle_err(got, want)
+        if fam in MOVEMENT:
+            assert np.array_equal(got.astype(np.float32), want.astype(np.float32)), (fam, u.output)
+        bar = 1e-2 if (dtype == 1 or heavy) else 1e-5
+        assert err <= bar, (fam, u.output, u.node_ids, err)
+        worst[fam] = max(worst.get(fam, 0.0), err)
+    return worst
+
+
+@pytest.mark.parametrize("name", ["small_cnn", "resnet18", "resnet50", "densenet", "mobilenet"])
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_inference_units(gpu, name, dtype):
+    batch = 3
+    gp, units = _compile(name, False, batch)
+    env = O.run_graph(gp, _inputs(gp, batch))
+    _check_units(gp, units, env, dtype, gpu)
+
+
+@pytest.mark.parametrize("name", ["small_cnn", "resnet18", "resnet50"])
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_training_units(gpu, name, dtype):
+    batch = 4
+    gp, units = _compile(name, True, batch)
+    env = O.run_graph(gp, _inputs(gp, batch))
+    _check_units(gp, units, env, dtype, gpu)
