@@ -212,6 +212,271 @@ __global__ void __launch_bounds__(THREADS) pointwise_kernel(const __grid_constan
 }
 
 // ---------------------------------------------------------------------------------------------
+// FAM_POINTWISE fast path: straight-line chains  y = act( bn0(x0) [+ bn1(x1)] )
+// (the BN / BN+Add / BN+Add+ReLU / BN+ReLU(6) / ReLU units that dominate CNN DFP traffic).
+// Both operands are loaded up front for U vectors per thread (memory-level parallelism); BN
+// coefficients come from L1 (they are tiny and shared by every pixel).
+// ---------------------------------------------------------------------------------------------
+
+struct ChainSpec {
+    int ok = 0;
+    int s0 = -1, s1 = -1;   // input slots
+    int bn0 = -1, bn1 = -1; // BN parameter base index (P[b..b+3]) or -1
+    int add = 0;
+    int act = 0;            // 0 none, 1 relu, 2 relu6
+};
+
+ChainSpec match_chain(const Program& p) {
+    ChainSpec c;
+    int k = 0;
+    auto at = [&](PwOp op) { return k < p.n && p.ins[k].op == op; };
+    if (!at(PW_LD) || p.ins[k].dst != 0) return c;
+    c.s0 = p.ins[k].a;
+    ++k;
+    if (at(PW_BN) && p.ins[k].dst == 0) c.bn0 = p.ins[k++].arg;
+    if (at(PW_LD) && p.ins[k].dst == 1) {
+        c.s1 = p.ins[k].a;
+        ++k;
+        if (at(PW_BN) && p.ins[k].dst == 1) c.bn1 = p.ins[k++].arg;
+        if (!(at(PW_ADD) && p.ins[k].dst == 0 && p.ins[k].a == 0 && p.ins[k].b == 1)) return c;
+        ++k;
+        c.add = 1;
+    }
+    if (at(PW_RELU) && p.ins[k].dst == 0) {
+        c.act = 1;
+        ++k;
+    } else if (at(PW_RELU6) && p.ins[k].dst == 0) {
+        c.act = 2;
+        ++k;
+    }
+    c.ok = (k == p.n);
+    return c;
+}
+
+template <int V>
+__device__ __forceinline__ void bn_apply(float* v, const float* const* P, int b, int c) {
+    float mh[V], ml[V], sc[V], bt[V];
+#pragma unroll
+    for (int i = 0; i < V; i += 4) {
+        *reinterpret_cast<float4*>(mh + i) = __ldg(reinterpret_cast<const float4*>(P[b] + c + i));
+        *reinterpret_cast<float4*>(ml + i) = __ldg(reinterpret_cast<const float4*>(P[b + 1] + c + i));
+        *reinterpret_cast<float4*>(sc + i) = __ldg(reinterpret_cast<const float4*>(P[b + 2] + c + i));
+        *reinterpret_cast<float4*>(bt + i) = __ldg(reinterpret_cast<const float4*>(P[b + 3] + c + i));
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = fmaf((v[i] - mh[i]) - ml[i], sc[i], bt[i]);
+}
+
+template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
+__global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
+    constexpr int V = VEC<T>;
+    constexpr int U = 2;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+    const T* x0 = static_cast<const T*>(a.in[cs.s0]);
+    const T* x1 = ADD ? static_cast<const T*>(a.in[cs.s1]) : nullptr;
+    const int ld0 = a.in_ld[cs.s0], ld1 = ADD ? a.in_ld[cs.s1] : 0;
+    T* out = static_cast<T*>(a.out);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v0 < total; v0 += stride * U) {
+        float r0[U][V], r1[U][V];
+        int64_t pix[U];
+        int cc[U];
+        bool live[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * stride;
+            live[u] = v < total;
+            const int64_t vv = live[u] ? v : v0;
+            pix[u] = vv / cv;
+            cc[u] = static_cast<int>(vv - pix[u] * cv) * V;
+            load16(x0 + pix[u] * ld0 + cc[u], r0[u]);
+            if (ADD) load16(x1 + pix[u] * ld1 + cc[u], r1[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (BN0) bn_apply<V>(r0[u], a.P, cs.bn0, cc[u]);
+            if (ADD) {
+                if (BN1) bn_apply<V>(r1[u], a.P, cs.bn1, cc[u]);
+#pragma unroll
+                for (int i = 0; i < V; ++i) r0[u][i] += r1[u][i];
+            }
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                if (ACT >= 1) r0[u][i] = fmaxf(r0[u][i], 0.f);
+                if (ACT == 2) r0[u][i] = fminf(r0[u][i], 6.f);
+            }
+            if (live[u]) store16(out + pix[u] * a.out_ld + a.out_coff + cc[u], r0[u]);
+        }
+    }
+}
+
+template <typename T, bool BN0, bool ADD, bool BN1>
+void chain_act(const DfpArgs& a, const ChainSpec& c, unsigned grid, cudaStream_t s) {
+    if (c.act == 0) chain_kernel<T, BN0, ADD, BN1, 0><<<grid, THREADS, 0, s>>>(a, c);
+    else if (c.act == 1) chain_kernel<T, BN0, ADD, BN1, 1><<<grid, THREADS, 0, s>>>(a, c);
+    else chain_kernel<T, BN0, ADD, BN1, 2><<<grid, THREADS, 0, s>>>(a, c);
+}
+
+template <typename T>
+bool launch_chain(const DfpArgs& a, cudaStream_t s) {
+    const ChainSpec c = match_chain(a.post);
+    if (!c.ok) return false;
+    if (a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+    if (c.add && (a.in_kind[c.s1] != IN_PIX || a.in_coff[c.s1] != 0)) return false;
+    const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / VEC<T>);
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(work, 2 * THREADS), static_cast<int64_t>(num_sms()) * 8)));
+    const bool b0 = c.bn0 >= 0, b1 = c.bn1 >= 0;
+    if (!c.add) {
+        if (b0) chain_act<T, true, false, false>(a, c, grid, s);
+        else chain_act<T, false, false, false>(a, c, grid, s);
+    } else if (b0 && b1) chain_act<T, true, true, true>(a, c, grid, s);
+    else if (b0) chain_act<T, true, true, false>(a, c, grid, s);
+    else if (b1) chain_act<T, false, true, true>(a, c, grid, s);
+    else chain_act<T, false, true, false>(a, c, grid, s);
+    return true;
+}
+
+// chain value at one pixel (pool / gap source programs)
+template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
+__device__ __forceinline__ void chain_at(const DfpArgs& a, const ChainSpec& cs, int64_t pix, int c, float* v) {
+    constexpr int V = VEC<T>;
+    load16(static_cast<const T*>(a.in[cs.s0]) + pix * a.in_ld[cs.s0] + c, v);
+    if (BN0) bn_apply<V>(v, a.P, cs.bn0, c);
+    if (ADD) {
+        float w[V];
+        load16(static_cast<const T*>(a.in[cs.s1]) + pix * a.in_ld[cs.s1] + c, w);
+        if (BN1) bn_apply<V>(w, a.P, cs.bn1, c);
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] += w[i];
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        if (ACT >= 1) v[i] = fmaxf(v[i], 0.f);
+        if (ACT == 2) v[i] = fminf(v[i], 6.f);
+    }
+}
+
+// Max/Avg pool whose source is a straight-line chain and whose post program is empty.
+template <typename T, bool IS_MAX, bool BN0, int ACT>
+__global__ void __launch_bounds__(THREADS) pool_chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t opix = v / cv;
+        const int c = static_cast<int>(v - opix * cv) * V;
+        const int ow = static_cast<int>(opix % a.OW);
+        const int oh = static_cast<int>((opix / a.OW) % a.OH);
+        const int n = static_cast<int>(opix / (static_cast<int64_t>(a.OW) * a.OH));
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = IS_MAX ? a.min_init : 0.f;
+        int cnt = 0;
+        const int h0 = oh * a.sh - a.ph, w0 = ow * a.sw - a.pw;
+        for (int kh = 0; kh < a.kh; ++kh) {
+            const int ih = h0 + kh;
+            if (ih < 0 || ih >= a.H) continue;
+            for (int kw = 0; kw < a.kw; ++kw) {
+                const int iw = w0 + kw;
+                if (iw < 0 || iw >= a.W) continue;
+                float x[V];
+                chain_at<T, BN0, false, false, ACT>(a, cs, (static_cast<int64_t>(n) * a.H + ih) * a.W + iw, c, x);
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] = IS_MAX ? fmaxf(acc[i], x[i]) : acc[i] + x[i];
+                ++cnt;
+            }
+        }
+        if (!IS_MAX) {
+            const float div = static_cast<float>(a.count_padding ? a.kh * a.kw : cnt);
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] /= div;
+        }
+        store_out<T>(a, opix, c, acc);
+    }
+}
+
+// Global average pool over a straight-line source chain; warps stride over pixels so every
+// thread keeps several independent 16-byte loads in flight.
+template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
+__global__ void __launch_bounds__(THREADS) gap_chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * cv;
+    const int hw = a.H * a.W;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int n = static_cast<int>(v / cv);
+        const int c = static_cast<int>(v - static_cast<int64_t>(n) * cv) * V;
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        int p = 0;
+        for (; p + 4 <= hw; p += 4) {
+            float x[4][V];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                chain_at<T, BN0, ADD, BN1, ACT>(a, cs, static_cast<int64_t>(n) * hw + p + q, c, x[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[i] += x[q][i];
+        }
+        for (; p < hw; ++p) {
+            float x[V];
+            chain_at<T, BN0, ADD, BN1, ACT>(a, cs, static_cast<int64_t>(n) * hw + p, c, x);
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] += x[i];
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] /= static_cast<float>(hw);
+        store_out<T>(a, n, c, acc);
+    }
+}
+
+template <typename T>
+bool launch_pool_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
+    if (a.post.n != 0) return false;
+    const ChainSpec c = match_chain(a.pre);
+    if (!c.ok || c.add || a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+#define SOL_POOL(MX, B, A) pool_chain_kernel<T, MX, B, A><<<grid, THREADS, 0, s>>>(a, c)
+    const bool b = c.bn0 >= 0;
+    if (a.pool_max) {
+        if (b) { if (c.act == 0) SOL_POOL(true, true, 0); else if (c.act == 1) SOL_POOL(true, true, 1); else SOL_POOL(true, true, 2); }
+        else { if (c.act == 0) SOL_POOL(true, false, 0); else if (c.act == 1) SOL_POOL(true, false, 1); else SOL_POOL(true, false, 2); }
+    } else {
+        if (b) { if (c.act == 0) SOL_POOL(false, true, 0); else if (c.act == 1) SOL_POOL(false, true, 1); else SOL_POOL(false, true, 2); }
+        else { if (c.act == 0) SOL_POOL(false, false, 0); else if (c.act == 1) SOL_POOL(false, false, 1); else SOL_POOL(false, false, 2); }
+    }
+#undef SOL_POOL
+    return true;
+}
+
+template <typename T>
+bool launch_gap_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
+    if (a.post.n != 0) return false;
+    const ChainSpec c = match_chain(a.pre);
+    if (!c.ok || a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+    if (c.add && (a.in_kind[c.s1] != IN_PIX || a.in_coff[c.s1] != 0)) return false;
+    const bool b0 = c.bn0 >= 0, b1 = c.bn1 >= 0;
+#define SOL_GAP(B0, AD, B1) \
+    do { \
+        if (c.act == 0) gap_chain_kernel<T, B0, AD, B1, 0><<<grid, THREADS, 0, s>>>(a, c); \
+        else if (c.act == 1) gap_chain_kernel<T, B0, AD, B1, 1><<<grid, THREADS, 0, s>>>(a, c); \
+        else gap_chain_kernel<T, B0, AD, B1, 2><<<grid, THREADS, 0, s>>>(a, c); \
+    } while (0)
+    if (!c.add) { if (b0) SOL_GAP(true, false, false); else SOL_GAP(false, false, false); }
+    else if (b0 && b1) SOL_GAP(true, true, true);
+    else if (b0) SOL_GAP(true, true, false);
+    else if (b1) SOL_GAP(false, true, true);
+    else SOL_GAP(false, true, false);
+#undef SOL_GAP
+    return true;
+}
+
+// ---------------------------------------------------------------------------------------------
 // FAM_POOL (max / avg window reduce over pre-program values)
 // ---------------------------------------------------------------------------------------------
 
@@ -482,6 +747,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
     if (a.C % V != 0) throw std::invalid_argument("dfp: channel count must be a multiple of 16 bytes");
     switch (a.family) {
         case FAM_POINTWISE: {
+            if (launch_chain<T>(a, s)) break;
             const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
             pointwise_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
@@ -489,12 +755,14 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
         case FAM_POOL: {
             const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
             if (a.pre.n == 0) throw std::invalid_argument("dfp: pool without source program");
+            if (launch_pool_chain<T>(a, s, grid_for(work, THREADS))) break;
             if (a.pool_max) pool_kernel<T, true><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             else pool_kernel<T, false><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
         }
         case FAM_GAP: {
             const int64_t work = static_cast<int64_t>(a.N) * (a.C / V);
+            if (launch_gap_chain<T>(a, s, grid_for(work, THREADS))) break;
             gap_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
         }

@@ -160,179 +160,6 @@ __device__ __forceinline__ void store_row16(TO* out, int n, int nout, int ld, co
 }
 
 // ---------------------------------------------------------------------------------------------
-// fprop / dgrad: A K-major gathered rows, B K-major packed weights
-// ---------------------------------------------------------------------------------------------
-
-template <typename T, typename TO, int BN, int MODE>
-__global__ void __launch_bounds__(THREADS, 1) igemm_kernel(IgemmArgs a) {
-    constexpr int VEC = 16 / sizeof(T);
-    constexpr int BK = ROWB / sizeof(T);
-    constexpr int A_BYTES = BM * ROWB;
-    constexpr int B_BYTES = BN * ROWB;
-    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    constexpr int STAGES = stages_for<STAGE_BYTES>();
-    constexpr uint32_t TCOLS = tmem_cols<BN>();
-    constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
-    constexpr int KSTEP_BYTES = 32;  // K=16 bf16 / K=8 tf32 per MMA instruction
-    static_assert(BN % 16 == 0 && BN <= 256, "bad BN");
-
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES);
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * BN;
-    const int num_kb = a.K_pad / BK;
-    const int M = a.N * a.OH * a.OW;
-
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&mbar[s]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-    }
-    if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_d = *tmem_slot;
-
-    // Per-thread gather rows: chunk j of rows rbase + 16*i.
-    const int j = tid & 7;
-    const int rbase = tid >> 3;
-    int rn[8], rh[8], rw[8];
-    const int ohw = a.OH * a.OW;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int m = m0 + rbase + 16 * i;
-        if (m < M) {
-            const int n = m / ohw;
-            const int rem = m - n * ohw;
-            const int oh = rem / a.OW;
-            const int ow = rem - oh * a.OW;
-            rn[i] = n;
-            if (MODE == IG_FPROP) {
-                rh[i] = oh * a.sh - a.ph;
-                rw[i] = ow * a.sw - a.pw;
-            } else {
-                rh[i] = oh + a.ph;
-                rw[i] = ow + a.pw;
-            }
-        } else {
-            rn[i] = -1;
-            rh[i] = rw[i] = 0;
-        }
-    }
-    const T* src = static_cast<const T*>(a.src);
-    const T* wt = static_cast<const T*>(a.wt);
-    const int ntaps = a.kh * a.kw;
-
-    auto load_stage = [&](int slot, int kb) {
-        uint8_t* sa = smem + slot * STAGE_BYTES;
-        uint8_t* sb = sa + A_BYTES;
-        const int k = kb * BK + j * VEC;
-        const int tap = k / a.SC;
-        const int c = k - tap * a.SC;
-        const int dkh = tap / a.kw;
-        const int dkw = tap - dkh * a.kw;
-        const bool tap_ok = tap < ntaps;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int r = rbase + 16 * i;
-            bool ok = tap_ok && rn[i] >= 0;
-            int hh, ww;
-            if (MODE == IG_FPROP) {
-                hh = rh[i] + dkh;
-                ww = rw[i] + dkw;
-            } else {
-                const int nh = rh[i] - dkh, nw = rw[i] - dkw;
-                ok = ok && nh >= 0 && nw >= 0 && (nh % a.sh) == 0 && (nw % a.sw) == 0;
-                hh = nh / a.sh;
-                ww = nw / a.sw;
-            }
-            ok = ok && hh >= 0 && hh < a.SH && ww >= 0 && ww < a.SW;
-            const T* g = ok ? src + ((static_cast<int64_t>(rn[i]) * a.SH + hh) * a.SW + ww) * a.SC + c : src;
-            cp_async16(smem_u32(sa + r * ROWB + ((j ^ (r & 7)) << 4)), g, ok);
-        }
-#pragma unroll
-        for (int i = 0; i < BN / 16; ++i) {
-            const int r = rbase + 16 * i;
-            const int row = n0 + r;
-            const bool ok = row < a.Nout;
-            const T* g = ok ? wt + static_cast<int64_t>(row) * a.K_pad + kb * BK + j * VEC : wt;
-            cp_async16(smem_u32(sb + r * ROWB + ((j ^ (r & 7)) << 4)), g, ok);
-        }
-    };
-
-    // prologue
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < num_kb) load_stage(s, s);
-        cp_async_commit();
-    }
-
-    for (int kb = 0; kb < num_kb; ++kb) {
-        const int nk = kb + STAGES - 1;
-        if (nk < num_kb) {
-            const int ns = nk % STAGES;
-            if (kb >= 1) mbar_wait(smem_u32(&mbar[ns]), ((kb - 1) / STAGES) & 1);  // MMA(kb-1) freed it
-            load_stage(ns, nk);
-        }
-        cp_async_commit();
-        cp_async_wait<STAGES - 1>();
-        fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            const int slot = kb % STAGES;
-            const uint32_t a_addr = smem_u32(smem + slot * STAGE_BYTES);
-            const uint32_t b_addr = a_addr + A_BYTES;
-#pragma unroll
-            for (int k = 0; k < ROWB / KSTEP_BYTES; ++k) {
-                const uint64_t ad = sw128_desc(a_addr + k * KSTEP_BYTES, 16, 1024);
-                const uint64_t bd = sw128_desc(b_addr + k * KSTEP_BYTES, 16, 1024);
-                mma<T>(tmem_d, ad, bd, IDESC, (kb | k) != 0);
-            }
-            mma_commit(smem_u32(&mbar[slot]));
-        }
-    }
-    {
-        const int last = num_kb - 1;
-        mbar_wait(smem_u32(&mbar[last % STAGES]), (last / STAGES) & 1);
-    }
-    tc_fence_after();
-
-    // epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
-    const int row = warp * 32 + lane;
-    const int m = m0 + row;
-    TO* out = static_cast<TO*>(a.out);
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem_d + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
-        const int n = n0 + c0;
-        if (m < M && n < a.ldo) {
-            float f[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                float x = __uint_as_float(v[q]);
-                if (a.bias != nullptr && n + q < a.Nout) x += __ldg(a.bias + n + q);
-                if (a.relu) x = fmaxf(x, 0.0f);
-                f[q] = x;
-            }
-            store_row16<TO>(out + static_cast<int64_t>(m) * a.ldo + n, n, a.Nout, a.ldo, f);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc<TCOLS>(tmem_d);
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
 // wgrad: D[Cout][Ncol] += dy^T[Cout][P] * Xcol^T[P][Ncol]; both operands MN-major in smem.
 // Tile layout per operand: [mn-block of 64 elems][k-group of 8 pixels][8 rows][128 B]
 //   -> LBO (mn-block stride) = (BK/8)*1024 B, SBO (k-group stride) = 1024 B.
@@ -516,35 +343,340 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restr
 }
 
 // ---------------------------------------------------------------------------------------------
-// host dispatch
+// Warp-specialised persistent implicit GEMM (fprop / dgrad).
+//
+//   warps 0-3  producers: 16-byte cp.async gathers of the A tile (im2col / transposed-conv
+//              gather with zero-fill), cp.async.mbarrier.arrive.noinc on the stage's full barrier;
+//              thread 0 also issues the TMA load of the B (packed weight) tile. When A is a plain
+//              [M][C] matrix (1x1, stride 1, no padding) thread 0 TMA-loads A as well.
+//   warps 4-7  epilogue: TMEM -> registers (tcgen05.ld, warp w%4 owns lanes 32(w%4)..), bias,
+//              NHWC stores; releases the accumulator stage.
+//   warp 8     TMEM allocation + the single-thread tcgen05.mma issuer.
+// Barriers: full[S] (128 cp.async arrivals + 1 expect_tx), empty[S] (tcgen05.commit),
+// tmem_full[2] (tcgen05.commit), tmem_empty[2] (128 epilogue arrivals). Two TMEM accumulator
+// stages let the epilogue of tile i overlap the mainloop of tile i+1.
 // ---------------------------------------------------------------------------------------------
 
+constexpr int WS_THREADS = 288;
+constexpr int IG_FPROP_TMA = 2;  // internal mode: A via TMA (1x1, stride 1, pad 0 fprop)
+
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(addr));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t addr, uint32_t bytes) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(addr),
+                 "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t addr) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(addr));
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(mbar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+template <int BN>
+constexpr uint32_t ws_tmem_cols() {
+    return 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+}
+
 template <typename T, typename TO, int BN, int MODE>
-void launch_igemm_t(const IgemmArgs& a, cudaStream_t s) {
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
+                    const __grid_constant__ CUtensorMap tmap_a) {
+    constexpr int VEC = 16 / sizeof(T);
+    constexpr int BK = ROWB / sizeof(T);
+    constexpr int A_BYTES = BM * ROWB;
+    constexpr int B_BYTES = BN * ROWB;
+    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    constexpr int STAGES = stages_for<STAGE_BYTES>();
+    constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
+    constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
+    constexpr int KSTEP_BYTES = 32;
+    constexpr bool A_TMA = MODE == IG_FPROP_TMA;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int M = a.N * a.OH * a.OW;
+    const int m_tiles = (M + BM - 1) / BM;
+    const int n_tiles = (a.Nout + BN - 1) / BN;
+    const int tiles = m_tiles * n_tiles;
+    const int num_kb = a.K_pad / BK;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), A_TMA ? 1 : 129);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(&tfull[s]), 1);
+            mbar_init(smem_u32(&tempty[s]), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        tma_prefetch(&tmap_b);
+        if (A_TMA) tma_prefetch(&tmap_a);
+    }
+    if (warp == 8) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < 4) {
+        // ------------------------------------------------------------------ producers
+        const T* src = static_cast<const T*>(a.src);
+        const int j = tid & 7;
+        const int rbase = tid >> 3;
+        const int ohw = a.OH * a.OW;
+        const int ntaps = a.kh * a.kw;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int m0 = (t / n_tiles) * BM;
+            const int n0 = (t % n_tiles) * BN;
+            int rn[8], rh[8], rw[8];
+            if (!A_TMA) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int m = m0 + rbase + 16 * i;
+                    if (m < M) {
+                        const int n = m / ohw;
+                        const int rem = m - n * ohw;
+                        const int oh = rem / a.OW;
+                        const int ow = rem - oh * a.OW;
+                        rn[i] = n;
+                        if (MODE == IG_FPROP) {
+                            rh[i] = oh * a.sh - a.ph;
+                            rw[i] = ow * a.sw - a.pw;
+                        } else {
+                            rh[i] = oh + a.ph;
+                            rw[i] = ow + a.pw;
+                        }
+                    } else {
+                        rn[i] = -1;
+                        rh[i] = rw[i] = 0;
+                    }
+                }
+            }
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                uint8_t* sa = smem + stage * STAGE_BYTES;
+                uint8_t* sb = sa + A_BYTES;
+                if (tid == 0) {
+                    mbar_arrive_tx(smem_u32(&full[stage]), A_TMA ? (A_BYTES + B_BYTES) : B_BYTES);
+                    tma_load_2d(smem_u32(sb), &tmap_b, kb * BK, n0, smem_u32(&full[stage]));
+                    if (A_TMA) tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
+                }
+                if (!A_TMA) {
+                    const int k = kb * BK + j * VEC;
+                    const int tap = k / a.SC;
+                    const int c = k - tap * a.SC;
+                    const int dkh = tap / a.kw;
+                    const int dkw = tap - dkh * a.kw;
+                    const bool tap_ok = tap < ntaps;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = rbase + 16 * i;
+                        bool ok = tap_ok && rn[i] >= 0;
+                        int hh, ww;
+                        if (MODE == IG_FPROP) {
+                            hh = rh[i] + dkh;
+                            ww = rw[i] + dkw;
+                        } else {
+                            const int nh = rh[i] - dkh, nw = rw[i] - dkw;
+                            ok = ok && nh >= 0 && nw >= 0 && (nh % a.sh) == 0 && (nw % a.sw) == 0;
+                            hh = nh / a.sh;
+                            ww = nw / a.sw;
+                        }
+                        ok = ok && hh >= 0 && hh < a.SH && ww >= 0 && ww < a.SW;
+                        const T* g = ok ? src + ((static_cast<int64_t>(rn[i]) * a.SH + hh) * a.SW + ww) * a.SC + c : src;
+                        cp_async16(smem_u32(sa + r * ROWB + ((j ^ (r & 7)) << 4)), g, ok);
+                    }
+                    cp_async_arrive_noinc(smem_u32(&full[stage]));
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        if (!A_TMA) cp_async_wait<0>();
+    } else if (warp == 8) {
+        // ------------------------------------------------------------------ MMA issuer
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(smem_u32(&full[stage]), phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < ROWB / KSTEP_BYTES; ++k) {
+                        const uint64_t ad = sw128_desc(a_addr + k * KSTEP_BYTES, 16, 1024);
+                        const uint64_t bd = sw128_desc(b_addr + k * KSTEP_BYTES, 16, 1024);
+                        mma<T>(dcol, ad, bd, IDESC, (kb | k) != 0);
+                    }
+                    mma_commit(smem_u32(&empty[stage]));
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (lane == 0) mma_commit(smem_u32(&tfull[acc]));
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue (warps 4-7)
+        const int q = warp & 3;  // TMEM lane quarter
+        const int row = q * 32 + lane;
+        TO* out = static_cast<TO*>(a.out);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int m0 = (t / n_tiles) * BM;
+            const int n0 = (t % n_tiles) * BN;
+            mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+            tc_fence_after();
+            const int m = m0 + row;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c0), v);
+                const int n = n0 + c0;
+                if (m < M && n < a.ldo) {
+                    float f[16];
+#pragma unroll
+                    for (int qq = 0; qq < 16; ++qq) {
+                        float x = __uint_as_float(v[qq]);
+                        if (a.bias != nullptr && n + qq < a.Nout) x += __ldg(a.bias + n + qq);
+                        if (a.relu) x = fmaxf(x, 0.0f);
+                        f[qq] = x;
+                    }
+                    store_row16<TO>(out + static_cast<int64_t>(m) * a.ldo + n, n, a.Nout, a.ldo, f);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(smem_u32(&tempty[acc]));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc<TCOLS>(tmem_base);
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link dependency).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SOL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D row-major [rows][cols] tensor, box = [box_rows][128 bytes], 128B swizzle (UMMA K-major atom).
+CUtensorMap make_tmap_2d(const void* base, int dtype, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
+                         uint32_t box_rows) {
+    CUtensorMap m;
+    const uint32_t es = dtype == DT_BF16 ? 2 : 4;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {row_stride_elems * es};
+    cuuint32_t box[2] = {128 / es, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                   2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    return m;
+}
+
+template <typename T, typename TO, int BN, int MODE>
+void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     constexpr int STAGE_BYTES = BM * ROWB + BN * ROWB;
     constexpr int STAGES = stages_for<STAGE_BYTES>();
-    constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + STAGES * 8 + 16;
+    constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 4) * 8 + 16;
     static std::once_flag once;
     std::call_once(once, [] {
-        SOL_CUDA(cudaFuncSetAttribute(igemm_kernel<T, TO, BN, MODE>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM));
     });
     const int M = a.N * a.OH * a.OW;
-    dim3 grid(static_cast<unsigned>(ceil_div(M, BM)), static_cast<unsigned>(ceil_div(a.Nout, BN)));
-    igemm_kernel<T, TO, BN, MODE><<<grid, THREADS, SMEM, s>>>(a);
+    const int dt = sizeof(T) == 2 ? DT_BF16 : DT_F32;
+    const int n_rows = static_cast<int>(ceil_div(a.Nout, BN)) * BN;  // packed B has >= Nout rows
+    CUtensorMap tb = make_tmap_2d(a.wt, dt, a.K_pad, static_cast<uint64_t>(a.Nout), a.K_pad, BN);
+    (void)n_rows;
+    CUtensorMap ta = tb;
+    if (MODE == IG_FPROP_TMA) ta = make_tmap_2d(a.src, dt, a.SC, static_cast<uint64_t>(M), a.SC, BM);
+    const int tiles = static_cast<int>(ceil_div(M, BM) * ceil_div(a.Nout, BN));
+    const int grid = std::min(tiles, num_sms());
+    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta);
     SOL_CUDA(cudaGetLastError());
 }
 
 template <typename T, typename TO, int MODE>
-void dispatch_bn(const IgemmArgs& a, cudaStream_t s) {
+void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
     switch (igemm_block_n(a.Nout)) {
-        case 16: return launch_igemm_t<T, TO, 16, MODE>(a, s);
-        case 32: return launch_igemm_t<T, TO, 32, MODE>(a, s);
-        case 64: return launch_igemm_t<T, TO, 64, MODE>(a, s);
-        case 128: return launch_igemm_t<T, TO, 128, MODE>(a, s);
-        default: return launch_igemm_t<T, TO, 256, MODE>(a, s);
+        case 16: return launch_ws_t<T, TO, 16, MODE>(a, s);
+        case 32: return launch_ws_t<T, TO, 32, MODE>(a, s);
+        case 64: return launch_ws_t<T, TO, 64, MODE>(a, s);
+        case 128: return launch_ws_t<T, TO, 128, MODE>(a, s);
+        default: return launch_ws_t<T, TO, 256, MODE>(a, s);
     }
 }
+
+template <typename T, typename TO>
+void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
+    const bool plain = a.mode == IG_FPROP && a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 &&
+                       a.pw == 0 && a.K_pad == a.SC;
+    if (plain) dispatch_ws<T, TO, IG_FPROP_TMA>(a, s);
+    else if (a.mode == IG_FPROP) dispatch_ws<T, TO, IG_FPROP>(a, s);
+    else dispatch_ws<T, TO, IG_DGRAD>(a, s);
+}
+
+// ---------------------------------------------------------------------------------------------
+// host dispatch
+// ---------------------------------------------------------------------------------------------
 
 template <typename T, int BN>
 void launch_wgrad_t(const WgradArgs& a, int ncol, int splits, int kb_per_split, cudaStream_t s) {
@@ -597,17 +729,11 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
     if (a.K_pad % bk != 0) throw std::invalid_argument("igemm: K_pad must be a multiple of the k-block");
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.dtype == DT_BF16) {
-        if (a.out_dtype == DT_BF16) {
-            if (a.mode == IG_FPROP) dispatch_bn<__nv_bfloat16, __nv_bfloat16, IG_FPROP>(a, s);
-            else dispatch_bn<__nv_bfloat16, __nv_bfloat16, IG_DGRAD>(a, s);
-        } else {
-            if (a.mode == IG_FPROP) dispatch_bn<__nv_bfloat16, float, IG_FPROP>(a, s);
-            else dispatch_bn<__nv_bfloat16, float, IG_DGRAD>(a, s);
-        }
+        if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
+        else dispatch_mode<__nv_bfloat16, float>(a, s);
     } else {
         if (a.out_dtype != DT_F32) throw std::invalid_argument("igemm: tf32 path writes f32");
-        if (a.mode == IG_FPROP) dispatch_bn<float, float, IG_FPROP>(a, s);
-        else dispatch_bn<float, float, IG_DGRAD>(a, s);
+        dispatch_mode<float, float>(a, s);
     }
 }
 

@@ -375,6 +375,59 @@ def model_to_json(g: ModelGraph) -> str:
     return json.dumps(j)
 
 
+def _pair(v):
+    return (int(v), int(v)) if isinstance(v, (int, float)) else (int(v[0]), int(v[1]))
+
+
+def model_from_json(text: str, weights: Optional[bytes] = None) -> ModelGraph:
+    """Parses the reference model schema (src/model_io.cpp:213-260, attrs :60-100) and binds
+    SOLW weights; validates and topologically sorts like load_model (:287-294)."""
+    j = json.loads(text)
+    g = ModelGraph()
+    for inp in j["inputs"]:
+        tags = [(d["tag"], d["index"]) for d in inp["dims"]]
+        ext = tuple(0 if d["extent"] == "B" else int(d["extent"]) for d in inp["dims"])
+        kind = "nchw" if tags == [("N", 0), ("C", 0), ("P", 1), ("P", 0)] else \
+            "nc" if tags == [("N", 0), ("C", 0)] else None
+        if kind is None:
+            raise MalformedModelError(f"unsupported input dims {tags}")
+        g.graph_inputs.append(GraphInput(inp["name"], Meta(kind, ext)))
+    for nj in j["nodes"]:
+        op = nj["op"]
+        if op not in USER_FACING:
+            raise MalformedModelError(f"unsupported op '{op}'")
+        aj = nj.get("attrs", {})
+        a = Attrs()
+        if op == "Conv2d":
+            a.out_channels = int(aj["out_channels"])
+            a.kh, a.kw = _pair(aj["kernel"])
+            a.sh, a.sw = _pair(aj.get("stride", 1))
+            a.ph, a.pw = _pair(aj.get("padding", 0))
+            a.groups = int(aj.get("groups", 1))
+            a.has_bias = bool(aj.get("bias", True))
+        elif op == "Linear":
+            a.out_features = int(aj["out_features"])
+            a.has_bias = bool(aj.get("bias", True))
+        elif op in ("MaxPool2d", "AvgPool2d"):
+            a.kh, a.kw = _pair(aj["kernel"])
+            a.sh, a.sw = _pair(aj.get("stride", [a.kh, a.kw]))   # stride defaults to kernel (:82)
+            a.ph, a.pw = _pair(aj.get("padding", 0))
+            if op == "MaxPool2d":
+                a.min_init = float(aj.get("min_init", -math.inf))
+            else:
+                a.count_padding = bool(aj.get("count_padding", False))
+        elif op == "BatchNorm2d":
+            a.eps = float(aj.get("eps", 1e-5))
+            a.momentum = float(aj.get("momentum", 0.1))
+        a.training = bool(aj.get("training", False))
+        g.nodes.append(LayerNode(nj["id"], op, a, list(nj.get("inputs", [])), list(nj.get("params", []))))
+    g.outputs = list(j["outputs"])
+    if weights is not None:
+        g.params = weights_from_bytes(weights)
+    g.validate_and_sort()
+    return g
+
+
 def weights_to_bytes(params: Dict[str, np.ndarray]) -> bytes:
     """SOLW v1 (src/model_io.cpp:339-364): name-sorted, u16 name len, u8 dtype, u8 rank, u32 dims."""
     out = bytearray(b"SOLW")
