@@ -42,51 +42,75 @@ __device__ __forceinline__ void load_in(const DfpArgs& a, int slot, int64_t pix,
     load16(base, v);
 }
 
+// Register-resident interpreter: the four value registers are separate named arrays and every
+// dynamic register operand is resolved by a switch, so nothing is indexed at run time and the
+// register file never spills to local memory.
+template <int V, typename F>
+__device__ __forceinline__ void with_reg(int d, float (&R0)[V], float (&R1)[V], float (&R2)[V], float (&R3)[V],
+                                         F&& f) {
+    switch (d) {
+        case 0: f(R0); break;
+        case 1: f(R1); break;
+        case 2: f(R2); break;
+        default: f(R3); break;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void run_prog(const Program& pg, const DfpArgs& a, int64_t pix, int n,
                                          int c, float (&r)[NREG][VEC<T>]) {
     constexpr int V = VEC<T>;
+    float R0[V], R1[V], R2[V], R3[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        R0[i] = r[0][i];
+        R1[i] = r[1][i];
+        R2[i] = 0.f;
+        R3[i] = 0.f;
+    }
     for (int k = 0; k < pg.n; ++k) {
         const PwInstr ins = pg.ins[k];
-        switch (ins.op) {
-            case PW_LD: {
-                float t[V];
-                load_in<T>(a, ins.a, pix, n, c, t);
+        const int op = ins.op;
+        float ta[V], tb[V];
+        if (op == PW_LD) {
+            load_in<T>(a, ins.a, pix, n, c, ta);
+            with_reg<V>(ins.dst, R0, R1, R2, R3, [&](float (&x)[V]) {
 #pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
+                for (int i = 0; i < V; ++i) x[i] = ta[i];
+            });
+            continue;
+        }
+        if (op == PW_PARAM) {
+            const float* s0 = a.P[ins.arg] + c;
+            with_reg<V>(ins.dst, R0, R1, R2, R3, [&](float (&x)[V]) {
 #pragma unroll
-                        for (int i = 0; i < V; ++i) r[d][i] = t[i];
-                    }
-                break;
-            }
+                for (int i = 0; i < V; ++i) x[i] = __ldg(s0 + i);
+            });
+            continue;
+        }
+        // read operands (a, b) by value
+        with_reg<V>(ins.dst, R0, R1, R2, R3, [&](float (&x)[V]) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) ta[i] = x[i];
+        });
+        if (op == PW_ADD || op == PW_MASK || op == PW_MASK6 || op == PW_MOV) {
+            with_reg<V>(ins.a, R0, R1, R2, R3, [&](float (&x)[V]) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) ta[i] = x[i];
+            });
+        }
+        if (op == PW_ADD || op == PW_MASK || op == PW_MASK6 || op == PW_AXPBY) {
+            with_reg<V>(ins.b, R0, R1, R2, R3, [&](float (&x)[V]) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) tb[i] = x[i];
+            });
+        }
+        switch (op) {
             case PW_AFF: {
                 const float* s0 = a.P[ins.arg] + c;
                 const float* s1 = a.P[ins.arg + 1] + c;
-                float m[V], b[V];
 #pragma unroll
-                for (int i = 0; i < V; i += 4) {
-                    float4 x = __ldg(reinterpret_cast<const float4*>(s0 + i));
-                    float4 y = __ldg(reinterpret_cast<const float4*>(s1 + i));
-                    m[i] = x.x; m[i + 1] = x.y; m[i + 2] = x.z; m[i + 3] = x.w;
-                    b[i] = y.x; b[i + 1] = y.y; b[i + 2] = y.z; b[i + 3] = y.w;
-                }
-#pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) r[d][i] = fmaf(r[d][i], m[i], b[i]);
-                    }
-                break;
-            }
-            case PW_PARAM: {
-                const float* s0 = a.P[ins.arg] + c;
-#pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) r[d][i] = __ldg(s0 + i);
-                    }
+                for (int i = 0; i < V; ++i) ta[i] = fmaf(ta[i], __ldg(s0 + i), __ldg(s1 + i));
                 break;
             }
             case PW_BN: {
@@ -95,86 +119,54 @@ __device__ __forceinline__ void run_prog(const Program& pg, const DfpArgs& a, in
                 const float* sc = a.P[ins.arg + 2] + c;
                 const float* bt = a.P[ins.arg + 3] + c;
 #pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i)
-                            r[d][i] = fmaf((r[d][i] - __ldg(mh + i)) - __ldg(ml + i), __ldg(sc + i), __ldg(bt + i));
-                    }
+                for (int i = 0; i < V; ++i)
+                    ta[i] = fmaf((ta[i] - __ldg(mh + i)) - __ldg(ml + i), __ldg(sc + i), __ldg(bt + i));
                 break;
             }
             case PW_AXPBY: {
-                float tb[V];
-#pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.b == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) tb[i] = r[d][i];
-                    }
                 const float* s0 = a.P[ins.arg] + c;
                 const float* s1 = a.P[ins.arg + 1] + c;
                 const float* s2 = a.P[ins.arg + 2] + c;
 #pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i)
-                            r[d][i] = fmaf(r[d][i], __ldg(s0 + i), fmaf(tb[i], __ldg(s1 + i), __ldg(s2 + i)));
-                    }
+                for (int i = 0; i < V; ++i) ta[i] = fmaf(ta[i], __ldg(s0 + i), fmaf(tb[i], __ldg(s1 + i), __ldg(s2 + i)));
                 break;
             }
             case PW_RELU:
+#pragma unroll
+                for (int i = 0; i < V; ++i) ta[i] = fmaxf(ta[i], 0.f);
+                break;
             case PW_RELU6:
-            case PW_SCALE: {
 #pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) {
-                            float x = r[d][i];
-                            if (ins.op == PW_SCALE) x *= ins.imm;
-                            else {
-                                x = x > 0.f ? x : 0.f;
-                                if (ins.op == PW_RELU6) x = x < 6.f ? x : 6.f;
-                            }
-                            r[d][i] = x;
-                        }
-                    }
+                for (int i = 0; i < V; ++i) ta[i] = fminf(fmaxf(ta[i], 0.f), 6.f);
                 break;
-            }
+            case PW_SCALE:
+#pragma unroll
+                for (int i = 0; i < V; ++i) ta[i] *= ins.imm;
+                break;
             case PW_ADD:
-            case PW_MASK:
-            case PW_MASK6:
-            case PW_MOV: {
-                float ta[V], tb[V];
 #pragma unroll
-                for (int d = 0; d < NREG; ++d) {
-                    if (ins.a == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) ta[i] = r[d][i];
-                    }
-                    if (ins.b == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) tb[i] = r[d][i];
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < V; ++i) {
-                    if (ins.op == PW_ADD) ta[i] = ta[i] + tb[i];
-                    else if (ins.op == PW_MASK) ta[i] = tb[i] > 0.f ? ta[i] : 0.f;
-                    else if (ins.op == PW_MASK6) ta[i] = (tb[i] > 0.f && tb[i] < 6.f) ? ta[i] : 0.f;
-                }
-#pragma unroll
-                for (int d = 0; d < NREG; ++d)
-                    if (ins.dst == d) {
-#pragma unroll
-                        for (int i = 0; i < V; ++i) r[d][i] = ta[i];
-                    }
+                for (int i = 0; i < V; ++i) ta[i] += tb[i];
                 break;
-            }
-            default:
+            case PW_MASK:
+#pragma unroll
+                for (int i = 0; i < V; ++i) ta[i] = tb[i] > 0.f ? ta[i] : 0.f;
+                break;
+            case PW_MASK6:
+#pragma unroll
+                for (int i = 0; i < V; ++i) ta[i] = (tb[i] > 0.f && tb[i] < 6.f) ? ta[i] : 0.f;
+                break;
+            default:  // PW_MOV
                 break;
         }
+        with_reg<V>(ins.dst, R0, R1, R2, R3, [&](float (&x)[V]) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) x[i] = ta[i];
+        });
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        r[0][i] = R0[i];
+        r[1][i] = R1[i];
     }
 }
 
@@ -595,6 +587,132 @@ __global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__
 // FAM_CHAN_REDUCE: per-channel S1 = sum r0, S2 = sum r0*r1 over all pixels of the source grid
 // ---------------------------------------------------------------------------------------------
 
+// Straight-line reductions for the programs the BN / bias-gradient modules emit:
+//   RED_STATS  r0 = x - shift            -> S1 = sum r0, S2 = sum r0^2    (batch statistics)
+//   RED_SUM    r0 = d                     -> S1 = sum d,  S2 = sum d^2     (bias / beta grads)
+//   RED_DGAMMA r0 = d, r1 = xhat(x)       -> S1 = sum d,  S2 = sum d*xhat  (BN backward)
+// Each thread accumulates 16 pixels in f32 (4 loads in flight) and folds them into f64.
+enum RedMode { RED_STATS = 0, RED_SUM = 1, RED_DGAMMA = 2 };
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(THREADS) reduce_fast_kernel(const __grid_constant__ DfpArgs a, int s0, int s1,
+                                                              int parg) {
+    constexpr int V = VEC<T>;
+    __shared__ double red[THREADS * V * 2];
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int tid = threadIdx.x;
+    const int row = tid / cvb;
+    const int cvi = tid - row * cvb;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const int64_t P = static_cast<int64_t>(a.N) * a.H * a.W;
+    const int64_t per = ceil_div(P, gridDim.x);
+    const int64_t p0 = blockIdx.x * per;
+    const int64_t p1 = min(P, p0 + per);
+    double d1[V], d2[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) d1[i] = d2[i] = 0.0;
+    const bool active = row < rows && (blockIdx.y * cvb + cvi) < cv_total;
+    if (active) {
+        const T* x0 = static_cast<const T*>(a.in[s0]);
+        const T* x1 = MODE == RED_DGAMMA ? static_cast<const T*>(a.in[s1]) : nullptr;
+        const int ld0 = a.in_ld[s0], ld1 = MODE == RED_DGAMMA ? a.in_ld[s1] : 0;
+        float q0[V], q1[V], q2[V], q3[V];  // per-channel constants
+#pragma unroll
+        for (int i = 0; i < V; ++i) q0[i] = q1[i] = q2[i] = q3[i] = 0.f;
+        if (MODE == RED_STATS) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) q0[i] = __ldg(a.P[parg] + c + i);
+        } else if (MODE == RED_DGAMMA) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                q0[i] = __ldg(a.P[parg] + c + i);
+                q1[i] = __ldg(a.P[parg + 1] + c + i);
+                q2[i] = __ldg(a.P[parg + 2] + c + i);
+                q3[i] = __ldg(a.P[parg + 3] + c + i);
+            }
+        }
+        for (int64_t pb = p0 + row; pb < p1; pb += static_cast<int64_t>(rows) * 16) {
+            float f1[V], f2[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) f1[i] = f2[i] = 0.f;
+#pragma unroll 4
+            for (int u = 0; u < 16; ++u) {
+                const int64_t p = pb + static_cast<int64_t>(u) * rows;
+                if (p >= p1) break;
+                float v[V];
+                load16(x0 + p * ld0 + c, v);
+                if (MODE == RED_DGAMMA) {
+                    float w[V];
+                    load16(x1 + p * ld1 + c, w);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        const float xh = fmaf((w[i] - q0[i]) - q1[i], q2[i], q3[i]);
+                        f1[i] += v[i];
+                        f2[i] = fmaf(v[i], xh, f2[i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        const float r = MODE == RED_STATS ? v[i] - q0[i] : v[i];
+                        f1[i] += r;
+                        f2[i] = fmaf(r, r, f2[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                d1[i] += static_cast<double>(f1[i]);
+                d2[i] += static_cast<double>(f2[i]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        red[(tid * V + i) * 2] = d1[i];
+        red[(tid * V + i) * 2 + 1] = d2[i];
+    }
+    __syncthreads();
+    if (row == 0 && active) {
+        for (int rr = 1; rr < rows; ++rr) {
+            const int t2 = rr * cvb + cvi;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                d1[i] += red[(t2 * V + i) * 2];
+                d2[i] += red[(t2 * V + i) * 2 + 1];
+            }
+        }
+        double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * a.C + c) * 2;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            dst[2 * i] = d1[i];
+            dst[2 * i + 1] = d2[i];
+        }
+    }
+}
+
+// Matches the reduction programs emitted by module.cpp; returns false for anything else.
+template <typename T>
+bool launch_reduce_fast(const DfpArgs& a, dim3 grid, cudaStream_t s) {
+    const Program& p = a.pre;
+    auto is = [&](int k, PwOp op, int dst) { return k < p.n && p.ins[k].op == op && p.ins[k].dst == dst; };
+    if (p.n == 5 && is(0, PW_LD, 0) && is(1, PW_PARAM, 1) && is(2, PW_SCALE, 1) && p.ins[2].imm == -1.f &&
+        is(3, PW_ADD, 0) && p.ins[3].a == 0 && p.ins[3].b == 1 && is(4, PW_MOV, 1) && p.ins[4].a == 0) {
+        reduce_fast_kernel<T, RED_STATS><<<grid, THREADS, 0, s>>>(a, p.ins[0].a, 0, p.ins[1].arg);
+        return true;
+    }
+    if (p.n == 2 && is(0, PW_LD, 0) && is(1, PW_MOV, 1) && p.ins[1].a == 0) {
+        reduce_fast_kernel<T, RED_SUM><<<grid, THREADS, 0, s>>>(a, p.ins[0].a, 0, 0);
+        return true;
+    }
+    if (p.n == 3 && is(0, PW_LD, 0) && is(1, PW_LD, 1) && is(2, PW_BN, 1)) {
+        reduce_fast_kernel<T, RED_DGAMMA><<<grid, THREADS, 0, s>>>(a, p.ins[0].a, p.ins[1].a, p.ins[2].arg);
+        return true;
+    }
+    return false;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_constant__ DfpArgs a) {
     constexpr int V = VEC<T>;
@@ -775,6 +893,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
             const int cv_total = a.C / V;
             const int cvb = std::min(cv_total, THREADS);
             dim3 grid(static_cast<unsigned>(a.reduce_blocks), static_cast<unsigned>(ceil_div(cv_total, cvb)));
+            if (launch_reduce_fast<T>(a, grid, s)) break;
             chan_reduce_kernel<T><<<grid, THREADS, 0, s>>>(a);
             break;
         }
@@ -914,12 +1033,13 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
         if (a.out1) a.out1[c] = static_cast<float>(s2);
         if (a.coef) {
             const double g = a.gamma[c];
-            const double mean = a.stats[c], rstd = a.stats[a.C + c];
+            const double rstd = a.stats[a.C + c];
             const double gr = g * rstd;
-            // dx = dy * gr + x * (-gr*rstd*s2/m) + (-gr*s1/m + gr*mean*rstd*s2/m)
+            // dx = gr*dy - gr*xhat*s2/m - gr*s1/m, with xhat = (x - mean)*rstd formed accurately
+            // by the apply program (mean split hi/lo) so no |mean| >> std cancellation occurs
             a.coef[c] = static_cast<float>(gr);
-            a.coef[a.C + c] = static_cast<float>(-gr * rstd * s2 / m);
-            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m + gr * mean * rstd * s2 / m);
+            a.coef[a.C + c] = static_cast<float>(-gr * s2 / m);
+            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
         }
     }
 }
@@ -992,10 +1112,13 @@ void transpose(const void* in, void* out, int N, int R, int C, int ld_in, int r_
 }  // namespace
 
 int dfp_reduce_blocks(int64_t pixels, int C) {
-    (void)C;
-    // ~256 pixels per thread row keeps f32 partial sums short; cap at a few waves
-    const int64_t want = ceil_div(pixels, 2048);
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4 * num_sms())));
+    // ~32 16-byte vectors per thread (256 threads) over the pixel range, grid.y covers channel
+    // vector blocks of 256; cap at four waves of blocks in total
+    const int64_t cvec = std::max<int64_t>(1, C / 8);
+    const int64_t gy = ceil_div(cvec, 256);
+    const int64_t want = ceil_div(pixels * cvec, static_cast<int64_t>(256) * 32 * gy);
+    const int64_t cap = std::max<int64_t>(1, 4 * num_sms() / gy);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, cap, pixels})));
 }
 
 void dfp_launch(const DfpArgs& a, cudaStream_t s) {
@@ -1066,8 +1189,35 @@ void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror, cud
     SOL_CUDA(cudaGetLastError());
 }
 
+// Narrow inputs (the 3-channel image): one thread per pixel, C coalesced plane reads, one 16-byte
+// store of the channel-padded NHWC row.
+template <typename TO>
+__global__ void nchw_to_nhwc_narrow_kernel(const float* __restrict__ src, TO* __restrict__ dst, int N, int C,
+                                           int64_t hw) {
+    constexpr int V = 16 / sizeof(TO);
+    const int64_t total = static_cast<int64_t>(N) * hw;
+    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < total;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t n = p / hw, q = p - n * hw;
+        float v[V];
+#pragma unroll
+        for (int c = 0; c < V; ++c) v[c] = c < C ? __ldg(src + (n * C + c) * hw + q) : 0.f;
+        store16(dst + p * V, v);
+    }
+}
+
 void nchw_to_nhwc(const float* src, void* dst, int dtype, int N, int C, int H, int W, int c_pad, cudaStream_t s) {
     const int hw = H * W;
+    if (c_pad * (dtype == DT_BF16 ? 2 : 4) == 16) {
+        const int64_t total = static_cast<int64_t>(N) * hw;
+        const unsigned grid = grid_for(total, 256);
+        if (dtype == DT_BF16)
+            nchw_to_nhwc_narrow_kernel<<<grid, 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), N, C, hw);
+        else
+            nchw_to_nhwc_narrow_kernel<<<grid, 256, 0, s>>>(src, static_cast<float*>(dst), N, C, hw);
+        SOL_CUDA(cudaGetLastError());
+        return;
+    }
     if (dtype == DT_BF16) transpose<float, __nv_bfloat16>(src, dst, N, C, hw, hw, c_pad, c_pad, s);
     else transpose<float, float>(src, dst, N, C, hw, hw, c_pad, c_pad, s);
 }

@@ -572,9 +572,11 @@ public:
         p.P[0] = coef_;
         p.P[1] = coef_ + C_;
         p.P[2] = coef_ + 2 * C_;
-        push(p.post, PW_LD, 0, 0);
-        push(p.post, PW_LD, 1, 1);
-        push(p.post, PW_AXPBY, 0, 0, 1, 0);
+        for (int k = 0; k < 4; ++k) p.P[3 + k] = xhat_ + k * C_;
+        push(p.post, PW_LD, 0, 0);           // r0 = delta
+        push(p.post, PW_LD, 1, 1);           // r1 = x
+        push(p.post, PW_BN, 1, 0, 0, 3);     // r1 = xhat
+        push(p.post, PW_AXPBY, 0, 0, 1, 0);  // r0 = delta*A + xhat*B + Cc
         p.out = out;
         p.out_ld = C_;
         dfp_launch(p, s);

@@ -79,10 +79,27 @@ def _check_units(gp, units, env, dtype, gpu, only_dfp=False):
             local[nid] = O.eval_node(n, [local[i] for i in n.inputs], params)
         want = np.asarray(local[u.output], np.float32)
         fam, got = run_unit(gp, u, env, dtype, gpu)
+        if fam in ("bias_grad", "bn_back_beta", "bn_back_gamma"):
+            # channel sums with heavy cancellation (a conv bias feeding a training BatchNorm has an
+            # analytically ~0 gradient): measure the error against the sum of |terms| per channel
+            d = np.asarray(sub[u.inputs[0]], np.float64)
+            terms = np.abs(d)
+            if fam == "bn_back_gamma":
+                x = np.asarray(sub[u.inputs[1]], np.float64)
+                mu, var = O.batch_stats(x)
+                terms = np.abs(d * (x - O._bc(mu, x)) / np.sqrt(O._bc(var, x) + 1e-5))
+            l1 = terms.sum(axis=(0, 2, 3) if terms.ndim == 4 else (0,))
+            bar = 1e-2 if dtype == 1 else 1e-6
+            assert np.max(np.abs(got - want)) <= bar * np.max(l1), (fam, u.output)
+            continue
         err = O.oracle_err(got, want)
         if fam in MOVEMENT:
             assert np.array_equal(got.astype(np.float32), want.astype(np.float32)), (fam, u.output)
         bar = 1e-2 if (dtype == 1 or heavy) else 1e-5
+        if fam == "bn_back_x" and dtype == 0:
+            # dx = g*rstd*(dy - mean(dy) - xhat*mean(dy*xhat)) cancels against dy when the batch is
+            # small (m = 16 here); f32 arithmetic then carries ~|dy|/|dx| * 6e-8 relative error
+            bar = 5e-5
         assert err <= bar, (fam, u.output, u.node_ids, err)
         worst[fam] = max(worst.get(fam, 0.0), err)
     return worst
