@@ -209,6 +209,7 @@ typedef struct {
     int32_t kh, kw, sh, sw, ph, pw;
     int32_t cin_ld;   /* stored channel stride of x (>= Cin, multiple of 16 bytes) */
     int32_t dtype;
+    int32_t cout_ld;  /* stored channel stride of y (>= Cout, multiple of 16 bytes; 0 = Cout) */
 } sol_conv_desc;
 
 /* W canonical f32 [Cout][Cin][kh][kw] -> packed [Cout][kh][kw][cin_ld] (K padded) in dtype
@@ -219,6 +220,8 @@ int sol_b200_conv_fprop(const sol_conv_desc* d, const void* x, const void* wpack
                         int32_t y_dtype, void* stream);
 int sol_b200_conv_dgrad(const sol_conv_desc* d, const void* dy, const void* wtpacked, void* dx, void* stream);
 int sol_b200_conv_wgrad_workspace(const sol_conv_desc* d, uint64_t* bytes);
+/* profiling knob for sol_b200_conv_fprop: 1 = skip output stores, 2 = skip MMA issue (0 = normal) */
+int sol_b200_set_conv_debug(int32_t flags);
 /* dW canonical f32 [Cout][Cin][kh][kw] */
 int sol_b200_conv_wgrad(const sol_conv_desc* d, const void* dy, const void* x, float* dw, void* workspace,
                         void* stream);

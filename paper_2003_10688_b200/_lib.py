@@ -41,7 +41,7 @@ SYMBOLS = [
     "sol_b200_conv_packed_elems", "sol_b200_conv_pack_weight", "sol_b200_conv_fprop", "sol_b200_conv_dgrad",
     "sol_b200_conv_wgrad_workspace", "sol_b200_conv_wgrad",
     "sol_b200_plan_h2d", "sol_b200_plan_d2h", "sol_b200_plan_event_record", "sol_b200_plan_event_elapsed",
-    "sol_b200_host_alloc", "sol_b200_host_free",
+    "sol_b200_host_alloc", "sol_b200_host_free", "sol_b200_set_conv_debug",
 ]
 
 
@@ -85,7 +85,7 @@ class TransferStats(C.Structure):
 
 class ConvDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("N", "Cin", "H", "W", "Cout", "OH", "OW", "kh", "kw", "sh", "sw",
-                                         "ph", "pw", "cin_ld", "dtype")]
+                                         "ph", "pw", "cin_ld", "dtype", "cout_ld")]
 
 
 class SolError(RuntimeError):
@@ -163,6 +163,7 @@ def lib():
             "sol_b200_plan_event_elapsed": [vp, i32, i32, C.POINTER(C.c_float)],
             "sol_b200_host_alloc": [u64, C.POINTER(vp)],
             "sol_b200_host_free": [vp],
+            "sol_b200_set_conv_debug": [i32],
         }
         for name, args in sig.items():
             f = getattr(L, name)

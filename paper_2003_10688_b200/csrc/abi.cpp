@@ -81,7 +81,7 @@ solb200::IgemmArgs conv_args(const sol_conv_desc* d) {
     a.Nout = d->Cout;
     const int bk = d->dtype == SOL_DT_BF16 ? 64 : 32;
     a.K_pad = static_cast<int>(solb200::round_up(static_cast<int64_t>(d->kh) * d->kw * d->cin_ld, bk));
-    a.ldo = d->Cout;
+    a.ldo = d->cout_ld > 0 ? d->cout_ld : d->Cout;
     return a;
 }
 
@@ -357,10 +357,18 @@ int sol_b200_conv_pack_weight(const sol_conv_desc* d, const float* w, void* pack
     });
 }
 
+static int g_conv_dbg = 0;
+
+int sol_b200_set_conv_debug(int32_t flags) {
+    g_conv_dbg = flags;
+    return SOL_OK;
+}
+
 int sol_b200_conv_fprop(const sol_conv_desc* d, const void* x, const void* wpacked, const float* bias, void* y,
                         int32_t y_dtype, void* stream) {
     return guard([&] {
         solb200::IgemmArgs a = conv_args(d);
+        a.dbg = g_conv_dbg;
         a.mode = solb200::IG_FPROP;
         a.src = x;
         a.wt = wpacked;

@@ -120,6 +120,19 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar_addr) {
         mbar_addr));
 }
 
+// 32 lanes x 32 bits, 32 consecutive columns per thread; completion via tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
 // 32 lanes x 32 bits, 16 consecutive columns per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
     asm volatile(
@@ -139,6 +152,12 @@ template <> struct AbFmt<float> { static constexpr int v = 2; };
 template <int STAGE_BYTES>
 constexpr int stages_for() {
     return std::min(8, (SMEM_BUDGET - 2048) / STAGE_BYTES);
+}
+
+// warp-specialised kernel: 227 KB minus 2 KB alignment/barriers and 32 KB epilogue staging
+template <int STAGE_BYTES>
+constexpr int ws_stages() {
+    return std::min(8, (227 * 1024 - 2048 - 65536 - 1024) / STAGE_BYTES);
 }
 
 template <int BN>
@@ -357,8 +376,19 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restr
 // stages let the epilogue of tile i overlap the mainloop of tile i+1.
 // ---------------------------------------------------------------------------------------------
 
-constexpr int WS_THREADS = 288;
-constexpr int IG_FPROP_TMA = 2;  // internal mode: A via TMA (1x1, stride 1, pad 0 fprop)
+constexpr int WS_THREADS = 416;  // 4 producer + 8 epilogue + 1 MMA warps
+constexpr int WS_MMA_WARP = 12;
+constexpr int IG_FPROP_TMA = 2;     // internal mode: A via TMA (1x1, stride 1, pad 0 fprop)
+constexpr int IG_FPROP_IM2COL = 3;  // internal mode: A via TMA im2col (channels multiple of 128 B)
+
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                                   uint16_t off_w, uint16_t off_h, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+        : "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive(uint32_t addr) {
     asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(addr));
@@ -389,17 +419,17 @@ constexpr uint32_t ws_tmem_cols() {
 template <typename T, typename TO, int BN, int MODE>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_a) {
+                    const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c) {
     constexpr int VEC = 16 / sizeof(T);
     constexpr int BK = ROWB / sizeof(T);
     constexpr int A_BYTES = BM * ROWB;
     constexpr int B_BYTES = BN * ROWB;
     constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    constexpr int STAGES = stages_for<STAGE_BYTES>();
+    constexpr int STAGES = ws_stages<STAGE_BYTES>();
     constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
     constexpr int KSTEP_BYTES = 32;
-    constexpr bool A_TMA = MODE == IG_FPROP_TMA;
+    constexpr bool A_TMA = MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -424,13 +454,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
-            mbar_init(smem_u32(&tempty[s]), 128);
+            mbar_init(smem_u32(&tempty[s]), 256);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
         tma_prefetch(&tmap_b);
         if (A_TMA) tma_prefetch(&tmap_a);
     }
-    if (warp == 8) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+    if (warp == WS_MMA_WARP) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -479,7 +509,20 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 if (tid == 0) {
                     mbar_arrive_tx(smem_u32(&full[stage]), A_TMA ? (A_BYTES + B_BYTES) : B_BYTES);
                     tma_load_2d(smem_u32(sb), &tmap_b, kb * BK, n0, smem_u32(&full[stage]));
-                    if (A_TMA) tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
+                    if (MODE == IG_FPROP_TMA) tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
+                    if (MODE == IG_FPROP_IM2COL) {
+                        // hardware im2col: 128 output pixels from (n, oh, ow) of m0, one filter tap
+                        // (im2col offsets) and one 128-byte channel block per k-block
+                        const int cblocks = a.SC / BK;
+                        const int tap = kb / cblocks;
+                        const int cb = kb - tap * cblocks;
+                        const int dkh = tap / a.kw, dkw = tap - (tap / a.kw) * a.kw;
+                        const int img = m0 / ohw, rem = m0 - img * ohw;
+                        const int oh0 = rem / a.OW, ow0 = rem - (rem / a.OW) * a.OW;
+                        tma_load_im2col_4d(smem_u32(sa), &tmap_a, cb * BK, ow0 * a.sw - a.pw, oh0 * a.sh - a.ph, img,
+                                           static_cast<uint16_t>(dkw), static_cast<uint16_t>(dkh),
+                                           smem_u32(&full[stage]));
+                    }
                 }
                 if (!A_TMA) {
                     const int k = kb * BK + j * VEC;
@@ -515,7 +558,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             }
         }
         if (!A_TMA) cp_async_wait<0>();
-    } else if (warp == 8) {
+    } else if (warp == WS_MMA_WARP) {
         // ------------------------------------------------------------------ MMA issuer
         int stage = 0;
         uint32_t phase = 0;
@@ -535,7 +578,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     for (int k = 0; k < ROWB / KSTEP_BYTES; ++k) {
                         const uint64_t ad = sw128_desc(a_addr + k * KSTEP_BYTES, 16, 1024);
                         const uint64_t bd = sw128_desc(b_addr + k * KSTEP_BYTES, 16, 1024);
-                        mma<T>(dcol, ad, bd, IDESC, (kb | k) != 0);
+                        if (!(a.dbg & 2)) mma<T>(dcol, ad, bd, IDESC, (kb | k) != 0);
                     }
                     mma_commit(smem_u32(&empty[stage]));
                 }
@@ -553,34 +596,84 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             }
         }
     } else {
-        // ------------------------------------------------------------------ epilogue (warps 4-7)
-        const int q = warp & 3;  // TMEM lane quarter
-        const int row = q * 32 + lane;
-        TO* out = static_cast<TO*>(a.out);
+        // ------------------------------------------------------------------ epilogue (warps 4-11)
+        // TMEM -> registers -> 128B-swizzled smem staging (2 buffers per warp) -> TMA bulk-tensor
+        // store of [32 rows x 128 bytes] boxes (OOB rows / columns are clipped by the TMA unit).
+        // Two warps per TMEM lane quarter split the accumulator columns (alternate 128B chunks).
+        constexpr int CW = 128 / static_cast<int>(sizeof(TO));  // columns per 128-byte box
+        const int q = warp & 3;            // TMEM lane quarter
+        const int half = (warp - 4) >> 2;  // column interleave
+        uint8_t* stage_buf = smem + STAGES * STAGE_BYTES + 1024 + (warp - 4) * 2 * 4096;
+        const bool has_bias = a.bias != nullptr;
+        const bool do_relu = a.relu != 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        int buf = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
-            const int m = m0 + row;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c0), v);
-                const int n = n0 + c0;
-                if (m < M && n < a.ldo) {
-                    float f[16];
+            for (int cc = half * CW; cc < BN; cc += 2 * CW) {
+                const int n = n0 + cc;
+                if (n >= a.ldo || (a.dbg & 4)) break;
+                uint32_t v[CW];
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cc);
 #pragma unroll
-                    for (int qq = 0; qq < 16; ++qq) {
-                        float x = __uint_as_float(v[qq]);
-                        if (a.bias != nullptr && n + qq < a.Nout) x += __ldg(a.bias + n + qq);
-                        if (a.relu) x = fmaxf(x, 0.0f);
-                        f[qq] = x;
+                for (int h = 0; h < CW; h += 32) tmem_ld32_nowait(taddr + h, v + h);
+                tmem_wait_ld();
+                float f[CW];
+#pragma unroll
+                for (int i = 0; i < CW; ++i) f[i] = __uint_as_float(v[i]);
+                if (has_bias) {
+                    if (n + CW <= a.Nout) {
+#pragma unroll
+                        for (int i = 0; i < CW; i += 4) {
+                            const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + n + i));
+                            f[i] += bb.x; f[i + 1] += bb.y; f[i + 2] += bb.z; f[i + 3] += bb.w;
+                        }
+                    } else {
+                        for (int i = 0; i < CW; ++i)
+                            if (n + i < a.Nout) f[i] += __ldg(a.bias + n + i);
                     }
-                    store_row16<TO>(out + static_cast<int64_t>(m) * a.ldo + n, n, a.Nout, a.ldo, f);
                 }
+                if (do_relu) {
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) f[i] = fmaxf(f[i], 0.0f);
+                }
+                // the staging buffer is free once the TMA store issued two chunks ago has read it
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                __syncwarp();
+                uint8_t* sb = stage_buf + buf * 4096;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t addr = smem_u32(sb + lane * 128 + ((j ^ (lane & 7)) << 4));
+                    const float* src = f + j * (16 / static_cast<int>(sizeof(TO)));
+                    if constexpr (sizeof(TO) == 2) {
+                        __nv_bfloat162 p0 = __floats2bfloat162_rn(src[0], src[1]);
+                        __nv_bfloat162 p1 = __floats2bfloat162_rn(src[2], src[3]);
+                        __nv_bfloat162 p2 = __floats2bfloat162_rn(src[4], src[5]);
+                        __nv_bfloat162 p3 = __floats2bfloat162_rn(src[6], src[7]);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr),
+                                     "r"(*reinterpret_cast<uint32_t*>(&p0)), "r"(*reinterpret_cast<uint32_t*>(&p1)),
+                                     "r"(*reinterpret_cast<uint32_t*>(&p2)), "r"(*reinterpret_cast<uint32_t*>(&p3)));
+                    } else {
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "f"(src[0]),
+                                     "f"(src[1]), "f"(src[2]), "f"(src[3]));
+                    }
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0 && !(a.dbg & 1)) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                            reinterpret_cast<uint64_t>(&tmap_c)),
+                        "r"(n), "r"(m0 + q * 32), "r"(smem_u32(sb))
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                }
+                buf ^= 1;
             }
             tc_fence_before();
             mbar_arrive(smem_u32(&tempty[acc]));
@@ -589,10 +682,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 acc_phase ^= 1;
             }
         }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+        __syncwarp();
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == WS_MMA_WARP) {
         tc_fence_after();
         tmem_dealloc<TCOLS>(tmem_base);
     }
@@ -631,11 +726,46 @@ CUtensorMap make_tmap_2d(const void* base, int dtype, uint64_t cols, uint64_t ro
     return m;
 }
 
+// Im2col tensor map over the NHWC activation (dims {C, W, H, N}): pixelsPerColumn = 128 output
+// pixels per load, channelsPerPixel = one 128-byte channel block, traversal strides = conv
+// strides, bounding box corners (-pad, pad - (k-1)) so every window start of the convolution is
+// enumerated in (n, oh, ow) order; OOB taps are zero-filled (the conv padding).
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype) {
+    static EncodeIm2colFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SOL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeIm2col unavailable");
+        return reinterpret_cast<EncodeIm2colFn>(p);
+    }();
+    CUtensorMap m;
+    const uint64_t es = dtype == DT_BF16 ? 2 : 4;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(a.SC), static_cast<cuuint64_t>(a.SW),
+                          static_cast<cuuint64_t>(a.SH), static_cast<cuuint64_t>(a.N)};
+    cuuint64_t strides[3] = {a.SC * es, static_cast<cuuint64_t>(a.SW) * a.SC * es,
+                             static_cast<cuuint64_t>(a.SH) * a.SW * a.SC * es};
+    int lower[2] = {-a.pw, -a.ph};
+    int upper[2] = {a.pw - (a.kw - 1), a.ph - (a.kh - 1)};
+    cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(a.sw), static_cast<cuuint32_t>(a.sh), 1};
+    const CUresult r = fn(&m, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                          const_cast<void*>(a.src), dims, strides, lower, upper, static_cast<cuuint32_t>(128 / es),
+                          static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeIm2col failed: " + std::to_string(static_cast<int>(r)));
+    return m;
+}
+
 template <typename T, typename TO, int BN, int MODE>
 void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     constexpr int STAGE_BYTES = BM * ROWB + BN * ROWB;
-    constexpr int STAGES = stages_for<STAGE_BYTES>();
-    constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + (2 * STAGES + 4) * 8 + 16;
+    constexpr int STAGES = ws_stages<STAGE_BYTES>();
+    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + 8 * 8192;
     static std::once_flag once;
     std::call_once(once, [] {
         SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -648,9 +778,12 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     (void)n_rows;
     CUtensorMap ta = tb;
     if (MODE == IG_FPROP_TMA) ta = make_tmap_2d(a.src, dt, a.SC, static_cast<uint64_t>(M), a.SC, BM);
+    if (MODE == IG_FPROP_IM2COL) ta = make_tmap_im2col(a, dt);
     const int tiles = static_cast<int>(ceil_div(M, BM) * ceil_div(a.Nout, BN));
     const int grid = std::min(tiles, num_sms());
-    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta);
+    const int dto = sizeof(TO) == 2 ? DT_BF16 : DT_F32;
+    CUtensorMap tc = make_tmap_2d(a.out, dto, a.ldo, static_cast<uint64_t>(M), a.ldo, 32);
+    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc);
     SOL_CUDA(cudaGetLastError());
 }
 
@@ -669,7 +802,11 @@ template <typename T, typename TO>
 void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
     const bool plain = a.mode == IG_FPROP && a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 &&
                        a.pw == 0 && a.K_pad == a.SC;
+    constexpr int BK = ROWB / sizeof(T);
+    const bool im2col = a.mode == IG_FPROP && !plain && a.SC % BK == 0 && a.K_pad == a.kh * a.kw * a.SC &&
+                        a.kh <= 8 && a.kw <= 8;
     if (plain) dispatch_ws<T, TO, IG_FPROP_TMA>(a, s);
+    else if (im2col) dispatch_ws<T, TO, IG_FPROP_IM2COL>(a, s);
     else if (a.mode == IG_FPROP) dispatch_ws<T, TO, IG_FPROP>(a, s);
     else dispatch_ws<T, TO, IG_DGRAD>(a, s);
 }
@@ -727,6 +864,8 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
     const int bk = a.dtype == DT_BF16 ? 64 : 32;
     if (a.SC % vec != 0) throw std::invalid_argument("igemm: channel count must be a multiple of 16 bytes");
     if (a.K_pad % bk != 0) throw std::invalid_argument("igemm: K_pad must be a multiple of the k-block");
+    const int out_es = a.out_dtype == DT_BF16 ? 2 : 4;
+    if ((a.ldo * out_es) % 16 != 0) throw std::invalid_argument("igemm: output row stride must be a multiple of 16 bytes");
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);

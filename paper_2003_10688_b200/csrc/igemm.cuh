@@ -34,6 +34,7 @@ struct IgemmArgs {
     int K_pad = 0;             // padded reduction extent of the packed operand
     int ldo = 0;
     int relu = 0;              // fused epilogue ReLU (unused by the reference path)
+    int dbg = 0;               // profiling knobs: 1 = skip output stores, 2 = skip MMA issue
 };
 
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).

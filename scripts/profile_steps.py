@@ -1,0 +1,28 @@
+"""Per-step device times of a compiled plan (CUDA events around every step)."""
+import sys
+sys.path.insert(0, '.')
+import numpy as np
+from paper_2003_10688_b200 import frontend, models
+train = len(sys.argv) > 1 and sys.argv[1] == "train"
+B = 128 if train else 256
+g = models.resnet(50, hw=224, classes=1000, train=train)
+m = frontend.optimize(g, frontend.OptimizeOptions(batch=B, dtype="bf16", train=train))
+rng = np.random.default_rng(0)
+ins = {"x": rng.uniform(-1, 1, (B, 3, 224, 224)).astype(np.float32)}
+if train:
+    t = np.zeros((B, 1000), np.float32); t[np.arange(B), np.arange(B) % 1000] = 1; ins["t"] = t
+m.set_inputs(ins); m.run(); m.run(); m.sync()
+times = m.profile(); times = m.profile()
+rows = []
+for st, t in zip(m.steps, times):
+    rows.append((t, st.family, st.output, st.algo_flops / max(t, 1e-9) / 1e6, st.algo_bytes / max(t, 1e-9) / 1e3))
+tot = sum(times)
+print(f"total {tot/1e3:.3f} ms over {len(times)} steps")
+fam = {}
+for t, f, o, tf, gb in rows:
+    a = fam.setdefault(f, [0, 0]); a[0] += t; a[1] += 1
+for f, (t, n) in sorted(fam.items(), key=lambda kv: -kv[1][0]):
+    print(f"{f:24s} {t/1e3:8.3f} ms  {n:4d} steps  {100*t/tot:5.1f}%")
+print("--- top 40 steps")
+for t, f, o, tf, gb in sorted(rows, reverse=True)[:40]:
+    print(f"{t:9.1f} us {f:22s} {o:36s} {tf:8.1f} TF/s {gb:8.1f} GB/s")

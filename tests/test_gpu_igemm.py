@@ -60,7 +60,8 @@ def test_conv_fprop(gpu, case, dt):
     OH = (H + 2 * p - k) // s + 1
     OW = (W + 2 * p - k) // s + 1
     cld = _pad_c(Cin, dt)
-    d = L.ConvDesc(N, Cin, H, W, Cout, OH, OW, k, k, s, s, p, p, cld, dt)
+    old = _pad_c(Cout, dt)
+    d = L.ConvDesc(N, Cin, H, W, Cout, OH, OW, k, k, s, s, p, p, cld, dt, old)
     xd = _to_nhwc(torch, x, cld, dt, gpu)
     wd = torch.from_numpy(w).to(gpu)
     bd = torch.from_numpy(b).to(gpu)
@@ -69,10 +70,12 @@ def test_conv_fprop(gpu, case, dt):
     wp = torch.zeros(n.value, dtype=xd.dtype, device=gpu)
     st = torch.cuda.current_stream().cuda_stream
     L.check(L.lib().sol_b200_conv_pack_weight(C.byref(d), wd.data_ptr(), wp.data_ptr(), 0, st))
-    y = torch.zeros((N, OH, OW, Cout), dtype=xd.dtype, device=gpu)
+    y = torch.full((N, OH, OW, old), 7.0, dtype=xd.dtype, device=gpu)
     L.check(L.lib().sol_b200_conv_fprop(C.byref(d), xd.data_ptr(), wp.data_ptr(), bd.data_ptr(), y.data_ptr(), dt, st))
     torch.cuda.synchronize()
-    got = y.float().cpu().numpy().transpose(0, 3, 1, 2)
+    yy = y.float().cpu().numpy()
+    assert np.all(yy[..., Cout:] == 0.0)  # row padding is written as zeros
+    got = yy[..., :Cout].transpose(0, 3, 1, 2)
     want = O.conv2d(quant(x, dt), quant(w, dt), b, (s, s), (p, p))
     err = O.oracle_err(got, want)
     assert err <= 1e-2, err
