@@ -259,7 +259,7 @@ def run_b200(args):
     x = rng.uniform(-1, 1, (B, 3, 224, 224)).astype(np.float32)
 
     g = models.resnet(50, hw=224, classes=1000)
-    m = frontend.optimize(g, frontend.OptimizeOptions(batch=B, dtype="bf16", device=device))
+    m = frontend.optimize(g, frontend.OptimizeOptions(batch=B, dtype="bf16", device=device, fuse_epilogue=True))
     sampler = ClockSampler(device) if ctx.rank == 0 else None
     if sampler:
         sampler.start()
@@ -269,7 +269,7 @@ def run_b200(args):
     world = ctx.world
     value = world * B / (dev_ms / 1e3)
     e2e = world * B / (e2e_ms / 1e3)
-    roof, times = roofline_of(m, peaks, peaks_kind, {"conv_fprop_tcgen05"}, "tensor")
+    roof, times = roofline_of(m, peaks, peaks_kind, {"conv_fprop_tcgen05", "conv_fprop_fused_tcgen05"}, "tensor")
     dfp_fams = {s.family for s in m.steps if s.family.startswith("dfp_")}
     roof_dfp, _ = roofline_of(m, peaks, peaks_kind, dfp_fams, "hbm")
     fam_time = {}

@@ -245,18 +245,35 @@ ChainSpec match_chain(const Program& p) {
     return c;
 }
 
-template <int V>
+// BatchNorm apply. f32 plans keep the reference's (x - mean) form with the mean split hi/lo so
+// the 1e-5 bar holds when |mean| >> std; bf16 plans (output rounded to 8 bits anyway) use the
+// folded per-channel scale/shift: y = x * scale + shift (P[b+2], P[b+4]).
+template <typename T>
 __device__ __forceinline__ void bn_apply(float* v, const float* const* P, int b, int c) {
-    float mh[V], ml[V], sc[V], bt[V];
+    constexpr int V = VEC<T>;
+    if constexpr (sizeof(T) == 2) {
 #pragma unroll
-    for (int i = 0; i < V; i += 4) {
-        *reinterpret_cast<float4*>(mh + i) = __ldg(reinterpret_cast<const float4*>(P[b] + c + i));
-        *reinterpret_cast<float4*>(ml + i) = __ldg(reinterpret_cast<const float4*>(P[b + 1] + c + i));
-        *reinterpret_cast<float4*>(sc + i) = __ldg(reinterpret_cast<const float4*>(P[b + 2] + c + i));
-        *reinterpret_cast<float4*>(bt + i) = __ldg(reinterpret_cast<const float4*>(P[b + 3] + c + i));
+        for (int i = 0; i < V; i += 4) {
+            const float4 sc = __ldg(reinterpret_cast<const float4*>(P[b + 2] + c + i));
+            const float4 sh = __ldg(reinterpret_cast<const float4*>(P[b + 4] + c + i));
+            v[i] = fmaf(v[i], sc.x, sh.x);
+            v[i + 1] = fmaf(v[i + 1], sc.y, sh.y);
+            v[i + 2] = fmaf(v[i + 2], sc.z, sh.z);
+            v[i + 3] = fmaf(v[i + 3], sc.w, sh.w);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; i += 4) {
+            const float4 mh = __ldg(reinterpret_cast<const float4*>(P[b] + c + i));
+            const float4 ml = __ldg(reinterpret_cast<const float4*>(P[b + 1] + c + i));
+            const float4 sc = __ldg(reinterpret_cast<const float4*>(P[b + 2] + c + i));
+            const float4 bt = __ldg(reinterpret_cast<const float4*>(P[b + 3] + c + i));
+            v[i] = fmaf((v[i] - mh.x) - ml.x, sc.x, bt.x);
+            v[i + 1] = fmaf((v[i + 1] - mh.y) - ml.y, sc.y, bt.y);
+            v[i + 2] = fmaf((v[i + 2] - mh.z) - ml.z, sc.z, bt.z);
+            v[i + 3] = fmaf((v[i + 3] - mh.w) - ml.w, sc.w, bt.w);
+        }
     }
-#pragma unroll
-    for (int i = 0; i < V; ++i) v[i] = fmaf((v[i] - mh[i]) - ml[i], sc[i], bt[i]);
 }
 
 template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
@@ -287,9 +304,9 @@ __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ 
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (BN0) bn_apply<V>(r0[u], a.P, cs.bn0, cc[u]);
+            if (BN0) bn_apply<T>(r0[u], a.P, cs.bn0, cc[u]);
             if (ADD) {
-                if (BN1) bn_apply<V>(r1[u], a.P, cs.bn1, cc[u]);
+                if (BN1) bn_apply<T>(r1[u], a.P, cs.bn1, cc[u]);
 #pragma unroll
                 for (int i = 0; i < V; ++i) r0[u][i] += r1[u][i];
             }
@@ -335,11 +352,11 @@ template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
 __device__ __forceinline__ void chain_at(const DfpArgs& a, const ChainSpec& cs, int64_t pix, int c, float* v) {
     constexpr int V = VEC<T>;
     load16(static_cast<const T*>(a.in[cs.s0]) + pix * a.in_ld[cs.s0] + c, v);
-    if (BN0) bn_apply<V>(v, a.P, cs.bn0, c);
+    if (BN0) bn_apply<T>(v, a.P, cs.bn0, c);
     if (ADD) {
         float w[V];
         load16(static_cast<const T*>(a.in[cs.s1]) + pix * a.in_ld[cs.s1] + c, w);
-        if (BN1) bn_apply<V>(w, a.P, cs.bn1, c);
+        if (BN1) bn_apply<T>(w, a.P, cs.bn1, c);
 #pragma unroll
         for (int i = 0; i < V; ++i) v[i] += w[i];
     }
@@ -1017,6 +1034,7 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
             a.coef[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
             a.coef[2 * a.C + c] = static_cast<float>(static_cast<double>(a.gamma[c]) * rstd);
             a.coef[3 * a.C + c] = a.beta[c];
+            a.coef[4 * a.C + c] = static_cast<float>(a.beta[c] - mean * static_cast<double>(a.gamma[c]) * rstd);
         }
         if (a.running_mean) {
             const double unbias = m > 1 ? m / (m - 1) : 1.0;
@@ -1053,6 +1071,7 @@ __global__ void bn_infer_coef_kernel(const float* g, const float* b, const float
     coef[C + c] = 0.f;
     coef[2 * C + c] = static_cast<float>(g[c] * rstd);
     coef[3 * C + c] = b[c];
+    coef[4 * C + c] = static_cast<float>(b[c] - mu[c] * g[c] * rstd);
 }
 
 template <typename T>

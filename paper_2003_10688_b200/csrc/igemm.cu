@@ -132,6 +132,13 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* v) {
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
 
 // 32 lanes x 32 bits, 16 consecutive columns per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
@@ -419,7 +426,8 @@ constexpr uint32_t ws_tmem_cols() {
 template <typename T, typename TO, int BN, int MODE>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
-                    const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c) {
+                    const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
+                    const __grid_constant__ CUtensorMap tmap_r) {
     constexpr int VEC = 16 / sizeof(T);
     constexpr int BK = ROWB / sizeof(T);
     constexpr int A_BYTES = BM * ROWB;
@@ -437,7 +445,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rbar = tempty + 2;  // [8 epilogue warps][2 staging buffers]: residual TMA loads
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 16);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -456,6 +465,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             mbar_init(smem_u32(&tfull[s]), 1);
             mbar_init(smem_u32(&tempty[s]), 256);
         }
+        for (int s = 0; s < 16; ++s) mbar_init(smem_u32(&rbar[s]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
         tma_prefetch(&tmap_b);
         if (A_TMA) tma_prefetch(&tmap_a);
@@ -605,27 +615,55 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const int half = (warp - 4) >> 2;  // column interleave
         uint8_t* stage_buf = smem + STAGES * STAGE_BYTES + 1024 + (warp - 4) * 2 * 4096;
         const bool has_bias = a.bias != nullptr;
-        const bool do_relu = a.relu != 0;
+        const bool has_fold = a.ep_scale != nullptr;
+        const bool has_res = a.residual != nullptr;
+        const int act = a.relu ? 1 : a.act;
         int acc = 0;
         uint32_t acc_phase = 0;
         int buf = 0;
+        uint32_t rphase = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
+            constexpr int SLOTS = (BN / CW + 1) / 2 > 0 ? (BN / CW + 1) / 2 : 1;
+            constexpr int LCOLS = BN < CW ? BN : CW;  // TMEM columns per chunk (never past the tile)
+            // residual boxes for this warp's first two chunks are TMA-loaded into the two staging
+            // buffers before waiting for the accumulator, so their latency hides behind the mainloop
+            if (has_res) {
+                if (lane == 0) {
+                    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                    for (int s = 0; s < 2 && s < SLOTS; ++s) {
+                        const int cc = half * CW + s * 2 * CW;
+                        if (cc >= BN || n0 + cc >= a.ldo) break;
+                        const int bi = buf ^ s;
+                        mbar_arrive_tx(smem_u32(&rbar[(warp - 4) * 2 + bi]), 4096);
+                        tma_load_2d(smem_u32(stage_buf + bi * 4096), &tmap_r, n0 + cc, m0 + q * 32,
+                                    smem_u32(&rbar[(warp - 4) * 2 + bi]));
+                    }
+                }
+                __syncwarp();
+            }
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
-#pragma unroll 1
-            for (int cc = half * CW; cc < BN; cc += 2 * CW) {
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s) {
+                const int cc = half * CW + s * 2 * CW;
+                if (cc >= BN) break;
                 const int n = n0 + cc;
-                if (n >= a.ldo || (a.dbg & 4)) break;
+                if (n >= a.ldo) break;
                 uint32_t v[CW];
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + cc);
+                if constexpr (LCOLS % 32 == 0) {
 #pragma unroll
-                for (int h = 0; h < CW; h += 32) tmem_ld32_nowait(taddr + h, v + h);
+                    for (int h = 0; h < LCOLS; h += 32) tmem_ld32_nowait(taddr + h, v + h);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < LCOLS; h += 16) tmem_ld16_nowait(taddr + h, v + h);
+                }
                 tmem_wait_ld();
                 float f[CW];
 #pragma unroll
-                for (int i = 0; i < CW; ++i) f[i] = __uint_as_float(v[i]);
+                for (int i = 0; i < CW; ++i) f[i] = i < LCOLS ? __uint_as_float(v[i]) : 0.0f;
                 if (has_bias) {
                     if (n + CW <= a.Nout) {
 #pragma unroll
@@ -638,14 +676,74 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                             if (n + i < a.Nout) f[i] += __ldg(a.bias + n + i);
                     }
                 }
-                if (do_relu) {
+                if (has_fold) {
+                    if (n + CW <= a.Nout) {
 #pragma unroll
-                    for (int i = 0; i < CW; ++i) f[i] = fmaxf(f[i], 0.0f);
+                        for (int i = 0; i < CW; i += 4) {
+                            const float4 sc = __ldg(reinterpret_cast<const float4*>(a.ep_scale + n + i));
+                            const float4 sh = __ldg(reinterpret_cast<const float4*>(a.ep_shift + n + i));
+                            f[i] = fmaf(f[i], sc.x, sh.x);
+                            f[i + 1] = fmaf(f[i + 1], sc.y, sh.y);
+                            f[i + 2] = fmaf(f[i + 2], sc.z, sh.z);
+                            f[i + 3] = fmaf(f[i + 3], sc.w, sh.w);
+                        }
+                    } else {
+                        for (int i = 0; i < CW; ++i)
+                            if (n + i < a.Nout) f[i] = fmaf(f[i], __ldg(a.ep_scale + n + i), __ldg(a.ep_shift + n + i));
+                    }
+                }
+                uint8_t* sb = stage_buf + buf * 4096;
+                if (has_res) {
+                    // residual box (zero-filled past the tensor edge) is in this chunk's staging
+                    // buffer in the same swizzled layout the output is written in
+                    if (s >= 2) {
+                        if (lane == 0) {
+                            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                            mbar_arrive_tx(smem_u32(&rbar[(warp - 4) * 2 + buf]), 4096);
+                            tma_load_2d(smem_u32(sb), &tmap_r, n, m0 + q * 32, smem_u32(&rbar[(warp - 4) * 2 + buf]));
+                        }
+                        __syncwarp();
+                    }
+                    mbar_wait(smem_u32(&rbar[(warp - 4) * 2 + buf]), (rphase >> buf) & 1);
+                    rphase ^= 1u << buf;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint32_t addr = smem_u32(sb + lane * 128 + ((j ^ (lane & 7)) << 4));
+                        float rr[16 / sizeof(TO)];
+                        uint32_t r0, r1, r2, r3;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                                     : "r"(addr));
+                        if constexpr (sizeof(TO) == 2) {
+                            const uint32_t w[4] = {r0, r1, r2, r3};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                rr[2 * k] = __uint_as_float(w[k] << 16);
+                                rr[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+                            }
+                        } else {
+                            rr[0] = __uint_as_float(r0);
+                            rr[1] = __uint_as_float(r1);
+                            rr[2] = __uint_as_float(r2);
+                            rr[3] = __uint_as_float(r3);
+                        }
+#pragma unroll
+                        for (int k = 0; k < static_cast<int>(16 / sizeof(TO)); ++k) f[j * (16 / sizeof(TO)) + k] += rr[k];
+                    }
+                }
+                if (act != 0) {
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) {
+                        f[i] = fmaxf(f[i], 0.0f);
+                        if (act == 2) f[i] = fminf(f[i], 6.0f);
+                    }
                 }
                 // the staging buffer is free once the TMA store issued two chunks ago has read it
-                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-                __syncwarp();
-                uint8_t* sb = stage_buf + buf * 4096;
+                // (with a residual, the buffer was drained before the residual load was issued)
+                if (!has_res) {
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const uint32_t addr = smem_u32(sb + lane * 128 + ((j ^ (lane & 7)) << 4));
@@ -783,7 +881,9 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     const int grid = std::min(tiles, num_sms());
     const int dto = sizeof(TO) == 2 ? DT_BF16 : DT_F32;
     CUtensorMap tc = make_tmap_2d(a.out, dto, a.ldo, static_cast<uint64_t>(M), a.ldo, 32);
-    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc);
+    CUtensorMap tr = tc;
+    if (a.residual) tr = make_tmap_2d(a.residual, dto, a.Nout, static_cast<uint64_t>(M), a.ld_res, 32);
+    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr);
     SOL_CUDA(cudaGetLastError());
 }
 
@@ -866,6 +966,8 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
     if (a.K_pad % bk != 0) throw std::invalid_argument("igemm: K_pad must be a multiple of the k-block");
     const int out_es = a.out_dtype == DT_BF16 ? 2 : 4;
     if ((a.ldo * out_es) % 16 != 0) throw std::invalid_argument("igemm: output row stride must be a multiple of 16 bytes");
+    if (a.residual && ((a.ld_res * out_es) % 16 != 0 || (reinterpret_cast<uintptr_t>(a.residual) & 15) != 0))
+        throw std::invalid_argument("igemm: residual must be 16-byte aligned with a 16-byte multiple row stride");
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);

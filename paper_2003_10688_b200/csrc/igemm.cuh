@@ -35,6 +35,13 @@ struct IgemmArgs {
     int ldo = 0;
     int relu = 0;              // fused epilogue ReLU (unused by the reference path)
     int dbg = 0;               // profiling knobs: 1 = skip output stores, 2 = skip MMA issue
+    // fused epilogue (inference BN folding, beyond the reference pass set):
+    //   y = act( (acc + bias) * ep_scale[c] + ep_shift[c] [+ residual[m, c]] )
+    const float* ep_scale = nullptr;
+    const float* ep_shift = nullptr;
+    const void* residual = nullptr;  // same dtype as the output, row stride ld_res
+    int ld_res = 0;
+    int act = 0;                     // 0 none, 1 relu, 2 relu6 (applied after the residual add)
 };
 
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).

@@ -174,10 +174,50 @@ public:
             default:
                 unsupported("not a heavy op");
         }
+        parse_epilogue(d);
     }
 
     size_t scratch_bytes() const override {
         return op_ == SOL_OP_CONV2DBACKW || op_ == SOL_OP_LINEARBACKW ? (packed_floats_ + ws_floats_) * 4 + 256 : 0;
+    }
+
+    // Fused epilogue chain after a Conv2d / Linear fprop (inference BatchNorm folding, the
+    // "epilogue fusion" of SURVEY §8f row 3): [BN] -> [Add(residual binding)] -> [ReLU | ReLU6].
+    // The plan compiler only forms such units when the conv output has no other consumer.
+    void parse_epilogue(const sol_unit_desc& d) {
+        if (d.n_ops == 1) return;
+        if (op_ != SOL_OP_CONV2D && op_ != SOL_OP_LINEAR) unsupported("epilogue fusion only after fprop");
+        int k = 1;
+        auto prev_ref = [&](int kk) { return -kk; };  // output of member op kk-1 is ref -(kk-1)-1 = -kk
+        if (k < d.n_ops && d.ops[k].op == SOL_OP_BATCHNORM2D) {
+            const sol_unit_op& b = d.ops[k];
+            if (b.attrs.training) unsupported("training BatchNorm cannot fold into the conv epilogue");
+            if (b.inputs[0] != prev_ref(k) || b.n_params < 4) unsupported("bad fused BatchNorm");
+            bn_g_ = b.params[0];
+            bn_b_ = b.params[1];
+            bn_m_ = b.params[2];
+            bn_v_ = b.params[3];
+            bn_eps_ = b.attrs.eps;
+            ep_coef_ = static_cast<float*>(dev_alloc(5 * static_cast<size_t>(out_.C) * 4));
+            ++k;
+        }
+        if (k < d.n_ops && d.ops[k].op == SOL_OP_ADD) {
+            const sol_unit_op& ad = d.ops[k];
+            const int x0 = ad.inputs[0], x1 = ad.inputs[1];
+            if (x0 == prev_ref(k) && x1 >= 0) res_idx_ = x1;
+            else if (x1 == prev_ref(k) && x0 >= 0) res_idx_ = x0;
+            else unsupported("fused Add must combine the conv chain with a unit input");
+            const Geo r = geo_b(d.bindings[res_idx_]);
+            if (r.ld != out_.ld || r.pixels() != out_.pixels()) unsupported("residual layout mismatch");
+            ++k;
+        }
+        if (k < d.n_ops && (d.ops[k].op == SOL_OP_RELU || d.ops[k].op == SOL_OP_RELU6)) {
+            if (d.ops[k].inputs[0] != prev_ref(k)) unsupported("bad fused activation");
+            act_ = d.ops[k].op == SOL_OP_RELU ? 1 : 2;
+            ++k;
+        }
+        if (k != d.n_ops) unsupported("unsupported fused conv epilogue");
+        family = op_ == SOL_OP_CONV2D ? "conv_fprop_fused_tcgen05" : "linear_fused_tcgen05";
     }
 
     WgradArgs wargs(const void* dy, const void* x, float* dw, float* ws) const {
@@ -228,6 +268,21 @@ public:
                 g.Nout = static_cast<int>(cout_);
                 g.K_pad = kpad_;
                 g.ldo = static_cast<int>(out_.ld);
+                if (ep_coef_) {
+                    if (!(frozen && coef_valid_)) {
+                        bn_infer_coef(static_cast<const float*>(args[bn_g_]), static_cast<const float*>(args[bn_b_]),
+                                      static_cast<const float*>(args[bn_m_]), static_cast<const float*>(args[bn_v_]),
+                                      bn_eps_, ep_coef_, static_cast<int>(cout_), s);
+                        coef_valid_ = true;
+                    }
+                    g.ep_scale = ep_coef_ + 2 * cout_;
+                    g.ep_shift = ep_coef_ + 4 * cout_;
+                }
+                if (res_idx_ >= 0) {
+                    g.residual = args[res_idx_];
+                    g.ld_res = static_cast<int>(out_.ld);
+                }
+                g.act = act_;
                 igemm_launch(g, s);
                 break;
             }
@@ -282,6 +337,13 @@ private:
     void* packed_ = nullptr;
     bool packed_valid_ = false;
     size_t ws_floats_ = 0, packed_floats_ = 0;
+    // fused epilogue
+    float* ep_coef_ = nullptr;
+    bool coef_valid_ = false;
+    int bn_g_ = -1, bn_b_ = -1, bn_m_ = -1, bn_v_ = -1;
+    float bn_eps_ = 1e-5f;
+    int res_idx_ = -1;
+    int act_ = 0;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -447,7 +509,7 @@ public:
             zeros_ = static_cast<float*>(dev_alloc(C_ * 4));
             shift_ = static_cast<float*>(dev_alloc(C_ * 4));
             stats_ = static_cast<float*>(dev_alloc(2 * C_ * 4));
-            xhat_ = static_cast<float*>(dev_alloc(4 * C_ * 4));
+            xhat_ = static_cast<float*>(dev_alloc(5 * C_ * 4));
             coef_ = static_cast<float*>(dev_alloc(3 * C_ * 4));
             gamma_idx_ = o.n_params > 0 ? o.params[0] : -1;
         }
@@ -572,7 +634,7 @@ public:
         p.P[0] = coef_;
         p.P[1] = coef_ + C_;
         p.P[2] = coef_ + 2 * C_;
-        for (int k = 0; k < 4; ++k) p.P[3 + k] = xhat_ + k * C_;
+        for (int k = 0; k < 5; ++k) p.P[3 + k] = xhat_ + k * C_;
         push(p.post, PW_LD, 0, 0);           // r0 = delta
         push(p.post, PW_LD, 1, 1);           // r1 = x
         push(p.post, PW_BN, 1, 0, 0, 3);     // r1 = xhat
@@ -763,7 +825,7 @@ int DfpModule::emit_value(int key) {
         case SOL_OP_BATCHNORM2D: {
             const int r = reg_take(in_key(0));
             const int bi = bn_of_op_.at(key);
-            push(p, PW_BN, r, 0, 0, 4 * bi);
+            push(p, PW_BN, r, 0, 0, 5 * bi);
             return r;
         }
         case SOL_OP_ADD: {
@@ -864,7 +926,7 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
         b.eps = o.attrs.eps;
         const Geo xg = geo_ref(o.inputs[0]);
         b.C = static_cast<int>(xg.C);
-        b.coef = static_cast<float*>(dev_alloc(4 * b.C * 4));
+        b.coef = static_cast<float*>(dev_alloc(5 * b.C * 4));
         if (b.training) {
             if (o.inputs[0] < 0) unsupported("training BatchNorm2d over a fused intermediate");
             b.x_binding = o.inputs[0];
@@ -880,7 +942,7 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
                                       static_cast<size_t>(dfp_reduce_blocks(b.pixels, b.C)) * b.C * 2 * 8 + 256);
         }
         bn_of_op_[k] = static_cast<int>(bn_.size());
-        if (4 * static_cast<int>(bn_.size()) + 3 >= DFP_MAX_P) unsupported("too many BatchNorms in one unit");
+        if (5 * static_cast<int>(bn_.size()) + 4 >= DFP_MAX_P) unsupported("too many BatchNorms in one unit");
         bn_.push_back(b);
     }
     if (std::any_of(bn_.begin(), bn_.end(), [](const BnPrep& b) { return b.training; })) {
@@ -1021,7 +1083,7 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
     }
     // parameter arrays: BN coefficient triples at P[3i..3i+2]
     for (size_t i = 0; i < bn_.size(); ++i) {
-        for (int k = 0; k < 4; ++k) tmpl_.P[4 * i + k] = bn_[i].coef + k * bn_[i].C;
+        for (int k = 0; k < 5; ++k) tmpl_.P[5 * i + k] = bn_[i].coef + k * bn_[i].C;
     }
     // algorithmic bytes: external activation inputs + output
     double bytes = binding_bytes(d.output);
@@ -1110,6 +1172,11 @@ std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
         }
     }
     const sol_unit_op& o0 = d.ops[0];
+    if (d.kind == 1 && d.n_ops > 1 && (o0.op == SOL_OP_CONV2D || o0.op == SOL_OP_LINEAR)) {
+        // heavy node + fused epilogue chain (plan-level fusion, see HeavyModule::parse_epilogue)
+        const Geo g = geo_b(d.bindings[o0.inputs[0]]);
+        if (o0.op == SOL_OP_LINEAR || !is_depthwise(o0, g.C)) return std::make_unique<HeavyModule>(d);
+    }
     if (d.n_ops == 1) {
         const int op = o0.op;
         if (is_heavy_op(op)) {

@@ -42,6 +42,7 @@ class OptimizeOptions:
     nccl_id: Optional[bytes] = None
     passes: bool = True        # reference rewrite pipeline (passes.cpp:168-178)
     keep_all: bool = False     # debug: every unit output persistent (no arena reuse)
+    fuse_epilogue: bool = False  # inference: fold BN(+Add)(+ReLU) units into the conv epilogue
 
 
 @dataclass
@@ -97,6 +98,9 @@ class OptimizedModel:
             cg = run_pipeline(cg)
         self.graph = cg
         self.units: List[ExecUnit] = partition(cg)
+        if options.fuse_epilogue and not options.train:
+            from .fusion import fuse_conv_epilogues
+            self.units = fuse_conv_epilogues(cg, self.units)
         self.params: Dict[str, np.ndarray] = {k: np.asarray(v, np.float32).copy() for k, v in g.params.items()}
         self._build_plan()
         self.compile_ms = (time.perf_counter() - t0) * 1e3

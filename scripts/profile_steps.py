@@ -6,7 +6,7 @@ from paper_2003_10688_b200 import frontend, models
 train = len(sys.argv) > 1 and sys.argv[1] == "train"
 B = 128 if train else 256
 g = models.resnet(50, hw=224, classes=1000, train=train)
-m = frontend.optimize(g, frontend.OptimizeOptions(batch=B, dtype="bf16", train=train))
+m = frontend.optimize(g, frontend.OptimizeOptions(batch=B, dtype="bf16", train=train, fuse_epilogue="fuse" in sys.argv))
 rng = np.random.default_rng(0)
 ins = {"x": rng.uniform(-1, 1, (B, 3, 224, 224)).astype(np.float32)}
 if train:

@@ -20,11 +20,12 @@ def _top1_ok(got, want, tol=1e-2):
 
 @pytest.mark.parametrize("name", ["small_cnn", "resnet18", "resnet50", "densenet", "mobilenet"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_predict(gpu, name, dtype):
+@pytest.mark.parametrize("fuse", [False, True], ids=["units", "fused"])
+def test_predict(gpu, name, dtype, fuse):
     from paper_2003_10688_b200 import frontend, graph
     batch = 4
     g = _graphs()[name](False)
-    m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype=dtype))
+    m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype=dtype, fuse_epilogue=fuse))
     ins = _inputs(graph.infer_shapes(g, batch), batch, seed=5)
     out = m.predict(ins)
     env = O.run_graph(graph.infer_shapes(g, batch), ins)
