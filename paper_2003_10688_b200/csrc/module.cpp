@@ -209,6 +209,7 @@ public:
             else unsupported("fused Add must combine the conv chain with a unit input");
             const Geo r = geo_b(d.bindings[res_idx_]);
             if (r.ld != out_.ld || r.pixels() != out_.pixels()) unsupported("residual layout mismatch");
+            algo_bytes += double(r.pixels()) * r.ld * elem_size(dtype_);  // the residual read
             ++k;
         }
         if (k < d.n_ops && (d.ops[k].op == SOL_OP_RELU || d.ops[k].op == SOL_OP_RELU6)) {

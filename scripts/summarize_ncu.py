@@ -1,0 +1,52 @@
+#!/usr/bin/env python3
+"""Summarise ncu CSV logs into markdown tables for profiles/ (launch list share per kernel; per
+launch DRAM traffic of the conv kernel)."""
+import csv
+import re
+import sys
+from collections import OrderedDict
+
+
+def rows(path):
+    with open(path) as f:
+        return list(csv.DictReader(l for l in f if l.startswith('"')))
+
+
+def short(name):
+    name = re.sub(r"\(.*$", "", name.replace("void ", "").replace("(anonymous namespace)::", ""))
+    return name.replace("unnamed>::", "")[:70]
+
+
+def by_launch(path):
+    out = OrderedDict()
+    for r in rows(path):
+        d = out.setdefault(r["ID"], {"name": r["Kernel Name"], "grid": r["Grid Size"], "block": r["Block Size"]})
+        d[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    return out
+
+
+def launch_table(path):
+    L = by_launch(path)
+    agg = OrderedDict()
+    for d in L.values():
+        a = agg.setdefault(short(d["name"]), [0, 0.0])
+        a[0] += 1
+        a[1] += d["gpu__time_duration.sum"]
+    tot = sum(a[1] for a in agg.values())
+    print(f"{len(L)} launches, {tot/1e6:.3f} ms total (serialised, cold-cache under ncu)\n")
+    print("| kernel | launches | total ms | share |\n|---|---:|---:|---:|")
+    for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"| `{k}` | {n} | {t/1e6:.3f} | {100*t/tot:.1f}% |")
+
+
+def traffic_table(path):
+    L = by_launch(path)
+    print("| # | kernel | us | DRAM read MB | DRAM write MB | DRAM GB/s |\n|---:|---|---:|---:|---:|---:|")
+    for i, d in L.items():
+        t = d["gpu__time_duration.sum"]
+        rd, wr = d["dram__bytes_read.sum"], d["dram__bytes_write.sum"]
+        print(f"| {i} | `{short(d['name'])}` | {t/1e3:.1f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {(rd+wr)/t:.0f} |")
+
+
+if __name__ == "__main__":
+    {"launches": launch_table, "traffic": traffic_table}[sys.argv[1]](sys.argv[2])
