@@ -96,6 +96,7 @@ struct DfpArgs {
     int out_ld = 0, out_coff = 0;
     int out_f32 = 0;               // output stored as f32 even in a bf16 plan
     double* partial = nullptr;     // FAM_CHAN_REDUCE: [blocks][C][2] (f64)
+    uint8_t* argmax = nullptr;     // FAM_MAXPOOL_BACK scratch: [windows][C] first-max tap (255 = none)
     int reduce_blocks = 0;
 };
 
@@ -118,6 +119,9 @@ enum FinalizeMode : int {
                         // coef[4C] = (mean_hi, mean_lo, gamma*rstd, beta) for PW_BN; optional running update
     FIN_SUMS = 1,       // out0[c] = S1, out1[c] = S2 (f32)
     FIN_BN_BACK = 2,    // dbeta = S1, dgamma = S2 (over xhat); coef[3C] for dx = dy*A + x*B + Cc
+    FIN_BN_BACK4 = 3,   // from bn_back_reduce's 4 sums: x statistics (mean, rstd) and the BN backward
+                        // sums in one pass; out0 = dbeta, out1 = dgamma, coef[3C] (A, B, Cc) and
+                        // xhat[3C] = (mean_hi, mean_lo, rstd) for bn_back_apply
 };
 struct FinalizeArgs {
     int mode = FIN_BN_STATS;
@@ -138,8 +142,18 @@ struct FinalizeArgs {
     float* coef = nullptr;
     float* out0 = nullptr;
     float* out1 = nullptr;
+    float* xhat = nullptr;         // FIN_BN_BACK4
 };
 void dfp_finalize(const FinalizeArgs& a, cudaStream_t s);
+
+// BatchNorm backward in two HBM passes (training; autodiff BNBackX/Gamma/Beta,
+// dfp_lower.cpp:709-753, 806-851): one reduction over (dy, x) producing, per channel and block,
+// [sum dy, sum dy*(x - shift), sum (x - shift), sum (x - shift)^2] (f64 partials [blocks][C][4]),
+// then (after FIN_BN_BACK4) dx = A*dy + B*xhat + Cc with xhat = ((x - mean_hi) - mean_lo) * rstd.
+void bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
+                    double* partial, int blocks, cudaStream_t s);
+void bn_back_apply(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* coef,
+                   const float* xhat, void* dx, cudaStream_t s);
 
 // BN inference coefficients for PW_BN: coef[4C] = (mean, 0, gamma/sqrt(var+eps), beta).
 void bn_infer_coef(const float* gamma, const float* beta, const float* mean, const float* var, float eps,

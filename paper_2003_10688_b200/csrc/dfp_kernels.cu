@@ -4,6 +4,8 @@
 #include "dfp.cuh"
 
 #include <algorithm>
+#include <cstring>
+#include <type_traits>
 
 namespace solb200 {
 namespace {
@@ -56,9 +58,26 @@ __device__ __forceinline__ void with_reg(int d, float (&R0)[V], float (&R1)[V], 
     }
 }
 
-template <typename T>
+__device__ __forceinline__ void unpack16(const uint4& r, float* v, __nv_bfloat16*) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ void unpack16(const uint4& r, float* v, float*) {
+    v[0] = __uint_as_float(r.x);
+    v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z);
+    v[3] = __uint_as_float(r.w);
+}
+
+// NP > 0: input slots 0..NP-1 were loaded up front (raw 16-byte vectors) by the caller, so every
+// global load of the program is in flight before any arithmetic starts.
+template <typename T, int NP = 0>
 __device__ __forceinline__ void run_prog(const Program& pg, const DfpArgs& a, int64_t pix, int n,
-                                         int c, float (&r)[NREG][VEC<T>]) {
+                                         int c, float (&r)[NREG][VEC<T>], const uint4* raw = nullptr) {
     constexpr int V = VEC<T>;
     float R0[V], R1[V], R2[V], R3[V];
 #pragma unroll
@@ -73,7 +92,16 @@ __device__ __forceinline__ void run_prog(const Program& pg, const DfpArgs& a, in
         const int op = ins.op;
         float ta[V], tb[V];
         if (op == PW_LD) {
-            load_in<T>(a, ins.a, pix, n, c, ta);
+            bool done = false;
+            if constexpr (NP > 0) {
+#pragma unroll
+                for (int k = 0; k < NP; ++k)
+                    if (ins.a == k) {
+                        unpack16(raw[k], ta, static_cast<T*>(nullptr));
+                        done = true;
+                    }
+            }
+            if (!done) load_in<T>(a, ins.a, pix, n, c, ta);
             with_reg<V>(ins.dst, R0, R1, R2, R3, [&](float (&x)[V]) {
 #pragma unroll
                 for (int i = 0; i < V; ++i) x[i] = ta[i];
@@ -203,6 +231,57 @@ __global__ void __launch_bounds__(THREADS) pointwise_kernel(const __grid_constan
     }
 }
 
+// Generic programs over plain pixel inputs: U positions per thread, the NP input vectors of all
+// of them loaded before the programs run (memory-level parallelism); 32-bit index math.
+template <typename T, int NP>
+__global__ void __launch_bounds__(THREADS) pointwise_pre_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    constexpr int U = 4;
+    const int cv = a.C / V;
+    const int hw = a.OH * a.OW;
+    const int total = a.N * hw * cv;
+    const int stride = gridDim.x * blockDim.x;
+    for (int v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < total; v0 += stride * U) {
+        uint4 raw[U][NP];
+        int pix[U], cc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int v = v0 + u * stride;
+            const int vv = v < total ? v : v0;
+            pix[u] = vv / cv;
+            cc[u] = (vv - pix[u] * cv) * V;
+#pragma unroll
+            for (int k = 0; k < NP; ++k)
+                raw[u][k] = __ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(a.in[k]) +
+                                                                 static_cast<int64_t>(pix[u]) * a.in_ld[k] +
+                                                                 a.in_coff[k] + cc[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (v0 + u * stride >= total) break;
+            float r[NREG][V];
+            run_prog<T, NP>(a.post, a, pix[u], pix[u] / hw, cc[u], r, raw[u]);
+            store_out<T>(a, pix[u], cc[u], r[0]);
+        }
+    }
+}
+
+template <typename T>
+bool launch_pointwise_pre(const DfpArgs& a, cudaStream_t s) {
+    constexpr int V = VEC<T>;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+    if (total > (int64_t(1) << 30) || a.n_in < 1 || a.n_in > 3) return false;
+    for (int k = 0; k < a.n_in; ++k)
+        if (a.in_kind[k] != IN_PIX || a.in_f32[k]) return false;
+    const unsigned grid = grid_for(ceil_div(total, 4), THREADS);
+    switch (a.n_in) {
+        case 1: pointwise_pre_kernel<T, 1><<<grid, THREADS, 0, s>>>(a); break;
+        case 2: pointwise_pre_kernel<T, 2><<<grid, THREADS, 0, s>>>(a); break;
+        default: pointwise_pre_kernel<T, 3><<<grid, THREADS, 0, s>>>(a); break;
+    }
+    return true;
+}
+
 // ---------------------------------------------------------------------------------------------
 // FAM_POINTWISE fast path: straight-line chains  y = act( bn0(x0) [+ bn1(x1)] )
 // (the BN / BN+Add / BN+Add+ReLU / BN+ReLU(6) / ReLU units that dominate CNN DFP traffic).
@@ -276,52 +355,108 @@ __device__ __forceinline__ void bn_apply(float* v, const float* const* P, int b,
     }
 }
 
+// Row-walking geometry shared by the channel-resident kernels: each thread owns one 16-byte
+// channel vector (per-channel coefficients stay in registers) and walks pixels; block = cvb
+// channel vectors x rows pixel lanes, grid = (pixel blocks, channel-vector blocks).
+struct RowGeo {
+    dim3 grid;
+};
+
+inline RowGeo row_geo(int C, int V, int64_t pixels, int per_thread = 4) {
+    const int cv_total = C / V;
+    const int cvb = std::min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int gy = static_cast<int>(ceil_div(cv_total, cvb));
+    const int64_t want = ceil_div(pixels, static_cast<int64_t>(rows) * per_thread);
+    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 32LL * num_sms() / gy)));
+    return RowGeo{dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy))};
+}
+
+// BN coefficients of one channel vector, held in registers
+template <typename T>
+struct BnRegs {
+    static constexpr int V = VEC<T>;
+    float k0[V], k1[V], k2[V], k3[V];
+    __device__ __forceinline__ void load(const float* const* P, int b, int c) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            if constexpr (sizeof(T) == 2) {
+                k0[i] = __ldg(P[b + 2] + c + i);  // scale
+                k1[i] = __ldg(P[b + 4] + c + i);  // shift
+            } else {
+                k0[i] = __ldg(P[b] + c + i);      // mean hi
+                k1[i] = __ldg(P[b + 1] + c + i);  // mean lo
+                k2[i] = __ldg(P[b + 2] + c + i);  // gamma * rstd
+                k3[i] = __ldg(P[b + 3] + c + i);  // beta
+            }
+        }
+    }
+    __device__ __forceinline__ void apply(float* v) const {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            if constexpr (sizeof(T) == 2) v[i] = fmaf(v[i], k0[i], k1[i]);
+            else v[i] = fmaf((v[i] - k0[i]) - k1[i], k2[i], k3[i]);
+        }
+    }
+};
+
+// y = act( bn0(x0) [+ bn1(x1)] )
 template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
 __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
     constexpr int V = VEC<T>;
-    constexpr int U = 2;
-    const int cv = a.C / V;
-    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
-    const T* x0 = static_cast<const T*>(a.in[cs.s0]);
-    const T* x1 = ADD ? static_cast<const T*>(a.in[cs.s1]) : nullptr;
+    constexpr int U = 4;
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int row = threadIdx.x / cvb;
+    const int cvi = threadIdx.x - row * cvb;
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
+    const T* x0 = static_cast<const T*>(a.in[cs.s0]) + c;
+    const T* x1 = ADD ? static_cast<const T*>(a.in[cs.s1]) + c : nullptr;
     const int ld0 = a.in_ld[cs.s0], ld1 = ADD ? a.in_ld[cs.s1] : 0;
-    T* out = static_cast<T*>(a.out);
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v0 < total; v0 += stride * U) {
-        float r0[U][V], r1[U][V];
-        int64_t pix[U];
-        int cc[U];
-        bool live[U];
+    T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    BnRegs<T> b0, b1;
+    if (BN0) b0.load(a.P, cs.bn0, c);
+    if (BN1) b1.load(a.P, cs.bn1, c);
+    const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
+    for (int64_t p0 = static_cast<int64_t>(blockIdx.x) * rows + row; p0 < P; p0 += step * U) {
+        uint4 r0[U], r1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t v = v0 + u * stride;
-            live[u] = v < total;
-            const int64_t vv = live[u] ? v : v0;
-            pix[u] = vv / cv;
-            cc[u] = static_cast<int>(vv - pix[u] * cv) * V;
-            load16(x0 + pix[u] * ld0 + cc[u], r0[u]);
-            if (ADD) load16(x1 + pix[u] * ld1 + cc[u], r1[u]);
+            const int64_t p = p0 + u * step;
+            if (p < P) {
+                r0[u] = __ldg(reinterpret_cast<const uint4*>(x0 + p * ld0));
+                if (ADD) r1[u] = __ldg(reinterpret_cast<const uint4*>(x1 + p * ld1));
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (BN0) bn_apply<T>(r0[u], a.P, cs.bn0, cc[u]);
+            const int64_t p = p0 + u * step;
+            if (p >= P) break;
+            float v[V];
+            unpack16(r0[u], v, static_cast<T*>(nullptr));
+            if (BN0) b0.apply(v);
             if (ADD) {
-                if (BN1) bn_apply<T>(r1[u], a.P, cs.bn1, cc[u]);
+                float w[V];
+                unpack16(r1[u], w, static_cast<T*>(nullptr));
+                if (BN1) b1.apply(w);
 #pragma unroll
-                for (int i = 0; i < V; ++i) r0[u][i] += r1[u][i];
+                for (int i = 0; i < V; ++i) v[i] += w[i];
             }
 #pragma unroll
             for (int i = 0; i < V; ++i) {
-                if (ACT >= 1) r0[u][i] = fmaxf(r0[u][i], 0.f);
-                if (ACT == 2) r0[u][i] = fminf(r0[u][i], 6.f);
+                if (ACT >= 1) v[i] = fmaxf(v[i], 0.f);
+                if (ACT == 2) v[i] = fminf(v[i], 6.f);
             }
-            if (live[u]) store16(out + pix[u] * a.out_ld + a.out_coff + cc[u], r0[u]);
+            store16(out + p * a.out_ld, v);
         }
     }
 }
 
 template <typename T, bool BN0, bool ADD, bool BN1>
-void chain_act(const DfpArgs& a, const ChainSpec& c, unsigned grid, cudaStream_t s) {
+void chain_act(const DfpArgs& a, const ChainSpec& c, dim3 grid, cudaStream_t s) {
     if (c.act == 0) chain_kernel<T, BN0, ADD, BN1, 0><<<grid, THREADS, 0, s>>>(a, c);
     else if (c.act == 1) chain_kernel<T, BN0, ADD, BN1, 1><<<grid, THREADS, 0, s>>>(a, c);
     else chain_kernel<T, BN0, ADD, BN1, 2><<<grid, THREADS, 0, s>>>(a, c);
@@ -333,9 +468,7 @@ bool launch_chain(const DfpArgs& a, cudaStream_t s) {
     if (!c.ok) return false;
     if (a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
     if (c.add && (a.in_kind[c.s1] != IN_PIX || a.in_coff[c.s1] != 0)) return false;
-    const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / VEC<T>);
-    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(work, 2 * THREADS), static_cast<int64_t>(num_sms()) * 8)));
+    const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW).grid;
     const bool b0 = c.bn0 >= 0, b1 = c.bn1 >= 0;
     if (!c.add) {
         if (b0) chain_act<T, true, false, false>(a, c, grid, s);
@@ -344,6 +477,139 @@ bool launch_chain(const DfpArgs& a, cudaStream_t s) {
     else if (b0) chain_act<T, true, true, false>(a, c, grid, s);
     else if (b1) chain_act<T, false, true, true>(a, c, grid, s);
     else chain_act<T, false, true, false>(a, c, grid, s);
+    return true;
+}
+
+// Gradient masks (ReluBack / ReLU6Back, optionally after a gradient Add):
+//   y = (m > 0 [&& m < 6]) ? (x0 [+ x1]) : 0
+// recognised by symbolic evaluation of the program, whatever registers it uses.
+struct MaskSpec {
+    int ok = 0, s0 = -1, s1 = -1, sm = -1, six = 0;
+};
+
+MaskSpec match_mask(const Program& p) {
+    // symbolic value of each register: LD(slot), ADD(LD, LD) or MASK(LD | ADD, LD)
+    struct Sym {
+        int kind = 0;  // 0 unknown, 1 LD, 2 ADD, 3 MASK
+        int s0 = -1, s1 = -1, sm = -1, six = 0;
+    };
+    Sym reg[NREG];
+    MaskSpec m;
+    for (int k = 0; k < p.n; ++k) {
+        const PwInstr& in = p.ins[k];
+        if (in.dst < 0 || in.dst >= NREG || in.a < 0 || in.b < 0) return m;
+        Sym r;
+        switch (in.op) {
+            case PW_LD:
+                r.kind = 1;
+                r.s0 = in.a;
+                break;
+            case PW_MOV:
+                if (in.a >= NREG) return m;
+                r = reg[in.a];
+                break;
+            case PW_ADD: {
+                if (in.a >= NREG || in.b >= NREG) return m;
+                const Sym &x = reg[in.a], &y = reg[in.b];
+                if (x.kind != 1 || y.kind != 1) return m;
+                r.kind = 2;
+                r.s0 = x.s0;
+                r.s1 = y.s0;
+                break;
+            }
+            case PW_MASK:
+            case PW_MASK6: {
+                if (in.a >= NREG || in.b >= NREG) return m;
+                const Sym &x = reg[in.a], &y = reg[in.b];
+                if ((x.kind != 1 && x.kind != 2) || y.kind != 1) return m;
+                r.kind = 3;
+                r.s0 = x.s0;
+                r.s1 = x.kind == 2 ? x.s1 : -1;
+                r.sm = y.s0;
+                r.six = in.op == PW_MASK6;
+                break;
+            }
+            default:
+                return m;
+        }
+        reg[in.dst] = r;
+    }
+    if (reg[0].kind != 3) return m;
+    m.ok = 1;
+    m.s0 = reg[0].s0;
+    m.s1 = reg[0].s1;
+    m.sm = reg[0].sm;
+    m.six = reg[0].six;
+    return m;
+}
+
+template <typename T, bool ADD, bool SIX>
+__global__ void __launch_bounds__(THREADS) mask_kernel(const __grid_constant__ DfpArgs a, MaskSpec ms) {
+    constexpr int V = VEC<T>;
+    constexpr int U = 4;
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int row = threadIdx.x / cvb;
+    const int cvi = threadIdx.x - row * cvb;
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
+    const T* x0 = static_cast<const T*>(a.in[ms.s0]) + a.in_coff[ms.s0] + c;
+    const T* x1 = ADD ? static_cast<const T*>(a.in[ms.s1]) + a.in_coff[ms.s1] + c : nullptr;
+    const T* xm = static_cast<const T*>(a.in[ms.sm]) + a.in_coff[ms.sm] + c;
+    const int ld0 = a.in_ld[ms.s0], ld1 = ADD ? a.in_ld[ms.s1] : 0, ldm = a.in_ld[ms.sm];
+    T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
+    for (int64_t p0 = static_cast<int64_t>(blockIdx.x) * rows + row; p0 < P; p0 += step * U) {
+        uint4 r0[U], r1[U], rm[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * step;
+            if (p < P) {
+                r0[u] = __ldg(reinterpret_cast<const uint4*>(x0 + p * ld0));
+                if (ADD) r1[u] = __ldg(reinterpret_cast<const uint4*>(x1 + p * ld1));
+                rm[u] = __ldg(reinterpret_cast<const uint4*>(xm + p * ldm));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * step;
+            if (p >= P) break;
+            float v[V], m[V];
+            unpack16(r0[u], v, static_cast<T*>(nullptr));
+            unpack16(rm[u], m, static_cast<T*>(nullptr));
+            if (ADD) {
+                float w[V];
+                unpack16(r1[u], w, static_cast<T*>(nullptr));
+#pragma unroll
+                for (int i = 0; i < V; ++i) v[i] += w[i];
+            }
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                const bool keep = SIX ? (m[i] > 0.f && m[i] < 6.f) : m[i] > 0.f;
+                v[i] = keep ? v[i] : 0.f;
+            }
+            store16(out + p * a.out_ld, v);
+        }
+    }
+}
+
+template <typename T>
+bool launch_mask(const DfpArgs& a, cudaStream_t s) {
+    const MaskSpec m = match_mask(a.post);
+    if (!m.ok) return false;
+    for (int sl : {m.s0, m.s1, m.sm})
+        if (sl >= 0 && (sl >= a.n_in || a.in_kind[sl] != IN_PIX)) return false;
+    const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW).grid;
+    const bool add = m.s1 >= 0;
+    if (add) {
+        if (m.six) mask_kernel<T, true, true><<<grid, THREADS, 0, s>>>(a, m);
+        else mask_kernel<T, true, false><<<grid, THREADS, 0, s>>>(a, m);
+    } else {
+        if (m.six) mask_kernel<T, false, true><<<grid, THREADS, 0, s>>>(a, m);
+        else mask_kernel<T, false, false><<<grid, THREADS, 0, s>>>(a, m);
+    }
     return true;
 }
 
@@ -604,108 +870,111 @@ __global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__
 // FAM_CHAN_REDUCE: per-channel S1 = sum r0, S2 = sum r0*r1 over all pixels of the source grid
 // ---------------------------------------------------------------------------------------------
 
-// Straight-line reductions for the programs the BN / bias-gradient modules emit:
-//   RED_STATS  r0 = x - shift            -> S1 = sum r0, S2 = sum r0^2    (batch statistics)
-//   RED_SUM    r0 = d                     -> S1 = sum d,  S2 = sum d^2     (bias / beta grads)
-//   RED_DGAMMA r0 = d, r1 = xhat(x)       -> S1 = sum d,  S2 = sum d*xhat  (BN backward)
-// Each thread accumulates 16 pixels in f32 (4 loads in flight) and folds them into f64.
-enum RedMode { RED_STATS = 0, RED_SUM = 1, RED_DGAMMA = 2 };
+// Per-channel reductions over the pixels of NHWC tensors (contiguous rows of C).
+//   RR_BNBACK (dy, x)  -> [sum dy, sum dy*(x-s), sum (x-s), sum (x-s)^2]  partial [blocks][C][4]
+//   RR_STATS  (x)      -> [sum (x-s), sum (x-s)^2]                         partial [blocks][C][2]
+//   RR_SUM    (d)      -> [sum d, sum d^2]                                 partial [blocks][C][2]
+// Threads of a block: cvb channel vectors x rows pixel lanes; each thread keeps UN pixels of every
+// input in flight (raw 16-byte registers), sums them in f32 and folds every UN pixels into the
+// thread accumulator: f64 for f32 plans (the 1e-5 bar), f32 for bf16 plans (8 channels per
+// thread; the block and grid combination is f64 either way).
+enum RRMode { RR_BNBACK = 0, RR_STATS = 1, RR_SUM = 2 };
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(THREADS) reduce_fast_kernel(const __grid_constant__ DfpArgs a, int s0, int s1,
-                                                              int parg) {
+__global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restrict__ x0, const T* __restrict__ x1,
+                                                               int C, int ld0, int ld1, int64_t P,
+                                                               const float* __restrict__ shift,
+                                                               double* __restrict__ partial) {
     constexpr int V = VEC<T>;
-    __shared__ double red[THREADS * V * 2];
-    const int cv_total = a.C / V;
+    constexpr int UN = 4;
+    constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
+    constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
+    __shared__ double red[THREADS * V];
+    const int cv_total = C / V;
     const int cvb = min(cv_total, THREADS);
     const int rows = THREADS / cvb;
     const int tid = threadIdx.x;
     const int row = tid / cvb;
     const int cvi = tid - row * cvb;
     const int c = (blockIdx.y * cvb + cvi) * V;
-    const int64_t P = static_cast<int64_t>(a.N) * a.H * a.W;
-    const int64_t per = ceil_div(P, gridDim.x);
+    const int64_t per = ceil_div(P, static_cast<int64_t>(gridDim.x));
     const int64_t p0 = blockIdx.x * per;
     const int64_t p1 = min(P, p0 + per);
-    double d1[V], d2[V];
+    using Acc = typename std::conditional<sizeof(T) == 2, float, double>::type;
+    Acc acc[NS][V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) d1[i] = d2[i] = 0.0;
+    for (int k = 0; k < NS; ++k)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[k][i] = Acc(0);
     const bool active = row < rows && (blockIdx.y * cvb + cvi) < cv_total;
     if (active) {
-        const T* x0 = static_cast<const T*>(a.in[s0]);
-        const T* x1 = MODE == RED_DGAMMA ? static_cast<const T*>(a.in[s1]) : nullptr;
-        const int ld0 = a.in_ld[s0], ld1 = MODE == RED_DGAMMA ? a.in_ld[s1] : 0;
-        float q0[V], q1[V], q2[V], q3[V];  // per-channel constants
+        float q[V];
 #pragma unroll
-        for (int i = 0; i < V; ++i) q0[i] = q1[i] = q2[i] = q3[i] = 0.f;
-        if (MODE == RED_STATS) {
+        for (int i = 0; i < V; ++i) q[i] = MODE == RR_SUM ? 0.f : __ldg(shift + c + i);
+        for (int64_t pb = p0 + row; pb < p1; pb += static_cast<int64_t>(rows) * UN) {
+            uint4 r0[UN], r1[UN];
 #pragma unroll
-            for (int i = 0; i < V; ++i) q0[i] = __ldg(a.P[parg] + c + i);
-        } else if (MODE == RED_DGAMMA) {
-#pragma unroll
-            for (int i = 0; i < V; ++i) {
-                q0[i] = __ldg(a.P[parg] + c + i);
-                q1[i] = __ldg(a.P[parg + 1] + c + i);
-                q2[i] = __ldg(a.P[parg + 2] + c + i);
-                q3[i] = __ldg(a.P[parg + 3] + c + i);
-            }
-        }
-        for (int64_t pb = p0 + row; pb < p1; pb += static_cast<int64_t>(rows) * 16) {
-            float f1[V], f2[V];
-#pragma unroll
-            for (int i = 0; i < V; ++i) f1[i] = f2[i] = 0.f;
-#pragma unroll 4
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < UN; ++u) {
                 const int64_t p = pb + static_cast<int64_t>(u) * rows;
-                if (p >= p1) break;
-                float v[V];
-                load16(x0 + p * ld0 + c, v);
-                if (MODE == RED_DGAMMA) {
-                    float w[V];
-                    load16(x1 + p * ld1 + c, w);
+                r0[u] = make_uint4(0, 0, 0, 0);
+                r1[u] = make_uint4(0, 0, 0, 0);
+                if (p < p1) {
+                    r0[u] = __ldg(reinterpret_cast<const uint4*>(x0 + p * ld0 + c));
+                    if (NI == 2) r1[u] = __ldg(reinterpret_cast<const uint4*>(x1 + p * ld1 + c));
+                }
+            }
+            float f[NS][V];
 #pragma unroll
-                    for (int i = 0; i < V; ++i) {
-                        const float xh = fmaf((w[i] - q0[i]) - q1[i], q2[i], q3[i]);
-                        f1[i] += v[i];
-                        f2[i] = fmaf(v[i], xh, f2[i]);
-                    }
-                } else {
+            for (int k = 0; k < NS; ++k)
 #pragma unroll
-                    for (int i = 0; i < V; ++i) {
-                        const float r = MODE == RED_STATS ? v[i] - q0[i] : v[i];
-                        f1[i] += r;
-                        f2[i] = fmaf(r, r, f2[i]);
+                for (int i = 0; i < V; ++i) f[k][i] = 0.f;
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                if (pb + static_cast<int64_t>(u) * rows >= p1) break;
+                float v0[V], v1[V];
+                unpack16(r0[u], v0, static_cast<T*>(nullptr));
+                if (NI == 2) unpack16(r1[u], v1, static_cast<T*>(nullptr));
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (MODE == RR_BNBACK) {
+                        const float xs = v1[i] - q[i];
+                        f[0][i] += v0[i];
+                        f[1][i] = fmaf(v0[i], xs, f[1][i]);
+                        f[2][i] += xs;
+                        f[3][i] = fmaf(xs, xs, f[3][i]);
+                    } else {
+                        const float xs = v0[i] - q[i];
+                        f[0][i] += xs;
+                        f[1][i] = fmaf(xs, xs, f[1][i]);
                     }
                 }
             }
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-                d1[i] += static_cast<double>(f1[i]);
-                d2[i] += static_cast<double>(f2[i]);
-            }
+            for (int k = 0; k < NS; ++k)
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[k][i] += static_cast<Acc>(f[k][i]);
         }
     }
+    // combine the pixel lanes of each channel vector, one sum at a time (fits static smem)
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-        red[(tid * V + i) * 2] = d1[i];
-        red[(tid * V + i) * 2 + 1] = d2[i];
-    }
-    __syncthreads();
-    if (row == 0 && active) {
-        for (int rr = 1; rr < rows; ++rr) {
-            const int t2 = rr * cvb + cvi;
+    for (int k = 0; k < NS; ++k) {
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-                d1[i] += red[(t2 * V + i) * 2];
-                d2[i] += red[(t2 * V + i) * 2 + 1];
+        for (int i = 0; i < V; ++i) red[tid * V + i] = static_cast<double>(acc[k][i]);
+        __syncthreads();
+        if (row == 0 && active) {
+            double t[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) t[i] = static_cast<double>(acc[k][i]);
+            for (int rr = 1; rr < rows; ++rr) {
+                const int t2 = rr * cvb + cvi;
+#pragma unroll
+                for (int i = 0; i < V; ++i) t[i] += red[t2 * V + i];
             }
-        }
-        double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * a.C + c) * 2;
+            double* dst = partial + (static_cast<int64_t>(blockIdx.x) * C + c) * NS + k;
 #pragma unroll
-        for (int i = 0; i < V; ++i) {
-            dst[2 * i] = d1[i];
-            dst[2 * i + 1] = d2[i];
+            for (int i = 0; i < V; ++i) dst[NS * i] = t[i];
         }
+        __syncthreads();
     }
 }
 
@@ -716,15 +985,19 @@ bool launch_reduce_fast(const DfpArgs& a, dim3 grid, cudaStream_t s) {
     auto is = [&](int k, PwOp op, int dst) { return k < p.n && p.ins[k].op == op && p.ins[k].dst == dst; };
     if (p.n == 5 && is(0, PW_LD, 0) && is(1, PW_PARAM, 1) && is(2, PW_SCALE, 1) && p.ins[2].imm == -1.f &&
         is(3, PW_ADD, 0) && p.ins[3].a == 0 && p.ins[3].b == 1 && is(4, PW_MOV, 1) && p.ins[4].a == 0) {
-        reduce_fast_kernel<T, RED_STATS><<<grid, THREADS, 0, s>>>(a, p.ins[0].a, 0, p.ins[1].arg);
+        const int sl = p.ins[0].a;
+        if (a.in_kind[sl] != IN_PIX) return false;
+        rowreduce_kernel<T, RR_STATS><<<grid, THREADS, 0, s>>>(static_cast<const T*>(a.in[sl]), nullptr, a.C,
+                                                               a.in_ld[sl], 0, static_cast<int64_t>(a.N) * a.H * a.W,
+                                                               a.P[p.ins[1].arg], a.partial);
         return true;
     }
     if (p.n == 2 && is(0, PW_LD, 0) && is(1, PW_MOV, 1) && p.ins[1].a == 0) {
-        reduce_fast_kernel<T, RED_SUM><<<grid, THREADS, 0, s>>>(a, p.ins[0].a, 0, 0);
-        return true;
-    }
-    if (p.n == 3 && is(0, PW_LD, 0) && is(1, PW_LD, 1) && is(2, PW_BN, 1)) {
-        reduce_fast_kernel<T, RED_DGAMMA><<<grid, THREADS, 0, s>>>(a, p.ins[0].a, p.ins[1].a, p.ins[2].arg);
+        const int sl = p.ins[0].a;
+        if (a.in_kind[sl] != IN_PIX) return false;
+        rowreduce_kernel<T, RR_SUM><<<grid, THREADS, 0, s>>>(static_cast<const T*>(a.in[sl]), nullptr, a.C,
+                                                             a.in_ld[sl], 0, static_cast<int64_t>(a.N) * a.H * a.W,
+                                                             nullptr, a.partial);
         return true;
     }
     return false;
@@ -792,6 +1065,63 @@ __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_const
 // (reference.cpp:294-327; dfp_lower.cpp:546-610).
 // ---------------------------------------------------------------------------------------------
 
+// First-max tap per (window, channel) in (kh, kw) scan order; 255 when the max does not exceed
+// min_init (the fused-ReLU clamp routes nothing). One pass over x; the gather below then reads one
+// byte per (window, channel) instead of re-scanning every window for each of its inputs.
+template <typename T>
+__global__ void __launch_bounds__(THREADS) maxpool_argmax_kernel(const __grid_constant__ DfpArgs a) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
+    const T* x = static_cast<const T*>(a.in[a.pool_x]);
+    const int ldx = a.in_ld[a.pool_x];
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t opix = v / cv;
+        const int c = static_cast<int>(v - opix * cv) * V;
+        const int ow = static_cast<int>(opix % a.OW);
+        const int64_t t = opix / a.OW;
+        const int oh = static_cast<int>(t % a.OH);
+        const int n = static_cast<int>(t / a.OH);
+        float best[V];
+        uint8_t bidx[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            best[i] = -INFINITY;
+            bidx[i] = 255;
+        }
+        for (int kh = 0; kh < a.kh; ++kh) {
+            const int hh = oh * a.sh - a.ph + kh;
+            if (hh < 0 || hh >= a.H) continue;
+            for (int kw = 0; kw < a.kw; ++kw) {
+                const int ww = ow * a.sw - a.pw + kw;
+                if (ww < 0 || ww >= a.W) continue;
+                float xv[V];
+                load16(x + ((static_cast<int64_t>(n) * a.H + hh) * a.W + ww) * ldx + c, xv);
+#pragma unroll
+                for (int i = 0; i < V; ++i)
+                    if (xv[i] > best[i]) {
+                        best[i] = xv[i];
+                        bidx[i] = static_cast<uint8_t>(kh * a.kw + kw);
+                    }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+            if (!(best[i] > a.min_init)) bidx[i] = 255;
+        uint8_t* dst = a.argmax + opix * a.C + c;
+        if constexpr (V == 8) {
+            uint2 r;
+            memcpy(&r, bidx, 8);
+            *reinterpret_cast<uint2*>(dst) = r;
+        } else {
+            uint32_t r;
+            memcpy(&r, bidx, 4);
+            *reinterpret_cast<uint32_t*>(dst) = r;
+        }
+    }
+}
+
 template <typename T, bool IS_MAX>
 __global__ void __launch_bounds__(THREADS) pool_back_kernel(const __grid_constant__ DfpArgs a) {
     constexpr int V = VEC<T>;
@@ -820,32 +1150,23 @@ __global__ void __launch_bounds__(THREADS) pool_back_kernel(const __grid_constan
                 const int64_t opix = (static_cast<int64_t>(n) * a.OH + oh) * a.OW + ow;
                 float take[V];
                 if (IS_MAX) {
-                    float best[V];
-                    int bidx[V];
-#pragma unroll
-                    for (int i = 0; i < V; ++i) {
-                        best[i] = -INFINITY;
-                        bidx[i] = -1;
-                    }
-                    for (int kh = 0; kh < a.kh; ++kh) {
-                        const int hh = oh * a.sh - a.ph + kh;
-                        if (hh < 0 || hh >= a.H) continue;
-                        for (int kw = 0; kw < a.kw; ++kw) {
-                            const int ww = ow * a.sw - a.pw + kw;
-                            if (ww < 0 || ww >= a.W) continue;
-                            float xv[V];
-                            load_in<T>(a, a.pool_x, (static_cast<int64_t>(n) * a.H + hh) * a.W + ww, n, c, xv);
-#pragma unroll
-                            for (int i = 0; i < V; ++i)
-                                if (xv[i] > best[i]) {
-                                    best[i] = xv[i];
-                                    bidx[i] = kh * a.kw + kw;
-                                }
-                        }
+                    // first-max tap of this window, computed once per window by maxpool_argmax_kernel
+                    uint8_t idx[V];
+                    if constexpr (V == 8) {
+                        const uint2 r = __ldg(reinterpret_cast<const uint2*>(a.argmax + opix * a.C + c));
+                        memcpy(idx, &r, 8);
+                    } else {
+                        const uint32_t r = __ldg(reinterpret_cast<const uint32_t*>(a.argmax + opix * a.C + c));
+                        memcpy(idx, &r, 4);
                     }
                     const int me = dkh * a.kw + dkw;
+                    bool any = false;
 #pragma unroll
-                    for (int i = 0; i < V; ++i) take[i] = (bidx[i] == me && best[i] > a.min_init) ? 1.f : 0.f;
+                    for (int i = 0; i < V; ++i) {
+                        take[i] = idx[i] == me ? 1.f : 0.f;
+                        any |= idx[i] == me;
+                    }
+                    if (!any) continue;
                 } else {
                     int cnt = a.kh * a.kw;
                     if (!a.count_padding) {
@@ -883,6 +1204,8 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
     switch (a.family) {
         case FAM_POINTWISE: {
             if (launch_chain<T>(a, s)) break;
+            if (launch_mask<T>(a, s)) break;
+            if (launch_pointwise_pre<T>(a, s)) break;
             const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
             pointwise_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
@@ -915,6 +1238,9 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
             break;
         }
         case FAM_MAXPOOL_BACK: {
+            if (a.argmax == nullptr || a.kh * a.kw > 254) throw std::invalid_argument("dfp: maxpool backward needs argmax scratch");
+            const int64_t windows = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+            maxpool_argmax_kernel<T><<<grid_for(windows, THREADS), THREADS, 0, s>>>(a);
             const int64_t work = static_cast<int64_t>(a.N) * a.H * a.W * (a.C / V);
             pool_back_kernel<T, true><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
@@ -1004,6 +1330,61 @@ __global__ void softmax_back_kernel(const T* __restrict__ d, const T* __restrict
 }
 
 // ---------------------------------------------------------------------------------------------
+// BatchNorm backward: one reduction pass over (dy, x), one apply pass
+// ---------------------------------------------------------------------------------------------
+
+
+// dx = A*dy + B*xhat + Cc, xhat = ((x - mean_hi) - mean_lo) * rstd. Each thread owns one channel
+// vector (coefficients in registers) and walks pixels; U pixels of both inputs in flight.
+template <typename T>
+__global__ void __launch_bounds__(THREADS) bnback_apply_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                               int C, int64_t P, const float* __restrict__ coef,
+                                                               const float* __restrict__ xh, T* __restrict__ dx) {
+    constexpr int V = VEC<T>;
+    constexpr int U = 4;
+    const int cv_total = C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int row = threadIdx.x / cvb;
+    const int cvi = threadIdx.x - row * cvb;
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    float A[V], B[V], D[V], mh[V], ml[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const float rstd = __ldg(xh + 2 * C + c + i);
+        A[i] = __ldg(coef + c + i);
+        B[i] = __ldg(coef + C + c + i) * rstd;  // B * xhat = (B * rstd) * ((x - mh) - ml)
+        D[i] = __ldg(coef + 2 * C + c + i);
+        mh[i] = __ldg(xh + c + i);
+        ml[i] = __ldg(xh + C + c + i);
+    }
+    const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
+    for (int64_t p0 = static_cast<int64_t>(blockIdx.x) * rows + row; p0 < P; p0 += step * U) {
+        uint4 rd[U], rx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * step;
+            if (p < P) {
+                rd[u] = __ldg(reinterpret_cast<const uint4*>(dy + p * C + c));
+                rx[u] = __ldg(reinterpret_cast<const uint4*>(x + p * C + c));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * step;
+            if (p >= P) break;
+            float dv[V], xv[V], o[V];
+            unpack16(rd[u], dv, static_cast<T*>(nullptr));
+            unpack16(rx[u], xv, static_cast<T*>(nullptr));
+#pragma unroll
+            for (int i = 0; i < V; ++i) o[i] = fmaf(dv[i], A[i], fmaf((xv[i] - mh[i]) - ml[i], B[i], D[i]));
+            store16(dx + p * C + c, o);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // finalisation of per-channel partial sums (f64)
 // ---------------------------------------------------------------------------------------------
 
@@ -1011,6 +1392,39 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= a.C) return;
     const int cs = a.Cstride > 0 ? a.Cstride : a.C;
+    if (a.mode == FIN_BN_BACK4) {
+        double sd = 0.0, sdx = 0.0, sx = 0.0, sxx = 0.0;
+        for (int b = 0; b < a.blocks; ++b) {
+            const double* q = a.partial + (static_cast<int64_t>(b) * cs + c) * 4;
+            sd += q[0];
+            sdx += q[1];
+            sx += q[2];
+            sxx += q[3];
+        }
+        const double m = a.count;
+        const double d = sx / m;  // mean - shift
+        double var = sxx / m - d * d;
+        if (var < 0) var = 0;
+        const double mean = static_cast<double>(a.shift[c]) + d;
+        const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
+        const double s1 = sd;                    // sum dy                 (dbeta)
+        const double s2 = rstd * (sdx - d * sd);  // sum dy * xhat         (dgamma)
+        if (a.out0) a.out0[c] = static_cast<float>(s1);
+        if (a.out1) a.out1[c] = static_cast<float>(s2);
+        if (a.coef) {
+            const double gr = static_cast<double>(a.gamma[c]) * rstd;
+            a.coef[c] = static_cast<float>(gr);
+            a.coef[a.C + c] = static_cast<float>(-gr * s2 / m);
+            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
+        }
+        if (a.xhat) {
+            const float hi = static_cast<float>(mean);
+            a.xhat[c] = hi;
+            a.xhat[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
+            a.xhat[2 * a.C + c] = static_cast<float>(rstd);
+        }
+        return;
+    }
     double s1 = 0.0, s2 = 0.0;
     for (int b = 0; b < a.blocks; ++b) {
         s1 += a.partial[(static_cast<int64_t>(b) * cs + c) * 2];
@@ -1138,6 +1552,44 @@ int dfp_reduce_blocks(int64_t pixels, int C) {
     const int64_t want = ceil_div(pixels * cvec, static_cast<int64_t>(256) * 32 * gy);
     const int64_t cap = std::max<int64_t>(1, 4 * num_sms() / gy);
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, cap, pixels})));
+}
+
+void bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
+                    double* partial, int blocks, cudaStream_t s) {
+    const int V = dtype == DT_BF16 ? 8 : 4;
+    if (C % V != 0) throw std::invalid_argument("bn_back_reduce: channel count must be a multiple of 16 bytes");
+    const int cv_total = C / V;
+    const int cvb = std::min(cv_total, THREADS);
+    dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ceil_div(cv_total, cvb)));
+    if (dtype == DT_BF16)
+        rowreduce_kernel<__nv_bfloat16, RR_BNBACK><<<grid, THREADS, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), C, C, C, pixels, shift, partial);
+    else
+        rowreduce_kernel<float, RR_BNBACK><<<grid, THREADS, 0, s>>>(static_cast<const float*>(dy),
+                                                                   static_cast<const float*>(x), C, C, C, pixels, shift,
+                                                                   partial);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void bn_back_apply(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* coef,
+                   const float* xhat, void* dx, cudaStream_t s) {
+    const int V = dtype == DT_BF16 ? 8 : 4;
+    const int cv_total = C / V;
+    const int cvb = std::min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int gy = static_cast<int>(ceil_div(cv_total, cvb));
+    // ~4 waves of 8 blocks per SM, each thread covering >= 4 pixels
+    const int64_t want = ceil_div(pixels, static_cast<int64_t>(rows) * 4);
+    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 32LL * num_sms() / gy)));
+    dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+    if (dtype == DT_BF16)
+        bnback_apply_kernel<__nv_bfloat16><<<grid, THREADS, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), C, pixels, coef, xhat,
+            static_cast<__nv_bfloat16*>(dx));
+    else
+        bnback_apply_kernel<float><<<grid, THREADS, 0, s>>>(static_cast<const float*>(dy), static_cast<const float*>(x),
+                                                           C, pixels, coef, xhat, static_cast<float*>(dx));
+    SOL_CUDA(cudaGetLastError());
 }
 
 void dfp_launch(const DfpArgs& a, cudaStream_t s) {

@@ -289,14 +289,17 @@ public:
             }
             case SOL_OP_CONV2DBACKX:
             case SOL_OP_LINEARBACKX: {
+                // stride 1: dx = conv(dy, mirrored transposed taps, padding k-1-p), which runs on the
+                // forward kernels' TMA (1x1) / TMA-im2col (k x k) operand paths
+                const bool as_fprop = sh_ == 1 && sw_ == 1 && ph_ <= kh_ - 1 && pw_ <= kw_ - 1;
                 if (!(frozen && packed_valid_)) {
                     pack_conv_weight_t(static_cast<const float*>(args[w_idx_]), packed_, dtype_,
                                        static_cast<int>(cout_), static_cast<int>(cin_), kh_, kw_,
-                                       static_cast<int>(in_.ld), kpad_, s);
+                                       static_cast<int>(in_.ld), kpad_, s, as_fprop);
                     packed_valid_ = true;
                 }
                 IgemmArgs g;
-                g.mode = (sh_ == 1 && sw_ == 1 && ph_ == 0 && pw_ == 0 && kh_ == 1 && kw_ == 1) ? IG_FPROP : IG_DGRAD;
+                g.mode = as_fprop ? IG_FPROP : IG_DGRAD;
                 g.dtype = dtype_;
                 g.out_dtype = dtype_;
                 g.src = args[0];
@@ -308,7 +311,9 @@ public:
                 g.SC = static_cast<int>(in_.ld);
                 g.OH = static_cast<int>(out_.H);
                 g.OW = static_cast<int>(out_.W);
-                g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
+                g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_;
+                g.ph = as_fprop ? kh_ - 1 - ph_ : ph_;
+                g.pw = as_fprop ? kw_ - 1 - pw_ : pw_;
                 g.Nout = static_cast<int>(cin_);
                 g.K_pad = kpad_;
                 g.ldo = static_cast<int>(out_.ld);
@@ -504,26 +509,21 @@ public:
         if (needs_x && C_ != Creal_) unsupported("BatchNorm backward over padded channel storage");
         if (needs_x) {
             x_idx_ = o.inputs[1];
-            ones_ = static_cast<float*>(dev_alloc(C_ * 4));
-            std::vector<float> ones(C_, 1.f);
-            SOL_CUDA(cudaMemcpy(ones_, ones.data(), C_ * 4, cudaMemcpyHostToDevice));
-            zeros_ = static_cast<float*>(dev_alloc(C_ * 4));
             shift_ = static_cast<float*>(dev_alloc(C_ * 4));
-            stats_ = static_cast<float*>(dev_alloc(2 * C_ * 4));
-            xhat_ = static_cast<float*>(dev_alloc(5 * C_ * 4));
+            xhat_ = static_cast<float*>(dev_alloc(3 * C_ * 4));
             coef_ = static_cast<float*>(dev_alloc(3 * C_ * 4));
             gamma_idx_ = o.n_params > 0 ? o.params[0] : -1;
         }
         switch (op_) {
-            case SOL_OP_BATCHNORMBACKX: family = "bn_back_x"; launches = 7; break;
-            case SOL_OP_BATCHNORMBACKGAMMA: family = "bn_back_gamma"; launches = 6; break;
+            case SOL_OP_BATCHNORMBACKX: family = "bn_back_x"; launches = 4; break;
+            case SOL_OP_BATCHNORMBACKGAMMA: family = "bn_back_gamma"; launches = 3; break;
             case SOL_OP_BATCHNORMBACKBETA: family = "bn_back_beta"; launches = 2; break;
             default: family = "bias_grad"; launches = 2; break;
         }
         const double es = double(elem_size(dtype_));
         algo_bytes = delta_.numel() * es * (needs_x ? 2 : 1) + (op_ == SOL_OP_BATCHNORMBACKX ? delta_.numel() * es : 0);
     }
-    size_t scratch_bytes() const override { return static_cast<size_t>(blocks_) * C_ * 2 * 8 + 256; }
+    size_t scratch_bytes() const override { return static_cast<size_t>(blocks_) * C_ * 4 * 8 + 256; }
 
     DfpArgs base(void* const* args, double* partial) const {
         DfpArgs a;
@@ -547,32 +547,6 @@ public:
         return a;
     }
 
-    // x statistics -> xhat coefficients (rstd, -mean*rstd) and (mean, rstd)
-    void x_stats(void* const* args, double* partial, cudaStream_t s) {
-        bn_shift(dtype_, args[x_idx_], C_, C_, shift_, s);
-        DfpArgs a = base(args, partial);
-        a.P[0] = shift_;
-        push(a.pre, PW_LD, 0, 1);                  // r0 = x
-        push(a.pre, PW_PARAM, 1, 0, 0, 0);         // r1 = shift
-        push(a.pre, PW_SCALE, 1, 0, 0, 0, -1.f);   // r1 = -shift
-        push(a.pre, PW_ADD, 0, 0, 1);              // r0 = x - shift
-        push(a.pre, PW_MOV, 1, 0);                 // r1 = r0
-        dfp_launch(a, s);
-        FinalizeArgs f;
-        f.mode = FIN_BN_STATS;
-        f.C = C_;
-        f.blocks = blocks_;
-        f.partial = partial;
-        f.count = static_cast<double>(delta_.pixels());
-        f.eps = eps_;
-        f.shift = shift_;
-        f.gamma = ones_;
-        f.beta = zeros_;
-        f.stats_out = stats_;
-        f.coef = xhat_;  // (mean, rstd, 0): PW_BN gives xhat
-        dfp_finalize(f, s);
-    }
-
     void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool) override {
         if (nargs != n_args) throw std::invalid_argument("reduce module: wrong argument count");
         double* partial = static_cast<double*>(scratch);
@@ -592,25 +566,17 @@ public:
             dfp_finalize(f, s);
             return;
         }
-        x_stats(args, partial, s);
-        // S1 = sum delta, S2 = sum delta * xhat
-        DfpArgs a = base(args, partial);
-        a.P[0] = xhat_;
-        a.P[1] = xhat_ + C_;
-        a.P[2] = xhat_ + 2 * C_;
-        a.P[3] = xhat_ + 3 * C_;
-        a.pre = Program();
-        push(a.pre, PW_LD, 0, 0);      // r0 = delta
-        push(a.pre, PW_LD, 1, 1);      // r1 = x
-        push(a.pre, PW_BN, 1, 0, 0, 0);   // r1 = xhat = (x - mean) * rstd
-        dfp_launch(a, s);
+        // BNBackX / BNBackGamma: one pass over (dy, x) gives the x statistics and both sums
+        bn_shift(dtype_, args[x_idx_], C_, C_, shift_, s);
+        bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), shift_, partial, blocks_, s);
         FinalizeArgs f;
-        f.mode = FIN_BN_BACK;
+        f.mode = FIN_BN_BACK4;
         f.C = C_;
         f.blocks = blocks_;
         f.partial = partial;
         f.count = static_cast<double>(delta_.pixels());
-        f.stats = stats_;
+        f.eps = eps_;
+        f.shift = shift_;
         if (op_ == SOL_OP_BATCHNORMBACKGAMMA) {
             f.out1 = out;
             dfp_finalize(f, s);
@@ -618,31 +584,9 @@ public:
         }
         f.gamma = static_cast<const float*>(args[gamma_idx_]);
         f.coef = coef_;
+        f.xhat = xhat_;
         dfp_finalize(f, s);
-        // dx = delta*A + x*B + Cc
-        DfpArgs p;
-        p.family = FAM_POINTWISE;
-        p.dtype = dtype_;
-        p.N = static_cast<int>(delta_.N);
-        p.H = p.OH = static_cast<int>(delta_.H);
-        p.W = p.OW = static_cast<int>(delta_.W);
-        p.C = C_;
-        p.n_in = 2;
-        p.in[0] = args[0];
-        p.in_ld[0] = C_;
-        p.in[1] = args[x_idx_];
-        p.in_ld[1] = C_;
-        p.P[0] = coef_;
-        p.P[1] = coef_ + C_;
-        p.P[2] = coef_ + 2 * C_;
-        for (int k = 0; k < 5; ++k) p.P[3 + k] = xhat_ + k * C_;
-        push(p.post, PW_LD, 0, 0);           // r0 = delta
-        push(p.post, PW_LD, 1, 1);           // r1 = x
-        push(p.post, PW_BN, 1, 0, 0, 3);     // r1 = xhat
-        push(p.post, PW_AXPBY, 0, 0, 1, 0);  // r0 = delta*A + xhat*B + Cc
-        p.out = out;
-        p.out_ld = C_;
-        dfp_launch(p, s);
+        bn_back_apply(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), coef_, xhat_, out, s);
     }
 
 private:
@@ -654,8 +598,7 @@ private:
     int C_ = 0, Creal_ = 0;
     int blocks_ = 1;
     int x_idx_ = -1, gamma_idx_ = -1;
-    float *ones_ = nullptr, *zeros_ = nullptr, *shift_ = nullptr, *stats_ = nullptr, *xhat_ = nullptr,
-          *coef_ = nullptr;
+    float *shift_ = nullptr, *xhat_ = nullptr, *coef_ = nullptr;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -712,6 +655,7 @@ private:
     int dtype_;
     int anchor_ = -1;
     size_t stats_scratch_ = 0;
+    size_t argmax_offset_ = 0;
     bool coef_ready_ = false;
     float* ones_ = nullptr;
     float* zeros_ = nullptr;
@@ -1043,6 +987,9 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
                 if (a.op == SOL_OP_MAXPOOL2DBACK) {
                     if (a.inputs[1] < 0) unsupported("MaxPool2dBack over a fused forward input");
                     tmpl_.pool_x = slot_for(a.inputs[1], IN_PIX, 0);
+                    // one argmax byte per (window, channel)
+                    argmax_offset_ = (stats_scratch_ + 255) / 256 * 256;
+                    stats_scratch_ = argmax_offset_ + static_cast<size_t>(src.pixels()) * tmpl_.C;
                 }
                 family = a.op == SOL_OP_MAXPOOL2DBACK ? "dfp_maxpool_back" : "dfp_avgpool_back";
                 break;
@@ -1156,6 +1103,7 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
         a.dw_b = dw_[0].bias >= 0 ? static_cast<const float*>(args[dw_[0].bias]) : nullptr;
     }
     a.out = args[nargs - 1];
+    if (a.family == FAM_MAXPOOL_BACK) a.argmax = static_cast<uint8_t*>(scratch) + argmax_offset_;
     dfp_launch(a, s);
 }
 

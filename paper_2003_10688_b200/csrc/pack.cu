@@ -25,10 +25,11 @@ __global__ void pack_fwd_kernel(const float* __restrict__ w, T* __restrict__ p, 
     }
 }
 
-// packed_t[ci][(kh*KW + kw)*ld_o + co] = w[co][ci][kh][kw]  (dgrad B operand)
+// packed_t[ci][(kh*KW + kw)*ld_o + co] = w[co][ci][kh][kw]  (dgrad B operand); with flip the
+// taps are mirrored, w[co][ci][KH-1-kh][KW-1-kw], so a stride-1 dgrad runs as a forward conv of dy
 template <typename T>
 __global__ void pack_t_kernel(const float* __restrict__ w, T* __restrict__ p, int Cout, int Cin, int KH, int KW,
-                              int ld_o, int kpad) {
+                              int ld_o, int kpad, bool flip) {
     const int64_t total = static_cast<int64_t>(Cin) * kpad;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -37,7 +38,11 @@ __global__ void pack_t_kernel(const float* __restrict__ w, T* __restrict__ p, in
         const int tap = k / ld_o, co = k - tap * ld_o;
         float v = 0.f;
         if (tap < KH * KW && co < Cout) {
-            const int kh = tap / KW, kw = tap - kh * KW;
+            int kh = tap / KW, kw = tap - kh * KW;
+            if (flip) {
+                kh = KH - 1 - kh;
+                kw = KW - 1 - kw;
+            }
             v = w[((static_cast<int64_t>(co) * Cin + ci) * KH + kh) * KW + kw];
         }
         p[i] = from_f32<T>(v);
@@ -84,12 +89,13 @@ void pack_conv_weight(const float* w, void* packed, int dtype, int Cout, int Cin
 }
 
 void pack_conv_weight_t(const float* w, void* packed, int dtype, int Cout, int Cin, int kh, int kw, int ld_o,
-                        int kpad, cudaStream_t s) {
+                        int kpad, cudaStream_t s, bool flip) {
     const int64_t n = static_cast<int64_t>(Cin) * kpad;
     if (dtype == DT_BF16)
-        pack_t_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<__nv_bfloat16*>(packed), Cout, Cin, kh, kw, ld_o, kpad);
+        pack_t_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<__nv_bfloat16*>(packed), Cout, Cin, kh, kw, ld_o, kpad,
+                                                 flip);
     else
-        pack_t_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<float*>(packed), Cout, Cin, kh, kw, ld_o, kpad);
+        pack_t_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<float*>(packed), Cout, Cin, kh, kw, ld_o, kpad, flip);
     SOL_CUDA(cudaGetLastError());
 }
 

@@ -9,7 +9,7 @@ namespace solb200 {
 void pack_conv_weight(const float* w, void* packed, int dtype, int Cout, int Cin, int kh, int kw, int ld, int kpad,
                       cudaStream_t s);
 void pack_conv_weight_t(const float* w, void* packed, int dtype, int Cout, int Cin, int kh, int kw, int ld_o,
-                        int kpad, cudaStream_t s);
+                        int kpad, cudaStream_t s, bool flip = false);
 void unpack_conv_grad(const float* packed, float* w, int Cout, int Cin, int kh, int kw, int ld, cudaStream_t s);
 void pack_dw_weight(const float* w, float* packed, int C, int kh, int kw, cudaStream_t s);
 

@@ -75,17 +75,21 @@ def test_train_step(gpu, name, hw, dtype):
         worst.append((cos, p))
     worst.sort()
     weights = [w for w in worst if g.params[w[1]].ndim >= 2]
-    # conditioning floor: the oracle's own gradient cosine when its weights carry the operand
-    # rounding of the tensor-core path (TF32 ~5e-4, bf16 ~2e-3 relative). Deep random-init
-    # BatchNorm nets are ill-conditioned (ResNet-50 here: ~0.7 / ~0.3), so the bar is relative.
-    rel = 5e-4 if dtype == "f32" else 2e-3
-    rng = np.random.default_rng(1)
+    # conditioning floor: the oracle's own gradient cosine when its weights carry the rounding of
+    # the tensor-core path (TF32 ~5e-4 relative; bf16 4e-3: bf16 rounds the weights AND every
+    # stored activation, 2^-9 each), worst of two perturbations. Deep random-init BatchNorm nets are
+    # ill-conditioned (ResNet-50 here: ~0.7 / ~0.3), so the bar is relative to this floor.
+    rel = 5e-4 if dtype == "f32" else 4e-3
     gp = graph.infer_shapes(tg.graph, batch)
-    gp.params = {k: (v * (1 + rel * rng.standard_normal(v.shape))).astype(np.float32) for k, v in g.params.items()}
-    env2 = O.run_graph(gp, ins)
-    floor = min(float(np.dot(env[gn].ravel(), env2[gn].ravel()) /
-                      (np.linalg.norm(env[gn]) * np.linalg.norm(env2[gn]) + 1e-30))
-                for p, gn in tg.param_grads if g.params[p].ndim >= 2)
+    floor = 1.0
+    for seed in (1, 2):
+        rng = np.random.default_rng(seed)
+        gp.params = {k: (v * (1 + rel * rng.standard_normal(v.shape))).astype(np.float32)
+                     for k, v in g.params.items()}
+        env2 = O.run_graph(gp, ins)
+        floor = min(floor, min(float(np.dot(env[gn].ravel(), env2[gn].ravel()) /
+                                     (np.linalg.norm(env[gn]) * np.linalg.norm(env2[gn]) + 1e-30))
+                               for p, gn in tg.param_grads if g.params[p].ndim >= 2))
     print(f"{name} {dtype}: min grad cosine conv/linear {weights[0][0]:.4f} "
           f"(oracle self-consistency under operand rounding {floor:.4f}), all params {worst[0][0]:.4f}")
     assert weights[0][0] >= min(0.95, 0.5 * floor), weights[:5]
