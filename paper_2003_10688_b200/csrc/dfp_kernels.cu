@@ -886,9 +886,9 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
                                                                const float* __restrict__ shift,
                                                                double* __restrict__ partial) {
     constexpr int V = VEC<T>;
-    constexpr int UN = 4;
     constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
     constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
+    constexpr int UN = NI == 2 ? 4 : 8;  // 8 16-byte loads in flight per thread
     __shared__ double red[THREADS * V];
     const int cv_total = C / V;
     const int cvb = min(cv_total, THREADS);
@@ -911,6 +911,7 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
         float q[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) q[i] = MODE == RR_SUM ? 0.f : __ldg(shift + c + i);
+        // (inactive lanes keep zero accumulators and still take part in the shuffles below)
         for (int64_t pb = p0 + row; pb < p1; pb += static_cast<int64_t>(rows) * UN) {
             uint4 r0[UN], r1[UN];
 #pragma unroll
@@ -955,24 +956,38 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
                 for (int i = 0; i < V; ++i) acc[k][i] += static_cast<Acc>(f[k][i]);
         }
     }
-    // combine the pixel lanes of each channel vector, one sum at a time (fits static smem)
+    // combine the pixel lanes of each channel vector: warp shuffles across the rows that share a
+    // warp, then one shared-memory slot per warp-row group, one sum at a time
+    const int lane = tid & 31;
+    const bool pow2 = (cvb & (cvb - 1)) == 0;
+    const int rows_w = (pow2 && cvb < 32) ? 32 / cvb : 1;  // rows per warp combined by shuffles
+    const int groups = rows / rows_w;
+    const int grp = row / rows_w;
+    const bool lead = row < rows && (rows_w == 1 || lane < cvb);  // first row of the warp
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
+        double t[V];
 #pragma unroll
-        for (int i = 0; i < V; ++i) red[tid * V + i] = static_cast<double>(acc[k][i]);
+        for (int i = 0; i < V; ++i) {
+            t[i] = static_cast<double>(acc[k][i]);
+            if (rows_w > 1)
+                for (int off = cvb; off < 32; off <<= 1) t[i] += __shfl_xor_sync(0xffffffffu, t[i], off);
+        }
+        if (lead && row % rows_w == 0) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) red[(grp * cvb + cvi) * V + i] = t[i];
+        }
         __syncthreads();
-        if (row == 0 && active) {
-            double t[V];
+        if (tid < cvb && (blockIdx.y * cvb + tid) < cv_total) {
+            double u[V];
 #pragma unroll
-            for (int i = 0; i < V; ++i) t[i] = static_cast<double>(acc[k][i]);
-            for (int rr = 1; rr < rows; ++rr) {
-                const int t2 = rr * cvb + cvi;
+            for (int i = 0; i < V; ++i) u[i] = 0.0;
+            for (int g2 = 0; g2 < groups; ++g2)
 #pragma unroll
-                for (int i = 0; i < V; ++i) t[i] += red[t2 * V + i];
-            }
-            double* dst = partial + (static_cast<int64_t>(blockIdx.x) * C + c) * NS + k;
+                for (int i = 0; i < V; ++i) u[i] += red[(g2 * cvb + tid) * V + i];
+            double* dst = partial + (static_cast<int64_t>(blockIdx.x) * C + (blockIdx.y * cvb + tid) * V) * NS + k;
 #pragma unroll
-            for (int i = 0; i < V; ++i) dst[NS * i] = t[i];
+            for (int i = 0; i < V; ++i) dst[NS * i] = u[i];
         }
         __syncthreads();
     }
@@ -1122,6 +1137,153 @@ __global__ void __launch_bounds__(THREADS) maxpool_argmax_kernel(const __grid_co
     }
 }
 
+// MaxPool2dBack fast path for the programs autodiff emits around it: the window program is a
+// gradient (or a sum of two gradients, an Add fused in front) and the output program is empty or a
+// ReluBack mask. Thread = one channel vector walking input pixels; per pixel it checks the <= 4
+// windows covering it against the argmax bytes and sums the routed gradients (deterministic).
+struct PoolBackSpec {
+    int ok = 0, s0 = -1, s1 = -1, sm = -1;
+};
+
+PoolBackSpec match_pool_back(const Program& pre, const Program& post) {
+    PoolBackSpec ps;
+    // pre: r0 = LD(s0) [+ LD(s1)]
+    int k = 0;
+    auto is = [&](const Program& p, int i, PwOp op) { return i < p.n && p.ins[i].op == op; };
+    if (!is(pre, 0, PW_LD)) return ps;
+    int reg_slot[NREG] = {-1, -1, -1, -1};
+    bool sum = false;
+    for (k = 0; k < pre.n; ++k) {
+        const PwInstr& in = pre.ins[k];
+        if (in.dst >= NREG) return ps;
+        if (in.op == PW_LD) {
+            reg_slot[in.dst] = in.a;
+        } else if (in.op == PW_ADD && in.a < NREG && in.b < NREG && reg_slot[in.a] >= 0 && reg_slot[in.b] >= 0 &&
+                   !sum) {
+            ps.s0 = reg_slot[in.a];
+            ps.s1 = reg_slot[in.b];
+            sum = true;
+            for (int r = 0; r < NREG; ++r) reg_slot[r] = -1;
+            reg_slot[in.dst] = -2;  // the sum
+        } else if (in.op == PW_MOV && in.a < NREG) {
+            reg_slot[in.dst] = reg_slot[in.a];
+        } else {
+            return ps;
+        }
+    }
+    if (!sum) {
+        if (reg_slot[0] < 0) return ps;
+        ps.s0 = reg_slot[0];
+    } else if (reg_slot[0] != -2) {
+        return ps;
+    }
+    // post: empty, or r1 = LD(sm); r0 = MASK(r0, r1)
+    if (post.n == 0) {
+        ps.ok = 1;
+        return ps;
+    }
+    if (post.n == 2 && post.ins[0].op == PW_LD && post.ins[0].dst != 0 && post.ins[1].op == PW_MASK &&
+        post.ins[1].dst == 0 && post.ins[1].a == 0 && post.ins[1].b == post.ins[0].dst) {
+        ps.sm = post.ins[0].a;
+        ps.ok = 1;
+    }
+    return ps;
+}
+
+template <typename T, bool ADD, bool MASK>
+__global__ void __launch_bounds__(THREADS) maxpool_back_fast_kernel(const __grid_constant__ DfpArgs a,
+                                                                    PoolBackSpec ps) {
+    constexpr int V = VEC<T>;
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int row = threadIdx.x / cvb;
+    const int cvi = threadIdx.x - row * cvb;
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const int P = a.N * a.H * a.W;
+    const T* d0 = static_cast<const T*>(a.in[ps.s0]) + c;
+    const T* d1 = ADD ? static_cast<const T*>(a.in[ps.s1]) + c : nullptr;
+    const T* xm = MASK ? static_cast<const T*>(a.in[ps.sm]) + c : nullptr;
+    const int ld0 = a.in_ld[ps.s0], ld1 = ADD ? a.in_ld[ps.s1] : 0, ldm = MASK ? a.in_ld[ps.sm] : 0;
+    T* out = static_cast<T*>(a.out) + c;
+    const uint8_t* am = a.argmax + c;
+    const int step = gridDim.x * rows;
+    for (int p = blockIdx.x * rows + row; p < P; p += step) {
+        const int iw = p % a.W;
+        const int t = p / a.W;
+        const int ih = t % a.H;
+        const int n = t / a.H;
+        float m[V];
+        if (MASK) load16(xm + static_cast<int64_t>(p) * ldm, m);
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = 0.f;
+        const int oh_lo = max(0, (ih + a.ph - a.kh + a.sh) / a.sh);
+        const int oh_hi = min(a.OH - 1, (ih + a.ph) / a.sh);
+        const int ow_lo = max(0, (iw + a.pw - a.kw + a.sw) / a.sw);
+        const int ow_hi = min(a.OW - 1, (iw + a.pw) / a.sw);
+        for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+            const int dkh = ih + a.ph - oh * a.sh;
+            if (dkh < 0 || dkh >= a.kh) continue;
+            for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+                const int dkw = iw + a.pw - ow * a.sw;
+                if (dkw < 0 || dkw >= a.kw) continue;
+                const int64_t opix = (static_cast<int64_t>(n) * a.OH + oh) * a.OW + ow;
+                uint32_t w0, w1 = 0;
+                if constexpr (V == 8) {
+                    const uint2 r = __ldg(reinterpret_cast<const uint2*>(am + opix * a.C));
+                    w0 = r.x;
+                    w1 = r.y;
+                } else {
+                    w0 = __ldg(reinterpret_cast<const uint32_t*>(am + opix * a.C));
+                }
+                const uint32_t me = static_cast<uint32_t>(dkh * a.kw + dkw);
+                bool hit[V];
+                bool any = false;
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    hit[i] = (((i < 4 ? w0 : w1) >> (8 * (i & 3))) & 0xffu) == me;
+                    any |= hit[i];
+                }
+                if (!any) continue;
+                float g[V];
+                load16(d0 + opix * ld0, g);
+                if (ADD) {
+                    float h[V];
+                    load16(d1 + opix * ld1, h);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) g[i] += h[i];
+                }
+#pragma unroll
+                for (int i = 0; i < V; ++i)
+                    if (hit[i]) acc[i] += g[i];
+            }
+        }
+        if (MASK) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] = m[i] > 0.f ? acc[i] : 0.f;
+        }
+        store16(out + static_cast<int64_t>(p) * a.out_ld, acc);
+    }
+}
+
+template <typename T>
+bool launch_maxpool_back_fast(const DfpArgs& a, cudaStream_t s) {
+    const PoolBackSpec ps = match_pool_back(a.pre, a.post);
+    if (!ps.ok || a.out_coff != 0) return false;
+    for (int sl : {ps.s0, ps.s1, ps.sm})
+        if (sl >= 0 && (a.in_kind[sl] != IN_PIX || a.in_coff[sl] != 0)) return false;
+    if (static_cast<int64_t>(a.N) * a.H * a.W >= (int64_t(1) << 31) / 2) return false;
+    const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.H * a.W).grid;
+    const bool add = ps.s1 >= 0, mask = ps.sm >= 0;
+    if (add && mask) maxpool_back_fast_kernel<T, true, true><<<grid, THREADS, 0, s>>>(a, ps);
+    else if (add) maxpool_back_fast_kernel<T, true, false><<<grid, THREADS, 0, s>>>(a, ps);
+    else if (mask) maxpool_back_fast_kernel<T, false, true><<<grid, THREADS, 0, s>>>(a, ps);
+    else maxpool_back_fast_kernel<T, false, false><<<grid, THREADS, 0, s>>>(a, ps);
+    return true;
+}
+
 template <typename T, bool IS_MAX>
 __global__ void __launch_bounds__(THREADS) pool_back_kernel(const __grid_constant__ DfpArgs a) {
     constexpr int V = VEC<T>;
@@ -1241,6 +1403,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
             if (a.argmax == nullptr || a.kh * a.kw > 254) throw std::invalid_argument("dfp: maxpool backward needs argmax scratch");
             const int64_t windows = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
             maxpool_argmax_kernel<T><<<grid_for(windows, THREADS), THREADS, 0, s>>>(a);
+            if (launch_maxpool_back_fast<T>(a, s)) break;
             const int64_t work = static_cast<int64_t>(a.N) * a.H * a.W * (a.C / V);
             pool_back_kernel<T, true><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
@@ -1388,19 +1551,31 @@ __global__ void __launch_bounds__(THREADS) bnback_apply_kernel(const T* __restri
 // finalisation of per-channel partial sums (f64)
 // ---------------------------------------------------------------------------------------------
 
+// One warp per channel: lanes stride over the partial blocks (independent loads in flight), a
+// fixed-order shuffle tree combines them (deterministic), lane 0 finalises.
 __global__ void finalize_kernel(const FinalizeArgs a) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (c >= a.C) return;
     const int cs = a.Cstride > 0 ? a.Cstride : a.C;
-    if (a.mode == FIN_BN_BACK4) {
-        double sd = 0.0, sdx = 0.0, sx = 0.0, sxx = 0.0;
-        for (int b = 0; b < a.blocks; ++b) {
-            const double* q = a.partial + (static_cast<int64_t>(b) * cs + c) * 4;
-            sd += q[0];
-            sdx += q[1];
-            sx += q[2];
-            sxx += q[3];
+    const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
+    double q[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b = lane; b < a.blocks; b += 32) {
+        const double* src = a.partial + (static_cast<int64_t>(b) * cs + c) * ns;
+        q[0] += src[0];
+        q[1] += src[1];
+        if (ns == 4) {
+            q[2] += src[2];
+            q[3] += src[3];
         }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
+    if (lane != 0) return;
+    if (a.mode == FIN_BN_BACK4) {
+        const double sd = q[0], sdx = q[1], sx = q[2], sxx = q[3];
         const double m = a.count;
         const double d = sx / m;  // mean - shift
         double var = sxx / m - d * d;
@@ -1425,11 +1600,7 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
         }
         return;
     }
-    double s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < a.blocks; ++b) {
-        s1 += a.partial[(static_cast<int64_t>(b) * cs + c) * 2];
-        s2 += a.partial[(static_cast<int64_t>(b) * cs + c) * 2 + 1];
-    }
+    const double s1 = q[0], s2 = q[1];
     const double m = a.count;
     if (a.mode == FIN_BN_STATS) {
         // sums over (x - shift): mean = shift + s1/m, var = s2/m - (s1/m)^2 (biased)
@@ -1546,12 +1717,13 @@ void transpose(const void* in, void* out, int N, int R, int C, int ld_in, int r_
 
 int dfp_reduce_blocks(int64_t pixels, int C) {
     // ~32 16-byte vectors per thread (256 threads) over the pixel range, grid.y covers channel
-    // vector blocks of 256; cap at four waves of blocks in total
+    // vector blocks of 256; whole waves of two resident blocks per SM, at most two waves
     const int64_t cvec = std::max<int64_t>(1, C / 8);
     const int64_t gy = ceil_div(cvec, 256);
     const int64_t want = ceil_div(pixels * cvec, static_cast<int64_t>(256) * 32 * gy);
-    const int64_t cap = std::max<int64_t>(1, 4 * num_sms() / gy);
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, cap, pixels})));
+    const int64_t wave = std::max<int64_t>(1, 2 * num_sms() / gy);
+    const int64_t blocks = want <= wave / 2 ? want : std::min<int64_t>(2, ceil_div(want, wave)) * wave;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, pixels)));
 }
 
 void bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
@@ -1638,7 +1810,7 @@ void softmax_back(int dtype, const void* d, const void* y, void* dx, int rows, i
 }
 
 void dfp_finalize(const FinalizeArgs& a, cudaStream_t s) {
-    finalize_kernel<<<static_cast<unsigned>(ceil_div(a.C, 128)), 128, 0, s>>>(a);
+    finalize_kernel<<<static_cast<unsigned>(ceil_div(a.C, 8)), 256, 0, s>>>(a);
     SOL_CUDA(cudaGetLastError());
 }
 
