@@ -497,7 +497,7 @@ MaskSpec match_mask(const Program& p) {
     MaskSpec m;
     for (int k = 0; k < p.n; ++k) {
         const PwInstr& in = p.ins[k];
-        if (in.dst < 0 || in.dst >= NREG || in.a < 0 || in.b < 0) return m;
+        if (in.dst >= NREG) return m;
         Sym r;
         switch (in.op) {
             case PW_LD:

@@ -47,6 +47,12 @@ struct IgemmArgs {
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).
 void igemm_launch(const IgemmArgs& a, cudaStream_t stream);
 
+// Few-channel stem convolution (stem.cu): bf16, input pixels of 8 channels holding Cin <= 4,
+// Cout = 64, kw <= 8, K packed (kh, kw in 8 slots, c in 4) to stem_kpad(kh) (pack_stem_weight).
+bool stem_supported(const IgemmArgs& a);
+void stem_launch(const IgemmArgs& a, cudaStream_t stream);
+int stem_kpad(int kh);
+
 // Tile configuration chosen for a GEMM (exposed for the roofline/bench bookkeeping).
 int igemm_block_n(int nout);
 

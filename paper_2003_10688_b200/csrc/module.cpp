@@ -133,6 +133,16 @@ public:
                 cin_ = in_.C;
                 cout_ = out_.C;
                 kpad_ = static_cast<int>(round_up(static_cast<int64_t>(kh_) * kw_ * in_.ld, bk));
+                if (op_ == SOL_OP_CONV2D) {
+                    // few-channel stem: halo-tile kernel with its own K order (stem.cu)
+                    IgemmArgs g = fprop_args(nullptr, nullptr);
+                    g.K_pad = stem_kpad(kh_);
+                    if (stem_supported(g)) {
+                        stem_ = true;
+                        kpad_ = g.K_pad;
+                        family = "conv_stem_tcgen05";
+                    }
+                }
                 packed_ = dev_alloc(static_cast<size_t>(cout_) * kpad_ * elem_size(dtype_));
                 algo_flops = 2.0 * out_.pixels() * cout_ * kh_ * kw_ * cin_;
                 algo_bytes = (in_.pixels() * in_.ld + out_.pixels() * out_.ld) * double(elem_size(dtype_)) +
@@ -218,7 +228,29 @@ public:
             ++k;
         }
         if (k != d.n_ops) unsupported("unsupported fused conv epilogue");
-        family = op_ == SOL_OP_CONV2D ? "conv_fprop_fused_tcgen05" : "linear_fused_tcgen05";
+        family = op_ == SOL_OP_CONV2D ? (stem_ ? "conv_stem_fused_tcgen05" : "conv_fprop_fused_tcgen05")
+                                      : "linear_fused_tcgen05";
+    }
+
+    IgemmArgs fprop_args(const void* src, void* out) const {
+        IgemmArgs g;
+        g.mode = IG_FPROP;
+        g.dtype = dtype_;
+        g.out_dtype = dtype_;
+        g.src = src;
+        g.wt = packed_;
+        g.out = out;
+        g.N = static_cast<int>(in_.N);
+        g.SH = static_cast<int>(in_.H);
+        g.SW = static_cast<int>(in_.W);
+        g.SC = static_cast<int>(in_.ld);
+        g.OH = static_cast<int>(out_.H);
+        g.OW = static_cast<int>(out_.W);
+        g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
+        g.Nout = static_cast<int>(cout_);
+        g.K_pad = kpad_;
+        g.ldo = static_cast<int>(out_.ld);
+        return g;
     }
 
     WgradArgs wargs(const void* dy, const void* x, float* dw, float* ws) const {
@@ -247,28 +279,17 @@ public:
             case SOL_OP_CONV2D:
             case SOL_OP_LINEAR: {
                 if (!(frozen && packed_valid_)) {
-                    pack_conv_weight(static_cast<const float*>(args[w_idx_]), packed_, dtype_, static_cast<int>(cout_),
-                                     static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), kpad_, s);
+                    if (stem_)
+                        pack_stem_weight(static_cast<const float*>(args[w_idx_]), packed_, static_cast<int>(cout_),
+                                         static_cast<int>(cin_), kh_, kw_, kpad_, s);
+                    else
+                        pack_conv_weight(static_cast<const float*>(args[w_idx_]), packed_, dtype_,
+                                         static_cast<int>(cout_), static_cast<int>(cin_), kh_, kw_,
+                                         static_cast<int>(in_.ld), kpad_, s);
                     packed_valid_ = true;
                 }
-                IgemmArgs g;
-                g.mode = IG_FPROP;
-                g.dtype = dtype_;
-                g.out_dtype = dtype_;
-                g.src = args[0];
-                g.wt = packed_;
+                IgemmArgs g = fprop_args(args[0], out);
                 g.bias = b_idx_ >= 0 ? static_cast<const float*>(args[b_idx_]) : nullptr;
-                g.out = out;
-                g.N = static_cast<int>(in_.N);
-                g.SH = static_cast<int>(in_.H);
-                g.SW = static_cast<int>(in_.W);
-                g.SC = static_cast<int>(in_.ld);
-                g.OH = static_cast<int>(out_.H);
-                g.OW = static_cast<int>(out_.W);
-                g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
-                g.Nout = static_cast<int>(cout_);
-                g.K_pad = kpad_;
-                g.ldo = static_cast<int>(out_.ld);
                 if (ep_coef_) {
                     if (!(frozen && coef_valid_)) {
                         bn_infer_coef(static_cast<const float*>(args[bn_g_]), static_cast<const float*>(args[bn_b_]),
@@ -284,7 +305,8 @@ public:
                     g.ld_res = static_cast<int>(out_.ld);
                 }
                 g.act = act_;
-                igemm_launch(g, s);
+                if (stem_) stem_launch(g, s);
+                else igemm_launch(g, s);
                 break;
             }
             case SOL_OP_CONV2DBACKX:
@@ -339,6 +361,7 @@ private:
     Geo in_, out_, x_;
     int64_t cin_ = 0, cout_ = 0;
     int kpad_ = 0;
+    bool stem_ = false;
     int w_idx_ = -1, b_idx_ = -1;
     void* packed_ = nullptr;
     bool packed_valid_ = false;

@@ -49,6 +49,18 @@ __global__ void pack_t_kernel(const float* __restrict__ w, T* __restrict__ p, in
     }
 }
 
+__global__ void pack_stem_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ p, int Cout, int Cin,
+                                 int KH, int KW, int kpad) {
+    const int total = Cout * kpad;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int co = i / kpad, k = i - co * kpad;
+        const int kh = k / 32, kw = (k % 32) / 4, c = k % 4;
+        float v = 0.f;
+        if (kh < KH && kw < KW && c < Cin) v = w[((static_cast<int64_t>(co) * Cin + c) * KH + kh) * KW + kw];
+        p[i] = __float2bfloat16_rn(v);
+    }
+}
+
 // canonical dw[co][ci][kh][kw] = packed[co][(kh*KW + kw)*ld + ci]
 __global__ void unpack_grad_kernel(const float* __restrict__ p, float* __restrict__ w, int Cout, int Cin, int KH,
                                    int KW, int ld) {
@@ -96,6 +108,12 @@ void pack_conv_weight_t(const float* w, void* packed, int dtype, int Cout, int C
                                                  flip);
     else
         pack_t_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<float*>(packed), Cout, Cin, kh, kw, ld_o, kpad, flip);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void pack_stem_weight(const float* w, void* packed, int Cout, int Cin, int kh, int kw, int kpad, cudaStream_t s) {
+    pack_stem_kernel<<<grid_of(static_cast<int64_t>(Cout) * kpad), 256, 0, s>>>(
+        w, static_cast<__nv_bfloat16*>(packed), Cout, Cin, kh, kw, kpad);
     SOL_CUDA(cudaGetLastError());
 }
 

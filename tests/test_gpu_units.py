@@ -121,3 +121,24 @@ def test_training_units(gpu, name, dtype):
     gp, units = _compile(name, True, batch)
     env = O.run_graph(gp, _inputs(gp, batch))
     _check_units(gp, units, env, dtype, gpu)
+
+
+@pytest.mark.parametrize("hw,k,s,p,bias", [(64, 7, 2, 3, False), (37, 7, 2, 3, True), (30, 3, 1, 1, True),
+                                            (33, 3, 2, 1, False)])
+def test_stem_conv(gpu, hw, k, s, p, bias):
+    """Few-channel stem conv (3 -> 64, stem.cu halo-tile kernel) vs the oracle on bf16 operands;
+    ragged sizes exercise partial output tiles and the out-of-bounds halo fill."""
+    from paper_2003_10688_b200 import graph, partition
+    b = graph.GraphBuilder(21)
+    b.input("x", graph.meta_nchw(0, 3, hw, hw))
+    c = b.conv("stem", "x", 3, 64, k, s, p, bias=bias)
+    batch = 3
+    g = graph.infer_shapes(b.done([c]), batch)
+    units = partition.partition(g)
+    x = np.random.default_rng(4).uniform(-1, 1, (batch, 3, hw, hw)).astype(np.float32)
+    fam, got = run_unit(g, units[0], {"x": x}, 1, gpu)
+    assert fam == "conv_stem_tcgen05"
+    params = {k2: np.asarray(quant(v, 1) if v.ndim >= 2 else v, np.float64) for k2, v in g.params.items()}
+    want = O.eval_node(g.find_node("stem"), [quant(x, 1).astype(np.float64)], params)
+    err = O.oracle_err(got, want)
+    assert got.shape == want.shape and err <= 1e-2, err
