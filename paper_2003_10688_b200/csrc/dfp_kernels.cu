@@ -633,35 +633,73 @@ __device__ __forceinline__ void chain_at(const DfpArgs& a, const ChainSpec& cs, 
     }
 }
 
-// Max/Avg pool whose source is a straight-line chain and whose post program is empty.
-template <typename T, bool IS_MAX, bool BN0, int ACT>
+// Max/Avg pool whose source is a straight-line chain (BN / activation, no Add) and whose post
+// program is empty. Thread = one channel vector (BN coefficients in registers) walking output
+// pixels; for 3x3 windows all nine 16-byte loads are issued before any arithmetic.
+template <typename T, bool IS_MAX, bool BN0, int ACT, bool K3>
 __global__ void __launch_bounds__(THREADS) pool_chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
     constexpr int V = VEC<T>;
-    const int cv = a.C / V;
-    const int64_t total = static_cast<int64_t>(a.N) * a.OH * a.OW * cv;
-    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
-         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t opix = v / cv;
-        const int c = static_cast<int>(v - opix * cv) * V;
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int row = threadIdx.x / cvb;
+    const int cvi = threadIdx.x - row * cvb;
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const T* x = static_cast<const T*>(a.in[cs.s0]) + c;
+    const int ldx = a.in_ld[cs.s0];
+    T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    BnRegs<T> bn;
+    if (BN0) bn.load(a.P, cs.bn0, c);
+    const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
+    for (int64_t opix = static_cast<int64_t>(blockIdx.x) * rows + row; opix < P; opix += step) {
         const int ow = static_cast<int>(opix % a.OW);
-        const int oh = static_cast<int>((opix / a.OW) % a.OH);
-        const int n = static_cast<int>(opix / (static_cast<int64_t>(a.OW) * a.OH));
+        const int64_t t = opix / a.OW;
+        const int oh = static_cast<int>(t % a.OH);
+        const int n = static_cast<int>(t / a.OH);
+        const int h0 = oh * a.sh - a.ph, w0 = ow * a.sw - a.pw;
+        const T* base = x + (static_cast<int64_t>(n) * a.H) * a.W * ldx;
         float acc[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = IS_MAX ? a.min_init : 0.f;
         int cnt = 0;
-        const int h0 = oh * a.sh - a.ph, w0 = ow * a.sw - a.pw;
-        for (int kh = 0; kh < a.kh; ++kh) {
-            const int ih = h0 + kh;
-            if (ih < 0 || ih >= a.H) continue;
-            for (int kw = 0; kw < a.kw; ++kw) {
-                const int iw = w0 + kw;
-                if (iw < 0 || iw >= a.W) continue;
-                float x[V];
-                chain_at<T, BN0, false, false, ACT>(a, cs, (static_cast<int64_t>(n) * a.H + ih) * a.W + iw, c, x);
+        auto take = [&](const uint4& r) {
+            float v[V];
+            unpack16(r, v, static_cast<T*>(nullptr));
+            if (BN0) bn.apply(v);
 #pragma unroll
-                for (int i = 0; i < V; ++i) acc[i] = IS_MAX ? fmaxf(acc[i], x[i]) : acc[i] + x[i];
-                ++cnt;
+            for (int i = 0; i < V; ++i) {
+                if (ACT >= 1) v[i] = fmaxf(v[i], 0.f);
+                if (ACT == 2) v[i] = fminf(v[i], 6.f);
+                acc[i] = IS_MAX ? fmaxf(acc[i], v[i]) : acc[i] + v[i];
+            }
+        };
+        if constexpr (K3) {
+            uint4 r[9];
+            bool ok[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int ih = h0 + k / 3, iw = w0 + k % 3;
+                ok[k] = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                if (ok[k]) r[k] = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * a.W + iw) * ldx));
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                if (ok[k]) {
+                    take(r[k]);
+                    ++cnt;
+                }
+        } else {
+            for (int kh = 0; kh < a.kh; ++kh) {
+                const int ih = h0 + kh;
+                if (ih < 0 || ih >= a.H) continue;
+                for (int kw = 0; kw < a.kw; ++kw) {
+                    const int iw = w0 + kw;
+                    if (iw < 0 || iw >= a.W) continue;
+                    take(__ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * a.W + iw) * ldx)));
+                    ++cnt;
+                }
             }
         }
         if (!IS_MAX) {
@@ -669,7 +707,7 @@ __global__ void __launch_bounds__(THREADS) pool_chain_kernel(const __grid_consta
 #pragma unroll
             for (int i = 0; i < V; ++i) acc[i] /= div;
         }
-        store_out<T>(a, opix, c, acc);
+        store16(out + opix * a.out_ld, acc);
     }
 }
 
@@ -716,7 +754,14 @@ bool launch_pool_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
     if (a.post.n != 0) return false;
     const ChainSpec c = match_chain(a.pre);
     if (!c.ok || c.add || a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
-#define SOL_POOL(MX, B, A) pool_chain_kernel<T, MX, B, A><<<grid, THREADS, 0, s>>>(a, c)
+    const dim3 g2 = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW, 2).grid;
+    (void)grid;
+    const bool k3 = a.kh == 3 && a.kw == 3;
+#define SOL_POOL(MX, B, A)                                                              \
+    do {                                                                                \
+        if (k3) pool_chain_kernel<T, MX, B, A, true><<<g2, THREADS, 0, s>>>(a, c);       \
+        else pool_chain_kernel<T, MX, B, A, false><<<g2, THREADS, 0, s>>>(a, c);         \
+    } while (0)
     const bool b = c.bn0 >= 0;
     if (a.pool_max) {
         if (b) { if (c.act == 0) SOL_POOL(true, true, 0); else if (c.act == 1) SOL_POOL(true, true, 1); else SOL_POOL(true, true, 2); }
