@@ -192,6 +192,11 @@ int sol_b200_plan_arena_bytes(sol_b200_plan_t p, uint64_t* bytes);
 /* Host <-> plan buffer copies, ordered on the plan stream (src/dst should be pinned host memory). */
 int sol_b200_plan_h2d(sol_b200_plan_t p, int32_t id, const void* src, uint64_t bytes);
 int sol_b200_plan_d2h(sol_b200_plan_t p, void* dst, int32_t id, uint64_t bytes);
+/* Pipelined input staging (serving): copies `src` (pinned) into a device staging area for buffer
+ * `id` on the plan's copy stream, after the previous staged copy of that buffer was consumed; the
+ * next plan_run starts by moving it into the buffer. The host-to-device copy of step i+1 thus
+ * overlaps the kernels of step i (the reference queue's copy/compute overlap, runtime.hpp:95-145). */
+int sol_b200_plan_stage_h2d(sol_b200_plan_t p, int32_t id, const void* src, uint64_t bytes);
 /* CUDA events on the plan stream (slots 0..15) for device-side timing. */
 int sol_b200_plan_event_record(sol_b200_plan_t p, int32_t slot);
 int sol_b200_plan_event_elapsed(sol_b200_plan_t p, int32_t a, int32_t b, float* ms);

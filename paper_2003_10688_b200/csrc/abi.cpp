@@ -296,6 +296,10 @@ int sol_b200_plan_h2d(sol_b200_plan_t p, int32_t id, const void* src, uint64_t b
     return guard([&] { p->p->h2d(id, src, bytes); });
 }
 
+int sol_b200_plan_stage_h2d(sol_b200_plan_t p, int32_t id, const void* src, uint64_t bytes) {
+    return guard([&] { p->p->stage_h2d(id, src, bytes); });
+}
+
 int sol_b200_plan_d2h(sol_b200_plan_t p, void* dst, int32_t id, uint64_t bytes) {
     return guard([&] { p->p->d2h(dst, id, bytes); });
 }

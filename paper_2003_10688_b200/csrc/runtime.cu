@@ -318,6 +318,13 @@ Plan::Plan(int device) : device_(device) {
 
 Plan::~Plan() {
     cudaStreamSynchronize(stream_);
+    if (copy_stream_) cudaStreamSynchronize(copy_stream_);
+    for (auto& kv : staged_) {
+        if (kv.second.dev) cudaFree(kv.second.dev);
+        if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+        if (kv.second.consumed) cudaEventDestroy(kv.second.consumed);
+    }
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     steps_.clear();
     if (base_) cudaFree(base_);
@@ -448,9 +455,42 @@ void Plan::run_steps(cudaStream_t st) {
     for (auto& s : steps_) run_step(s, st);
 }
 
+void Plan::stage_h2d(int id, const void* src, uint64_t bytes) {
+    if (!finalized_) finalize();
+    if (bytes > bufs_.at(id).bytes) throw std::invalid_argument("staged h2d larger than buffer");
+    SOL_CUDA(cudaSetDevice(device_));
+    if (!copy_stream_) SOL_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    Staged& st = staged_[id];
+    if (!st.dev) {
+        SOL_CUDA(cudaMalloc(&st.dev, bufs_[id].bytes));
+        SOL_CUDA(cudaEventCreateWithFlags(&st.ready, cudaEventDisableTiming));
+        SOL_CUDA(cudaEventCreateWithFlags(&st.consumed, cudaEventDisableTiming));
+    }
+    if (st.pending) throw std::invalid_argument("plan: staged input not consumed by a run yet");
+    // the staging area is free once the previous run moved its content into the plan buffer
+    if (st.consumed_valid) SOL_CUDA(cudaStreamWaitEvent(copy_stream_, st.consumed, 0));
+    SOL_CUDA(cudaMemcpyAsync(st.dev, src, bytes, cudaMemcpyHostToDevice, copy_stream_));
+    SOL_CUDA(cudaEventRecord(st.ready, copy_stream_));
+    st.bytes = bytes;
+    st.pending = true;
+}
+
+void Plan::consume_staged() {
+    for (auto& kv : staged_) {
+        Staged& st = kv.second;
+        if (!st.pending) continue;
+        SOL_CUDA(cudaStreamWaitEvent(stream_, st.ready, 0));
+        SOL_CUDA(cudaMemcpyAsync(base_ + bufs_[kv.first].off, st.dev, st.bytes, cudaMemcpyDeviceToDevice, stream_));
+        SOL_CUDA(cudaEventRecord(st.consumed, stream_));
+        st.consumed_valid = true;
+        st.pending = false;
+    }
+}
+
 void Plan::run(bool use_graph) {
     if (!finalized_) finalize();
     SOL_CUDA(cudaSetDevice(device_));
+    consume_staged();
     if (!use_graph) {
         run_steps(stream_);
         has_run_ = true;

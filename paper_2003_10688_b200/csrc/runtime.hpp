@@ -116,6 +116,7 @@ public:
     uint64_t arena_bytes() const { return total_; }
     void set_comm(const uint8_t id[128], int rank, int nranks);
     void h2d(int id, const void* src, uint64_t bytes);
+    void stage_h2d(int id, const void* src, uint64_t bytes);
     void d2h(void* dst, int id, uint64_t bytes);
     void event_record(int slot);
     float event_elapsed(int a, int b);
@@ -138,6 +139,13 @@ private:
     };
     void run_step(Step& s, cudaStream_t st);
     void run_steps(cudaStream_t st);
+    void consume_staged();
+    struct Staged {
+        void* dev = nullptr;
+        uint64_t bytes = 0;
+        bool pending = false, consumed_valid = false;
+        cudaEvent_t ready = nullptr, consumed = nullptr;
+    };
 
     int device_;
     cudaStream_t stream_ = nullptr;
@@ -150,6 +158,8 @@ private:
     void* comm_ = nullptr;  // ncclComm_t
     int nranks_ = 1;
     cudaEvent_t events_[16] = {};
+    cudaStream_t copy_stream_ = nullptr;
+    std::map<int, Staged> staged_;
 };
 
 }  // namespace solb200

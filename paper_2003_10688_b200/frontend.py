@@ -229,6 +229,18 @@ class OptimizedModel:
         for name, meta in self.inputs.items():
             L.check(lib.sol_b200_plan_h2d(self.plan, self.in_canon[name], self.pin_in[name].ptr, 4 * meta.numel))
 
+    def stage_inputs(self, inputs: Optional[Dict[str, np.ndarray]] = None):
+        """Pipelined serving: (optionally fill the pinned input buffers, then) start the host-to-device
+        copy for the NEXT run() on the plan's copy stream. It overlaps the kernels of the run in
+        flight; the next run() first moves the staged batch into the plan's input buffers."""
+        lib = L.lib()
+        if inputs is not None:
+            for name, meta in self.inputs.items():
+                self.pin_in[name].view(np.float32, meta.shape)[...] = np.asarray(inputs[name], np.float32).reshape(
+                    meta.shape)
+        for name, meta in self.inputs.items():
+            L.check(lib.sol_b200_plan_stage_h2d(self.plan, self.in_canon[name], self.pin_in[name].ptr, 4 * meta.numel))
+
     def run(self):
         """One pass of the plan on its stream (no host synchronisation)."""
         lib = L.lib()

@@ -140,3 +140,22 @@ def test_plan_composition(gpu, name):
         if not np.all(np.isfinite(got)) or err > 2e-2:
             bad.append((u.output, err))
     assert not bad, bad
+
+
+def test_pipelined_staging_matches_predict(gpu):
+    """stage_inputs() (copy-stream H2D of the next batch overlapping the current run) gives the
+    same answers as predict(), batch after batch."""
+    from paper_2003_10688_b200 import frontend, graph, models
+    batch = 4
+    g = models.resnet(18, hw=32, classes=16, width=16)
+    m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16", fuse_epilogue=True))
+    gi = graph.infer_shapes(g, batch)
+    batches = [_inputs(gi, batch, seed=s) for s in (11, 12, 13)]
+    want = [m.predict(b)["prob"] for b in batches]
+    got = []
+    for b in batches:
+        m.stage_inputs(b)
+        m.run()
+        got.append(m.fetch_outputs(["prob"])["prob"])
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
