@@ -643,7 +643,7 @@ using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype) {
+CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype, int rows = BM) {
     static EncodeIm2colFn fn = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -662,7 +662,7 @@ CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype) {
     cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(a.sw), static_cast<cuuint32_t>(a.sh), 1};
     const CUresult r = fn(&m, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           const_cast<void*>(a.src), dims, strides, lower, upper, static_cast<cuuint32_t>(128 / es),
-                          static_cast<cuuint32_t>(BM), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          static_cast<cuuint32_t>(rows), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         throw std::runtime_error("cuTensorMapEncodeIm2col failed: " + std::to_string(static_cast<int>(r)));
@@ -741,22 +741,269 @@ void launch_wgrad_t(const WgradArgs& a, int ncol, int splits, int kb_per_split, 
     SOL_CUDA(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------------------------
+// wgrad, bf16 fast path: persistent warp-specialised tcgen05 GEMM with both operands by TMA.
+//   D[M][N] = sum_p A[p][m] * B[p][n], both operands MN-major in shared memory (pixels = K):
+//     dy    [P][Cout]        2-D tiled TMA, boxes of 64 channels x 64 pixels
+//     xcol  [P][(tap, ci)]   TMA im2col, one box = 64 pixels x 64 channels of one tap
+//   normal:  M = Cout (dy), N = columns (xcol);  swapped (Cout < 128): M = columns, N = Cout.
+// Work items = (m tile, n tile, pixel split); each writes its f32 tile to the split's slice of
+// the workspace [split][Cout][ncol] (or straight to dW with one split), reduced afterwards.
+//   warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue (TMEM double-buffered).
+// ---------------------------------------------------------------------------------------------
+constexpr int WG_THREADS = 192;
+constexpr int WG_BK = 64;  // pixels per k-block
+
+template <int BN>
+constexpr int wg_stages() {
+    return std::min(8, (227 * 1024 - 2048) / (128 * WG_BK * 2 + BN * WG_BK * 2));
+}
+
+template <int BN, bool SWAP>
+__global__ void __launch_bounds__(WG_THREADS, 1)
+    wgrad_ws_kernel(const WgradArgs a, const __grid_constant__ CUtensorMap tm_dy,
+                    const __grid_constant__ CUtensorMap tm_x, int ncol, int m_tiles, int n_tiles, int splits,
+                    int kb_per_split) {
+    constexpr int A_BYTES = 128 * WG_BK * 2;
+    constexpr int B_BYTES = BN * WG_BK * 2;
+    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    constexpr int STAGES = wg_stages<BN>();
+    constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
+    constexpr uint32_t IDESC = make_idesc(1, BN, 128, 1, 1);
+    constexpr uint32_t LBO = (WG_BK / 8) * 1024;  // stride between 64-element MN blocks
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int P = a.N * a.OH * a.OW;
+    const int total_kb = (P + WG_BK - 1) / WG_BK;
+    const int items = m_tiles * n_tiles * splits;
+    const int ohw = a.OH * a.OW;
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(&tfull[s]), 1);
+            mbar_init(smem_u32(&tempty[s]), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        tma_prefetch(&tm_dy);
+        tma_prefetch(&tm_x);
+    }
+    if (warp == 1) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto decode = [&](int it, int& tm, int& tn, int& kb0, int& kb1) {
+        const int sp = it % splits;
+        const int t = it / splits;
+        tm = t / n_tiles;
+        tn = t - tm * n_tiles;
+        kb0 = sp * kb_per_split;
+        kb1 = min(total_kb, kb0 + kb_per_split);
+    };
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                int tm, tn, kb0, kb1;
+                decode(it, tm, tn, kb0, kb1);
+                const int co_base = SWAP ? tn * BN : tm * 128;
+                const int col_base = SWAP ? tm * 128 : tn * BN;
+                constexpr int CO_BLOCKS = SWAP ? BN / 64 : 2;
+                constexpr int COL_BLOCKS = SWAP ? 2 : BN / 64;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    uint8_t* sb = sa + A_BYTES;
+                    uint8_t* s_dy = SWAP ? sb : sa;
+                    uint8_t* s_x = SWAP ? sa : sb;
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_arrive_tx(fb, STAGE_BYTES);
+                    const int p0 = kb * WG_BK;
+#pragma unroll
+                    for (int j = 0; j < CO_BLOCKS; ++j)
+                        tma_load_2d(smem_u32(s_dy + j * WG_BK * 128), &tm_dy, co_base + 64 * j, p0, fb);
+                    const int img = p0 / ohw, rem = p0 - img * ohw;
+                    const int oh0 = rem / a.OW, ow0 = rem - (rem / a.OW) * a.OW;
+#pragma unroll
+                    for (int j = 0; j < COL_BLOCKS; ++j) {
+                        int col = col_base + 64 * j;
+                        if (col >= ncol) col = 0;  // tile padding: any in-range box (discarded)
+                        const int tap = col / a.SC, ci = col - tap * a.SC;
+                        const int dkh = tap / a.kw, dkw = tap - dkh * a.kw;
+                        tma_load_im2col_4d(smem_u32(s_x + j * WG_BK * 128), &tm_x, ci, ow0 * a.sw - a.pw,
+                                           oh0 * a.sh - a.ph, img, static_cast<uint16_t>(dkw),
+                                           static_cast<uint16_t>(dkh), fb);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer
+        int stage = 0, acc = 0;
+        uint32_t phase = 0, acc_phase = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            int tm, tn, kb0, kb1;
+            decode(it, tm, tn, kb0, kb1);
+            mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(smem_u32(&full[stage]), phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < WG_BK / 16; ++k) {
+                        const uint64_t ad = sw128_desc(a_addr + k * 2048, LBO, 1024);
+                        const uint64_t bd = sw128_desc(b_addr + k * 2048, LBO, 1024);
+                        mma<__nv_bfloat16>(dcol, ad, bd, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+                    }
+                    mma_commit(smem_u32(&empty[stage]));
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (lane == 0) mma_commit(smem_u32(&tfull[acc]));
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue
+        const int q = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            int tm, tn, kb0, kb1;
+            decode(it, tm, tn, kb0, kb1);
+            const int sp = it % splits;
+            float* dst = a.workspace ? a.workspace + static_cast<int64_t>(sp) * a.Cout * ncol : a.dw;
+            mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+            tc_fence_after();
+            const int row = tm * 128 + q * 32 + lane;  // M index
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32_nowait(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c0), v);
+                tmem_wait_ld();
+                const int nb = tn * BN + c0;  // first N index of this chunk
+                if (!SWAP) {
+                    if (row < a.Cout) {
+                        float* o = dst + static_cast<int64_t>(row) * ncol + nb;
+                        if (nb + 32 <= ncol) {
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4)
+                                *reinterpret_cast<float4*>(o + i) =
+                                    make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+                        } else {
+                            for (int i = 0; i < 32 && nb + i < ncol; ++i) o[i] = __uint_as_float(v[i]);
+                        }
+                    }
+                } else if (row < ncol) {
+                    // row = column of dW, the chunk's 32 values = 32 consecutive Cout
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (nb + i < a.Cout) dst[static_cast<int64_t>(nb + i) * ncol + row] = __uint_as_float(v[i]);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(smem_u32(&tempty[acc]));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<TCOLS>(tmem_base);
+    }
+}
+
 struct WgradPlan {
     int ncol, bn, splits, kb_per_split;
+    bool fast = false, swap = false;
+    int m_tiles = 1, n_tiles = 1;
 };
 
 WgradPlan plan_wgrad(const WgradArgs& a) {
     WgradPlan p;
     p.ncol = a.kh * a.kw * a.SC;
+    const int total_kb = static_cast<int>(ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, 64));
+    if (a.dtype == DT_BF16 && a.SC % 64 == 0 && (a.ld_dy * 2) % 16 == 0) {
+        p.fast = true;
+        p.swap = a.Cout < 128 && p.ncol > a.Cout;
+        const int Mt = p.swap ? p.ncol : a.Cout, Nt = p.swap ? a.Cout : p.ncol;
+        p.bn = Nt <= 64 ? 64 : (Nt <= 128 ? 128 : 256);
+        p.m_tiles = static_cast<int>(ceil_div(Mt, 128));
+        p.n_tiles = static_cast<int>(ceil_div(Nt, p.bn));
+        const int tiles = p.m_tiles * p.n_tiles;
+        // ~2 work items per SM, each at least 4 k-blocks deep
+        int splits = std::max(1, std::min(std::max(1, total_kb / 4), (2 * num_sms() + tiles - 1) / tiles));
+        p.kb_per_split = static_cast<int>(ceil_div(total_kb, splits));
+        p.splits = static_cast<int>(ceil_div(total_kb, p.kb_per_split));
+        return p;
+    }
     const int epb = a.dtype == DT_BF16 ? 64 : 32;
     p.bn = p.ncol <= epb ? epb : (p.ncol <= 2 * epb ? 2 * epb : 256);
     if (a.dtype == DT_F32 && p.bn > 128) p.bn = 128;
     const int tiles = static_cast<int>(ceil_div(a.Cout, BM) * ceil_div(p.ncol, p.bn));
-    const int total_kb = static_cast<int>(ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, 64));
     int splits = std::max(1, std::min(total_kb, (2 * num_sms() + tiles - 1) / tiles));
     p.kb_per_split = static_cast<int>(ceil_div(total_kb, splits));
     p.splits = static_cast<int>(ceil_div(total_kb, p.kb_per_split));
     return p;
+}
+
+template <int BN, bool SWAP>
+void launch_wgrad_ws(const WgradArgs& a, const WgradPlan& p, cudaStream_t s) {
+    constexpr int STAGE_BYTES = 128 * WG_BK * 2 + BN * WG_BK * 2;
+    constexpr int SMEM = wg_stages<BN>() * STAGE_BYTES + 2048;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        SOL_CUDA(cudaFuncSetAttribute(wgrad_ws_kernel<BN, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    });
+    const int P = a.N * a.OH * a.OW;
+    const CUtensorMap tdy = make_tmap_2d(a.dy, DT_BF16, a.Cout, static_cast<uint64_t>(P), a.ld_dy, WG_BK);
+    IgemmArgs g;
+    g.src = a.x;
+    g.N = a.N; g.SH = a.SH; g.SW = a.SW; g.SC = a.SC;
+    g.OH = a.OH; g.OW = a.OW;
+    g.kh = a.kh; g.kw = a.kw; g.sh = a.sh; g.sw = a.sw; g.ph = a.ph; g.pw = a.pw;
+    const CUtensorMap tx = make_tmap_im2col(g, DT_BF16, WG_BK);
+    const int items = p.m_tiles * p.n_tiles * p.splits;
+    const int grid = std::min(items, num_sms());
+    wgrad_ws_kernel<BN, SWAP><<<grid, WG_THREADS, SMEM, s>>>(a, tdy, tx, p.ncol, p.m_tiles, p.n_tiles, p.splits,
+                                                            p.kb_per_split);
+    SOL_CUDA(cudaGetLastError());
 }
 
 }  // namespace
@@ -801,7 +1048,21 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
     WgradPlan p = plan_wgrad(a);
     if (p.splits <= 1) a.workspace = nullptr;
     else if (a.workspace == nullptr) throw std::invalid_argument("wgrad: workspace required");
-    if (a.dtype == DT_BF16) {
+    if (p.fast) {
+        if (p.swap) {
+            switch (p.bn) {
+                case 64: launch_wgrad_ws<64, true>(a, p, s); break;
+                case 128: launch_wgrad_ws<128, true>(a, p, s); break;
+                default: launch_wgrad_ws<256, true>(a, p, s); break;
+            }
+        } else {
+            switch (p.bn) {
+                case 64: launch_wgrad_ws<64, false>(a, p, s); break;
+                case 128: launch_wgrad_ws<128, false>(a, p, s); break;
+                default: launch_wgrad_ws<256, false>(a, p, s); break;
+            }
+        }
+    } else if (a.dtype == DT_BF16) {
         switch (p.bn) {
             case 64: launch_wgrad_t<__nv_bfloat16, 64>(a, p.ncol, p.splits, p.kb_per_split, s); break;
             case 128: launch_wgrad_t<__nv_bfloat16, 128>(a, p.ncol, p.splits, p.kb_per_split, s); break;

@@ -22,6 +22,8 @@ CASES = [
     (2, 3, 32, 32, 64, 7, 2, 3),      # stem (channels padded to 16 bytes)
     (4, 64, 1, 1, 10, 1, 1, 0),       # linear-shaped, ragged N
     (1, 32, 9, 9, 48, 3, 1, 1),
+    (16, 64, 28, 28, 64, 3, 1, 1),    # many pixel k-blocks: split wgrad (swapped orientation)
+    (8, 64, 28, 28, 256, 1, 1, 0),
 ]
 
 
