@@ -146,6 +146,11 @@ int sol_b200_set_device(int device);
 int sol_b200_module_create(const sol_unit_desc* desc, sol_b200_module_t* out);
 int sol_b200_module_destroy(sol_b200_module_t m);
 int sol_b200_module_info(sol_b200_module_t m, sol_module_info* info);
+/* Sibling-unit fusion: a BatchNormBackX module additionally writes the outputs of the sibling
+ * BatchNormBackGamma (mask bit 0) / BatchNormBackBeta (bit 1) units over the same (dy, x) from its
+ * single reduction pass; their buffers follow the output in the run arguments (n_args grows).
+ * Returns SOL_E_UNSUPPORTED for modules that cannot. */
+int sol_b200_module_set_sibling_outputs(sol_b200_module_t m, int32_t mask);
 /* Raw-pointer launch on a CUDA stream (cudaStream_t passed as void*): args = bindings in order,
  * then the output; scratch must hold info.scratch_bytes. `frozen_params` lets a module cache
  * parameter-derived constants (BN coefficients, packed weights) across runs. */

@@ -42,6 +42,7 @@ SYMBOLS = [
     "sol_b200_conv_wgrad_workspace", "sol_b200_conv_wgrad",
     "sol_b200_plan_h2d", "sol_b200_plan_d2h", "sol_b200_plan_event_record", "sol_b200_plan_event_elapsed",
     "sol_b200_host_alloc", "sol_b200_host_free", "sol_b200_set_conv_debug", "sol_b200_plan_stage_h2d",
+    "sol_b200_module_set_sibling_outputs",
 ]
 
 
@@ -159,6 +160,7 @@ def lib():
             "sol_b200_conv_wgrad": [C.POINTER(ConvDesc), vp, vp, vp, vp, vp],
             "sol_b200_plan_h2d": [vp, i32, vp, u64],
             "sol_b200_plan_stage_h2d": [vp, i32, vp, u64],
+            "sol_b200_module_set_sibling_outputs": [vp, i32],
             "sol_b200_plan_d2h": [vp, vp, i32, u64],
             "sol_b200_plan_event_record": [vp, i32],
             "sol_b200_plan_event_elapsed": [vp, i32, i32, C.POINTER(C.c_float)],

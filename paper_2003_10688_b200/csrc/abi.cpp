@@ -131,6 +131,13 @@ int sol_b200_module_info(sol_b200_module_t m, sol_module_info* info) {
     });
 }
 
+int sol_b200_module_set_sibling_outputs(sol_b200_module_t m, int32_t mask) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null module");
+        if (!m->m->set_sibling_outputs(mask)) throw solb200::UnsupportedError("module has no sibling outputs");
+    });
+}
+
 int sol_b200_module_run(sol_b200_module_t m, void* const* args, int32_t nargs, void* scratch, void* stream,
                         int32_t frozen) {
     return guard([&] {

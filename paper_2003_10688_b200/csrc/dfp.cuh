@@ -163,6 +163,17 @@ void bn_shift(int dtype, const void* x, int ld, int C, float* shift, cudaStream_
 
 // w -= lr * g over n f32 elements (SgdUpdate, reference.cpp:580-584); optional bf16 mirror.
 void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror_bf16, cudaStream_t s);
+// One launch updating many parameters: w_i -= lr * g_i for i < count (multi-tensor SGD).
+constexpr int SGD_MULTI_MAX = 512;
+struct SgdMultiArgs {
+    int count = 0;
+    float lr = 0.f;
+    float* w[SGD_MULTI_MAX];
+    const float* g[SGD_MULTI_MAX];
+    int64_t n[SGD_MULTI_MAX];
+    int block0[SGD_MULTI_MAX + 1];  // first block of each tensor (prefix over ceil(n / 1024))
+};
+void sgd_multi(const SgdMultiArgs& a, cudaStream_t s);
 
 // Layout/dtype conversion between canonical NCHW f32 (host-facing) and NHWC plan storage.
 // c_pad >= C channels; padded channels are zero.

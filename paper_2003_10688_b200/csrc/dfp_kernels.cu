@@ -1872,6 +1872,39 @@ void bn_shift(int dtype, const void* x, int ld, int C, float* shift, cudaStream_
     SOL_CUDA(cudaGetLastError());
 }
 
+// Each block owns 1024 consecutive elements of one tensor (4 per thread, float4 when aligned).
+__global__ void __launch_bounds__(256) sgd_multi_kernel(const __grid_constant__ SgdMultiArgs a) {
+    int lo = 0, hi = a.count;  // tensor t with block0[t] <= blockIdx.x < block0[t + 1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (a.block0[mid] <= static_cast<int>(blockIdx.x)) lo = mid;
+        else hi = mid;
+    }
+    const int t = lo;
+    const int64_t base = static_cast<int64_t>(blockIdx.x - a.block0[t]) * 1024 + threadIdx.x * 4;
+    float* w = a.w[t];
+    const float* g = a.g[t];
+    const int64_t n = a.n[t];
+    if (base + 4 <= n && (reinterpret_cast<uintptr_t>(w + base) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(g + base) & 15) == 0) {
+        float4 wv = *reinterpret_cast<float4*>(w + base);
+        const float4 gv = __ldg(reinterpret_cast<const float4*>(g + base));
+        wv.x -= a.lr * gv.x;
+        wv.y -= a.lr * gv.y;
+        wv.z -= a.lr * gv.z;
+        wv.w -= a.lr * gv.w;
+        *reinterpret_cast<float4*>(w + base) = wv;
+    } else {
+        for (int64_t i = base; i < base + 4 && i < n; ++i) w[i] = w[i] - a.lr * g[i];
+    }
+}
+
+void sgd_multi(const SgdMultiArgs& a, cudaStream_t s) {
+    if (a.count <= 0) return;
+    sgd_multi_kernel<<<static_cast<unsigned>(a.block0[a.count]), 256, 0, s>>>(a);
+    SOL_CUDA(cudaGetLastError());
+}
+
 void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror, cudaStream_t s) {
     sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, g, n, lr, static_cast<__nv_bfloat16*>(mirror));
     SOL_CUDA(cudaGetLastError());

@@ -491,6 +491,43 @@ private:
     int64_t n_;
 };
 
+// Many SgdUpdate ops in one unit (plan-level multi-tensor update): bindings are (param, grad)
+// pairs, every parameter is updated in place, the unit output aliases the first parameter.
+class SgdMultiModule : public Module {
+public:
+    explicit SgdMultiModule(const sol_unit_desc& d) {
+        fill_arg_bytes(*this, d);
+        family = "sgd_update";
+        if (d.n_ops > SGD_MULTI_MAX) unsupported("too many parameters for one SGD unit");
+        a_.count = d.n_ops;
+        a_.lr = d.ops[0].attrs.lr;
+        int blocks = 0;
+        for (int i = 0; i < d.n_ops; ++i) {
+            const sol_unit_op& o = d.ops[i];
+            if (o.op != SOL_OP_SGDUPDATE || o.inputs[0] != 2 * i || o.inputs[1] != 2 * i + 1)
+                unsupported("multi-SGD unit must list (param, grad) pairs");
+            if (o.attrs.lr != a_.lr) unsupported("multi-SGD unit with mixed learning rates");
+            a_.n[i] = param_numel(d.bindings[2 * i]);
+            a_.block0[i] = blocks;
+            blocks += static_cast<int>(ceil_div(a_.n[i], 1024));
+            algo_bytes += 12.0 * a_.n[i];
+        }
+        a_.block0[d.n_ops] = blocks;
+    }
+    void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
+        if (nargs != n_args) throw std::invalid_argument("sgd: wrong argument count");
+        SgdMultiArgs a = a_;
+        for (int i = 0; i < a.count; ++i) {
+            a.w[i] = static_cast<float*>(args[2 * i]);
+            a.g[i] = static_cast<const float*>(args[2 * i + 1]);
+        }
+        sgd_multi(a, s);
+    }
+
+private:
+    SgdMultiArgs a_;
+};
+
 // ---------------------------------------------------------------------------------------------
 // per-channel reductions: BatchNormBack{X,Gamma,Beta} (training), Conv2dBackB, LinearBackB
 // ---------------------------------------------------------------------------------------------
@@ -548,6 +585,17 @@ public:
     }
     size_t scratch_bytes() const override { return static_cast<size_t>(blocks_) * C_ * 4 * 8 + 256; }
 
+    // BatchNormBackX also writes its siblings' outputs (bit 0: BatchNormBackGamma, bit 1:
+    // BatchNormBackBeta) from the same reduction pass ("fuse sibling BN-backward units").
+    bool set_sibling_outputs(int mask) override {
+        if (op_ != SOL_OP_BATCHNORMBACKX || (mask & ~3)) return mask == 0;
+        n_args += __builtin_popcount(static_cast<unsigned>(mask)) - __builtin_popcount(static_cast<unsigned>(sib_));
+        for (int b = 0; b < 2; ++b)
+            if ((mask >> b) & 1) arg_bytes.push_back(static_cast<size_t>(Creal_) * 4);
+        sib_ = mask;
+        return true;
+    }
+
     DfpArgs base(void* const* args, double* partial) const {
         DfpArgs a;
         a.family = FAM_CHAN_REDUCE;
@@ -573,7 +621,15 @@ public:
     void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool) override {
         if (nargs != n_args) throw std::invalid_argument("reduce module: wrong argument count");
         double* partial = static_cast<double*>(scratch);
-        float* out = static_cast<float*>(args[nargs - 1]);
+        const int n_sib = __builtin_popcount(static_cast<unsigned>(sib_));
+        float* out = static_cast<float*>(args[nargs - 1 - n_sib]);
+        float* sib_gamma = nullptr;
+        float* sib_beta = nullptr;
+        {
+            int k = nargs - n_sib;
+            if (sib_ & 1) sib_gamma = static_cast<float*>(args[k++]);
+            if (sib_ & 2) sib_beta = static_cast<float*>(args[k++]);
+        }
         if (op_ == SOL_OP_BATCHNORMBACKBETA || op_ == SOL_OP_CONV2DBACKB || op_ == SOL_OP_LINEARBACKB) {
             DfpArgs a = base(args, partial);
             a.pre = prog_load(0);
@@ -608,6 +664,8 @@ public:
         f.gamma = static_cast<const float*>(args[gamma_idx_]);
         f.coef = coef_;
         f.xhat = xhat_;
+        f.out1 = sib_gamma;
+        f.out0 = sib_beta;
         dfp_finalize(f, s);
         bn_back_apply(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), coef_, xhat_, out, s);
     }
@@ -621,6 +679,7 @@ private:
     int C_ = 0, Creal_ = 0;
     int blocks_ = 1;
     int x_idx_ = -1, gamma_idx_ = -1;
+    int sib_ = 0;
     float *shift_ = nullptr, *xhat_ = nullptr, *coef_ = nullptr;
 };
 
@@ -1149,6 +1208,7 @@ std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
         const Geo g = geo_b(d.bindings[o0.inputs[0]]);
         if (o0.op == SOL_OP_LINEAR || !is_depthwise(o0, g.C)) return std::make_unique<HeavyModule>(d);
     }
+    if (d.n_ops > 1 && o0.op == SOL_OP_SGDUPDATE) return std::make_unique<SgdMultiModule>(d);
     if (d.n_ops == 1) {
         const int op = o0.op;
         if (is_heavy_op(op)) {

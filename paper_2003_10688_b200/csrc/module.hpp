@@ -24,6 +24,9 @@ public:
     // args: bindings in order, then the output (device pointers)
     virtual void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) = 0;
     virtual size_t scratch_bytes() const { return 0; }
+    // Extra outputs written by this module on behalf of sibling units (mask bits; see
+    // sol_b200_module_set_sibling_outputs). Returns false if the module cannot produce them.
+    virtual bool set_sibling_outputs(int mask) { return mask == 0; }
 
     std::string family;
     int n_args = 0;

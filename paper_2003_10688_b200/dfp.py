@@ -187,6 +187,40 @@ def reorder_module(meta: Meta, dtype: int, inbound: bool) -> UnitModule:
                       info.algo_flops, info.launches)
 
 
+def sgd_multi_module(shapes, lr: float, dtype: int) -> UnitModule:
+    """All SgdUpdate units of a training plan as ONE module (one multi-tensor launch): bindings are
+    (param, grad) pairs, updates are in place; the unit output aliases the first parameter."""
+    n = len(shapes)
+    ops = (L.UnitOp * n)()
+    bindings = (L.Binding * (2 * n))()
+    for i, shape in enumerate(shapes):
+        o = ops[i]
+        o.op = OP_ID["SgdUpdate"]
+        o.n_inputs = 2
+        o.inputs[0] = 2 * i
+        o.inputs[1] = 2 * i + 1
+        o.attrs = L.Attrs()
+        o.attrs.lr = lr
+        meta = Meta("plain", tuple(shape))
+        o.out_rank = _dims(meta, o.out_dims)
+        bindings[2 * i] = binding_for(meta, dtype, True)
+        bindings[2 * i + 1] = binding_for(meta, dtype, True)
+    d = L.UnitDesc()
+    d.kind = 0
+    d.n_ops = n
+    d.ops = C.cast(ops, C.POINTER(L.UnitOp))
+    d.n_bindings = 2 * n
+    d.bindings = C.cast(bindings, C.POINTER(L.Binding))
+    d.output = binding_for(Meta("plain", tuple(shapes[0])), dtype, True)
+    d.dtype = dtype
+    h = C.c_void_p()
+    L.check(L.lib().sol_b200_module_create(C.byref(d), C.byref(h)))
+    info = L.ModuleInfo()
+    L.check(L.lib().sol_b200_module_info(h, C.byref(info)))
+    return UnitModule(h, info.family.decode(), info.n_args, info.scratch_bytes, info.algo_bytes,
+                      info.algo_flops, info.launches)
+
+
 def sgd_module(shape, lr: float, dtype: int) -> UnitModule:
     """SgdUpdate unit (dfp_lower.cpp:780-783) over a parameter and its gradient (f32)."""
     ops = (L.UnitOp * 1)()

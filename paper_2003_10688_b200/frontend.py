@@ -22,7 +22,8 @@ import numpy as np
 
 from . import _lib as L
 from .autodiff import build_training_graph
-from .dfp import (DTYPES, ELEM, create_module, is_f32_tensor, reorder_module, sgd_module, storage_bytes)
+from .dfp import (DTYPES, ELEM, create_module, is_f32_tensor, reorder_module, sgd_module, sgd_multi_module,
+                  storage_bytes)
 from .graph import Meta, ModelGraph, infer_shapes
 from .partition import ExecUnit, partition
 from .passes import run_pipeline
@@ -43,6 +44,8 @@ class OptimizeOptions:
     passes: bool = True        # reference rewrite pipeline (passes.cpp:168-178)
     keep_all: bool = False     # debug: every unit output persistent (no arena reuse)
     fuse_epilogue: bool = False  # inference: fold BN(+Add)(+ReLU) units into the conv epilogue
+    fuse_bn_backward: bool = True  # training: BatchNormBackX also writes its Gamma/Beta siblings
+    multi_sgd: bool = True         # training: every SgdUpdate in one multi-tensor launch
 
 
 @dataclass
@@ -143,13 +146,28 @@ class OptimizedModel:
                      StepInfo("reorder", "", gi.name))
         # unit outputs
         self.modules = []
+        siblings = self._bn_back_siblings() if (o.train and o.fuse_bn_backward) else {}
+        absorbed = {v for sib in siblings.values() for v in sib if v is not None}
+
+        def out_buf(name):
+            if name not in self.buf:
+                meta = g.meta_of(name)
+                self.buf[name] = add_buf(storage_bytes(meta, self.dtype, is_f32_tensor(g, name)),
+                                         name in outputs or o.keep_all)
+            return self.buf[name]
+
         for u in self.units:
-            meta = g.meta_of(u.output)
-            f32 = is_f32_tensor(g, u.output)
-            self.buf[u.output] = add_buf(storage_bytes(meta, self.dtype, f32),
-                                         u.output in outputs or o.keep_all)
+            out_buf(u.output)
+            if u.output in absorbed:
+                continue  # computed by its BatchNormBackX sibling's step
             mod = create_module(g, u, self.dtype)
             ids = [self.buf[n] for n in list(u.inputs) + list(u.params)] + [self.buf[u.output]]
+            if u.output in siblings:
+                gam, bet = siblings[u.output]
+                mask = (1 if gam else 0) | (2 if bet else 0)
+                L.check(lib.sol_b200_module_set_sibling_outputs(mod.handle, mask))
+                mod.n_args += bin(mask).count("1")
+                ids += [out_buf(x) for x in (gam, bet) if x]
             add_step(mod, ids, StepInfo("unit", "", u.output, node_ids=list(u.node_ids)))
         # graph outputs: canonical f32 copies for the host
         self.out_canon: Dict[str, int] = {}
@@ -169,9 +187,16 @@ class OptimizedModel:
                                                             L.DT_F32, 1.0 / o.world_size))
                     self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname,
                                                algo_bytes=4.0 * self.params[pname].size))
-            for pname, gname in self.param_grads:
-                mod = sgd_module(self.params[pname].shape, o.lr, self.dtype)
-                add_step(mod, [self.buf[pname], self.buf[gname], self.buf[pname]], StepInfo("sgd", "", pname))
+            if o.multi_sgd and self.param_grads:
+                for k in range(0, len(self.param_grads), 512):
+                    chunk = self.param_grads[k:k + 512]
+                    mod = sgd_multi_module([self.params[p].shape for p, _ in chunk], o.lr, self.dtype)
+                    ids = [i for p, gname in chunk for i in (self.buf[p], self.buf[gname])] + [self.buf[chunk[0][0]]]
+                    add_step(mod, ids, StepInfo("sgd", "", chunk[0][0]))
+            else:
+                for pname, gname in self.param_grads:
+                    mod = sgd_module(self.params[pname].shape, o.lr, self.dtype)
+                    add_step(mod, [self.buf[pname], self.buf[gname], self.buf[pname]], StepInfo("sgd", "", pname))
         if o.world_size > 1:
             if o.nccl_id is None:
                 raise ValueError("world_size > 1 needs the rank-0 NCCL unique id")
@@ -185,6 +210,27 @@ class OptimizedModel:
         # pinned staging for the host interface
         self.pin_in = {n: PinnedBuffer(4 * m.numel) for n, m in self.inputs.items()}
         self.pin_out = {n: PinnedBuffer(4 * g.meta_of(n).numel) for n in g.outputs}
+
+    def _bn_back_siblings(self):
+        """BatchNormBackX unit output -> (BatchNormBackGamma output, BatchNormBackBeta output) of the
+        same BatchNorm (same delta and x inputs); each sibling is a single-op unit."""
+        g = self.graph
+        single = {}
+        for u in self.units:
+            if len(u.node_ids) == 1:
+                n = g.find_node(u.node_ids[0])
+                if n.op in ("BatchNormBackX", "BatchNormBackGamma", "BatchNormBackBeta"):
+                    single[u.output] = n
+        xs = {nm: n for nm, n in single.items() if n.op == "BatchNormBackX"}
+        out = {}
+        for nm, nx in xs.items():
+            gam = next((k for k, n in single.items() if n.op == "BatchNormBackGamma"
+                        and list(n.inputs[:2]) == list(nx.inputs[:2])), None)
+            bet = next((k for k, n in single.items() if n.op == "BatchNormBackBeta"
+                        and n.inputs[0] == nx.inputs[0]), None)
+            if gam or bet:
+                out[nm] = (gam, bet)
+        return out
 
     def _upload_params(self):
         lib = L.lib()
