@@ -34,10 +34,16 @@ constexpr int stages_for() {
     return std::min(8, (SMEM_BUDGET - 2048) / STAGE_BYTES);
 }
 
-// warp-specialised kernel: 227 KB minus 2 KB alignment/barriers and 32 KB epilogue staging
-template <int STAGE_BYTES>
+// Epilogue staging of the warp-specialised kernel: 8 KB per storing warp; when the tile has a
+// single 128-byte output chunk per row (BN <= CW) only the first four epilogue warps store.
+template <typename TO, int BN>
+constexpr int ws_epi_bytes() {
+    return (BN <= 128 / static_cast<int>(sizeof(TO)) ? 4 : 8) * 8192;
+}
+// pipeline depth: 227 KB minus 2 KB alignment/barriers and the epilogue staging
+template <int STAGE_BYTES, int EPI_BYTES>
 constexpr int ws_stages() {
-    return std::min(8, (227 * 1024 - 2048 - 65536 - 1024) / STAGE_BYTES);
+    return std::min(12, (227 * 1024 - 2048 - EPI_BYTES - 1024) / STAGE_BYTES);
 }
 
 template <int BN>
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     constexpr int A_BYTES = BM * ROWB;
     constexpr int B_BYTES = BN * ROWB;
     constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    constexpr int STAGES = ws_stages<STAGE_BYTES>();
+    constexpr int STAGES = ws_stages<STAGE_BYTES, ws_epi_bytes<TO, BN>()>();
     constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
     constexpr int KSTEP_BYTES = 32;
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         constexpr int CW = 128 / static_cast<int>(sizeof(TO));  // columns per 128-byte box
         const int q = warp & 3;            // TMEM lane quarter
         const int half = (warp - 4) >> 2;  // column interleave
+        // (with 4 staging slots the half-1 warps own no chunk and never touch their pointer)
         uint8_t* stage_buf = smem + STAGES * STAGE_BYTES + 1024 + (warp - 4) * 2 * 4096;
         const bool has_bias = a.bias != nullptr;
         const bool has_fold = a.ep_scale != nullptr;
@@ -672,8 +679,9 @@ CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype, int rows = BM) {
 template <typename T, typename TO, int BN, int MODE>
 void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     constexpr int STAGE_BYTES = BM * ROWB + BN * ROWB;
-    constexpr int STAGES = ws_stages<STAGE_BYTES>();
-    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + 8 * 8192;
+    constexpr int EPI = ws_epi_bytes<TO, BN>();
+    constexpr int STAGES = ws_stages<STAGE_BYTES, EPI>();
+    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + EPI;
     static std::once_flag once;
     std::call_once(once, [] {
         SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1026,6 +1034,7 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
     if (a.residual && ((a.ld_res * out_es) % 16 != 0 || (reinterpret_cast<uintptr_t>(a.residual) & 15) != 0))
         throw std::invalid_argument("igemm: residual must be 16-byte aligned with a 16-byte multiple row stride");
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
+    if (halo_supported(a)) return halo_launch(a, s);
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
         else dispatch_mode<__nv_bfloat16, float>(a, s);

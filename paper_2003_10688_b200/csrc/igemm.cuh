@@ -53,6 +53,10 @@ bool stem_supported(const IgemmArgs& a);
 void stem_launch(const IgemmArgs& a, cudaStream_t stream);
 int stem_kpad(int kh);
 
+// Row-padded halo-tile path for stride-1 "same" k x k convolutions with <= 48 KB halos (halo.cu).
+bool halo_supported(const IgemmArgs& a);
+void halo_launch(const IgemmArgs& a, cudaStream_t stream);
+
 // Tile configuration chosen for a GEMM (exposed for the roofline/bench bookkeeping).
 int igemm_block_n(int nout);
 

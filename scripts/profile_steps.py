@@ -23,6 +23,16 @@ for t, f, o, tf, gb in rows:
     a = fam.setdefault(f, [0, 0]); a[0] += t; a[1] += 1
 for f, (t, n) in sorted(fam.items(), key=lambda kv: -kv[1][0]):
     print(f"{f:24s} {t/1e3:8.3f} ms  {n:4d} steps  {100*t/tot:5.1f}%")
+fam_filter = [a.split("=", 1)[1] for a in sys.argv if a.startswith("family=")]
+if fam_filter:
+    ops = {}
+    for st in m.steps:
+        ops[st.output] = "+".join(m.graph.find_node(n).op for n in st.node_ids) if st.node_ids else ""
+    print("--- steps of", fam_filter[0])
+    for t, f, o, tf, gb in sorted(rows, reverse=True):
+        if f == fam_filter[0]:
+            print(f"{t:9.1f} us {o:36s} {ops.get(o, ''):40s} {gb:8.1f} GB/s")
+    sys.exit(0)
 print("--- top 40 steps")
 for t, f, o, tf, gb in sorted(rows, reverse=True)[:40]:
     print(f"{t:9.1f} us {f:22s} {o:36s} {tf:8.1f} TF/s {gb:8.1f} GB/s")
