@@ -175,6 +175,16 @@ struct SgdMultiArgs {
 };
 void sgd_multi(const SgdMultiArgs& a, cudaStream_t s);
 
+// Strided dgrad: dx[n, h, w, :] = cls[(h % sh) * sw + w % sw][n, h / sh, w / sw, :] (zero where the
+// class pointer is null); class c has grid ch[c] x cw[c], all rows `ld` elements.
+struct InterleaveArgs {
+    const void* cls[16] = {};
+    int ch[16] = {}, cw[16] = {};
+    int sh = 1, sw = 1, N = 0, H = 0, W = 0, ld = 0;
+    void* out = nullptr;
+};
+void subpixel_interleave(int dtype, const InterleaveArgs& a, cudaStream_t s);
+
 // Layout/dtype conversion between canonical NCHW f32 (host-facing) and NHWC plan storage.
 // c_pad >= C channels; padded channels are zero.
 void nchw_to_nhwc(const float* src, void* dst, int dtype, int N, int C, int H, int W, int c_pad,

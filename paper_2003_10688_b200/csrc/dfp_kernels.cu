@@ -1905,6 +1905,35 @@ void sgd_multi(const SgdMultiArgs& a, cudaStream_t s) {
     SOL_CUDA(cudaGetLastError());
 }
 
+__global__ void __launch_bounds__(256) interleave_kernel(const __grid_constant__ InterleaveArgs a, int es) {
+    const int vpr = a.ld * es / 16;  // 16-byte vectors per pixel row
+    const int64_t total = static_cast<int64_t>(a.N) * a.H * a.W * vpr;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t pix = v / vpr;
+        const int j = static_cast<int>(v - pix * vpr);
+        const int w = static_cast<int>(pix % a.W);
+        const int64_t t = pix / a.W;
+        const int h = static_cast<int>(t % a.H);
+        const int n = static_cast<int>(t / a.H);
+        const int c = (h % a.sh) * a.sw + w % a.sw;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (a.cls[c] != nullptr) {
+            const int64_t cp = (static_cast<int64_t>(n) * a.ch[c] + h / a.sh) * a.cw[c] + w / a.sw;
+            val = __ldg(reinterpret_cast<const uint4*>(a.cls[c]) + cp * vpr + j);
+        }
+        reinterpret_cast<uint4*>(a.out)[v] = val;
+    }
+}
+
+void subpixel_interleave(int dtype, const InterleaveArgs& a, cudaStream_t s) {
+    const int es = dtype == DT_BF16 ? 2 : 4;
+    if ((a.ld * es) % 16 != 0) throw std::invalid_argument("interleave: row stride must be 16-byte aligned");
+    const int64_t total = static_cast<int64_t>(a.N) * a.H * a.W * (a.ld * es / 16);
+    interleave_kernel<<<grid_for(total, 256), 256, 0, s>>>(a, es);
+    SOL_CUDA(cudaGetLastError());
+}
+
 void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror, cudaStream_t s) {
     sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, g, n, lr, static_cast<__nv_bfloat16*>(mirror));
     SOL_CUDA(cudaGetLastError());

@@ -664,8 +664,9 @@ CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype, int rows = BM) {
                           static_cast<cuuint64_t>(a.SH), static_cast<cuuint64_t>(a.N)};
     cuuint64_t strides[3] = {a.SC * es, static_cast<cuuint64_t>(a.SW) * a.SC * es,
                              static_cast<cuuint64_t>(a.SH) * a.SW * a.SC * es};
+    // base positions run from `lower` to (S - 1 + upper) in steps of the stride: exactly O of them
     int lower[2] = {-a.pw, -a.ph};
-    int upper[2] = {a.pw - (a.kw - 1), a.ph - (a.kh - 1)};
+    int upper[2] = {(a.OW - 1) * a.sw - (a.SW - 1) - a.pw, (a.OH - 1) * a.sh - (a.SH - 1) - a.ph};
     cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(a.sw), static_cast<cuuint32_t>(a.sh), 1};
     const CUresult r = fn(&m, dtype == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                           const_cast<void*>(a.src), dims, strides, lower, upper, static_cast<cuuint32_t>(128 / es),

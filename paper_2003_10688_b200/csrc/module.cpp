@@ -159,6 +159,7 @@ public:
                 cout_ = in_.C;
                 kpad_ = static_cast<int>(round_up(static_cast<int64_t>(kh_) * kw_ * in_.ld, bk));
                 packed_ = dev_alloc(static_cast<size_t>(cin_) * kpad_ * elem_size(dtype_));
+                if (op_ == SOL_OP_CONV2DBACKX && (sh_ > 1 || sw_ > 1) && sh_ * sw_ <= 16) plan_subpixel(bk);
                 algo_flops = 2.0 * in_.pixels() * cout_ * kh_ * kw_ * cin_;
                 algo_bytes = (in_.pixels() * in_.ld + out_.pixels() * out_.ld) * double(elem_size(dtype_)) +
                              double(cout_) * cin_ * kh_ * kw_ * elem_size(dtype_);
@@ -188,7 +189,103 @@ public:
     }
 
     size_t scratch_bytes() const override {
+        if (!classes_.empty()) return sub_scratch_;
         return op_ == SOL_OP_CONV2DBACKW || op_ == SOL_OP_LINEARBACKW ? (packed_floats_ + ws_floats_) * 4 + 256 : 0;
+    }
+
+    // Strided dgrad by sub-pixel decomposition: the dx pixels of parity class (a, b) only receive
+    // the taps kh = a + ph (mod sh), kw = b + pw (mod sw), whose dy offsets are contiguous, so each
+    // class is a stride-1 convolution of dy (forward-kernel operand paths, no zero taps); the class
+    // grids are interleaved into dx afterwards. Replaces the transposed-conv gather, which spends
+    // (sh*sw - 1)/(sh*sw) of its MMAs on structural zeros.
+    struct SubClass {
+        int th = 0, tw = 0, kh0 = 0, kw0 = 0, offh = 0, offw = 0, OHc = 0, OWc = 0, kpad = 0;
+        void* packed = nullptr;
+        size_t scratch_off = 0;
+    };
+    void plan_subpixel(int bk) {
+        const int H = static_cast<int>(out_.H), W = static_cast<int>(out_.W);
+        size_t off = 0;
+        classes_.assign(sh_ * sw_, SubClass{});
+        for (int a = 0; a < sh_; ++a) {
+            for (int b = 0; b < sw_; ++b) {
+                SubClass c;
+                int omin_h = 1 << 30, omax_h = -(1 << 30), omin_w = 1 << 30, omax_w = -(1 << 30);
+                for (int kh = 0; kh < kh_; ++kh) {
+                    const int d = a + ph_ - kh;
+                    if (((d % sh_) + sh_) % sh_ != 0) continue;
+                    omin_h = std::min(omin_h, d / sh_ - (d < 0 && d % sh_ ? 1 : 0));
+                    omax_h = std::max(omax_h, d / sh_ - (d < 0 && d % sh_ ? 1 : 0));
+                }
+                for (int kw = 0; kw < kw_; ++kw) {
+                    const int d = b + pw_ - kw;
+                    if (((d % sw_) + sw_) % sw_ != 0) continue;
+                    omin_w = std::min(omin_w, d / sw_ - (d < 0 && d % sw_ ? 1 : 0));
+                    omax_w = std::max(omax_w, d / sw_ - (d < 0 && d % sw_ ? 1 : 0));
+                }
+                c.OHc = (H - a + sh_ - 1) / sh_;
+                c.OWc = (W - b + sw_ - 1) / sw_;
+                if (omin_h <= omax_h && omin_w <= omax_w && c.OHc > 0 && c.OWc > 0) {
+                    c.th = omax_h - omin_h + 1;
+                    c.tw = omax_w - omin_w + 1;
+                    c.offh = omin_h;
+                    c.offw = omin_w;
+                    c.kh0 = a + ph_ - sh_ * omin_h;
+                    c.kw0 = b + pw_ - sw_ * omin_w;
+                    c.kpad = static_cast<int>(round_up(static_cast<int64_t>(c.th) * c.tw * in_.ld, bk));
+                    c.packed = dev_alloc(static_cast<size_t>(cin_) * c.kpad * elem_size(dtype_));
+                    c.scratch_off = off;
+                    off += round_up(static_cast<int64_t>(in_.N) * c.OHc * c.OWc * out_.ld * elem_size(dtype_), 256);
+                }
+                classes_[a * sw_ + b] = c;
+            }
+        }
+        sub_scratch_ = off + 256;
+        launches = 1;
+        for (auto& c : classes_) launches += c.th ? 2 : 0;
+    }
+
+    void run_subpixel(void* const* args, void* out, void* scratch, cudaStream_t s, bool frozen) {
+        InterleaveArgs il;
+        il.sh = sh_;
+        il.sw = sw_;
+        il.N = static_cast<int>(out_.N);
+        il.H = static_cast<int>(out_.H);
+        il.W = static_cast<int>(out_.W);
+        il.ld = static_cast<int>(out_.ld);
+        il.out = out;
+        for (size_t ci = 0; ci < classes_.size(); ++ci) {
+            SubClass& c = classes_[ci];
+            il.ch[ci] = c.OHc;
+            il.cw[ci] = c.OWc;
+            if (!c.th) continue;
+            void* dst = static_cast<uint8_t*>(scratch) + c.scratch_off;
+            il.cls[ci] = dst;
+            if (!(frozen && packed_valid_))
+                pack_dgrad_class(static_cast<const float*>(args[w_idx_]), c.packed, dtype_, static_cast<int>(cout_),
+                                 static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), c.kpad, c.th, c.tw, c.kh0,
+                                 c.kw0, sh_, sw_, s);
+            IgemmArgs g;
+            g.mode = IG_FPROP;
+            g.dtype = dtype_;
+            g.out_dtype = dtype_;
+            g.src = args[0];
+            g.wt = c.packed;
+            g.out = dst;
+            g.N = static_cast<int>(in_.N);
+            g.SH = static_cast<int>(in_.H);
+            g.SW = static_cast<int>(in_.W);
+            g.SC = static_cast<int>(in_.ld);
+            g.OH = c.OHc;
+            g.OW = c.OWc;
+            g.kh = c.th; g.kw = c.tw; g.sh = 1; g.sw = 1; g.ph = -c.offh; g.pw = -c.offw;
+            g.Nout = static_cast<int>(cin_);
+            g.K_pad = c.kpad;
+            g.ldo = static_cast<int>(out_.ld);
+            igemm_launch(g, s);
+        }
+        packed_valid_ = true;
+        subpixel_interleave(dtype_, il, s);
     }
 
     // Fused epilogue chain after a Conv2d / Linear fprop (inference BatchNorm folding, the
@@ -311,6 +408,10 @@ public:
             }
             case SOL_OP_CONV2DBACKX:
             case SOL_OP_LINEARBACKX: {
+                if (!classes_.empty()) {
+                    run_subpixel(args, out, scratch, s, frozen);
+                    break;
+                }
                 // stride 1: dx = conv(dy, mirrored transposed taps, padding k-1-p), which runs on the
                 // forward kernels' TMA (1x1) / TMA-im2col (k x k) operand paths
                 const bool as_fprop = sh_ == 1 && sw_ == 1 && ph_ <= kh_ - 1 && pw_ <= kw_ - 1;
@@ -362,6 +463,8 @@ private:
     int64_t cin_ = 0, cout_ = 0;
     int kpad_ = 0;
     bool stem_ = false;
+    std::vector<SubClass> classes_;
+    size_t sub_scratch_ = 0;
     int w_idx_ = -1, b_idx_ = -1;
     void* packed_ = nullptr;
     bool packed_valid_ = false;

@@ -61,6 +61,26 @@ __global__ void pack_stem_kernel(const float* __restrict__ w, __nv_bfloat16* __r
     }
 }
 
+template <typename T>
+__global__ void pack_class_kernel(const float* __restrict__ w, T* __restrict__ p, int Cout, int Cin, int KH, int KW,
+                                  int ld_o, int kpad, int TW, int ntap, int kh0, int kw0, int sh, int sw) {
+    const int64_t total = static_cast<int64_t>(Cin) * kpad;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int ci = static_cast<int>(i / kpad);
+        const int k = static_cast<int>(i - static_cast<int64_t>(ci) * kpad);
+        const int tap = k / ld_o, co = k - tap * ld_o;
+        float v = 0.f;
+        if (tap < ntap && co < Cout) {
+            const int th = tap / TW, tw = tap - th * TW;
+            const int kh = kh0 - sh * th, kw = kw0 - sw * tw;  // kh0 = a + ph - sh * off_h
+            if (kh >= 0 && kh < KH && kw >= 0 && kw < KW)
+                v = w[((static_cast<int64_t>(co) * Cin + ci) * KH + kh) * KW + kw];
+        }
+        p[i] = from_f32<T>(v);
+    }
+}
+
 // canonical dw[co][ci][kh][kw] = packed[co][(kh*KW + kw)*ld + ci]
 __global__ void unpack_grad_kernel(const float* __restrict__ p, float* __restrict__ w, int Cout, int Cin, int KH,
                                    int KW, int ld) {
@@ -114,6 +134,18 @@ void pack_conv_weight_t(const float* w, void* packed, int dtype, int Cout, int C
 void pack_stem_weight(const float* w, void* packed, int Cout, int Cin, int kh, int kw, int kpad, cudaStream_t s) {
     pack_stem_kernel<<<grid_of(static_cast<int64_t>(Cout) * kpad), 256, 0, s>>>(
         w, static_cast<__nv_bfloat16*>(packed), Cout, Cin, kh, kw, kpad);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void pack_dgrad_class(const float* w, void* packed, int dtype, int Cout, int Cin, int KH, int KW, int ld_o, int kpad,
+                      int TH, int TW, int kh0, int kw0, int sh, int sw, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(Cin) * kpad;
+    if (dtype == DT_BF16)
+        pack_class_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<__nv_bfloat16*>(packed), Cout, Cin, KH, KW, ld_o,
+                                                     kpad, TW, TH * TW, kh0, kw0, sh, sw);
+    else
+        pack_class_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<float*>(packed), Cout, Cin, KH, KW, ld_o, kpad,
+                                                     TW, TH * TW, kh0, kw0, sh, sw);
     SOL_CUDA(cudaGetLastError());
 }
 

@@ -10,6 +10,10 @@ void pack_conv_weight(const float* w, void* packed, int dtype, int Cout, int Cin
                       cudaStream_t s);
 // stem K order: packed[co][kh*32 + kw*4 + c] (kw < 8 slots, c < 4), zero elsewhere (stem.cu)
 void pack_stem_weight(const float* w, void* packed, int Cout, int Cin, int kh, int kw, int kpad, cudaStream_t s);
+// Strided dgrad, parity class (a, b): packed[ci][(th, tw)][co] = w[co][ci][kh][kw] with
+// kh = a + ph - sh * (off_h + th), kw = b + pw - sw * (off_w + tw) (sub-pixel decomposition).
+void pack_dgrad_class(const float* w, void* packed, int dtype, int Cout, int Cin, int KH, int KW, int ld_o, int kpad,
+                      int TH, int TW, int kh0, int kw0, int sh, int sw, cudaStream_t s);
 void pack_conv_weight_t(const float* w, void* packed, int dtype, int Cout, int Cin, int kh, int kw, int ld_o,
                         int kpad, cudaStream_t s, bool flip = false);
 void unpack_conv_grad(const float* packed, float* w, int Cout, int Cin, int kh, int kw, int ld, cudaStream_t s);
