@@ -301,7 +301,8 @@ def run_b200(args):
     world = ctx.world
     value = world * B / (dev_ms / 1e3)
     e2e = world * B / (e2e_ms / 1e3)
-    roof, times = roofline_of(m, peaks, peaks_kind, {"conv_fprop_tcgen05", "conv_fprop_fused_tcgen05"}, "tensor")
+    conv_fams = {"conv_fprop_tcgen05", "conv_fprop_fused_tcgen05", "conv_stem_tcgen05", "conv_stem_fused_tcgen05"}
+    roof, times = roofline_of(m, peaks, peaks_kind, conv_fams, "tensor")
     dfp_fams = {s.family for s in m.steps if s.family.startswith("dfp_")}
     roof_dfp, _ = roofline_of(m, peaks, peaks_kind, dfp_fams, "hbm")
     fam_time = {}
@@ -319,7 +320,8 @@ def run_b200(args):
         xt = x[:Bt] if Bt <= B else rng.uniform(-1, 1, (Bt, 3, 224, 224)).astype(np.float32)
         tdev, te2e, th2d, td2h = bench_model(mt, {"x": xt, "t": t}, args.train_steps, args.warmup, ["loss"])
         troof, ttimes = roofline_of(mt, peaks, peaks_kind,
-                                    {"conv_fprop_tcgen05", "conv_dgrad_tcgen05", "conv_wgrad_tcgen05"}, "tensor")
+                                    {"conv_fprop_tcgen05", "conv_dgrad_tcgen05", "conv_wgrad_tcgen05",
+                                     "conv_stem_tcgen05", "conv_stem_wgrad_tcgen05"}, "tensor")
         tfam = {}
         for st, tt in zip(mt.steps, ttimes):
             tfam[st.family] = tfam.get(st.family, 0.0) + tt

@@ -52,6 +52,11 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t stream);
 bool stem_supported(const IgemmArgs& a);
 void stem_launch(const IgemmArgs& a, cudaStream_t stream);
 int stem_kpad(int kh);
+// Stem weight gradient (same halo / im2col machinery): dW canonical [Cout=64][Cin][kh][kw] f32 from
+// dy [N, OH, OW, 64] and x (a.src); `ws` holds stem_wgrad_workspace_floats() partial sums.
+bool stem_wgrad_supported(const IgemmArgs& a, int ld_dy);
+size_t stem_wgrad_workspace_floats();
+void stem_wgrad_launch(const IgemmArgs& a, const void* dy, int Cin, float* ws, float* dw, cudaStream_t stream);
 
 // Row-padded halo-tile path for stride-1 "same" k x k convolutions with <= 48 KB halos (halo.cu).
 bool halo_supported(const IgemmArgs& a);

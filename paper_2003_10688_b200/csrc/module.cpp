@@ -176,6 +176,12 @@ public:
                 WgradArgs w = wargs(nullptr, nullptr, nullptr, nullptr);
                 ws_floats_ = wgrad_workspace_floats(w);
                 packed_floats_ = static_cast<size_t>(cout_) * kh_ * kw_ * x_.ld;
+                if (op_ == SOL_OP_CONV2DBACKW && cin_ <= 4 && stem_wgrad_supported(stem_wgrad_args(), static_cast<int>(in_.ld))) {
+                    stem_wg_ = true;  // few-channel stem: halo-tile weight gradient (stem.cu)
+                    ws_floats_ = stem_wgrad_workspace_floats();
+                    packed_floats_ = 0;
+                    family = "conv_stem_wgrad_tcgen05";
+                }
                 algo_flops = 2.0 * in_.pixels() * cout_ * kh_ * kw_ * cin_;
                 algo_bytes = (in_.pixels() * in_.ld + x_.pixels() * x_.ld) * double(elem_size(dtype_)) +
                              double(cout_) * cin_ * kh_ * kw_ * 4.0;
@@ -350,6 +356,23 @@ public:
         return g;
     }
 
+    // the stem conv's forward geometry (x = input, dy = output grid) for the stem wgrad kernel
+    IgemmArgs stem_wgrad_args() const {
+        IgemmArgs g;
+        g.mode = IG_FPROP;
+        g.dtype = dtype_;
+        g.out_dtype = dtype_;
+        g.N = static_cast<int>(x_.N);
+        g.SH = static_cast<int>(x_.H);
+        g.SW = static_cast<int>(x_.W);
+        g.SC = static_cast<int>(x_.ld);
+        g.OH = static_cast<int>(in_.H);
+        g.OW = static_cast<int>(in_.W);
+        g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
+        g.Nout = static_cast<int>(cout_);
+        return g;
+    }
+
     WgradArgs wargs(const void* dy, const void* x, float* dw, float* ws) const {
         WgradArgs w;
         w.dtype = dtype_;
@@ -444,6 +467,13 @@ public:
                 break;
             }
             default: {
+                if (stem_wg_) {
+                    IgemmArgs g = stem_wgrad_args();
+                    g.src = args[1];
+                    stem_wgrad_launch(g, args[0], static_cast<int>(cin_), static_cast<float*>(scratch),
+                                      static_cast<float*>(out), s);
+                    break;
+                }
                 float* packed = static_cast<float*>(scratch);
                 float* ws = ws_floats_ ? packed + round_up(static_cast<int64_t>(packed_floats_), 64) : nullptr;
                 WgradArgs w = wargs(args[0], args[1], packed, ws);
@@ -462,7 +492,7 @@ private:
     Geo in_, out_, x_;
     int64_t cin_ = 0, cout_ = 0;
     int kpad_ = 0;
-    bool stem_ = false;
+    bool stem_ = false, stem_wg_ = false;
     std::vector<SubClass> classes_;
     size_t sub_scratch_ = 0;
     int w_idx_ = -1, b_idx_ = -1;

@@ -52,10 +52,14 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
 
 __device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
-template <bool SW2>
+// WG: weight gradient instead of fprop. The im2col tile the builders produce is, read per 64-column
+// block, exactly the MN-major operand of dW = xcol^T dy (pixels = K), and the dy tile arrives by a
+// [8 rows][16 cols][64 ch] TMA box (tm_w holds dy's map); every CTA accumulates dW^T over all its
+// tiles in TMEM (2 M tiles of 128 K columns x 64 Cout) and writes one f32 partial to `ws`.
+template <bool SW2, bool WG>
 __global__ void __launch_bounds__(ST_THREADS, 1)
     stem_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-                const __grid_constant__ CUtensorMap tm_o, int HH, int HWp) {
+                const __grid_constant__ CUtensorMap tm_o, int HH, int HWp, float* ws) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -66,7 +70,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     uint64_t* a_empty = bar + 5;  // [2]
     uint64_t* tfull = bar + 7;    // [2]
     uint64_t* tempty = bar + 9;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+    uint64_t* dy_full = bar + 11;   // [2] (WG)
+    uint64_t* dy_empty = bar + 13;  // [2] (WG)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tiles_y = (a.OH + ST_TH - 1) / ST_TH, tiles_x = (a.OW + ST_TW - 1) / ST_TW;
@@ -84,6 +90,8 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
             mbar_init(smem_u32(&a_empty[s]), 1);
             mbar_init(smem_u32(&tfull[s]), 1);
             mbar_init(smem_u32(&tempty[s]), 128);
+            mbar_init(smem_u32(&dy_full[s]), 1);
+            mbar_init(smem_u32(&dy_empty[s]), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
         tma_prefetch(&tm_x);
@@ -99,14 +107,27 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     if (warp == 0) {
         // ---------------------------------------------------------------- TMA producer
         if (lane == 0) {
-            mbar_arrive_tx(smem_u32(b_full), static_cast<uint32_t>(nkb * ST_BN * 128));
-            for (int kb = 0; kb < nkb; ++kb)
-                tma_load_2d(smem_u32(smem + OFF_B + kb * ST_BN * 128), &tm_w, kb * 64, 0, smem_u32(b_full));
-            uint32_t hphase = 0;
+            if (!WG) {
+                mbar_arrive_tx(smem_u32(b_full), static_cast<uint32_t>(nkb * ST_BN * 128));
+                for (int kb = 0; kb < nkb; ++kb)
+                    tma_load_2d(smem_u32(smem + OFF_B + kb * ST_BN * 128), &tm_w, kb * 64, 0, smem_u32(b_full));
+            }
+            uint32_t hphase = 0, dphase = 0;
+            int ds = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int n = t / (tiles_y * tiles_x);
                 const int rem = t - n * tiles_y * tiles_x;
                 const int oy0 = (rem / tiles_x) * ST_TH, ox0 = (rem % tiles_x) * ST_TW;
+                if (WG) {
+                    // dy tile [8][16][64] -> 128 pixel rows x 128 B (MN-major operand)
+                    mbar_wait(smem_u32(&dy_empty[ds]), dphase ^ 1);
+                    mbar_arrive_tx(smem_u32(&dy_full[ds]), 16384);
+                    tma_load_4d(smem_u32(smem + OFF_B + ds * 16384), &tm_w, 0, ox0, oy0, n, smem_u32(&dy_full[ds]));
+                    if (++ds == 2) {
+                        ds = 0;
+                        dphase ^= 1;
+                    }
+                }
                 mbar_wait(smem_u32(halo_empty), hphase ^ 1);
                 mbar_arrive_tx(smem_u32(halo_full), halo_bytes);
                 tma_load_4d(smem_u32(smem + OFF_HALO), &tm_x, 0, ox0 * a.sw - a.pw, oy0 * a.sh - a.ph, n,
@@ -159,6 +180,59 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                 s = 0;
                 aphase ^= 1;
             }
+        }
+    } else if (warp == 5 && WG) {
+        // ---------------------------------------------------------------- MMA issuer (dW^T)
+        constexpr uint32_t IDESC = make_idesc(1, ST_BN, 128, 1, 1);
+        uint32_t aphase = 0;
+        int s = 0;
+        bool first = true;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(smem_u32(&a_full[s]), aphase);
+            mbar_wait(smem_u32(&dy_full[s]), aphase);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t a_addr = smem_u32(smem + OFF_A + s * ST_A_BYTES);
+                const uint32_t d_addr = smem_u32(smem + OFF_B + s * 16384);
+                for (int ks = 0; ks < 8; ++ks) {  // 16 pixels per step
+                    const uint64_t bd = sw128_desc(d_addr + ks * 2048, 16384, 1024);
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        if (mt * 128 >= a.kh * 32) break;
+                        const uint64_t ad = sw128_desc(a_addr + mt * 2 * 16384 + ks * 2048, 16384, 1024);
+                        mma<__nv_bfloat16>(tmem_base + static_cast<uint32_t>(mt * ST_BN), ad, bd, IDESC,
+                                           (first && ks == 0) ? 0u : 1u);
+                    }
+                }
+                mma_commit(smem_u32(&a_empty[s]));
+                mma_commit(smem_u32(&dy_empty[s]));
+            }
+            first = false;
+            __syncwarp();
+            if (++s == 2) {
+                s = 0;
+                aphase ^= 1;
+            }
+        }
+        if (lane == 0) mma_commit(smem_u32(&tfull[0]));
+        __syncwarp();
+    } else if (warp >= 6 && WG) {
+        // ---------------------------------------------------------------- dW^T partial -> ws
+        const int q = warp & 3;
+        mbar_wait(smem_u32(&tfull[0]), 0);
+        tc_fence_after();
+        for (int mt = 0; mt < 2; ++mt) {
+            uint32_t v[ST_BN];
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(mt * ST_BN);
+            tmem_ld32_nowait(taddr, v);
+            tmem_ld32_nowait(taddr + 32, v + 32);
+            tmem_wait_ld();
+            const int kcol = mt * 128 + q * 32 + lane;
+            float* dst = ws + (static_cast<int64_t>(blockIdx.x) * 256 + kcol) * ST_BN;
+#pragma unroll
+            for (int i = 0; i < ST_BN; i += 4)
+                *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                                  __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
         }
     } else if (warp == 5) {
         // ---------------------------------------------------------------- MMA issuer
@@ -322,16 +396,64 @@ void stem_launch(const IgemmArgs& a, cudaStream_t s) {
     stem_geometry(a, HH, HWp);
     static std::once_flag once;
     std::call_once(once, [] {
-        SOL_CUDA(cudaFuncSetAttribute(stem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
-        SOL_CUDA(cudaFuncSetAttribute(stem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
+        SOL_CUDA(cudaFuncSetAttribute(stem_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
+        SOL_CUDA(cudaFuncSetAttribute(stem_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
     });
     const CUtensorMap tx = tmap_4d(a.src, 8, a.SW, a.SH, a.N, 8, HWp, HH, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap tw = make_tmap_2d(a.wt, DT_BF16, a.K_pad, ST_BN, a.K_pad, ST_BN);
     const CUtensorMap to = tmap_4d(a.out, a.ldo, a.OW, a.OH, a.N, 64, ST_TW, 2, CU_TENSOR_MAP_SWIZZLE_128B);
     const int tiles = a.N * ((a.OH + ST_TH - 1) / ST_TH) * ((a.OW + ST_TW - 1) / ST_TW);
     const int grid = std::min(tiles, num_sms());
-    if (a.sw % 2 == 0) stem_kernel<true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp);
-    else stem_kernel<false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp);
+    if (a.sw % 2 == 0) stem_kernel<true, false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp, nullptr);
+    else stem_kernel<false, false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp, nullptr);
+    SOL_CUDA(cudaGetLastError());
+}
+
+namespace {
+// dW[co][c][kh][kw] = sum over CTA partials of dW^T[kh*32 + kw*4 + c][co]
+__global__ void stem_wgrad_reduce(const float* __restrict__ ws, int parts, float* __restrict__ dw, int Cout, int Cin,
+                                  int KH, int KW) {
+    const int total = Cout * Cin * KH * KW;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int kw = i % KW, kh = (i / KW) % KH, c = (i / (KW * KH)) % Cin, co = i / (KW * KH * Cin);
+        const int kcol = kh * 32 + kw * 4 + c;
+        float acc = 0.f;
+        for (int p = 0; p < parts; ++p) acc += ws[(static_cast<int64_t>(p) * 256 + kcol) * ST_BN + co];
+        dw[i] = acc;
+    }
+}
+}  // namespace
+
+bool stem_wgrad_supported(const IgemmArgs& a, int ld_dy) {
+    IgemmArgs f = a;
+    f.mode = IG_FPROP;
+    f.Nout = ST_BN;
+    f.ldo = ST_BN;
+    f.K_pad = stem_kpad(a.kh);
+    f.out_dtype = DT_BF16;
+    f.residual = nullptr;
+    return ld_dy == ST_BN && stem_supported(f);
+}
+
+size_t stem_wgrad_workspace_floats() { return static_cast<size_t>(num_sms()) * 256 * ST_BN; }
+
+void stem_wgrad_launch(const IgemmArgs& a, const void* dy, int Cin, float* ws, float* dw, cudaStream_t s) {
+    int HH, HWp;
+    stem_geometry(a, HH, HWp);
+    static std::once_flag once;
+    std::call_once(once, [] {
+        SOL_CUDA(cudaFuncSetAttribute(stem_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
+        SOL_CUDA(cudaFuncSetAttribute(stem_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
+    });
+    const CUtensorMap tx = tmap_4d(a.src, 8, a.SW, a.SH, a.N, 8, HWp, HH, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const CUtensorMap tdy = tmap_4d(dy, ST_BN, a.OW, a.OH, a.N, 64, ST_TW, ST_TH, CU_TENSOR_MAP_SWIZZLE_128B);
+    const int tiles = a.N * ((a.OH + ST_TH - 1) / ST_TH) * ((a.OW + ST_TW - 1) / ST_TW);
+    const int grid = std::min(tiles, num_sms());
+    if (a.sw % 2 == 0) stem_kernel<true, true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tdy, tdy, HH, HWp, ws);
+    else stem_kernel<false, true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tdy, tdy, HH, HWp, ws);
+    SOL_CUDA(cudaGetLastError());
+    const int total = ST_BN * Cin * a.kh * a.kw;
+    stem_wgrad_reduce<<<(total + 255) / 256, 256, 0, s>>>(ws, grid, dw, ST_BN, Cin, a.kh, a.kw);
     SOL_CUDA(cudaGetLastError());
 }
 

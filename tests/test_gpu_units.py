@@ -142,3 +142,34 @@ def test_stem_conv(gpu, hw, k, s, p, bias):
     want = O.eval_node(g.find_node("stem"), [quant(x, 1).astype(np.float64)], params)
     err = O.oracle_err(got, want)
     assert got.shape == want.shape and err <= 1e-2, err
+
+
+@pytest.mark.parametrize("hw", [64, 37])
+def test_stem_wgrad(gpu, hw):
+    """Stem weight gradient (stem.cu WG mode: halo im2col tiles as the MN-major operand, per-CTA
+    TMEM accumulation, f32 partial reduction) vs the oracle's Conv2dBackW on bf16 operands."""
+    from paper_2003_10688_b200 import autodiff, graph, partition, passes
+    b = graph.GraphBuilder(23)
+    b.input("x", graph.meta_nchw(0, 3, hw, hw))
+    c = b.conv("stem", "x", 3, 64, 7, 2, 3, bias=False)
+    p = b.node("gap", "GlobalAvgPool", [c], graph.Attrs())
+    f = b.linear("fc", p, 64, 8)
+    prob = b.softmax("prob", f)
+    b.input("t", graph.meta_nc(0, 8))
+    batch = 3
+    g = graph.infer_shapes(b.done([b.ce("loss", prob, "t")]), batch)
+    tg = graph.infer_shapes(autodiff.build_training_graph(g).graph, batch)
+    gp = passes.run_pipeline(tg)
+    units = partition.partition(gp)
+    ins = _inputs(gp, batch, seed=6)
+    env = O.run_graph(gp, ins)
+    u = next(u for u in units if gp.find_node(u.node_ids[0]).op == "Conv2dBackW")
+    local = {nm: quant(env[nm], 1).astype(np.float64) for nm in u.inputs}
+    params = {k: np.asarray(v, np.float64) for k, v in gp.params.items()}
+    for nid in u.node_ids:
+        n = gp.find_node(nid)
+        local[nid] = O.eval_node(n, [local[i] for i in n.inputs], params)
+    fam, got = run_unit(gp, u, env, 1, gpu)
+    assert fam == "conv_stem_wgrad_tcgen05"
+    err = O.oracle_err(got, local[u.output])
+    assert err <= 1e-2, err
