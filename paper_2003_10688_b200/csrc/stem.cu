@@ -5,11 +5,11 @@
 // built in shared memory:
 //
 //   warp 0      TMA: packed weights once, then one halo box [HH][HWp][8 ch] per tile
-//   warps 1-4   builders: halo -> compact [HH][HWp][4 ch] (8 B / pixel) -> A tile rows in the
+//   warps 1-8   builders: halo -> compact [HH][HWp][4 ch] (8 B / pixel) -> A tile rows in the
 //               UMMA K-major SWIZZLE_128B layout, K ordered (kh, kw in 8 slots, c in 4), i.e. one
 //               16-byte chunk = two horizontally adjacent taps x 4 channels
-//   warp 5      tcgen05.mma issuer (M = 128 pixels, N = Cout = 64, K = kh * 32)
-//   warps 6-9   epilogue: TMEM -> (bias, folded BN, activation) -> bf16 -> 128B-swizzled staging ->
+//   warp 9      tcgen05.mma issuer (M = 128 pixels, N = Cout = 64, K = kh * 32)
+//   warps 10-13 epilogue: TMEM -> (bias, folded BN, activation) -> bf16 -> 128B-swizzled staging ->
 //               TMA store of [2 rows][16 cols][64 ch] boxes
 //
 // Semantics are exactly the generic fprop's (reference.cpp:138-161): zero padding comes from the
@@ -27,17 +27,17 @@ using namespace tc;
 
 constexpr int ST_TH = 8, ST_TW = 16;  // output tile: 8 rows x 16 columns = 128 pixels
 constexpr int ST_BN = 64;             // Cout
-constexpr int ST_THREADS = 320;
+constexpr int ST_THREADS = 448;  // TMA warp, 8 builder warps, MMA warp, 4 epilogue warps
 constexpr int ST_A_BYTES = 65536;     // 4 k-blocks x 128 rows x 128 B
 constexpr int ST_B_BYTES = 4 * ST_BN * 128;
-constexpr int ST_STAGE_BYTES = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 buffers
-constexpr int ST_HALO_MAX = 16384;            // raw halo bytes (16 B / pixel)
+constexpr int ST_STAGE_BYTES = 4 * 4096;      // epilogue staging: 4 warps x 1 buffer
+constexpr int ST_HALO_MAX = 13312;            // raw halo bytes (16 B / pixel), double-buffered
 constexpr int ST_COMPACT_MAX = 8192 + 64;     // compact halo (8 B / pixel, + overrun pad)
 constexpr int OFF_A = 0;
 constexpr int OFF_B = OFF_A + 2 * ST_A_BYTES;
 constexpr int OFF_STG = OFF_B + ST_B_BYTES;
 constexpr int OFF_HALO = OFF_STG + ST_STAGE_BYTES;
-constexpr int OFF_CMP = OFF_HALO + ST_HALO_MAX;
+constexpr int OFF_CMP = OFF_HALO + 2 * ST_HALO_MAX;
 constexpr int OFF_BAR = OFF_CMP + ST_COMPACT_MAX;
 constexpr int ST_SMEM = OFF_BAR + 256 + 1024;  // barriers + 1 KB alignment slack
 
@@ -50,7 +50,7 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-__device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 // WG: weight gradient instead of fprop. The im2col tile the builders produce is, read per 64-column
 // block, exactly the MN-major operand of dW = xcol^T dy (pixels = K), and the dy tile arrives by a
@@ -64,15 +64,15 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     uint64_t* b_full = bar + 0;
-    uint64_t* halo_full = bar + 1;
-    uint64_t* halo_empty = bar + 2;
+    uint64_t* halo_full = bar + 15;   // [2]
+    uint64_t* halo_empty = bar + 17;  // [2]
     uint64_t* a_full = bar + 3;   // [2]
     uint64_t* a_empty = bar + 5;  // [2]
     uint64_t* tfull = bar + 7;    // [2]
     uint64_t* tempty = bar + 9;   // [2]
     uint64_t* dy_full = bar + 11;   // [2] (WG)
     uint64_t* dy_empty = bar + 13;  // [2] (WG)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tiles_y = (a.OH + ST_TH - 1) / ST_TH, tiles_x = (a.OW + ST_TW - 1) / ST_TW;
@@ -83,10 +83,12 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
 
     if (tid == 0) {
         mbar_init(smem_u32(b_full), 1);
-        mbar_init(smem_u32(halo_full), 1);
-        mbar_init(smem_u32(halo_empty), 128);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(smem_u32(&a_full[s]), 128);
+            mbar_init(smem_u32(&halo_full[s]), 1);
+            mbar_init(smem_u32(&halo_empty[s]), 256);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(smem_u32(&a_full[s]), 256);
             mbar_init(smem_u32(&a_empty[s]), 1);
             mbar_init(smem_u32(&tfull[s]), 1);
             mbar_init(smem_u32(&tempty[s]), 128);
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
         tma_prefetch(&tm_w);
         tma_prefetch(&tm_o);
     }
-    if (warp == 5) tmem_alloc<2 * ST_BN>(smem_u32(tmem_slot));
+    if (warp == 9) tmem_alloc<2 * ST_BN>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                     tma_load_2d(smem_u32(smem + OFF_B + kb * ST_BN * 128), &tm_w, kb * 64, 0, smem_u32(b_full));
             }
             uint32_t hphase = 0, dphase = 0;
-            int ds = 0;
+            int ds = 0, hb = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int n = t / (tiles_y * tiles_x);
                 const int rem = t - n * tiles_y * tiles_x;
@@ -128,35 +130,44 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                         dphase ^= 1;
                     }
                 }
-                mbar_wait(smem_u32(halo_empty), hphase ^ 1);
-                mbar_arrive_tx(smem_u32(halo_full), halo_bytes);
-                tma_load_4d(smem_u32(smem + OFF_HALO), &tm_x, 0, ox0 * a.sw - a.pw, oy0 * a.sh - a.ph, n,
-                            smem_u32(halo_full));
-                hphase ^= 1;
+                mbar_wait(smem_u32(&halo_empty[hb]), hphase ^ 1);
+                mbar_arrive_tx(smem_u32(&halo_full[hb]), halo_bytes);
+                tma_load_4d(smem_u32(smem + OFF_HALO + hb * ST_HALO_MAX), &tm_x, 0, ox0 * a.sw - a.pw,
+                            oy0 * a.sh - a.ph, n, smem_u32(&halo_full[hb]));
+                if (++hb == 2) {
+                    hb = 0;
+                    hphase ^= 1;
+                }
             }
         }
-    } else if (warp <= 4) {
-        // ---------------------------------------------------------------- builders
-        const int r = tid - 32;  // A row = output pixel of the tile
+    } else if (warp <= 8) {
+        // ---------------------------------------------------------------- builders (8 warps)
+        const int b = tid - 32;
+        const int r = b & 127;   // A row = output pixel of the tile
+        const int kh_first = b >> 7;  // the two builder halves take alternate kernel rows
         const int ty = r / ST_TW, tx = r % ST_TW;
-        const uint4* raw = reinterpret_cast<const uint4*>(smem + OFF_HALO);
+        int hb = 0;
         uint2* cmp = reinterpret_cast<uint2*>(smem + OFF_CMP);
         const int npix = HH * HWp;
         uint32_t hphase = 0, aphase = 0;
         int s = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             builders_sync();  // every builder is done reading the previous compact halo
-            mbar_wait(smem_u32(halo_full), hphase);
-            hphase ^= 1;
-            for (int i = r; i < npix; i += 128) {
+            mbar_wait(smem_u32(&halo_full[hb]), hphase);
+            const uint4* raw = reinterpret_cast<const uint4*>(smem + OFF_HALO + hb * ST_HALO_MAX);
+            for (int i = b; i < npix; i += 256) {
                 const uint4 v = raw[i];
                 cmp[i] = make_uint2(v.x, v.y);  // channels 0..3
             }
             builders_sync();
-            mbar_arrive(smem_u32(halo_empty));
+            mbar_arrive(smem_u32(&halo_empty[hb]));
+            if (++hb == 2) {
+                hb = 0;
+                hphase ^= 1;
+            }
             mbar_wait(smem_u32(&a_empty[s]), aphase ^ 1);
             uint8_t* A = smem + OFF_A + s * ST_A_BYTES;
-            for (int khi = 0; khi < a.kh; ++khi) {
+            for (int khi = kh_first; khi < a.kh; khi += 2) {
                 const int pix = (ty * a.sh + khi) * HWp + tx * a.sw;
 #pragma unroll
                 for (int jc = 0; jc < 4; ++jc) {
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                 aphase ^= 1;
             }
         }
-    } else if (warp == 5 && WG) {
+    } else if (warp == 9 && WG) {
         // ---------------------------------------------------------------- MMA issuer (dW^T)
         constexpr uint32_t IDESC = make_idesc(1, ST_BN, 128, 1, 1);
         uint32_t aphase = 0;
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
         }
         if (lane == 0) mma_commit(smem_u32(&tfull[0]));
         __syncwarp();
-    } else if (warp >= 6 && WG) {
+    } else if (warp >= 10 && WG) {
         // ---------------------------------------------------------------- dW^T partial -> ws
         const int q = warp & 3;
         mbar_wait(smem_u32(&tfull[0]), 0);
@@ -234,7 +245,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                 *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
                                                                   __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ---------------------------------------------------------------- MMA issuer
         constexpr uint32_t IDESC = make_idesc(1, ST_BN, 128, 0, 0);
         mbar_wait(smem_u32(b_full), 0);
@@ -269,7 +280,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     } else {
         // ---------------------------------------------------------------- epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access = tile rows 2q, 2q+1
-        uint8_t* stage = smem + OFF_STG + q * 8192;
+        uint8_t* stage = smem + OFF_STG + q * 4096;
         const bool has_bias = a.bias != nullptr, has_fold = a.ep_scale != nullptr;
         const int act = a.relu ? 1 : a.act;
         uint32_t acc_phase = 0;
@@ -315,9 +326,9 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                     if (act == 2) f[i] = fminf(f[i], 6.f);
                 }
             }
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
             __syncwarp();
-            uint8_t* sb = stage + buf * 4096;
+            uint8_t* sb = stage;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const float* src = f + j * 8;
@@ -351,7 +362,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc<2 * ST_BN>(tmem_base);
     }
