@@ -207,6 +207,20 @@ def roofline_of(m, peaks, peaks_kind, families, bound):
             tot_w += st.algo_flops if bound == "tensor" else st.algo_bytes
     if tot_t <= 0:
         return None, times
+    # speed of light per launch: max(FLOPs / tensor peak, bytes / HBM peak) -- many convolutions of
+    # the network are HBM-bound, so this is the fraction that can actually approach 1
+    tc_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
+    hbm_peak = peaks["hbm_gbs"] * 1e9
+    sol_t = sum(max(st.algo_flops / tc_peak, st.algo_bytes / hbm_peak) for st, t in zip(info, times)
+                if st.family in families)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "conv_traffic_latest.json")) as f:
+            tj = json.load(f)
+        if bound == "tensor":
+            traffic = tj.get("mean_dram_bytes_per_launch")
+    except Exception:
+        pass
     if bound == "tensor":
         achieved = tot_w / (tot_t * 1e-6) / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
@@ -216,8 +230,8 @@ def roofline_of(m, peaks, peaks_kind, families, bound):
         peak = peaks["hbm_gbs"]
         unit = "GB/s"
     return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-            "traffic": None, "kernel": "+".join(sorted(families)), "peak_source": peaks_kind,
-            "share_of_step": tot_t / sum(times)}, times
+            "traffic": traffic, "kernel": "+".join(sorted(families)), "peak_source": peaks_kind,
+            "share_of_step": tot_t / sum(times), "sol_frac": sol_t / (tot_t * 1e-6)}, times
 
 
 def bench_model(m, inputs, steps, warmup, out_names):

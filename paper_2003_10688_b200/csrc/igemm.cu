@@ -266,6 +266,7 @@ constexpr int WS_THREADS = 416;  // 4 producer + 8 epilogue + 1 MMA warps
 constexpr int WS_MMA_WARP = 12;
 constexpr int IG_FPROP_TMA = 2;     // internal mode: A via TMA (1x1, stride 1, pad 0 fprop)
 constexpr int IG_FPROP_IM2COL = 3;  // internal mode: A via TMA im2col (channels multiple of 128 B)
+constexpr int IG_DUAL = 4;          // internal mode: two 1x1 convs summed in one accumulator (TMA)
 
 template <int BN>
 constexpr uint32_t ws_tmem_cols() {
@@ -276,7 +277,7 @@ template <typename T, typename TO, int BN, int MODE>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
-                    const __grid_constant__ CUtensorMap tmap_r) {
+                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
     constexpr int VEC = 16 / sizeof(T);
     constexpr int BK = ROWB / sizeof(T);
     constexpr int A_BYTES = BM * ROWB;
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
     constexpr int KSTEP_BYTES = 32;
-    constexpr bool A_TMA = MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL;
+    constexpr bool A_TMA = MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL || MODE == IG_DUAL;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -369,6 +370,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     mbar_arrive_tx(smem_u32(&full[stage]), A_TMA ? (A_BYTES + B_BYTES) : B_BYTES);
                     tma_load_2d(smem_u32(sb), &tmap_b, kb * BK, n0, smem_u32(&full[stage]));
                     if (MODE == IG_FPROP_TMA) tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
+                    if (MODE == IG_DUAL) {
+                        const int kb1 = a.K1 / BK;
+                        if (kb < kb1) {
+                            tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
+                        } else if (a.s2 == 1) {
+                            tma_load_2d(smem_u32(sa), &tmap_a2, (kb - kb1) * BK, m0, smem_u32(&full[stage]));
+                        } else {
+                            const int img = m0 / ohw, rem = m0 - img * ohw;
+                            const int oh0 = rem / a.OW, ow0 = rem - (rem / a.OW) * a.OW;
+                            tma_load_im2col_4d(smem_u32(sa), &tmap_a2, (kb - kb1) * BK, ow0 * a.s2, oh0 * a.s2, img, 0,
+                                               0, smem_u32(&full[stage]));
+                        }
+                    }
                     if (MODE == IG_FPROP_IM2COL) {
                         // hardware im2col: 128 output pixels from (n, oh, ow) of m0, one filter tap
                         // (im2col offsets) and one 128-byte channel block per k-block
@@ -693,16 +707,27 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     const int n_rows = static_cast<int>(ceil_div(a.Nout, BN)) * BN;  // packed B has >= Nout rows
     CUtensorMap tb = make_tmap_2d(a.wt, dt, a.K_pad, static_cast<uint64_t>(a.Nout), a.K_pad, BN);
     (void)n_rows;
-    CUtensorMap ta = tb;
-    if (MODE == IG_FPROP_TMA) ta = make_tmap_2d(a.src, dt, a.SC, static_cast<uint64_t>(M), a.SC, BM);
+    CUtensorMap ta = tb, ta2 = tb;
+    if (MODE == IG_FPROP_TMA || MODE == IG_DUAL) ta = make_tmap_2d(a.src, dt, a.SC, static_cast<uint64_t>(M), a.SC, BM);
     if (MODE == IG_FPROP_IM2COL) ta = make_tmap_im2col(a, dt);
+    if (MODE == IG_DUAL) {
+        if (a.s2 == 1) {
+            ta2 = make_tmap_2d(a.src2, dt, a.SC2, static_cast<uint64_t>(M), a.SC2, BM);
+        } else {
+            IgemmArgs g2 = a;
+            g2.src = a.src2;
+            g2.SH = a.SH2; g2.SW = a.SW2; g2.SC = a.SC2;
+            g2.kh = g2.kw = 1; g2.sh = g2.sw = a.s2; g2.ph = g2.pw = 0;
+            ta2 = make_tmap_im2col(g2, dt);
+        }
+    }
     const int tiles = static_cast<int>(ceil_div(M, BM) * ceil_div(a.Nout, BN));
     const int grid = std::min(tiles, num_sms());
     const int dto = sizeof(TO) == 2 ? DT_BF16 : DT_F32;
     CUtensorMap tc = make_tmap_2d(a.out, dto, a.ldo, static_cast<uint64_t>(M), a.ldo, 32);
     CUtensorMap tr = tc;
     if (a.residual) tr = make_tmap_2d(a.residual, dto, a.Nout, static_cast<uint64_t>(M), a.ld_res, 32);
-    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr);
+    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2);
     SOL_CUDA(cudaGetLastError());
 }
 
@@ -724,6 +749,10 @@ void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
     constexpr int BK = ROWB / sizeof(T);
     const bool im2col = a.mode == IG_FPROP && !plain && a.SC % BK == 0 && a.K_pad == a.kh * a.kw * a.SC &&
                         a.kh <= 8 && a.kw <= 8;
+    if constexpr (sizeof(T) == 2 && sizeof(TO) == 2) {
+        if (a.src2) return dispatch_ws<T, TO, IG_DUAL>(a, s);
+    }
+    if (a.src2) throw std::invalid_argument("igemm: dual GEMM is bf16 only");
     if (plain) dispatch_ws<T, TO, IG_FPROP_TMA>(a, s);
     else if (im2col) dispatch_ws<T, TO, IG_FPROP_IM2COL>(a, s);
     else if (a.mode == IG_FPROP) dispatch_ws<T, TO, IG_FPROP>(a, s);
@@ -1035,7 +1064,9 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
     if (a.residual && ((a.ld_res * out_es) % 16 != 0 || (reinterpret_cast<uintptr_t>(a.residual) & 15) != 0))
         throw std::invalid_argument("igemm: residual must be 16-byte aligned with a 16-byte multiple row stride");
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
-    if (halo_supported(a)) return halo_launch(a, s);
+    if (a.src2 && (a.SC % 64 || a.SC2 % 64 || a.K1 != a.SC || a.K_pad != a.SC + a.SC2 || a.mode != IG_FPROP))
+        throw std::invalid_argument("igemm: dual GEMM needs two 1x1 convs over 128-byte channel blocks");
+    if (!a.src2 && halo_supported(a)) return halo_launch(a, s);
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
         else dispatch_mode<__nv_bfloat16, float>(a, s);

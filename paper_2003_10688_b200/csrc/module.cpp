@@ -99,6 +99,113 @@ void fill_arg_bytes(Module& m, const sol_unit_desc& d) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// fused bottleneck tail (inference, plan-level fusion): relu( bn1(conv1x1(h)) + bn2(conv1x1_s(x)) )
+// as ONE dual GEMM: both BatchNorm scales folded into the packed weights, shifts into one bias;
+// the downsample branch's output never round-trips through HBM. Unit ops:
+//   [Conv2d(h), BatchNorm2d, Conv2d(x), BatchNorm2d, Add, (ReLU | ReLU6)]
+// ---------------------------------------------------------------------------------------------
+
+class DualConvModule : public Module {
+public:
+    explicit DualConvModule(const sol_unit_desc& d) : dtype_(d.dtype) {
+        fill_arg_bytes(*this, d);
+        if (d.n_ops < 5 || d.n_ops > 6) unsupported("dual conv unit: bad op count");
+        const sol_unit_op &c1 = d.ops[0], &n1 = d.ops[1], &c2 = d.ops[2], &n2 = d.ops[3], &ad = d.ops[4];
+        if (c1.op != SOL_OP_CONV2D || n1.op != SOL_OP_BATCHNORM2D || c2.op != SOL_OP_CONV2D ||
+            n2.op != SOL_OP_BATCHNORM2D || ad.op != SOL_OP_ADD)
+            unsupported("dual conv unit: op pattern");
+        if (n1.inputs[0] != -1 || n2.inputs[0] != -3 || c1.inputs[0] < 0 || c2.inputs[0] < 0)
+            unsupported("dual conv unit: operand wiring");
+        if (!((ad.inputs[0] == -2 && ad.inputs[1] == -4) || (ad.inputs[0] == -4 && ad.inputs[1] == -2)))
+            unsupported("dual conv unit: Add must join both branches");
+        if (n1.attrs.training || n2.attrs.training) unsupported("dual conv unit: inference BatchNorm only");
+        for (const sol_unit_op* c : {&c1, &c2}) {
+            if (c->attrs.kh != 1 || c->attrs.kw != 1 || c->attrs.ph || c->attrs.pw || c->attrs.groups > 1)
+                unsupported("dual conv unit: 1x1 convolutions only");
+        }
+        if (c1.attrs.sh != 1 || c1.attrs.sw != 1 || c2.attrs.sh != c2.attrs.sw) unsupported("dual conv unit: strides");
+        act_ = 0;
+        if (d.n_ops == 6) {
+            const sol_unit_op& r = d.ops[5];
+            if (r.inputs[0] != -5 || (r.op != SOL_OP_RELU && r.op != SOL_OP_RELU6)) unsupported("dual conv unit: activation");
+            act_ = r.op == SOL_OP_RELU ? 1 : 2;
+        }
+        if (dtype_ != DT_BF16) unsupported("dual conv unit: bf16 only");
+        i1_ = c1.inputs[0];
+        i2_ = c2.inputs[0];
+        in1_ = geo_b(d.bindings[i1_]);
+        in2_ = geo_b(d.bindings[i2_]);
+        out_ = geo_b(d.output);
+        s2_ = static_cast<int>(c2.attrs.sh ? c2.attrs.sh : 1);
+        if (in1_.C % 64 || in2_.C % 64 || in1_.ld != in1_.C || in2_.ld != in2_.C || out_.ld % 8)
+            unsupported("dual conv unit: channels must be 128-byte blocks");
+        w1_ = c1.params[0];
+        cb1_ = (c1.attrs.has_bias && c1.n_params > 1) ? c1.params[1] : -1;
+        w2_ = c2.params[0];
+        cb2_ = (c2.attrs.has_bias && c2.n_params > 1) ? c2.params[1] : -1;
+        for (int k = 0; k < 4; ++k) {
+            bn1_[k] = n1.params[k];
+            bn2_[k] = n2.params[k];
+        }
+        eps1_ = n1.attrs.eps;
+        eps2_ = n2.attrs.eps;
+        cout_ = static_cast<int>(out_.C);
+        packed_ = dev_alloc(static_cast<size_t>(cout_) * (in1_.C + in2_.C) * 2);
+        bias_ = static_cast<float*>(dev_alloc(static_cast<size_t>(cout_) * 4));
+        family = "conv_fprop_fused_tcgen05";
+        algo_flops = 2.0 * out_.pixels() * cout_ * (in1_.C + in2_.C);
+        algo_bytes = (in1_.pixels() * in1_.ld + double(out_.pixels()) * in2_.ld + out_.pixels() * out_.ld) * 2.0 +
+                     double(cout_) * (in1_.C + in2_.C) * 2.0;
+        launches = 2;
+    }
+    void run(void* const* args, int nargs, void*, cudaStream_t s, bool frozen) override {
+        if (nargs != n_args) throw std::invalid_argument("dual conv: wrong argument count");
+        if (!(frozen && packed_valid_)) {
+            auto P = [&](int i) { return i >= 0 ? static_cast<const float*>(args[i]) : nullptr; };
+            DualFold f{P(w1_), P(cb1_), P(bn1_[0]), P(bn1_[1]), P(bn1_[2]), P(bn1_[3]),
+                       P(w2_), P(cb2_), P(bn2_[0]), P(bn2_[1]), P(bn2_[2]), P(bn2_[3]),
+                       eps1_, eps2_, cout_, static_cast<int>(in1_.C), static_cast<int>(in2_.C)};
+            pack_dual_weight(f, packed_, bias_, s);
+            packed_valid_ = true;
+        }
+        IgemmArgs g;
+        g.mode = IG_FPROP;
+        g.dtype = DT_BF16;
+        g.out_dtype = DT_BF16;
+        g.src = args[i1_];
+        g.wt = packed_;
+        g.bias = bias_;
+        g.out = args[nargs - 1];
+        g.N = static_cast<int>(out_.N);
+        g.SH = static_cast<int>(in1_.H);
+        g.SW = static_cast<int>(in1_.W);
+        g.SC = static_cast<int>(in1_.C);
+        g.OH = static_cast<int>(out_.H);
+        g.OW = static_cast<int>(out_.W);
+        g.Nout = cout_;
+        g.K_pad = static_cast<int>(in1_.C + in2_.C);
+        g.K1 = static_cast<int>(in1_.C);
+        g.ldo = static_cast<int>(out_.ld);
+        g.act = act_;
+        g.src2 = args[i2_];
+        g.SH2 = static_cast<int>(in2_.H);
+        g.SW2 = static_cast<int>(in2_.W);
+        g.SC2 = static_cast<int>(in2_.C);
+        g.s2 = s2_;
+        igemm_launch(g, s);
+    }
+
+private:
+    int dtype_, act_ = 0, i1_ = -1, i2_ = -1, s2_ = 1, cout_ = 0;
+    Geo in1_, in2_, out_;
+    int w1_ = -1, cb1_ = -1, w2_ = -1, cb2_ = -1, bn1_[4] = {}, bn2_[4] = {};
+    float eps1_ = 1e-5f, eps2_ = 1e-5f;
+    void* packed_ = nullptr;
+    float* bias_ = nullptr;
+    bool packed_valid_ = false;
+};
+
+// ---------------------------------------------------------------------------------------------
 // heavy layers: tcgen05 implicit GEMM (KernelProvider::execute replacement, dnn.hpp:61-63)
 // ---------------------------------------------------------------------------------------------
 
@@ -1336,6 +1443,8 @@ std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
         }
     }
     const sol_unit_op& o0 = d.ops[0];
+    if (d.kind == 1 && d.n_ops >= 5 && o0.op == SOL_OP_CONV2D && d.ops[2].op == SOL_OP_CONV2D)
+        return std::make_unique<DualConvModule>(d);
     if (d.kind == 1 && d.n_ops > 1 && (o0.op == SOL_OP_CONV2D || o0.op == SOL_OP_LINEAR)) {
         // heavy node + fused epilogue chain (plan-level fusion, see HeavyModule::parse_epilogue)
         const Geo g = geo_b(d.bindings[o0.inputs[0]]);

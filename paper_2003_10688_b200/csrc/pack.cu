@@ -81,6 +81,31 @@ __global__ void pack_class_kernel(const float* __restrict__ w, T* __restrict__ p
     }
 }
 
+__global__ void pack_dual_kernel(const DualFold f, __nv_bfloat16* __restrict__ p, float* __restrict__ bias) {
+    const int K = f.C1 + f.C2;
+    const int64_t total = static_cast<int64_t>(f.Cout) * K;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int co = static_cast<int>(i / K), k = static_cast<int>(i - static_cast<int64_t>(co) * K);
+        float v;
+        if (k < f.C1) {
+            const double sc = static_cast<double>(f.g1[co]) / sqrt(static_cast<double>(f.v1[co]) + f.eps1);
+            v = static_cast<float>(f.w1[static_cast<int64_t>(co) * f.C1 + k] * sc);
+        } else {
+            const double sc = static_cast<double>(f.g2[co]) / sqrt(static_cast<double>(f.v2[co]) + f.eps2);
+            v = static_cast<float>(f.w2[static_cast<int64_t>(co) * f.C2 + (k - f.C1)] * sc);
+        }
+        p[i] = __float2bfloat16_rn(v);
+        if (k == 0) {
+            const double s1 = static_cast<double>(f.g1[co]) / sqrt(static_cast<double>(f.v1[co]) + f.eps1);
+            const double s2 = static_cast<double>(f.g2[co]) / sqrt(static_cast<double>(f.v2[co]) + f.eps2);
+            const double t1 = ((f.cb1 ? f.cb1[co] : 0.f) - static_cast<double>(f.m1[co])) * s1 + f.b1[co];
+            const double t2 = ((f.cb2 ? f.cb2[co] : 0.f) - static_cast<double>(f.m2[co])) * s2 + f.b2[co];
+            bias[co] = static_cast<float>(t1 + t2);
+        }
+    }
+}
+
 // canonical dw[co][ci][kh][kw] = packed[co][(kh*KW + kw)*ld + ci]
 __global__ void unpack_grad_kernel(const float* __restrict__ p, float* __restrict__ w, int Cout, int Cin, int KH,
                                    int KW, int ld) {
@@ -146,6 +171,12 @@ void pack_dgrad_class(const float* w, void* packed, int dtype, int Cout, int Cin
     else
         pack_class_kernel<<<grid_of(n), 256, 0, s>>>(w, static_cast<float*>(packed), Cout, Cin, KH, KW, ld_o, kpad,
                                                      TW, TH * TW, kh0, kw0, sh, sw);
+    SOL_CUDA(cudaGetLastError());
+}
+
+void pack_dual_weight(const DualFold& f, void* packed, float* bias, cudaStream_t s) {
+    pack_dual_kernel<<<grid_of(static_cast<int64_t>(f.Cout) * (f.C1 + f.C2)), 256, 0, s>>>(
+        f, static_cast<__nv_bfloat16*>(packed), bias);
     SOL_CUDA(cudaGetLastError());
 }
 

@@ -102,8 +102,10 @@ class OptimizedModel:
         self.graph = cg
         self.units: List[ExecUnit] = partition(cg)
         if options.fuse_epilogue and not options.train:
-            from .fusion import fuse_conv_epilogues
+            from .fusion import fuse_bottleneck_tails, fuse_conv_epilogues
             self.units = fuse_conv_epilogues(cg, self.units)
+            if options.dtype == "bf16":
+                self.units = fuse_bottleneck_tails(cg, self.units)
         self.params: Dict[str, np.ndarray] = {k: np.asarray(v, np.float32).copy() for k, v in g.params.items()}
         self._build_plan()
         self.compile_ms = (time.perf_counter() - t0) * 1e3

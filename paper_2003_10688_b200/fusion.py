@@ -74,3 +74,56 @@ def fuse_conv_epilogues(g: ModelGraph, units: List[ExecUnit]) -> List[ExecUnit]:
         params = list(u.params) + [p for p in v.params if p not in u.params]
         out.append(ExecUnit("dnn", list(u.node_ids) + list(v.node_ids), v.output, inputs, params))
     return out
+
+
+def _ops(g: ModelGraph, u: ExecUnit):
+    return [g.find_node(i).op for i in u.node_ids]
+
+
+def _is_1x1(n, stride_one: bool) -> bool:
+    a = n.attrs
+    return (a.kh == 1 and a.kw == 1 and a.ph == 0 and a.pw == 0 and a.groups <= 1 and a.sh == a.sw
+            and (a.sh == 1 or not stride_one))
+
+
+def fuse_bottleneck_tails(g: ModelGraph, units: List[ExecUnit], block: int = 64) -> List[ExecUnit]:
+    """Merges a fused [Conv1x1, BN, Add, ReLU] unit with the fused [Conv1x1(stride s), BN] unit that
+    produces its residual (ResNet bottleneck tail + downsample) into ONE dual-GEMM unit
+    [conv, bn, conv_ds, bn_ds, add, relu]: both BN scales fold into the weights, the downsample
+    output never touches HBM. Needs both conv inputs in 128-byte channel blocks (`block`)."""
+    cons = g.consumers()
+    outputs = set(g.outputs)
+    by_out = {u.output: i for i, u in enumerate(units)}
+    drop, repl = set(), {}
+    for j, v in enumerate(units):
+        if v.kind != "dnn":
+            continue
+        ops = _ops(g, v)
+        if ops[:3] != ["Conv2d", "BatchNorm2d", "Add"] or len(ops) not in (3, 4):
+            continue
+        if len(ops) == 4 and ops[3] not in ("ReLU", "ReLU6"):
+            continue
+        conv = g.find_node(v.node_ids[0])
+        add = g.find_node(v.node_ids[2])
+        res = add.inputs[1] if add.inputs[0] == v.node_ids[1] else add.inputs[0]
+        i = by_out.get(res)
+        if i is None or i in drop:
+            continue
+        u = units[i]
+        if u.kind != "dnn" or _ops(g, u) != ["Conv2d", "BatchNorm2d"] or res in outputs:
+            continue
+        if len(cons.get(res, [])) != 1:
+            continue
+        ds = g.find_node(u.node_ids[0])
+        if not (_is_1x1(conv, True) and _is_1x1(ds, False)):
+            continue
+        c_main = g.meta_of(conv.inputs[0]).shape[1]
+        c_ds = g.meta_of(ds.inputs[0]).shape[1]
+        if c_main % block or c_ds % block:
+            continue
+        node_ids = list(v.node_ids[:2]) + list(u.node_ids) + list(v.node_ids[2:])
+        inputs = [x for x in v.inputs if x != res] + [x for x in u.inputs if x not in v.inputs]
+        params = list(v.params) + [p for p in u.params if p not in v.params]
+        repl[j] = ExecUnit("dnn", node_ids, v.output, inputs, params)
+        drop.add(i)
+    return [repl.get(j, w) for j, w in enumerate(units) if j not in drop]

@@ -48,5 +48,18 @@ def traffic_table(path):
         print(f"| {i} | `{short(d['name'])}` | {t/1e3:.1f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {(rd+wr)/t:.0f} |")
 
 
+def traffic_json(path, out):
+    """Mean DRAM bytes per launch of the conv kernels in an ncu metrics CSV (for bench.py)."""
+    import json
+    L = by_launch(path)
+    vals = [d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in L.values()]
+    with open(out, "w") as f:
+        json.dump({"source": path, "launches": len(vals), "mean_dram_bytes_per_launch": sum(vals) / max(1, len(vals)),
+                   "note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per conv launch, one inference step"}, f)
+
+
 if __name__ == "__main__":
-    {"launches": launch_table, "traffic": traffic_table}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "traffic-json":
+        traffic_json(sys.argv[2], sys.argv[3])
+    else:
+        {"launches": launch_table, "traffic": traffic_table}[sys.argv[1]](sys.argv[2])

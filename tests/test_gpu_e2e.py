@@ -159,3 +159,35 @@ def test_pipelined_staging_matches_predict(gpu):
         got.append(m.fetch_outputs(["prob"])["prob"])
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("stride,conv_bias", [(1, False), (2, False), (2, True)])
+def test_bottleneck_dual_gemm(gpu, stride, conv_bias):
+    """Bottleneck tail + downsample fused into one dual GEMM (fusion.fuse_bottleneck_tails): both
+    BN scales folded into bf16 weights, stride-2 downsample read by TMA im2col; predict() matches
+    the oracle within the bf16 bar and the unfused plan's answers."""
+    from paper_2003_10688_b200 import frontend, graph
+    from paper_2003_10688_b200.models import _bottleneck, _head
+    b = graph.GraphBuilder(31)
+    b.input("x", graph.meta_nchw(0, 64, 16, 16))
+    y, cout = _bottleneck(b, "x", 64, 64, stride, "blk")
+    if conv_bias:
+        for k in ("blk.conv3.b", "blk.down.b"):
+            b.g.params[k] = np.random.default_rng(2).uniform(-0.2, 0.2, cout).astype(np.float32)
+        for nid in ("blk.conv3", "blk.down"):
+            n = next(n for n in b.g.nodes if n.id == nid)
+            n.attrs.has_bias = True
+            n.params = [nid + ".W", nid + ".b"]
+    y = b.conv("tail", y, cout, 64, 1, 1, 0)  # a heavy consumer keeps the block's ReLU unit closed
+    p = b.gap("gap", y)
+    g = _head(b, p, 64, 10, False)
+    batch = 4
+    gi = graph.infer_shapes(g, batch)
+    ins = _inputs(gi, batch, seed=7)
+    fused = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16", fuse_epilogue=True))
+    assert any(len(u.node_ids) >= 5 for u in fused.units), "dual GEMM unit not formed"
+    plain = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16"))
+    got, ref = fused.predict(ins)["prob"], plain.predict(ins)["prob"]
+    want = O.run_graph(gi, ins)["prob"]
+    assert O.oracle_err(got, want) <= 1e-2
+    assert O.oracle_err(got, ref) <= 1e-2
