@@ -273,7 +273,12 @@ constexpr uint32_t ws_tmem_cols() {
     return 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
 }
 
-template <typename T, typename TO, int BN, int MODE>
+// RESB: the whole packed weight matrix of the single N tile (<= WS_RESB_MAX bytes) is loaded once
+// per CTA and stays resident; pipeline stages then carry only the A tile (one third less
+// L2 -> shared-memory traffic for the narrow 3x3 convolutions, whose im2col A is L2-bound).
+constexpr int WS_RESB_MAX = 80 * 1024;
+
+template <typename T, typename TO, int BN, int MODE, bool RESB = false>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
@@ -282,8 +287,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     constexpr int BK = ROWB / sizeof(T);
     constexpr int A_BYTES = BM * ROWB;
     constexpr int B_BYTES = BN * ROWB;
-    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    constexpr int STAGES = ws_stages<STAGE_BYTES, ws_epi_bytes<TO, BN>()>();
+    constexpr int STAGE_BYTES = RESB ? A_BYTES : A_BYTES + B_BYTES;
+    constexpr int EPI_BYTES = ws_epi_bytes<TO, BN>();
+    constexpr int STAGES = ws_stages<STAGE_BYTES, EPI_BYTES + (RESB ? WS_RESB_MAX : 0)>();
     constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
     constexpr int KSTEP_BYTES = 32;
@@ -296,7 +302,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* rbar = tempty + 2;  // [8 epilogue warps][2 staging buffers]: residual TMA loads
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 16);
+    uint64_t* bres = rbar + 16;   // resident weights loaded (RESB)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+    uint8_t* bres_smem = smem + STAGES * STAGE_BYTES + 1024 + EPI_BYTES;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -316,6 +324,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             mbar_init(smem_u32(&tempty[s]), 256);
         }
         for (int s = 0; s < 16; ++s) mbar_init(smem_u32(&rbar[s]), 1);
+        mbar_init(smem_u32(bres), 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
         tma_prefetch(&tmap_b);
         if (A_TMA) tma_prefetch(&tmap_a);
@@ -335,6 +344,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const int ntaps = a.kh * a.kw;
         int stage = 0;
         uint32_t phase = 0;
+        if (RESB && tid == 0) {
+            mbar_arrive_tx(smem_u32(bres), static_cast<uint32_t>(num_kb * B_BYTES));
+            for (int kb = 0; kb < num_kb; ++kb)
+                tma_load_2d(smem_u32(bres_smem + kb * B_BYTES), &tmap_b, kb * BK, 0, smem_u32(bres));
+        }
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
@@ -367,8 +381,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 uint8_t* sa = smem + stage * STAGE_BYTES;
                 uint8_t* sb = sa + A_BYTES;
                 if (tid == 0) {
-                    mbar_arrive_tx(smem_u32(&full[stage]), A_TMA ? (A_BYTES + B_BYTES) : B_BYTES);
-                    tma_load_2d(smem_u32(sb), &tmap_b, kb * BK, n0, smem_u32(&full[stage]));
+                    mbar_arrive_tx(smem_u32(&full[stage]), RESB ? A_BYTES : (A_TMA ? (A_BYTES + B_BYTES) : B_BYTES));
+                    if (!RESB) tma_load_2d(smem_u32(sb), &tmap_b, kb * BK, n0, smem_u32(&full[stage]));
                     if (MODE == IG_FPROP_TMA) tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
                     if (MODE == IG_DUAL) {
                         const int kb1 = a.K1 / BK;
@@ -437,6 +451,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
+        if (RESB) mbar_wait(smem_u32(bres), 0);
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
             tc_fence_after();
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint32_t b_addr = a_addr + A_BYTES;
+                    const uint32_t b_addr = RESB ? smem_u32(bres_smem + kb * B_BYTES) : a_addr + A_BYTES;
 #pragma unroll
                     for (int k = 0; k < ROWB / KSTEP_BYTES; ++k) {
                         const uint64_t ad = sw128_desc(a_addr + k * KSTEP_BYTES, 16, 1024);
@@ -691,16 +706,16 @@ CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype, int rows = BM) {
     return m;
 }
 
-template <typename T, typename TO, int BN, int MODE>
+template <typename T, typename TO, int BN, int MODE, bool RESB = false>
 void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
-    constexpr int STAGE_BYTES = BM * ROWB + BN * ROWB;
+    constexpr int STAGE_BYTES = RESB ? BM * ROWB : BM * ROWB + BN * ROWB;
     constexpr int EPI = ws_epi_bytes<TO, BN>();
-    constexpr int STAGES = ws_stages<STAGE_BYTES, EPI>();
-    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + EPI;
+    constexpr int STAGES = ws_stages<STAGE_BYTES, EPI + (RESB ? WS_RESB_MAX : 0)>();
+    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + EPI + (RESB ? WS_RESB_MAX : 0);
     static std::once_flag once;
     std::call_once(once, [] {
-        SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SMEM));
+        SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE, RESB>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     });
     const int M = a.N * a.OH * a.OW;
     const int dt = sizeof(T) == 2 ? DT_BF16 : DT_F32;
@@ -727,12 +742,17 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     CUtensorMap tc = make_tmap_2d(a.out, dto, a.ldo, static_cast<uint64_t>(M), a.ldo, 32);
     CUtensorMap tr = tc;
     if (a.residual) tr = make_tmap_2d(a.residual, dto, a.Nout, static_cast<uint64_t>(M), a.ld_res, 32);
-    igemm_ws_kernel<T, TO, BN, MODE><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2);
+    igemm_ws_kernel<T, TO, BN, MODE, RESB><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2);
     SOL_CUDA(cudaGetLastError());
 }
 
 template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
+    if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
+        const int bn = igemm_block_n(a.Nout);
+        if (bn == 64 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX && a.K_pad >= 256 && !(a.dbg & 1024))
+            return launch_ws_t<T, TO, 64, MODE, true>(a, s);
+    }
     switch (igemm_block_n(a.Nout)) {
         case 16: return launch_ws_t<T, TO, 16, MODE>(a, s);
         case 32: return launch_ws_t<T, TO, 32, MODE>(a, s);
