@@ -452,7 +452,36 @@ void Plan::run_step(Step& s, cudaStream_t st) {
 }
 
 void Plan::run_steps(cudaStream_t st) {
-    for (auto& s : steps_) run_step(s, st);
+    for (size_t i = 0; i < steps_.size();) {
+        if (steps_[i].module || !comm_) {
+            run_step(steps_[i], st);
+            ++i;
+            continue;
+        }
+        // a run of gradient all-reduces: one NCCL group (aggregated launches); the 1/G mean is
+        // ncclAvg when the scale is exactly the replica count, else a scale kernel afterwards
+        size_t j = i;
+        nccl_check(ncclGroupStart(), "group");
+        for (; j < steps_.size() && !steps_[j].module; ++j) {
+            Step& s = steps_[j];
+            void* buf = base_ + bufs_[s.ar_id].off;
+            const bool avg = s.ar_scale == 1.f / static_cast<float>(nranks_);
+            nccl_check(ncclAllReduce(buf, buf, s.ar_count, s.ar_dtype == DT_BF16 ? ncclBfloat16 : ncclFloat32,
+                                     avg ? ncclAvg : ncclSum, static_cast<ncclComm_t>(comm_), st),
+                       "allreduce");
+        }
+        nccl_check(ncclGroupEnd(), "group");
+        for (size_t k = i; k < j; ++k) {
+            Step& s = steps_[k];
+            if (s.ar_scale == 1.f || s.ar_scale == 1.f / static_cast<float>(nranks_)) continue;
+            void* buf = base_ + bufs_[s.ar_id].off;
+            const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(s.ar_count, 256), 4096));
+            if (s.ar_dtype == DT_BF16) scale_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(buf), s.ar_count, s.ar_scale);
+            else scale_kernel<<<grid, 256, 0, st>>>(static_cast<float*>(buf), s.ar_count, s.ar_scale);
+            SOL_CUDA(cudaGetLastError());
+        }
+        i = j;
+    }
 }
 
 void Plan::stage_h2d(int id, const void* src, uint64_t bytes) {

@@ -46,6 +46,7 @@ class OptimizeOptions:
     fuse_epilogue: bool = False  # inference: fold BN(+Add)(+ReLU) units into the conv epilogue
     fuse_bn_backward: bool = True  # training: BatchNormBackX also writes its Gamma/Beta siblings
     multi_sgd: bool = True         # training: every SgdUpdate in one multi-tensor launch
+    nccl_allreduce: bool = False   # test hook: run the NCCL gradient all-reduce even with one replica
 
 
 @dataclass
@@ -184,7 +185,7 @@ class OptimizedModel:
         # native training: all-reduce gradients across ranks, then SGD on the device
         if o.train:
             for pname, gname in self.param_grads:
-                if o.world_size > 1:
+                if o.world_size > 1 or o.nccl_allreduce:
                     L.check(lib.sol_b200_plan_add_allreduce(self.plan, self.buf[gname], self.params[pname].size,
                                                             L.DT_F32, 1.0 / o.world_size))
                     self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname,
@@ -199,7 +200,9 @@ class OptimizedModel:
                 for pname, gname in self.param_grads:
                     mod = sgd_module(self.params[pname].shape, o.lr, self.dtype)
                     add_step(mod, [self.buf[pname], self.buf[gname], self.buf[pname]], StepInfo("sgd", "", pname))
-        if o.world_size > 1:
+        if o.world_size > 1 or (o.train and o.nccl_allreduce):
+            if o.nccl_id is None and o.world_size == 1:
+                o.nccl_id = nccl_unique_id()
             if o.nccl_id is None:
                 raise ValueError("world_size > 1 needs the rank-0 NCCL unique id")
             idb = (C.c_uint8 * 128)(*o.nccl_id)

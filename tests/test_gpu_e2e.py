@@ -191,3 +191,22 @@ def test_bottleneck_dual_gemm(gpu, stride, conv_bias):
     want = O.run_graph(gi, ins)["prob"]
     assert O.oracle_err(got, want) <= 1e-2
     assert O.oracle_err(got, ref) <= 1e-2
+
+
+def test_nccl_allreduce_plumbing_single_rank(gpu):
+    """The data-parallel training plan (grouped NCCL all-reduce of every gradient, ncclAvg, inside
+    the captured CUDA graph) run with one replica: must reproduce the plain plan bit for bit.
+    (Multi-replica runs need one process per GPU; this box has one GPU.)"""
+    from paper_2003_10688_b200 import frontend, graph, models
+    batch = 8
+    g = models.resnet(18, hw=32, classes=16, width=16, train=True)
+    ins = _inputs(graph.infer_shapes(g, batch), batch, seed=4)
+    res = []
+    for force in (False, True):
+        m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16", train=True, lr=0.01,
+                                                          nccl_allreduce=force))
+        losses = [m.train_step(ins) for _ in range(3)]
+        res.append((losses, m.host_params()))
+    assert res[0][0] == res[1][0]
+    for k in res[0][1]:
+        assert np.array_equal(res[0][1][k], res[1][1][k]), k
