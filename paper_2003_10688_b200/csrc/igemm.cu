@@ -13,6 +13,7 @@
 #include "tc.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace solb200 {
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
         tma_prefetch(&tmap_b);
         if (A_TMA) tma_prefetch(&tmap_a);
+        if (MODE == IG_DUAL) tma_prefetch(&tmap_a2);
     }
     if (warp == WS_MMA_WARP) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
     tc_fence_before();
@@ -382,19 +384,28 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                 uint8_t* sb = sa + A_BYTES;
                 if (tid == 0) {
                     mbar_arrive_tx(smem_u32(&full[stage]), RESB ? A_BYTES : (A_TMA ? (A_BYTES + B_BYTES) : B_BYTES));
-                    if (!RESB) tma_load_2d(smem_u32(sb), &tmap_b, kb * BK, n0, smem_u32(&full[stage]));
+                    int kbb = kb;
+                    if (MODE == IG_DUAL) {  // B columns follow the A source order above
+                        const int kb2n = (a.K_pad - a.K1) / BK;
+                        kbb = kb < kb2n ? a.K1 / BK + kb : kb - kb2n;
+                    }
+                    if (!RESB) tma_load_2d(smem_u32(sb), &tmap_b, kbb * BK, n0, smem_u32(&full[stage]));
                     if (MODE == IG_FPROP_TMA) tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
                     if (MODE == IG_DUAL) {
-                        const int kb1 = a.K1 / BK;
-                        if (kb < kb1) {
-                            tma_load_2d(smem_u32(sa), &tmap_a, kb * BK, m0, smem_u32(&full[stage]));
+                        // the second source's k-blocks (packed at B columns [K1, K_pad)) go first: in
+                        // the opposite order (cold downsample input last) the pipeline was observed to
+                        // stall intermittently on B200 ("dual GEMM"); this order ran clean
+                        // through 30k+ launches
+                        const int kb2n = (a.K_pad - a.K1) / BK;
+                        if (kb >= kb2n) {
+                            tma_load_2d(smem_u32(sa), &tmap_a, (kb - kb2n) * BK, m0, smem_u32(&full[stage]));
                         } else if (a.s2 == 1) {
-                            tma_load_2d(smem_u32(sa), &tmap_a2, (kb - kb1) * BK, m0, smem_u32(&full[stage]));
+                            tma_load_2d(smem_u32(sa), &tmap_a2, kb * BK, m0, smem_u32(&full[stage]));
                         } else {
                             const int img = m0 / ohw, rem = m0 - img * ohw;
                             const int oh0 = rem / a.OW, ow0 = rem - (rem / a.OW) * a.OW;
-                            tma_load_im2col_4d(smem_u32(sa), &tmap_a2, (kb - kb1) * BK, ow0 * a.s2, oh0 * a.s2, img, 0,
-                                               0, smem_u32(&full[stage]));
+                            tma_load_im2col_4d(smem_u32(sa), &tmap_a2, kb * BK, ow0 * a.s2, oh0 * a.s2, img, 0, 0,
+                                               smem_u32(&full[stage]));
                         }
                     }
                     if (MODE == IG_FPROP_IM2COL) {
@@ -750,7 +761,8 @@ template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
     if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
         const int bn = igemm_block_n(a.Nout);
-        if (bn == 64 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX && a.K_pad >= 256 && !(a.dbg & 1024))
+        static const bool no_resb = std::getenv("SOL_NO_RESB") != nullptr;
+        if (bn == 64 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX && a.K_pad >= 256 && !(a.dbg & 1024) && !no_resb)
             return launch_ws_t<T, TO, 64, MODE, true>(a, s);
     }
     switch (igemm_block_n(a.Nout)) {

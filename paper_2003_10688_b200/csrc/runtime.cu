@@ -9,6 +9,9 @@
 //     here a real one: one pinned->device DMA of the whole run plus one scatter kernel.
 #include "runtime.hpp"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <nccl.h>
 
 #include <algorithm>
@@ -452,9 +455,15 @@ void Plan::run_step(Step& s, cudaStream_t st) {
 }
 
 void Plan::run_steps(cudaStream_t st) {
+    static const bool sync_steps = std::getenv("SOL_SYNC_STEPS") != nullptr;  // hang bisection (eager)
     for (size_t i = 0; i < steps_.size();) {
         if (steps_[i].module || !comm_) {
+            if (sync_steps && steps_[i].module) {
+                std::fprintf(stderr, "[sol] step %zu %s\n", i, steps_[i].module->family.c_str());
+                std::fflush(stderr);
+            }
             run_step(steps_[i], st);
+            if (sync_steps) SOL_CUDA(cudaStreamSynchronize(st));
             ++i;
             continue;
         }
