@@ -413,9 +413,21 @@ __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ 
     if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
     const int c = (blockIdx.y * cvb + cvi) * V;
     const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
-    const T* x0 = static_cast<const T*>(a.in[cs.s0]) + c;
+    const T* x0;
+    int ld0;
+    if (a.in_kind[cs.s0] == IN_CAT) {
+        // Concat source: this thread's channel vector lives in one segment (widths are multiples
+        // of the vector), resolved once
+        int sg = 0;
+        while (sg + 1 < a.n_cat && c >= a.cat_off[sg + 1]) ++sg;
+        ld0 = a.cat_off[sg + 1] - a.cat_off[sg];
+        x0 = static_cast<const T*>(a.cat_ptr[sg]) + (c - a.cat_off[sg]);
+    } else {
+        x0 = static_cast<const T*>(a.in[cs.s0]) + c;
+        ld0 = a.in_ld[cs.s0];
+    }
     const T* x1 = ADD ? static_cast<const T*>(a.in[cs.s1]) + c : nullptr;
-    const int ld0 = a.in_ld[cs.s0], ld1 = ADD ? a.in_ld[cs.s1] : 0;
+    const int ld1 = ADD ? a.in_ld[cs.s1] : 0;
     T* out = static_cast<T*>(a.out) + a.out_coff + c;
     BnRegs<T> b0, b1;
     if (BN0) b0.load(a.P, cs.bn0, c);
@@ -466,7 +478,12 @@ template <typename T>
 bool launch_chain(const DfpArgs& a, cudaStream_t s) {
     const ChainSpec c = match_chain(a.post);
     if (!c.ok) return false;
-    if (a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+    if (a.in_kind[c.s0] == IN_CAT) {
+        for (int k = 0; k < a.n_cat; ++k)
+            if ((a.cat_off[k + 1] - a.cat_off[k]) % VEC<T>) return false;
+    } else if (a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) {
+        return false;
+    }
     if (c.add && (a.in_kind[c.s1] != IN_PIX || a.in_coff[c.s1] != 0)) return false;
     const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW).grid;
     const bool b0 = c.bn0 >= 0, b1 = c.bn1 >= 0;
@@ -873,6 +890,114 @@ __global__ void __launch_bounds__(THREADS) gap_kernel(const __grid_constant__ Df
 // ---------------------------------------------------------------------------------------------
 // FAM_DWCONV (depthwise conv as weighted pooling, dfp_lower.cpp:519-540)
 // ---------------------------------------------------------------------------------------------
+
+// Post programs of the form r0 = act(bn(r0)) (no loads): what follows a window / depthwise anchor.
+struct PostSpec {
+    int ok = 0, bn = -1, act = 0;
+};
+PostSpec match_post(const Program& p) {
+    PostSpec ps;
+    int k = 0;
+    if (k < p.n && p.ins[k].op == PW_BN && p.ins[k].dst == 0) ps.bn = p.ins[k++].arg;
+    if (k < p.n && p.ins[k].dst == 0 && (p.ins[k].op == PW_RELU || p.ins[k].op == PW_RELU6)) {
+        ps.act = p.ins[k].op == PW_RELU ? 1 : 2;
+        ++k;
+    }
+    ps.ok = k == p.n;
+    return ps;
+}
+
+// Depthwise 3x3 conv between straight-line chains (MobileNet-V2's BN-ReLU6-DW-BN-ReLU6 units):
+// thread = one channel vector with the 9 taps, bias and both BN coefficient sets in registers,
+// walking output pixels with all nine 16-byte window loads in flight.
+template <typename T, bool BN0, int ACT0, bool BN1, int ACT1>
+__global__ void __launch_bounds__(THREADS, 1) dwconv3_chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs,
+                                                                   PostSpec ps) {
+    constexpr int V = VEC<T>;
+    const int cv_total = a.C / V;
+    const int cvb = min(cv_total, THREADS);
+    const int rows = THREADS / cvb;
+    const int row = threadIdx.x / cvb;
+    const int cvi = threadIdx.x - row * cvb;
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = (blockIdx.y * cvb + cvi) * V;
+    const T* x = static_cast<const T*>(a.in[cs.s0]) + c;
+    const int ldx = a.in_ld[cs.s0];
+    T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    BnRegs<T> b0, b1;
+    if (BN0) b0.load(a.P, cs.bn0, c);
+    if (BN1) b1.load(a.P, ps.bn, c);
+    float w[9][V], bias[V];
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+#pragma unroll
+        for (int i = 0; i < V; ++i) w[k][i] = __ldg(a.dw_w + k * a.C + c + i);
+#pragma unroll
+    for (int i = 0; i < V; ++i) bias[i] = a.dw_b ? __ldg(a.dw_b + c + i) : 0.f;
+    const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
+    for (int64_t opix = static_cast<int64_t>(blockIdx.x) * rows + row; opix < P; opix += step) {
+        const int ow = static_cast<int>(opix % a.OW);
+        const int64_t t = opix / a.OW;
+        const int oh = static_cast<int>(t % a.OH);
+        const int n = static_cast<int>(t / a.OH);
+        const int h0 = oh * a.sh - a.ph, w0 = ow * a.sw - a.pw;
+        const T* base = x + static_cast<int64_t>(n) * a.H * a.W * ldx;
+        uint4 r[9];
+        bool ok[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const int ih = h0 + k / 3, iw = w0 + k % 3;
+            ok[k] = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+            if (ok[k]) r[k] = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * a.W + iw) * ldx));
+        }
+        float acc[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = bias[i];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            if (!ok[k]) continue;
+            float v[V];
+            unpack16(r[k], v, static_cast<T*>(nullptr));
+            if (BN0) b0.apply(v);
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                if (ACT0 >= 1) v[i] = fmaxf(v[i], 0.f);
+                if (ACT0 == 2) v[i] = fminf(v[i], 6.f);
+                acc[i] = fmaf(v[i], w[k][i], acc[i]);
+            }
+        }
+        if (BN1) b1.apply(acc);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            if (ACT1 >= 1) acc[i] = fmaxf(acc[i], 0.f);
+            if (ACT1 == 2) acc[i] = fminf(acc[i], 6.f);
+        }
+        store16(out + opix * a.out_ld, acc);
+    }
+}
+
+template <typename T>
+bool launch_dwconv3_chain(const DfpArgs& a, cudaStream_t s) {
+    if (a.kh != 3 || a.kw != 3) return false;
+    const ChainSpec c = match_chain(a.pre);
+    const PostSpec ps = match_post(a.post);
+    if (!c.ok || c.add || !ps.ok || a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+    const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW, 2).grid;
+    const bool b0 = c.bn0 >= 0, b1 = ps.bn >= 0;
+#define SOL_DW(B0, A0, B1, A1) dwconv3_chain_kernel<T, B0, A0, B1, A1><<<grid, THREADS, 0, s>>>(a, c, ps)
+#define SOL_DW_A1(B0, A0, B1) \
+    do { if (ps.act == 0) SOL_DW(B0, A0, B1, 0); else if (ps.act == 1) SOL_DW(B0, A0, B1, 1); else SOL_DW(B0, A0, B1, 2); } while (0)
+#define SOL_DW_B1(B0, A0) do { if (b1) SOL_DW_A1(B0, A0, true); else SOL_DW_A1(B0, A0, false); } while (0)
+#define SOL_DW_A0(B0) do { if (c.act == 0) SOL_DW_B1(B0, 0); else if (c.act == 1) SOL_DW_B1(B0, 1); else SOL_DW_B1(B0, 2); } while (0)
+    if (b0) SOL_DW_A0(true);
+    else SOL_DW_A0(false);
+#undef SOL_DW_A0
+#undef SOL_DW_B1
+#undef SOL_DW_A1
+#undef SOL_DW
+    return true;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__ DfpArgs a) {
@@ -1433,6 +1558,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
         }
         case FAM_DWCONV: {
             const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
+            if (launch_dwconv3_chain<T>(a, s)) break;
             dwconv_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
             break;
         }
