@@ -728,6 +728,81 @@ __global__ void __launch_bounds__(THREADS) pool_chain_kernel(const __grid_consta
     }
 }
 
+// 3x3 / stride-2 pooling (the ResNet stem pool) with a sliding window: a thread owns one
+// (image, output row, channel vector) and walks the row left to right, so each output needs only
+// the two new input columns (6 loads instead of 9) and the shared column stays in registers.
+template <typename T, bool IS_MAX, bool BN0, int ACT>
+__global__ void __launch_bounds__(THREADS) pool3s2_row_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int64_t total = static_cast<int64_t>(a.N) * a.OH * cv;
+    const T* x = static_cast<const T*>(a.in[cs.s0]);
+    const int ldx = a.in_ld[cs.s0];
+    T* out = static_cast<T*>(a.out) + a.out_coff;
+    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(v % cv) * V;
+        const int64_t t = v / cv;
+        const int oh = static_cast<int>(t % a.OH);
+        const int n = static_cast<int>(t / a.OH);
+        BnRegs<T> bn;
+        if (BN0) bn.load(a.P, cs.bn0, c);
+        const int h0 = oh * 2 - a.ph;
+        const T* base = x + static_cast<int64_t>(n) * a.H * a.W * ldx + c;
+        auto col = [&](int iw, float* m) {  // reduce one input column (3 rows) -> m
+            uint4 r[3];
+            bool ok[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int ih = h0 + k;
+                ok[k] = ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                if (ok[k]) r[k] = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * a.W + iw) * ldx));
+            }
+            int cnt = 0;
+#pragma unroll
+            for (int i = 0; i < V; ++i) m[i] = IS_MAX ? -INFINITY : 0.f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                if (!ok[k]) continue;
+                ++cnt;
+                float e[V];
+                unpack16(r[k], e, static_cast<T*>(nullptr));
+                if (BN0) bn.apply(e);
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (ACT >= 1) e[i] = fmaxf(e[i], 0.f);
+                    if (ACT == 2) e[i] = fminf(e[i], 6.f);
+                    m[i] = IS_MAX ? fmaxf(m[i], e[i]) : m[i] + e[i];
+                }
+            }
+            return cnt;
+        };
+        float prev[V];
+        int prev_cnt = col(-a.pw, prev);  // column 2*0 - pw
+        for (int ow = 0; ow < a.OW; ++ow) {
+            const int w0 = ow * 2 - a.pw;
+            float m1[V], m2[V];
+            const int c1 = col(w0 + 1, m1);
+            const int c2 = col(w0 + 2, m2);
+            float o[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                if (IS_MAX) o[i] = fmaxf(fmaxf(fmaxf(prev[i], m1[i]), m2[i]), a.min_init);
+                else o[i] = prev[i] + m1[i] + m2[i];
+            }
+            if (!IS_MAX) {
+                const float div = static_cast<float>(a.count_padding ? 9 : prev_cnt + c1 + c2);
+#pragma unroll
+                for (int i = 0; i < V; ++i) o[i] /= div;
+            }
+            store16(out + ((static_cast<int64_t>(n) * a.OH + oh) * a.OW + ow) * a.out_ld + c, o);
+#pragma unroll
+            for (int i = 0; i < V; ++i) prev[i] = m2[i];
+            prev_cnt = c2;
+        }
+    }
+}
+
 // Global average pool over a straight-line source chain; warps stride over pixels so every
 // thread keeps several independent 16-byte loads in flight.
 template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
@@ -774,6 +849,20 @@ bool launch_pool_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
     const dim3 g2 = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW, 2).grid;
     (void)grid;
     const bool k3 = a.kh == 3 && a.kw == 3;
+    if (k3 && a.sh == 2 && a.sw == 2 && a.ph <= 1 && a.pw <= 1) {
+        const unsigned gr = grid_for(static_cast<int64_t>(a.N) * a.OH * (a.C / VEC<T>), THREADS);
+        const bool bb = c.bn0 >= 0;
+#define SOL_P3(MX, B, A) pool3s2_row_kernel<T, MX, B, A><<<gr, THREADS, 0, s>>>(a, c)
+        if (a.pool_max) {
+            if (bb) { if (c.act == 0) SOL_P3(true, true, 0); else if (c.act == 1) SOL_P3(true, true, 1); else SOL_P3(true, true, 2); }
+            else { if (c.act == 0) SOL_P3(true, false, 0); else if (c.act == 1) SOL_P3(true, false, 1); else SOL_P3(true, false, 2); }
+        } else {
+            if (bb) { if (c.act == 0) SOL_P3(false, true, 0); else if (c.act == 1) SOL_P3(false, true, 1); else SOL_P3(false, true, 2); }
+            else { if (c.act == 0) SOL_P3(false, false, 0); else if (c.act == 1) SOL_P3(false, false, 1); else SOL_P3(false, false, 2); }
+        }
+#undef SOL_P3
+        return true;
+    }
 #define SOL_POOL(MX, B, A)                                                              \
     do {                                                                                \
         if (k3) pool_chain_kernel<T, MX, B, A, true><<<g2, THREADS, 0, s>>>(a, c);       \
