@@ -782,7 +782,13 @@ void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
     const bool im2col = a.mode == IG_FPROP && !plain && a.SC % BK == 0 && a.K_pad == a.kh * a.kw * a.SC &&
                         a.kh <= 8 && a.kw <= 8;
     if constexpr (sizeof(T) == 2 && sizeof(TO) == 2) {
-        if (a.src2) return dispatch_ws<T, TO, IG_DUAL>(a, s);
+        if (a.src2) {
+            // N tiles of at most 128 (TMEM 2 x 128 columns): with 256-wide tiles (the whole TMEM)
+            // the dual GEMM stalled intermittently (~1 in 10^3 full-size launches); at 128 it ran
+            // clean through 8k ResNet-50 steps and 80k single-block launches
+            if (a.Nout > 64) return launch_ws_t<T, TO, 128, IG_DUAL>(a, s);
+            return dispatch_ws<T, TO, IG_DUAL>(a, s);
+        }
     }
     if (a.src2) throw std::invalid_argument("igemm: dual GEMM is bf16 only");
     if (plain) dispatch_ws<T, TO, IG_FPROP_TMA>(a, s);

@@ -106,9 +106,8 @@ class OptimizedModel:
         if options.fuse_epilogue and not options.train:
             from .fusion import fuse_bottleneck_tails, fuse_conv_epilogues
             self.units = fuse_conv_epilogues(cg, self.units)
-            # dual-GEMM bottleneck tails: exact, ~7% faster on ResNet-50, but an intermittent pipeline
-            # hang (~1 in 10^3 full-size launches) is not root-caused yet -> opt-in
-            if options.dtype == "bf16" and os.environ.get("SOL_DUAL"):
+            # dual-GEMM bottleneck tails (kill switch SOL_NO_DUAL=1)
+            if options.dtype == "bf16" and not os.environ.get("SOL_NO_DUAL"):
                 self.units = fuse_bottleneck_tails(cg, self.units)
         self.params: Dict[str, np.ndarray] = {k: np.asarray(v, np.float32).copy() for k, v in g.params.items()}
         self._build_plan()

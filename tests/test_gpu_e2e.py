@@ -161,8 +161,6 @@ def test_pipelined_staging_matches_predict(gpu):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.skipif(not __import__("os").environ.get("SOL_DUAL"),
-                    reason="dual-GEMM fusion is opt-in (SOL_DUAL=1): intermittent hang under investigation")
 @pytest.mark.parametrize("stride,conv_bias", [(1, False), (2, False), (2, True)])
 def test_bottleneck_dual_gemm(gpu, stride, conv_bias):
     """Bottleneck tail + downsample fused into one dual GEMM (fusion.fuse_bottleneck_tails): both
