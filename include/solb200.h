@@ -102,7 +102,8 @@ typedef struct {
  * dims are canonical ([N,C,H,W] / [N,C] / [] / plain param extents); activations are stored
  * NHWC (ActLayout::ChannelsLast) with row stride `ld` elements (>= C); params are plain f32. */
 typedef struct {
-    int32_t is_param;
+    int32_t is_param;   /* 0 activation (plan layout), 1 parameter (canonical f32), 2 activation in
+                           the canonical host layout (NCHW f32), accepted by few-channel stem convs */
     int32_t dtype;
     int32_t rank;
     int64_t dims[4];

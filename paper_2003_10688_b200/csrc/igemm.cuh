@@ -47,6 +47,9 @@ struct IgemmArgs {
     // [N, SH2, SW2, SC2] on the same output grid; B packs both weight matrices side by side.
     const void* src2 = nullptr;
     int SH2 = 0, SW2 = 0, SC2 = 0, s2 = 1, K1 = 0;
+    // stem only: `src` is the canonical NCHW f32 input with SC = Cin channels (the layout
+    // conversion of the graph input is folded into the stem's halo load)
+    int src_nchw_f32 = 0;
 };
 
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).

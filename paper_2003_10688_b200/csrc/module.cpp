@@ -240,6 +240,8 @@ public:
                 cin_ = in_.C;
                 cout_ = out_.C;
                 kpad_ = static_cast<int>(round_up(static_cast<int64_t>(kh_) * kw_ * in_.ld, bk));
+                nchw_in_ = d.bindings[o.inputs[0]].is_param == 2;
+                if (nchw_in_ && op_ != SOL_OP_CONV2D) unsupported("canonical NCHW input only for stem convolutions");
                 if (op_ == SOL_OP_CONV2D) {
                     // few-channel stem: halo-tile kernel with its own K order (stem.cu)
                     IgemmArgs g = fprop_args(nullptr, nullptr);
@@ -248,6 +250,8 @@ public:
                         stem_ = true;
                         kpad_ = g.K_pad;
                         family = "conv_stem_tcgen05";
+                    } else if (nchw_in_) {
+                        unsupported("canonical NCHW input needs the stem kernel");
                     }
                 }
                 packed_ = dev_alloc(static_cast<size_t>(cout_) * kpad_ * elem_size(dtype_));
@@ -453,7 +457,8 @@ public:
         g.N = static_cast<int>(in_.N);
         g.SH = static_cast<int>(in_.H);
         g.SW = static_cast<int>(in_.W);
-        g.SC = static_cast<int>(in_.ld);
+        g.SC = static_cast<int>(nchw_in_ ? in_.C : in_.ld);
+        g.src_nchw_f32 = nchw_in_ ? 1 : 0;
         g.OH = static_cast<int>(out_.H);
         g.OW = static_cast<int>(out_.W);
         g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
@@ -599,7 +604,7 @@ private:
     Geo in_, out_, x_;
     int64_t cin_ = 0, cout_ = 0;
     int kpad_ = 0;
-    bool stem_ = false, stem_wg_ = false;
+    bool stem_ = false, stem_wg_ = false, nchw_in_ = false;
     std::vector<SubClass> classes_;
     size_t sub_scratch_ = 0;
     int w_idx_ = -1, b_idx_ = -1;

@@ -59,7 +59,7 @@ __device__ __forceinline__ void builders_sync() { asm volatile("bar.sync 1, 256;
 template <bool SW2, bool WG>
 __global__ void __launch_bounds__(ST_THREADS, 1)
     stem_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-                const __grid_constant__ CUtensorMap tm_o, int HH, int HWp, float* ws) {
+                const __grid_constant__ CUtensorMap tm_o, int HH, int HWp, float* ws, int nbw, int ndelta) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -79,7 +79,11 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
     const int tiles = a.N * tiles_y * tiles_x;
     const int nkb = (a.kh * 32 + 63) / 64;
     const int ksteps = a.kh * 2;  // k16 steps over the kh * 32 real K elements
-    const uint32_t halo_bytes = static_cast<uint32_t>(HH * HWp * 16);
+    // NCHW f32 halo: TMA boxes must start on 16-byte boundaries along W, so the box starts
+    // `ndelta` columns early (constant per conv: tile origins are multiples of 16 columns) and is
+    // `nbw` columns wide; the repack shifts it back
+    const uint32_t halo_bytes =
+        static_cast<uint32_t>(a.src_nchw_f32 ? HH * nbw * 4 * a.SC : HH * HWp * 16);
 
     if (tid == 0) {
         mbar_init(smem_u32(b_full), 1);
@@ -132,8 +136,12 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
                 }
                 mbar_wait(smem_u32(&halo_empty[hb]), hphase ^ 1);
                 mbar_arrive_tx(smem_u32(&halo_full[hb]), halo_bytes);
-                tma_load_4d(smem_u32(smem + OFF_HALO + hb * ST_HALO_MAX), &tm_x, 0, ox0 * a.sw - a.pw,
-                            oy0 * a.sh - a.ph, n, smem_u32(&halo_full[hb]));
+                if (a.src_nchw_f32)  // box {nbw, HH, Cin, 1} over the NCHW f32 input
+                    tma_load_4d(smem_u32(smem + OFF_HALO + hb * ST_HALO_MAX), &tm_x, ox0 * a.sw - a.pw - ndelta,
+                                oy0 * a.sh - a.ph, 0, n, smem_u32(&halo_full[hb]));
+                else
+                    tma_load_4d(smem_u32(smem + OFF_HALO + hb * ST_HALO_MAX), &tm_x, 0, ox0 * a.sw - a.pw,
+                                oy0 * a.sh - a.ph, n, smem_u32(&halo_full[hb]));
                 if (++hb == 2) {
                     hb = 0;
                     hphase ^= 1;
@@ -149,15 +157,33 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
         int hb = 0;
         uint2* cmp = reinterpret_cast<uint2*>(smem + OFF_CMP);
         const int npix = HH * HWp;
+        const int nchw = a.src_nchw_f32;
+        const int cin = a.SC;
         uint32_t hphase = 0, aphase = 0;
         int s = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             builders_sync();  // every builder is done reading the previous compact halo
             mbar_wait(smem_u32(&halo_full[hb]), hphase);
-            const uint4* raw = reinterpret_cast<const uint4*>(smem + OFF_HALO + hb * ST_HALO_MAX);
-            for (int i = b; i < npix; i += 256) {
-                const uint4 v = raw[i];
-                cmp[i] = make_uint2(v.x, v.y);  // channels 0..3
+            if (nchw) {
+                // f32 planes [Cin][HH][HWp] -> 4 bf16 channels per pixel (channels >= Cin zero)
+                const float* plane = reinterpret_cast<const float*>(smem + OFF_HALO + hb * ST_HALO_MAX);
+                const int pplane = HH * nbw;
+                for (int i = b; i < npix; i += 256) {
+                    const int hy = i / HWp, hx = i - (i / HWp) * HWp;
+                    const int src = hy * nbw + hx + ndelta;
+                    float f[4];
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) f[ch] = ch < cin ? plane[ch * pplane + src] : 0.f;
+                    const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]);
+                    const __nv_bfloat162 hi = __floats2bfloat162_rn(f[2], f[3]);
+                    cmp[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+                }
+            } else {
+                const uint4* raw = reinterpret_cast<const uint4*>(smem + OFF_HALO + hb * ST_HALO_MAX);
+                for (int i = b; i < npix; i += 256) {
+                    const uint4 v = raw[i];
+                    cmp[i] = make_uint2(v.x, v.y);  // channels 0..3
+                }
             }
             builders_sync();
             mbar_arrive(smem_u32(&halo_empty[hb]));
@@ -382,10 +408,29 @@ CUtensorMap tmap_4d(const void* base, uint64_t c, uint64_t w, uint64_t h, uint64
     return m;
 }
 
-void stem_geometry(const IgemmArgs& a, int& HH, int& HWp) {
+void stem_geometry(const IgemmArgs& a, int& HH, int& HWp, int* nbw = nullptr, int* ndelta = nullptr) {
     HH = (ST_TH - 1) * a.sh + a.kh;
     const int HW = (ST_TW - 1) * a.sw + a.kw;
     HWp = HW + (HW & 1);
+    // NCHW f32 box: start aligned down to 4 floats (tile origins are 16 * sw columns apart)
+    const int delta = ((a.pw % 4) == 0) ? 0 : 4 - a.pw % 4;
+    if (ndelta) *ndelta = delta;
+    if (nbw) *nbw = (HWp + 1 + delta + 3) / 4 * 4;  // covers column HWp (cmp over-read pad)
+}
+
+CUtensorMap tmap_nchw_f32(const void* base, int N, int C, int H, int W, int bw, int bh) {
+    CUtensorMap m;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(C),
+                          static_cast<cuuint64_t>(N)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(W) * 4, static_cast<cuuint64_t>(H) * W * 4,
+                             static_cast<cuuint64_t>(C) * H * W * 4};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), static_cast<cuuint32_t>(C), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("stem: NCHW tensor map failed: " + std::to_string(static_cast<int>(r)));
+    return m;
 }
 
 }  // namespace
@@ -394,29 +439,33 @@ int stem_kpad(int kh) { return (kh * 32 + 63) / 64 * 64; }
 
 bool stem_supported(const IgemmArgs& a) {
     if (a.mode != IG_FPROP || a.dtype != DT_BF16 || a.out_dtype != DT_BF16) return false;
-    if (a.SC != 8 || a.Nout != ST_BN || a.ldo != ST_BN || a.residual != nullptr) return false;
+    if ((a.src_nchw_f32 ? (a.SC < 1 || a.SC > 4) : a.SC != 8) || a.Nout != ST_BN || a.ldo != ST_BN ||
+        a.residual != nullptr)
+        return false;
     if (a.kw > 8 || a.kh * 32 > 256 || a.K_pad != stem_kpad(a.kh)) return false;
-    int HH, HWp;
-    stem_geometry(a, HH, HWp);
-    return HH * HWp * 16 <= ST_HALO_MAX && HWp <= 256 && HH <= 256 && a.N > 0 && a.OH > 0 && a.OW > 0;
+    int HH, HWp, nbw, nd;
+    stem_geometry(a, HH, HWp, &nbw, &nd);
+    const int halo = a.src_nchw_f32 ? HH * nbw * 4 * a.SC : HH * HWp * 16;
+    return halo <= ST_HALO_MAX && HWp <= 256 && HH <= 256 && a.N > 0 && a.OH > 0 && a.OW > 0;
 }
 
 void stem_launch(const IgemmArgs& a, cudaStream_t s) {
     if (!stem_supported(a)) throw std::invalid_argument("stem conv: unsupported shape");
-    int HH, HWp;
-    stem_geometry(a, HH, HWp);
+    int HH, HWp, nbw, nd;
+    stem_geometry(a, HH, HWp, &nbw, &nd);
     static std::once_flag once;
     std::call_once(once, [] {
         SOL_CUDA(cudaFuncSetAttribute(stem_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
         SOL_CUDA(cudaFuncSetAttribute(stem_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
     });
-    const CUtensorMap tx = tmap_4d(a.src, 8, a.SW, a.SH, a.N, 8, HWp, HH, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const CUtensorMap tx = a.src_nchw_f32 ? tmap_nchw_f32(a.src, a.N, a.SC, a.SH, a.SW, nbw, HH)
+                                          : tmap_4d(a.src, 8, a.SW, a.SH, a.N, 8, HWp, HH, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap tw = make_tmap_2d(a.wt, DT_BF16, a.K_pad, ST_BN, a.K_pad, ST_BN);
     const CUtensorMap to = tmap_4d(a.out, a.ldo, a.OW, a.OH, a.N, 64, ST_TW, 2, CU_TENSOR_MAP_SWIZZLE_128B);
     const int tiles = a.N * ((a.OH + ST_TH - 1) / ST_TH) * ((a.OW + ST_TW - 1) / ST_TW);
     const int grid = std::min(tiles, num_sms());
-    if (a.sw % 2 == 0) stem_kernel<true, false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp, nullptr);
-    else stem_kernel<false, false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp, nullptr);
+    if (a.sw % 2 == 0) stem_kernel<true, false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp, nullptr, nbw, nd);
+    else stem_kernel<false, false><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tw, to, HH, HWp, nullptr, nbw, nd);
     SOL_CUDA(cudaGetLastError());
 }
 
@@ -449,19 +498,20 @@ bool stem_wgrad_supported(const IgemmArgs& a, int ld_dy) {
 size_t stem_wgrad_workspace_floats() { return static_cast<size_t>(num_sms()) * 256 * ST_BN; }
 
 void stem_wgrad_launch(const IgemmArgs& a, const void* dy, int Cin, float* ws, float* dw, cudaStream_t s) {
-    int HH, HWp;
-    stem_geometry(a, HH, HWp);
+    int HH, HWp, nbw, nd;
+    stem_geometry(a, HH, HWp, &nbw, &nd);
     static std::once_flag once;
     std::call_once(once, [] {
         SOL_CUDA(cudaFuncSetAttribute(stem_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
         SOL_CUDA(cudaFuncSetAttribute(stem_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM));
     });
-    const CUtensorMap tx = tmap_4d(a.src, 8, a.SW, a.SH, a.N, 8, HWp, HH, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const CUtensorMap tx = a.src_nchw_f32 ? tmap_nchw_f32(a.src, a.N, a.SC, a.SH, a.SW, nbw, HH)
+                                          : tmap_4d(a.src, 8, a.SW, a.SH, a.N, 8, HWp, HH, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap tdy = tmap_4d(dy, ST_BN, a.OW, a.OH, a.N, 64, ST_TW, ST_TH, CU_TENSOR_MAP_SWIZZLE_128B);
     const int tiles = a.N * ((a.OH + ST_TH - 1) / ST_TH) * ((a.OW + ST_TW - 1) / ST_TW);
     const int grid = std::min(tiles, num_sms());
-    if (a.sw % 2 == 0) stem_kernel<true, true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tdy, tdy, HH, HWp, ws);
-    else stem_kernel<false, true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tdy, tdy, HH, HWp, ws);
+    if (a.sw % 2 == 0) stem_kernel<true, true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tdy, tdy, HH, HWp, ws, nbw, nd);
+    else stem_kernel<false, true><<<grid, ST_THREADS, ST_SMEM, s>>>(a, tx, tdy, tdy, HH, HWp, ws, nbw, nd);
     SOL_CUDA(cudaGetLastError());
     const int total = ST_BN * Cin * a.kh * a.kw;
     stem_wgrad_reduce<<<(total + 255) / 256, 256, 0, s>>>(ws, grid, dw, ST_BN, Cin, a.kh, a.kw);

@@ -107,14 +107,21 @@ def _attrs(a) -> L.Attrs:
     return x
 
 
-def build_desc(g: ModelGraph, unit: ExecUnit, dtype: int):
-    """sol_unit_desc for a unit of shape-inferred graph `g` (keeps the ctypes arrays alive)."""
+def build_desc(g: ModelGraph, unit: ExecUnit, dtype: int, nchw_inputs=()):
+    """sol_unit_desc for a unit of shape-inferred graph `g` (keeps the ctypes arrays alive).
+    Names in `nchw_inputs` are bound in the canonical host layout (NCHW f32, is_param = 2)."""
     names = list(unit.inputs) + list(unit.params)
     index = {n: i for i, n in enumerate(names)}
     bindings = (L.Binding * max(1, len(names)))()
     for i, nm in enumerate(names):
         if nm in g.params:
             bindings[i] = binding_for(Meta("plain", tuple(g.params[nm].shape)), dtype, True)
+        elif nm in nchw_inputs:
+            b = binding_for(g.meta_of(nm), dtype, False)
+            b.is_param = 2
+            b.dtype = L.DT_F32
+            b.ld = g.meta_of(nm).shape[1]
+            bindings[i] = b
         else:
             bindings[i] = binding_for(g.meta_of(nm), dtype, False, is_f32_tensor(g, nm))
     pos = {nid: k for k, nid in enumerate(unit.node_ids)}
@@ -145,8 +152,8 @@ def build_desc(g: ModelGraph, unit: ExecUnit, dtype: int):
     return d, (ops, bindings)
 
 
-def create_module(g: ModelGraph, unit: ExecUnit, dtype: int) -> UnitModule:
-    d, keep = build_desc(g, unit, dtype)
+def create_module(g: ModelGraph, unit: ExecUnit, dtype: int, nchw_inputs=()) -> UnitModule:
+    d, keep = build_desc(g, unit, dtype, nchw_inputs)
     h = C.c_void_p()
     L.check(L.lib().sol_b200_module_create(C.byref(d), C.byref(h)))
     info = L.ModuleInfo()

@@ -143,9 +143,14 @@ class OptimizedModel:
         # graph inputs: canonical f32 staging buffer + NHWC plan buffer + reorder step
         self.inputs: Dict[str, Meta] = {}
         self.in_canon: Dict[str, int] = {}
+        direct = self._direct_stem_inputs()
         for gi in g.graph_inputs:
             self.inputs[gi.name] = gi.meta
             self.in_canon[gi.name] = add_buf(4 * gi.meta.numel, True)
+            if gi.name in direct:
+                # the stem conv reads the canonical NCHW f32 buffer itself (no reorder pass)
+                self.buf[gi.name] = self.in_canon[gi.name]
+                continue
             self.buf[gi.name] = add_buf(storage_bytes(gi.meta, self.dtype), True)
             add_step(reorder_module(gi.meta, self.dtype, True), [self.in_canon[gi.name], self.buf[gi.name]],
                      StepInfo("reorder", "", gi.name))
@@ -165,7 +170,7 @@ class OptimizedModel:
             out_buf(u.output)
             if u.output in absorbed:
                 continue  # computed by its BatchNormBackX sibling's step
-            mod = create_module(g, u, self.dtype)
+            mod = create_module(g, u, self.dtype, [n for n in u.inputs if n in direct])
             ids = [self.buf[n] for n in list(u.inputs) + list(u.params)] + [self.buf[u.output]]
             if u.output in siblings:
                 gam, bet = siblings[u.output]
@@ -217,6 +222,25 @@ class OptimizedModel:
         # pinned staging for the host interface
         self.pin_in = {n: PinnedBuffer(4 * m.numel) for n, m in self.inputs.items()}
         self.pin_out = {n: PinnedBuffer(4 * g.meta_of(n).numel) for n in g.outputs}
+
+    def _direct_stem_inputs(self):
+        """Graph inputs whose only consumer is a few-channel (<= 4) stem Conv2d unit in a bf16
+        inference plan: that conv's halo loads read the canonical NCHW f32 input directly."""
+        g, o = self.graph, self.options
+        if o.dtype != "bf16" or o.train or os.environ.get("SOL_NO_DIRECT_STEM"):
+            return set()
+        out = set()
+        for gi in g.graph_inputs:
+            users = [u for u in self.units if gi.name in u.inputs]
+            if len(users) != 1 or gi.meta.kind != "nchw" or gi.meta.shape[1] > 4:
+                continue
+            u = users[0]
+            n0 = g.find_node(u.node_ids[0])
+            if (u.kind == "dnn" and n0.op == "Conv2d" and n0.inputs[0] == gi.name and n0.attrs.groups <= 1
+                    and n0.attrs.out_channels == 64 and n0.attrs.kw <= 8 and n0.attrs.kh * 32 <= 256
+                    and sum(1 for n in u.node_ids for i in g.find_node(n).inputs if i == gi.name) == 1):
+                out.add(gi.name)
+        return out
 
     def _bn_back_siblings(self):
         """BatchNormBackX unit output -> (BatchNormBackGamma output, BatchNormBackBeta output) of the

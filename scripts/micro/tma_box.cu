@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -24,7 +25,9 @@ __global__ void box_kernel(const __grid_constant__ CUtensorMap m, int loads, int
         asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(su32(&bar[b])), "r"(bytes));
         const int tile = blockIdx.x + i * gridDim.x;  // distinct 4-row blocks: DRAM-sourced
         const int img = (tile / 14) % 256, rb = tile % 14;
-        if (dims4)
+        if (dims4 == 2)
+            asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(su32(sm + b * 32768)), "l"(&m), "r"(-3), "r"(rb * 4 - 3), "r"(0), "r"(img), "r"(su32(&bar[b])) : "memory");
+        else if (dims4)
             asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(su32(sm + b * 32768)), "l"(&m), "r"(0), "r"(w0), "r"(rb * 4), "r"(img), "r"(su32(&bar[b])) : "memory");
         else
             asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(sm + b * 32768)), "l"(&m), "r"(0), "r"((img * 14 + rb) * 224), "r"(su32(&bar[b])) : "memory");
@@ -45,15 +48,24 @@ int main() {
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
     Enc enc = (Enc)fn;
     const int N = 256, H = 56, W = 56, C = 64;
-    void* x; cudaMalloc(&x, (size_t)N * H * W * C * 2);
+    void* x; cudaMalloc(&x, (size_t)N * 3 * 224 * 224 * 4 + (size_t)N * H * W * C * 2);
     cudaMemset(x, 0, (size_t)N * H * W * C * 2);
     cudaFuncSetAttribute(box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     struct Cfg { const char* name; int dims4, bw, bh, w0, nbuf; };
-    Cfg cfgs[] = {{"4d 64x58x4 w0=-1", 1, 58, 4, -1, 5}, {"4d 64x56x4 w0=0", 1, 56, 4, 0, 5}, {"4d 64x58x4 nbuf2", 1, 58, 4, -1, 2},
+    const int bwv = getenv("BW") ? atoi(getenv("BW")) : 40, bhv = getenv("BH") ? atoi(getenv("BH")) : 21;
+    Cfg cfgs[] = {{"nchw f32", 2, bwv, bhv, 0, 5}, {"4d 64x58x4 w0=-1", 1, 58, 4, -1, 5}, {"4d 64x56x4 w0=0", 1, 56, 4, 0, 5}, {"4d 64x58x4 nbuf2", 1, 58, 4, -1, 2},
                   {"2d 64x224", 0, 0, 0, 0, 5}, {"4d 64x56x4 nbuf6", 1, 56, 4, 0, 6}, {"2d 64x224 nbuf2", 0, 0, 0, 0, 2}};
     for (auto& c : cfgs) {
         CUtensorMap m;
-        if (c.dims4) {
+        if (c.dims4 == 2) {
+            cuuint64_t dims[4] = {224, 224, 3, (cuuint64_t)N};
+            cuuint64_t str[3] = {224 * 4, 224 * 224 * 4, 3ull * 224 * 224 * 4};
+            cuuint32_t box[4] = {(cuuint32_t)c.bw, (cuuint32_t)c.bh, 3, 1};
+            cuuint32_t es[4] = {1, 1, 1, 1};
+            CUresult rr = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            fprintf(stderr, "encode %d box %u %u %u\n", (int)rr, box[0], box[1], box[2]);
+        } else if (c.dims4) {
             cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
             cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
             cuuint32_t box[4] = {64, (cuuint32_t)c.bw, (cuuint32_t)c.bh, 1};
@@ -68,7 +80,7 @@ int main() {
             enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         }
-        const int bytes = c.dims4 ? 128 * c.bw * c.bh : 128 * 224;
+        const int bytes = c.dims4 == 2 ? 4 * 3 * c.bw * c.bh : (c.dims4 ? 128 * c.bw * c.bh : 128 * 224);
         const int loads = 24;
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         for (int r = 0; r < 1; ++r) {

@@ -210,3 +210,22 @@ def test_nccl_allreduce_plumbing_single_rank(gpu):
     assert res[0][0] == res[1][0]
     for k in res[0][1]:
         assert np.array_equal(res[0][1][k], res[1][1][k]), k
+
+
+def test_direct_nchw_stem_input(gpu, monkeypatch):
+    """A bf16 inference plan whose stem is the graph input's only consumer skips the reorder pass:
+    the stem's halo TMA reads the canonical NCHW f32 input (ragged 60x60 images: partial tiles)."""
+    from paper_2003_10688_b200 import frontend, graph, models
+    batch = 3
+    g = models.resnet(18, hw=60, classes=16, width=64)
+    gi = graph.infer_shapes(g, batch)
+    ins = _inputs(gi, batch, seed=12)
+    m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16", fuse_epilogue=True))
+    assert not any(st.kind == "reorder" and st.output == "x" for st in m.steps)
+    assert any(st.family.startswith("conv_stem") for st in m.steps)
+    got = m.predict(ins)["prob"]
+    monkeypatch.setenv("SOL_NO_DIRECT_STEM", "1")
+    ref = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16", fuse_epilogue=True)).predict(ins)["prob"]
+    want = O.run_graph(gi, ins)["prob"]
+    assert O.oracle_err(got, want) <= 1e-2
+    assert O.oracle_err(got, ref) <= 1e-2
