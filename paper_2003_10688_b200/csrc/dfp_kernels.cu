@@ -841,6 +841,63 @@ __global__ void __launch_bounds__(THREADS) gap_chain_kernel(const __grid_constan
     }
 }
 
+// Global average pool, straight-line source chain without Add: block = 32 channel vectors x 8
+// pixel lanes of one image (BN coefficients in registers), lanes combined through shared memory.
+template <typename T, bool BN0, int ACT>
+__global__ void __launch_bounds__(256) gap_fast_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
+    constexpr int V = VEC<T>;
+    __shared__ float red[8][32][V + 1];
+    const int cv_total = a.C / V;
+    const int cvi = threadIdx.x & 31, lanep = threadIdx.x >> 5;
+    const int cvec = blockIdx.y * 32 + cvi;
+    const int n = blockIdx.x;
+    const int hw = a.H * a.W;
+    float acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+    if (cvec < cv_total) {
+        const int c = cvec * V;
+        BnRegs<T> bn;
+        if (BN0) bn.load(a.P, cs.bn0, c);
+        const T* x = static_cast<const T*>(a.in[cs.s0]) + static_cast<int64_t>(n) * hw * a.in_ld[cs.s0] + c;
+        for (int p0 = lanep; p0 < hw; p0 += 8 * 4) {
+            uint4 r[4];
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int p = p0 + u * 8;
+                ok[u] = p < hw;
+                if (ok[u]) r[u] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(p) * a.in_ld[cs.s0]));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (!ok[u]) continue;
+                float v[V];
+                unpack16(r[u], v, static_cast<T*>(nullptr));
+                if (BN0) bn.apply(v);
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (ACT >= 1) v[i] = fmaxf(v[i], 0.f);
+                    if (ACT == 2) v[i] = fminf(v[i], 6.f);
+                    acc[i] += v[i];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) red[lanep][cvi][i] = acc[i];
+    __syncthreads();
+    if (lanep == 0 && cvec < cv_total) {
+#pragma unroll
+        for (int l = 1; l < 8; ++l)
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[i] += red[l][cvi][i];
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] /= static_cast<float>(hw);
+        store_out<T>(a, n, cvec * V, acc);
+    }
+}
+
 template <typename T>
 bool launch_pool_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
     if (a.post.n != 0) return false;
@@ -885,6 +942,20 @@ bool launch_gap_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
     if (a.post.n != 0) return false;
     const ChainSpec c = match_chain(a.pre);
     if (!c.ok || a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+    if (!c.add) {
+        const dim3 g2(static_cast<unsigned>(a.N), static_cast<unsigned>(ceil_div(a.C / VEC<T>, 32)));
+        const bool bb = c.bn0 >= 0;
+        if (bb) {
+            if (c.act == 0) gap_fast_kernel<T, true, 0><<<g2, 256, 0, s>>>(a, c);
+            else if (c.act == 1) gap_fast_kernel<T, true, 1><<<g2, 256, 0, s>>>(a, c);
+            else gap_fast_kernel<T, true, 2><<<g2, 256, 0, s>>>(a, c);
+        } else {
+            if (c.act == 0) gap_fast_kernel<T, false, 0><<<g2, 256, 0, s>>>(a, c);
+            else if (c.act == 1) gap_fast_kernel<T, false, 1><<<g2, 256, 0, s>>>(a, c);
+            else gap_fast_kernel<T, false, 2><<<g2, 256, 0, s>>>(a, c);
+        }
+        return true;
+    }
     if (c.add && (a.in_kind[c.s1] != IN_PIX || a.in_coff[c.s1] != 0)) return false;
     const bool b0 = c.bn0 >= 0, b1 = c.bn1 >= 0;
 #define SOL_GAP(B0, AD, B1) \
@@ -2171,8 +2242,28 @@ __global__ void nchw_to_nhwc_narrow_kernel(const float* __restrict__ src, TO* __
     }
 }
 
+template <typename TO>
+__global__ void rows_from_f32_kernel(const float* __restrict__ in, TO* __restrict__ out, int N, int C, int ld) {
+    const int64_t total = static_cast<int64_t>(N) * ld;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t n = i / ld;
+        const int c = static_cast<int>(i - n * ld);
+        out[i] = from_f32<TO>(c < C ? in[n * C + c] : 0.f);
+    }
+}
+
 void nchw_to_nhwc(const float* src, void* dst, int dtype, int N, int C, int H, int W, int c_pad, cudaStream_t s) {
     const int hw = H * W;
+    if (hw == 1) {  // [N, C] rows (labels, features): a strided cast with zeroed padding
+        const unsigned grid = grid_for(static_cast<int64_t>(N) * c_pad, 256);
+        if (dtype == DT_BF16)
+            rows_from_f32_kernel<<<grid, 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), N, C, c_pad);
+        else
+            rows_from_f32_kernel<<<grid, 256, 0, s>>>(src, static_cast<float*>(dst), N, C, c_pad);
+        SOL_CUDA(cudaGetLastError());
+        return;
+    }
     if (c_pad * (dtype == DT_BF16 ? 2 : 4) == 16) {
         const int64_t total = static_cast<int64_t>(N) * hw;
         const unsigned grid = grid_for(total, 256);
@@ -2187,8 +2278,27 @@ void nchw_to_nhwc(const float* src, void* dst, int dtype, int N, int C, int H, i
     else transpose<float, float>(src, dst, N, C, hw, hw, c_pad, c_pad, s);
 }
 
+template <typename TI>
+__global__ void rows_to_f32_kernel(const TI* __restrict__ in, float* __restrict__ out, int N, int C, int ld) {
+    const int64_t total = static_cast<int64_t>(N) * C;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t n = i / C;
+        out[i] = to_f32(in[n * ld + (i - n * C)]);
+    }
+}
+
 void nhwc_to_nchw(const void* src, float* dst, int dtype, int N, int C, int H, int W, int ld, cudaStream_t s) {
     const int hw = H * W;
+    if (hw == 1) {  // [N, C] rows: a strided cast (the tiled transpose would launch N x C/32 idle tiles)
+        const unsigned grid = grid_for(static_cast<int64_t>(N) * C, 256);
+        if (dtype == DT_BF16)
+            rows_to_f32_kernel<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src), dst, N, C, ld);
+        else
+            rows_to_f32_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(src), dst, N, C, ld);
+        SOL_CUDA(cudaGetLastError());
+        return;
+    }
     if (dtype == DT_BF16) transpose<__nv_bfloat16, float>(src, dst, N, hw, C, ld, hw, hw, s);
     else transpose<float, float>(src, dst, N, hw, C, ld, hw, hw, s);
 }

@@ -765,7 +765,11 @@ void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
         if (bn == 64 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX && a.K_pad >= 256 && !(a.dbg & 1024) && !no_resb)
             return launch_ws_t<T, TO, 64, MODE, true>(a, s);
     }
-    switch (igemm_block_n(a.Nout)) {
+    int bn_sel = igemm_block_n(a.Nout);
+    // small-M GEMMs (the classifier: M = batch): narrower N tiles put more SMs on the long K loop
+    const int64_t m_tiles = ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, BM);
+    if (bn_sel > 64 && m_tiles * ceil_div(a.Nout, bn_sel) < num_sms() / 4) bn_sel = 64;
+    switch (bn_sel) {
         case 16: return launch_ws_t<T, TO, 16, MODE>(a, s);
         case 32: return launch_ws_t<T, TO, 32, MODE>(a, s);
         case 64: return launch_ws_t<T, TO, 64, MODE>(a, s);

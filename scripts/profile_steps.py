@@ -33,6 +33,13 @@ if fam_filter:
         if f == fam_filter[0]:
             print(f"{t:9.1f} us {o:36s} {ops.get(o, ''):40s} {gb:8.1f} GB/s")
     sys.exit(0)
+print("--- steps by lost time vs speed of light (max(FLOP/1416T, bytes/6551G))")
+sol = []
+for st, t in zip(m.steps, times):
+    tmin = max(st.algo_flops / 1416e12, st.algo_bytes / 6551e9) * 1e6
+    sol.append((t - tmin, t, tmin, st.family, st.output))
+for lost, t, tmin, f, o in sorted(sol, reverse=True)[:25]:
+    print(f"{lost:8.1f} us lost  {t:8.1f} us  sol {tmin:7.1f} us ({100 * tmin / max(t, 1e-9):4.0f}%)  {f:26s} {o}")
 print("--- top 40 steps")
 for t, f, o, tf, gb in sorted(rows, reverse=True)[:40]:
     print(f"{t:9.1f} us {f:22s} {o:36s} {tf:8.1f} TF/s {gb:8.1f} GB/s")
