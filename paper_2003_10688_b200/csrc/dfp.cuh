@@ -97,6 +97,8 @@ struct DfpArgs {
     int out_f32 = 0;               // output stored as f32 even in a bf16 plan
     double* partial = nullptr;     // FAM_CHAN_REDUCE: [blocks][C][2] (f64)
     uint8_t* argmax = nullptr;     // FAM_MAXPOOL_BACK scratch: [windows][C] first-max tap (255 = none)
+    void* out2 = nullptr;          // straight-line chains: second output act2(value) (sibling ReLU unit)
+    int act2 = 0;
     int reduce_blocks = 0;
 };
 

@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ 
     const T* x1 = ADD ? static_cast<const T*>(a.in[cs.s1]) + c : nullptr;
     const int ld1 = ADD ? a.in_ld[cs.s1] : 0;
     T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    T* out2 = a.out2 ? static_cast<T*>(a.out2) + a.out_coff + c : nullptr;
     BnRegs<T> b0, b1;
     if (BN0) b0.load(a.P, cs.bn0, c);
     if (BN1) b1.load(a.P, cs.bn1, c);
@@ -463,6 +464,14 @@ __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ 
                 if (ACT == 2) v[i] = fminf(v[i], 6.f);
             }
             store16(out + p * a.out_ld, v);
+            if (out2) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    v[i] = fmaxf(v[i], 0.f);
+                    if (a.act2 == 2) v[i] = fminf(v[i], 6.f);
+                }
+                store16(out2 + p * a.out_ld, v);
+            }
         }
     }
 }
@@ -478,6 +487,7 @@ template <typename T>
 bool launch_chain(const DfpArgs& a, cudaStream_t s) {
     const ChainSpec c = match_chain(a.post);
     if (!c.ok) return false;
+    if (a.out2 && c.act != 0) throw std::invalid_argument("dfp: activation sibling after an activation");
     if (a.in_kind[c.s0] == IN_CAT) {
         for (int k = 0; k < a.n_cat; ++k)
             if ((a.cat_off[k + 1] - a.cat_off[k]) % VEC<T>) return false;
@@ -1696,6 +1706,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
     switch (a.family) {
         case FAM_POINTWISE: {
             if (launch_chain<T>(a, s)) break;
+            if (a.out2) throw std::invalid_argument("dfp: activation sibling needs a straight-line chain unit");
             if (launch_mask<T>(a, s)) break;
             if (launch_pointwise_pre<T>(a, s)) break;
             const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);

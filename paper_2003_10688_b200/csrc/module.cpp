@@ -937,6 +937,15 @@ public:
     explicit DfpModule(const sol_unit_desc& d);
     void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) override;
     size_t scratch_bytes() const override { return stats_scratch_; }
+    // bit 2: also write relu(output) (bit 3: relu6) for a sibling ReLU unit reading this output
+    bool set_sibling_outputs(int mask) override {
+        if (mask == 0) return true;
+        if ((mask != 4 && mask != 8) || tmpl_.family != FAM_POINTWISE || act_sib_) return false;
+        act_sib_ = mask == 4 ? 1 : 2;
+        n_args += 1;
+        arg_bytes.push_back(arg_bytes.back());
+        return true;
+    }
 
 private:
     struct SlotSrc {
@@ -983,6 +992,7 @@ private:
     int anchor_ = -1;
     size_t stats_scratch_ = 0;
     size_t argmax_offset_ = 0;
+    int act_sib_ = 0;
     bool coef_ready_ = false;
     float* ones_ = nullptr;
     float* zeros_ = nullptr;
@@ -1429,7 +1439,11 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
         a.dw_w = dw_[0].packed;
         a.dw_b = dw_[0].bias >= 0 ? static_cast<const float*>(args[dw_[0].bias]) : nullptr;
     }
-    a.out = args[nargs - 1];
+    a.out = args[nargs - 1 - (act_sib_ ? 1 : 0)];
+    if (act_sib_) {
+        a.out2 = args[nargs - 1];
+        a.act2 = act_sib_;
+    }
     if (a.family == FAM_MAXPOOL_BACK) a.argmax = static_cast<uint8_t*>(scratch) + argmax_offset_;
     dfp_launch(a, s);
 }

@@ -158,6 +158,8 @@ class OptimizedModel:
         self.modules = []
         siblings = self._bn_back_siblings() if (o.train and o.fuse_bn_backward) else {}
         absorbed = {v for sib in siblings.values() for v in sib if v is not None}
+        act_sibs = self._activation_siblings() if o.fuse_bn_backward else {}
+        absorbed |= {v[0] for v in act_sibs.values()}
 
         def out_buf(name):
             if name not in self.buf:
@@ -172,6 +174,11 @@ class OptimizedModel:
                 continue  # computed by its BatchNormBackX sibling's step
             mod = create_module(g, u, self.dtype, [n for n in u.inputs if n in direct])
             ids = [self.buf[n] for n in list(u.inputs) + list(u.params)] + [self.buf[u.output]]
+            if u.output in act_sibs:
+                relu_out, mask = act_sibs[u.output]
+                L.check(lib.sol_b200_module_set_sibling_outputs(mod.handle, mask))
+                mod.n_args += 1
+                ids += [out_buf(relu_out)]
             if u.output in siblings:
                 gam, bet = siblings[u.output]
                 mask = (1 if gam else 0) | (2 if bet else 0)
@@ -240,6 +247,28 @@ class OptimizedModel:
                     and n0.attrs.out_channels == 64 and n0.attrs.kw <= 8 and n0.attrs.kh * 32 <= 256
                     and sum(1 for n in u.node_ids for i in g.find_node(n).inputs if i == gi.name) == 1):
                 out.add(gi.name)
+        return out
+
+    def _activation_siblings(self):
+        """DFP unit output -> (ReLU unit output, mask) where a single-op ReLU / ReLU6 unit reads the
+        output of a straight-line BatchNorm [+ Add] unit (training graphs keep them apart because
+        ReluBack needs the pre-activation tensor): one kernel writes both tensors."""
+        g = self.graph
+        by_out = {u.output: u for u in self.units}
+        out = {}
+        for u in self.units:
+            if u.kind != "dfp" or len(u.node_ids) != 1:
+                continue
+            n = g.find_node(u.node_ids[0])
+            if n.op not in ("ReLU", "ReLU6"):
+                continue
+            p = by_out.get(n.inputs[0])
+            if p is None or p.kind != "dfp" or p.output in out:
+                continue
+            ops = [g.find_node(i).op for i in p.node_ids]
+            if ops not in (["BatchNorm2d"], ["BatchNorm2d", "Add"]):
+                continue
+            out[p.output] = (u.output, 4 if n.op == "ReLU" else 8)
         return out
 
     def _bn_back_siblings(self):
