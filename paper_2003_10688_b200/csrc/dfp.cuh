@@ -95,7 +95,7 @@ struct DfpArgs {
     void* out = nullptr;
     int out_ld = 0, out_coff = 0;
     int out_f32 = 0;               // output stored as f32 even in a bf16 plan
-    double* partial = nullptr;     // FAM_CHAN_REDUCE: [blocks][C][2] (f64)
+    double* partial = nullptr;     // FAM_CHAN_REDUCE: [C][blocks][2] (f64, channel-major)
     uint8_t* argmax = nullptr;     // FAM_MAXPOOL_BACK scratch: [windows][C] first-max tap (255 = none)
     void* out2 = nullptr;          // straight-line chains: second output act2(value) (sibling ReLU unit)
     int act2 = 0;
@@ -145,6 +145,8 @@ struct FinalizeArgs {
     float* out0 = nullptr;
     float* out1 = nullptr;
     float* xhat = nullptr;         // FIN_BN_BACK4
+    const void* shift_x = nullptr; // FIN_BN_BACK4 with shift == nullptr: the shift is x's first pixel
+    int shift_dtype = DT_BF16;
 };
 void dfp_finalize(const FinalizeArgs& a, cudaStream_t s);
 

@@ -1249,8 +1249,10 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
     const bool active = row < rows && (blockIdx.y * cvb + cvi) < cv_total;
     if (active) {
         float q[V];
+        const T* xs = MODE == RR_BNBACK ? x1 : x0;  // the tensor whose statistics are shifted
 #pragma unroll
-        for (int i = 0; i < V; ++i) q[i] = MODE == RR_SUM ? 0.f : __ldg(shift + c + i);
+        for (int i = 0; i < V; ++i)
+            q[i] = MODE == RR_SUM ? 0.f : (shift ? __ldg(shift + c + i) : to_f32(xs[c + i]));
         // (inactive lanes keep zero accumulators and still take part in the shuffles below)
         for (int64_t pb = p0 + row; pb < p1; pb += static_cast<int64_t>(rows) * UN) {
             uint4 r0[UN], r1[UN];
@@ -1325,9 +1327,10 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
             for (int g2 = 0; g2 < groups; ++g2)
 #pragma unroll
                 for (int i = 0; i < V; ++i) u[i] += red[(g2 * cvb + tid) * V + i];
-            double* dst = partial + (static_cast<int64_t>(blockIdx.x) * C + (blockIdx.y * cvb + tid) * V) * NS + k;
+            // channel-major partials [C][blocks][NS]: finalize reads each channel contiguously
+            const int64_t c0 = (blockIdx.y * cvb + tid) * V;
 #pragma unroll
-            for (int i = 0; i < V; ++i) dst[NS * i] = u[i];
+            for (int i = 0; i < V; ++i) partial[((c0 + i) * gridDim.x + blockIdx.x) * NS + k] = u[i];
         }
         __syncthreads();
     }
@@ -1404,11 +1407,11 @@ __global__ void __launch_bounds__(THREADS) chan_reduce_kernel(const __grid_const
                 s2[i] += red[(t2 * V + i) * 2 + 1];
             }
         }
-        double* dst = a.partial + (static_cast<int64_t>(blockIdx.x) * a.C + c) * 2;
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-            dst[2 * i] = s1[i];
-            dst[2 * i + 1] = s2[i];
+            double* dst = a.partial + ((static_cast<int64_t>(c) + i) * gridDim.x + blockIdx.x) * 2;
+            dst[0] = s1[i];
+            dst[1] = s2[i];
         }
     }
 }
@@ -1899,11 +1902,10 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
     const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (c >= a.C) return;
-    const int cs = a.Cstride > 0 ? a.Cstride : a.C;
     const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
     double q[4] = {0.0, 0.0, 0.0, 0.0};
     for (int b = lane; b < a.blocks; b += 32) {
-        const double* src = a.partial + (static_cast<int64_t>(b) * cs + c) * ns;
+        const double* src = a.partial + (static_cast<int64_t>(c) * a.blocks + b) * ns;
         q[0] += src[0];
         q[1] += src[1];
         if (ns == 4) {
@@ -1922,7 +1924,11 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
         const double d = sx / m;  // mean - shift
         double var = sxx / m - d * d;
         if (var < 0) var = 0;
-        const double mean = static_cast<double>(a.shift[c]) + d;
+        const double shift = a.shift ? a.shift[c]
+                                     : (a.shift_dtype == DT_BF16
+                                            ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.shift_x)[c]))
+                                            : static_cast<double>(static_cast<const float*>(a.shift_x)[c]));
+        const double mean = shift + d;
         const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
         const double s1 = sd;                    // sum dy                 (dbeta)
         const double s2 = rstd * (sdx - d * sd);  // sum dy * xhat         (dgamma)

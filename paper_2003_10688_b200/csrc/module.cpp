@@ -820,8 +820,8 @@ public:
             gamma_idx_ = o.n_params > 0 ? o.params[0] : -1;
         }
         switch (op_) {
-            case SOL_OP_BATCHNORMBACKX: family = "bn_back_x"; launches = 4; break;
-            case SOL_OP_BATCHNORMBACKGAMMA: family = "bn_back_gamma"; launches = 3; break;
+            case SOL_OP_BATCHNORMBACKX: family = "bn_back_x"; launches = 3; break;
+            case SOL_OP_BATCHNORMBACKGAMMA: family = "bn_back_gamma"; launches = 2; break;
             case SOL_OP_BATCHNORMBACKBETA: family = "bn_back_beta"; launches = 2; break;
             default: family = "bias_grad"; launches = 2; break;
         }
@@ -891,8 +891,8 @@ public:
             return;
         }
         // BNBackX / BNBackGamma: one pass over (dy, x) gives the x statistics and both sums
-        bn_shift(dtype_, args[x_idx_], C_, C_, shift_, s);
-        bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), shift_, partial, blocks_, s);
+        // shifted sums about x's first pixel, read in place by the reduction and the finalisation
+        bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), nullptr, partial, blocks_, s);
         FinalizeArgs f;
         f.mode = FIN_BN_BACK4;
         f.C = C_;
@@ -900,7 +900,9 @@ public:
         f.partial = partial;
         f.count = static_cast<double>(delta_.pixels());
         f.eps = eps_;
-        f.shift = shift_;
+        f.shift = nullptr;
+        f.shift_x = args[x_idx_];
+        f.shift_dtype = dtype_;
         if (op_ == SOL_OP_BATCHNORMBACKGAMMA) {
             f.out1 = out;
             dfp_finalize(f, s);
