@@ -1896,16 +1896,17 @@ __global__ void __launch_bounds__(THREADS) bnback_apply_kernel(const T* __restri
 // finalisation of per-channel partial sums (f64)
 // ---------------------------------------------------------------------------------------------
 
-// One warp per channel: lanes stride over the partial blocks (independent loads in flight), a
-// fixed-order shuffle tree combines them (deterministic), lane 0 finalises.
-__global__ void finalize_kernel(const FinalizeArgs a) {
-    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (c >= a.C) return;
+// One 128-thread block per channel: threads stride over the channel's contiguous partials,
+// a fixed-order shuffle + shared-memory tree combines them (deterministic), thread 0 finalises.
+__global__ void __launch_bounds__(128) finalize_kernel(const FinalizeArgs a) {
+    __shared__ double wsum[4][4];
+    const int c = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
     double q[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int b = lane; b < a.blocks; b += 32) {
-        const double* src = a.partial + (static_cast<int64_t>(c) * a.blocks + b) * ns;
+    const double* base = a.partial + static_cast<int64_t>(c) * a.blocks * ns;
+    for (int b = threadIdx.x; b < a.blocks; b += 128) {
+        const double* src = base + static_cast<int64_t>(b) * ns;
         q[0] += src[0];
         q[1] += src[1];
         if (ns == 4) {
@@ -1914,10 +1915,15 @@ __global__ void finalize_kernel(const FinalizeArgs a) {
         }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 4; ++k) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
-    if (lane != 0) return;
+        if (lane == 0) wsum[w][k] = q[k];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
     if (a.mode == FIN_BN_BACK4) {
         const double sd = q[0], sdx = q[1], sx = q[2], sxx = q[3];
         const double m = a.count;
@@ -2158,7 +2164,7 @@ void softmax_back(int dtype, const void* d, const void* y, void* dx, int rows, i
 }
 
 void dfp_finalize(const FinalizeArgs& a, cudaStream_t s) {
-    finalize_kernel<<<static_cast<unsigned>(ceil_div(a.C, 8)), 256, 0, s>>>(a);
+    finalize_kernel<<<static_cast<unsigned>(a.C), 128, 0, s>>>(a);
     SOL_CUDA(cudaGetLastError());
 }
 
