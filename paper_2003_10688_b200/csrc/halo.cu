@@ -7,9 +7,9 @@
 // (out-of-bounds fill = the zero padding) and every tap's MMA reads it through a shifted UMMA
 // descriptor. Weights stream through a TMA ring of [BN][64] K-blocks.
 //
-//   warp 0      TMA producer (halo per tile, weight blocks per (tap, channel block))
-//   warp 1      tcgen05.mma issuer (M = 128 row-padded pixels, N = BN, K = taps x C)
-//   warps 2-5   epilogue: TMEM -> bias / folded BN / residual / activation -> bf16 -> global
+//   warps 0-3   producers: resident weights once (TMA), the halo per tile by 16-byte cp.async
+//   warp 4      tcgen05.mma issuer (M = 128 row-padded pixels, N = BN, K = taps x C)
+//   warps 5-8   epilogue: TMEM -> bias / folded BN / residual / activation -> bf16 -> global
 //               (junk columns and rows past the tile are skipped)
 //
 // Semantics are the generic fprop's (reference.cpp:138-161; igemm.cuh).
@@ -23,8 +23,9 @@ namespace solb200 {
 namespace {
 
 using namespace tc;
+using T_BF16 = __nv_bfloat16;
 
-constexpr int HL_THREADS = 192;
+constexpr int HL_THREADS = 288;  // 4 producer warps (halo cp.async), MMA warp, 4 epilogue warps
 constexpr int HL_HALO_MAX = 49152;  // bytes of one halo buffer (all channel blocks)
 
 __device__ __forceinline__ void tma_load_4d_tile(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < NH; ++s) {
-            mbar_init(smem_u32(&hfull[s]), 1);
+            mbar_init(smem_u32(&hfull[s]), RESB ? 128 : 1);  // RESB: 128 cp.async producer arrivals
             mbar_init(smem_u32(&hempty[s]), 1);
         }
         for (int s = 0; s < NA; ++s) {
@@ -117,38 +118,65 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         tma_prefetch(&tm_x);
         tma_prefetch(&tm_w);
     }
-    if (warp == 1) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+    if (warp == 4) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
-        // ---------------------------------------------------------------- TMA producer
-        if (lane == 0) {
+    if (warp < 4 && RESB) {
+        // ---------------------------------------------------------------- producers (RESB):
+        // weights once by TMA; per tile the halo by 16-byte cp.async into the 128B-swizzled rows
+        // (zero fill = conv padding), completion counted on hfull by the 128 producer threads
+        if (tid == 0) {
+            mbar_arrive_tx(smem_u32(&bfull[0]), static_cast<uint32_t>(taps * G.ncb * B_BYTES));
+            for (int j = 0; j < taps * G.ncb; ++j)
+                tma_load_2d(smem_u32(bring + j * B_BYTES), &tm_w, j * 64, 0, smem_u32(&bfull[0]));
+        }
+        const T_BF16* x = static_cast<const T_BF16*>(a.src);
+        const int rows = G.HR * G.Wp;
+        const int nchunks = G.ncb * rows * 8;
+        int hb = 0;
+        uint32_t hph = 0;
+        for (int j = 0; j < t_end - t_begin; ++j) {
+            const int t = tile_at(j);
+            const int rb = (t / n_tiles) % G.row_blocks;
+            const int img = t / (n_tiles * G.row_blocks);
+            mbar_wait(smem_u32(&hempty[hb]), ((hph >> hb) & 1) ^ 1);
+            uint8_t* hbuf = halo + hb * HB;
+            for (int q = tid; q < nchunks; q += 128) {
+                const int j8 = q & 7;
+                const int rest = q >> 3;
+                const int cb = rest / rows;
+                const int r = rest - cb * rows;
+                const int hy = r / G.Wp, hx = r - (r / G.Wp) * G.Wp;
+                const int iy = rb * G.R - a.ph + hy, ix = hx - a.pw;
+                const bool ok = iy >= 0 && iy < a.SH && ix >= 0 && ix < a.SW;
+                const T_BF16* src = ok ? x + ((static_cast<int64_t>(img) * a.SH + iy) * a.SW + ix) * a.SC + cb * 64 + j8 * 8 : x;
+                cp_async16(smem_u32(hbuf + cb * G.cb_bytes + r * 128 + ((j8 ^ (r & 7)) << 4)), src, ok);
+            }
+            cp_async_arrive_noinc(smem_u32(&hfull[hb]));
+            hph ^= 1u << hb;
+            if (++hb == NH) hb = 0;
+        }
+        cp_async_wait<0>();
+    } else if (warp < 4) {
+        // ---------------------------------------------------------------- TMA producer (streamed B)
+        if (warp == 0 && lane == 0) {
             int stage = 0, hb = 0;
             uint32_t phase = 0, hph = 0;  // hph bit b = phase of halo buffer b
-            if (RESB) {
-                mbar_arrive_tx(smem_u32(&bfull[0]), static_cast<uint32_t>(taps * G.ncb * B_BYTES));
-                for (int j = 0; j < taps * G.ncb; ++j)
-                    tma_load_2d(smem_u32(bring + j * B_BYTES), &tm_w, j * 64, 0, smem_u32(&bfull[0]));
-            }
             for (int j = 0; j < t_end - t_begin; ++j) {
-            const int t = tile_at(j);
+                const int t = tile_at(j);
                 const int nt = t % n_tiles;
                 const int rb = (t / n_tiles) % G.row_blocks;
                 const int img = t / (n_tiles * G.row_blocks);
                 mbar_wait(smem_u32(&hempty[hb]), ((hph >> hb) & 1) ^ 1);
                 mbar_arrive_tx(smem_u32(&hfull[hb]), static_cast<uint32_t>(G.ncb * G.HR * G.Wp * 128));
                 for (int cb = 0; cb < G.ncb; ++cb)
-                    tma_load_4d_tile(smem_u32(halo + hb * HB + cb * G.cb_bytes), &tm_x, cb * 64,
-                                     (a.dbg & 128) ? 0 : -a.pw, (a.dbg & 256) ? rb * G.R : rb * G.R - a.ph, img,
-                                     smem_u32(&hfull[hb]));
-                if ((a.dbg & 64) && blockIdx.x == 0 && j < 64)
-                    reinterpret_cast<long long*>(a.out)[j] = clock64();
+                    tma_load_4d_tile(smem_u32(halo + hb * HB + cb * G.cb_bytes), &tm_x, cb * 64, -a.pw,
+                                     rb * G.R - a.ph, img, smem_u32(&hfull[hb]));
                 hph ^= 1u << hb;
                 if (++hb == NH) hb = 0;
-                if (RESB) continue;
                 for (int tap = 0; tap < taps; ++tap) {
                     for (int cb = 0; cb < G.ncb; ++cb) {
                         mbar_wait(smem_u32(&bempty[stage]), phase ^ 1);
@@ -163,7 +191,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 4) {
         // ---------------------------------------------------------------- MMA issuer
         int stage = 0, hb = 0, acc = 0;
         uint32_t phase = 0, hph = 0, acc_phase = 0;
@@ -300,7 +328,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 4) {
         tc_fence_after();
         tmem_dealloc<TCOLS>(tmem_base);
     }
