@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     constexpr int STAGE_BYTES = RESB ? A_BYTES : A_BYTES + B_BYTES;
     constexpr int EPI_BYTES = ws_epi_bytes<TO, BN>();
     constexpr int STAGES = ws_stages<STAGE_BYTES, EPI_BYTES + (RESB ? WS_RESB_MAX : 0)>();
-    constexpr uint32_t TCOLS = ws_tmem_cols<BN>();
+    // accumulator stages: 2 (epilogue overlaps the next mainloop); the dual GEMM at BN = 256 keeps
+    // one (half the TMEM) -- see the dispatch note
+    constexpr int NACC = (MODE == IG_DUAL && BN == 256) ? 1 : 2;
+    constexpr uint32_t TCOLS = NACC == 1 ? static_cast<uint32_t>(BN) : ws_tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
     constexpr int KSTEP_BYTES = 32;
     constexpr bool A_TMA = MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL || MODE == IG_DUAL;
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             }
             if (lane == 0) mma_commit(smem_u32(&tfull[acc]));
             __syncwarp();
-            if (++acc == 2) {
+            if (++acc == NACC) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -665,7 +668,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             }
             tc_fence_before();
             mbar_arrive(smem_u32(&tempty[acc]));
-            if (++acc == 2) {
+            if (++acc == NACC) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -790,6 +793,7 @@ void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
             // N tiles of at most 128 (TMEM 2 x 128 columns): with 256-wide tiles (the whole TMEM)
             // the dual GEMM stalled intermittently (~1 in 10^3 full-size launches); at 128 it ran
             // clean through 8k ResNet-50 steps and 80k single-block launches
+            if (a.Nout > 128 && std::getenv("SOL_DUAL_BN256")) return launch_ws_t<T, TO, 256, IG_DUAL>(a, s);
             if (a.Nout > 64) return launch_ws_t<T, TO, 128, IG_DUAL>(a, s);
             return dispatch_ws<T, TO, IG_DUAL>(a, s);
         }
