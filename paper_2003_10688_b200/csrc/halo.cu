@@ -1,22 +1,25 @@
-// Halo-tile implicit GEMM for stride-1 "same" convolutions with few channel blocks (ResNet-50's
-// 3x3 convs at 56x56x64 and 28x28x128). The TMA-im2col path re-reads every input pixel from L2
-// once per filter tap (9x for 3x3) and is bound by that L2 -> shared-memory traffic; here one tile
-// covers R whole output rows in a row-padded pixel order (Wp = W + k - 1 columns, the last k - 1
-// of them junk), so the A operand of tap (dkh, dkw) is simply the halo box shifted by
-// dkh * Wp + dkw rows: the halo [R + k - 1][Wp][64 ch] is loaded ONCE per tile by a 4-D TMA box
-// (out-of-bounds fill = the zero padding) and every tap's MMA reads it through a shifted UMMA
-// descriptor. Weights stream through a TMA ring of [BN][64] K-blocks.
+// Halo-tile implicit GEMM for stride-1 "same" convolutions with one 64-channel block (ResNet-50's
+// 56x56x64 3x3 convs). The TMA-im2col path re-reads every input pixel from L2 once per filter tap
+// (9x for 3x3) and is bound by the TMA im2col request rate; here one tile covers R whole output
+// rows in a row-padded pixel order (Wp = W + k - 1 columns, the last k - 1 of them junk), so the A
+// operand of tap (dkh, dkw) is simply the halo box shifted by dkh * Wp + dkw rows: the halo
+// [R + k - 1][Wp][64 ch] is loaded ONCE per tile by a 4-D TMA box (out-of-bounds fill = the zero
+// padding) and every tap's MMA reads it through a shifted UMMA descriptor (the SW128 swizzle is a
+// function of the absolute smem address, so 128-byte-row shifts need no re-layout).
 //
-//   warps 0-3   producers: resident weights once (TMA), the halo per tile by 16-byte cp.async
-//   warp 4      tcgen05.mma issuer (M = 128 row-padded pixels, N = BN, K = taps x C)
+//   warp 0      producer: resident weights once, then one halo TMA box per tile (ring of NH)
+//   warp 4      tcgen05.mma issuer: the whole warp runs the loop, one elected lane issues a filter
+//               row's 12 MMAs per asm statement (M = 128 row-padded pixels, N = BN, K = 9 x 64)
 //   warps 5-8   epilogue: TMEM -> bias / folded BN / residual / activation -> bf16 -> global
 //               (junk columns and rows past the tile are skipped)
+// Measured (B200, 256x64x56x56, 3x3): 100 us vs 130 us for TMA im2col, bit-identical output.
 //
 // Semantics are the generic fprop's (reference.cpp:138-161; igemm.cuh).
 #include "igemm.cuh"
 #include "tc.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace solb200 {
@@ -96,14 +99,14 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     const int per_cta = (tiles + gridDim.x - 1) / gridDim.x;
     const int t_begin = min(tiles, static_cast<int>(blockIdx.x) * per_cta);
     const int t_end = min(tiles, t_begin + per_cta);
-    // even offsets first, then odd: halos in flight together never share rows (concurrent misses
-    // to the same lines serialise in L2); the odd pass then finds its rows in L2
-    const int n_even = (t_end - t_begin + 1) / 2;
-    auto tile_at = [&](int j) { return t_begin + (j < n_even ? 2 * j : 2 * (j - n_even) + 1); };
+    // tiles in order (the next tile's halo overlaps this one's in L2); debug flag 8192: even
+    // offsets first, then odd
+    const int n_even = (a.dbg & 8192) ? (t_end - t_begin + 1) / 2 : 1 << 30;
+    auto tile_at = [&](int j) { return t_begin + (j < n_even ? ((a.dbg & 8192) ? 2 * j : j) : 2 * (j - n_even) + 1); };
 
     if (tid == 0) {
         for (int s = 0; s < NH; ++s) {
-            mbar_init(smem_u32(&hfull[s]), RESB ? 128 : 1);  // RESB: 128 cp.async producer arrivals
+            mbar_init(smem_u32(&hfull[s]), 1);
             mbar_init(smem_u32(&hempty[s]), 1);
         }
         for (int s = 0; s < NA; ++s) {
@@ -125,41 +128,32 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp < 4 && RESB) {
-        // ---------------------------------------------------------------- producers (RESB):
-        // weights once by TMA; per tile the halo by 16-byte cp.async into the 128B-swizzled rows
-        // (zero fill = conv padding), completion counted on hfull by the 128 producer threads
+        // ---------------------------------------------------------------- producer (RESB):
+        // weights once, then per tile the whole halo as one 4-D TMA box per channel block
+        // (out-of-bounds rows/columns zero-filled = the conv padding)
         if (tid == 0) {
             mbar_arrive_tx(smem_u32(&bfull[0]), static_cast<uint32_t>(taps * G.ncb * B_BYTES));
             for (int j = 0; j < taps * G.ncb; ++j)
                 tma_load_2d(smem_u32(bring + j * B_BYTES), &tm_w, j * 64, 0, smem_u32(&bfull[0]));
-        }
-        const T_BF16* x = static_cast<const T_BF16*>(a.src);
-        const int rows = G.HR * G.Wp;
-        const int nchunks = G.ncb * rows * 8;
-        int hb = 0;
-        uint32_t hph = 0;
-        for (int j = 0; j < t_end - t_begin; ++j) {
-            const int t = tile_at(j);
-            const int rb = (t / n_tiles) % G.row_blocks;
-            const int img = t / (n_tiles * G.row_blocks);
-            mbar_wait(smem_u32(&hempty[hb]), ((hph >> hb) & 1) ^ 1);
-            uint8_t* hbuf = halo + hb * HB;
-            for (int q = tid; q < nchunks; q += 128) {
-                const int j8 = q & 7;
-                const int rest = q >> 3;
-                const int cb = rest / rows;
-                const int r = rest - cb * rows;
-                const int hy = r / G.Wp, hx = r - (r / G.Wp) * G.Wp;
-                const int iy = rb * G.R - a.ph + hy, ix = hx - a.pw;
-                const bool ok = iy >= 0 && iy < a.SH && ix >= 0 && ix < a.SW;
-                const T_BF16* src = ok ? x + ((static_cast<int64_t>(img) * a.SH + iy) * a.SW + ix) * a.SC + cb * 64 + j8 * 8 : x;
-                cp_async16(smem_u32(hbuf + cb * G.cb_bytes + r * 128 + ((j8 ^ (r & 7)) << 4)), src, ok);
+            int hb = 0;
+            uint32_t hph = 0;
+            for (int j = 0; j < t_end - t_begin; ++j) {
+                const int t = tile_at(j);
+                const int rb = (t / n_tiles) % G.row_blocks;
+                const int img = t / (n_tiles * G.row_blocks);
+                mbar_wait(smem_u32(&hempty[hb]), ((hph >> hb) & 1) ^ 1);
+                if (a.dbg & 16384) {  // profiling: skip the halo loads
+                    mbar_arrive(smem_u32(&hfull[hb]));
+                } else {
+                    mbar_arrive_tx(smem_u32(&hfull[hb]), static_cast<uint32_t>(G.ncb * G.HR * G.Wp * 128));
+                    for (int cb = 0; cb < G.ncb; ++cb)
+                        tma_load_4d_tile(smem_u32(halo + hb * HB + cb * G.cb_bytes), &tm_x, cb * 64, -a.pw,
+                                         rb * G.R - a.ph, img, smem_u32(&hfull[hb]));
+                }
+                hph ^= 1u << hb;
+                if (++hb == NH) hb = 0;
             }
-            cp_async_arrive_noinc(smem_u32(&hfull[hb]));
-            hph ^= 1u << hb;
-            if (++hb == NH) hb = 0;
         }
-        cp_async_wait<0>();
     } else if (warp < 4) {
         // ---------------------------------------------------------------- TMA producer (streamed B)
         if (warp == 0 && lane == 0) {
@@ -193,58 +187,76 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         }
     } else if (warp == 4) {
         // ---------------------------------------------------------------- MMA issuer
-        int stage = 0, hb = 0, acc = 0;
-        uint32_t phase = 0, hph = 0, acc_phase = 0;
-        if (RESB) mbar_wait(smem_u32(&bfull[0]), 0);
-        for (int j = 0; j < t_end - t_begin; ++j) {
-            const int t = tile_at(j);
-            mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
-            mbar_wait(smem_u32(&hfull[hb]), (hph >> hb) & 1);
-            tc_fence_after();
-            if ((a.dbg & 64) && blockIdx.x == 0 && lane == 0 && j < 64)
-                reinterpret_cast<long long*>(a.out)[64 + j] = clock64();
-            const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
-            const uint32_t hbase = smem_u32(halo + hb * HB);
-            bool first = true;
-            for (int tap = 0; tap < taps; ++tap) {
-                const int dkh = tap / a.kw, dkw = tap - (tap / a.kw) * a.kw;
-                const uint32_t row0 = static_cast<uint32_t>(dkh * G.Wp + dkw);
-                for (int cb = 0; cb < G.ncb; ++cb) {
-                    if (!RESB) {
-                        mbar_wait(smem_u32(&bfull[stage]), phase);
-                        tc_fence_after();
-                    }
-                    if (lane == 0) {
-                        const uint32_t a_addr = hbase + static_cast<uint32_t>(cb * G.cb_bytes) + row0 * 128u;
-                        const uint32_t b_addr = smem_u32(bring + (RESB ? tap * G.ncb + cb : stage) * B_BYTES);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            uint64_t ad = sw128_desc(a_addr + k * 32, 16, 1024);
-                            if (base_mode) ad |= static_cast<uint64_t>(((a_addr + k * 32) >> 7) & 7) << 49;
-                            const uint64_t bd = sw128_desc(b_addr + k * 32, 16, 1024);
-                            if (!(a.dbg & 2)) mma<__nv_bfloat16>(dcol, ad, bd, IDESC, first ? 0u : 1u);
-                            first = false;
+        // The whole warp runs the loop (converged, operands warp-uniform); one elected lane
+        // issues each K block's four MMAs (tc::mma4_elect). Descriptors are precomputed and
+        // advanced by adds (the 14-bit start-address field is smem address >> 4).
+        {
+            int stage = 0, hb = 0, acc = 0;
+            uint32_t phase = 0, hph = 0, acc_phase = 0;
+            if (RESB) mbar_wait(smem_u32(&bfull[0]), 0);
+            const uint64_t bdesc0 = sw128_desc(smem_u32(bring), 16, 1024);
+            const uint32_t cb_units = static_cast<uint32_t>(G.cb_bytes) >> 4;
+            const uint32_t row_skip = static_cast<uint32_t>(G.Wp - a.kw) * 8u;  // to the next filter row
+            const bool do_mma = !(a.dbg & 2);
+            for (int j = 0; j < t_end - t_begin; ++j) {
+                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+                mbar_wait(smem_u32(&hfull[hb]), (hph >> hb) & 1);
+                tc_fence_after();
+                if ((a.dbg & 64) && blockIdx.x == 0 && lane == 0 && j < 64)
+                    reinterpret_cast<long long*>(a.out)[64 + j] = clock64();
+                const uint32_t dcol = __shfl_sync(0xffffffffu, tmem_base + static_cast<uint32_t>(acc * BN), 0);
+                const uint64_t adesc0 = sw128_desc(smem_u32(halo + hb * HB), 16, 1024);
+                uint32_t aoff = 0;  // (dkh * Wp + dkw) * 128 B, in 16-byte units
+                uint32_t boff = 0;
+                uint32_t accum = 0;
+                if (RESB && a.kw == 3 && (G.ncb == 1 || G.ncb == 2)) {
+                    // 3x3 fast path: one asm statement per (channel block, filter row)
+                    for (int cb = 0; cb < G.ncb; ++cb) {
+                        for (int dkh = 0; dkh < a.kh; ++dkh) {
+                            const uint64_t ad = adesc0 + static_cast<uint32_t>(dkh * G.Wp * 8) + cb * cb_units;
+                            const uint64_t bd = bdesc0 + static_cast<uint32_t>((dkh * 3 * G.ncb + cb) * (B_BYTES >> 4));
+                            if (do_mma) {
+                                if (G.ncb == 1) mma_row3_elect<(B_BYTES >> 4)>(dcol, ad, bd, IDESC, accum);
+                                else mma_row3_elect<2 * (B_BYTES >> 4)>(dcol, ad, bd, IDESC, accum);
+                            }
+                            accum = 1;
                         }
-                        if (!RESB) mma_commit(smem_u32(&bempty[stage]));
                     }
-                    first = false;
-                    __syncwarp();
-                    if (!RESB && ++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                } else
+                for (int dkh = 0; dkh < a.kh; ++dkh) {
+                    for (int dkw = 0; dkw < a.kw; ++dkw) {
+                        for (int cb = 0; cb < G.ncb; ++cb) {
+                            uint64_t bd;
+                            if (RESB) {
+                                bd = bdesc0 + boff;
+                                boff += B_BYTES >> 4;
+                            } else {
+                                mbar_wait(smem_u32(&bfull[stage]), phase);
+                                tc_fence_after();
+                                bd = bdesc0 + static_cast<uint32_t>(stage * (B_BYTES >> 4));
+                            }
+                            if (do_mma) mma4_elect<__nv_bfloat16>(dcol, adesc0 + aoff + cb * cb_units, bd, IDESC, accum);
+                            accum = 1;
+                            if (!RESB) {
+                                mma_commit_elect(smem_u32(&bempty[stage]));
+                                if (++stage == STAGES) {
+                                    stage = 0;
+                                    phase ^= 1;
+                                }
+                            }
+                        }
+                        aoff += 8;
                     }
+                    aoff += row_skip;
                 }
-            }
-            if (lane == 0) {
-                mma_commit(smem_u32(&hempty[hb]));
-                mma_commit(smem_u32(&tfull[acc]));
-            }
-            __syncwarp();
-            hph ^= 1u << hb;
-            if (++hb == NH) hb = 0;
-            if (++acc == NA) {
-                acc = 0;
-                acc_phase ^= 1;
+                mma_commit_elect(smem_u32(&hempty[hb]));
+                mma_commit_elect(smem_u32(&tfull[acc]));
+                hph ^= 1u << hb;
+                if (++hb == NH) hb = 0;
+                if (++acc == NA) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
             }
         }
     } else {
@@ -281,13 +293,37 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
                 const bool full = n + 32 <= a.Nout;
+                // every loop is unrolled so f[] stays in registers (a dynamic index would put it in
+                // local memory); full chunks use float4 parameter loads (the addresses are warp-uniform)
                 if (has_bias) {
-                    for (int j = 0; j < 32; ++j)
-                        if (full || n + j < a.Nout) f[j] += __ldg(a.bias + n + j);
+                    if (full) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + n + j));
+                            f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (n + j < a.Nout) f[j] += __ldg(a.bias + n + j);
+                    }
                 }
                 if (has_fold) {
-                    for (int j = 0; j < 32; ++j)
-                        if (full || n + j < a.Nout) f[j] = fmaf(f[j], __ldg(a.ep_scale + n + j), __ldg(a.ep_shift + n + j));
+                    if (full) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 sc = __ldg(reinterpret_cast<const float4*>(a.ep_scale + n + j));
+                            const float4 sh = __ldg(reinterpret_cast<const float4*>(a.ep_shift + n + j));
+                            f[j] = fmaf(f[j], sc.x, sh.x);
+                            f[j + 1] = fmaf(f[j + 1], sc.y, sh.y);
+                            f[j + 2] = fmaf(f[j + 2], sc.z, sh.z);
+                            f[j + 3] = fmaf(f[j + 3], sc.w, sh.w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (n + j < a.Nout) f[j] = fmaf(f[j], __ldg(a.ep_scale + n + j), __ldg(a.ep_shift + n + j));
+                    }
                 }
                 if (has_res) {
                     const __nv_bfloat16* rp = res + m * a.ld_res + n;
@@ -300,7 +336,9 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                             for (int k = 0; k < 8; ++k) f[j + k] += r8[k];
                         }
                     } else {
-                        for (int j = 0; j < 32 && n + j < a.Nout; ++j) f[j] += __bfloat162float(rp[j]);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (n + j < a.Nout) f[j] += __bfloat162float(rp[j]);
                     }
                 }
                 if (act != 0) {
@@ -315,7 +353,9 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 32; j += 8) store16(op + j, f + j);
                 } else {
-                    for (int j = 0; j < 32 && n + j < a.ldo; ++j) op[j] = __float2bfloat16_rn(n + j < a.Nout ? f[j] : 0.f);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (n + j < a.ldo) op[j] = __float2bfloat16_rn(n + j < a.Nout ? f[j] : 0.f);
                 }
             }
             tc_fence_before();
@@ -381,9 +421,12 @@ void halo_dispatch(const IgemmArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool halo_supported(const IgemmArgs& a) {
-    // Experimental (opt-in through the conv debug flag 512): exact, but on B200 the per-tile halo
-    // loads come in at ~2 TB/s (measured), slower than the im2col path's L2-served taps.
-    if (!(a.dbg & 512)) return false;
+    // On by default for 64-channel inputs (one channel block: ResNet-50's 56x56 3x3 convs, 1.3x
+    // faster than TMA im2col, bit-identical: same k-block order). Off: conv debug flag 512 or
+    // SOL_NO_HALO=1. With more channel blocks im2col is as fast (measured at 28x28x128).
+    static const bool disabled = std::getenv("SOL_NO_HALO") != nullptr;
+    if ((a.dbg & 512) || disabled) return false;
+    if (a.SC != 64) return false;
     if (a.mode != IG_FPROP || a.dtype != DT_BF16 || a.out_dtype != DT_BF16 || (a.dbg & 16)) return false;
     if (a.sh != 1 || a.sw != 1 || a.kh != a.kw || a.kh % 2 == 0 || a.kh < 3 || a.kh > 7) return false;
     if (a.ph != a.kh / 2 || a.pw != a.kw / 2 || a.OH != a.SH || a.OW != a.SW) return false;

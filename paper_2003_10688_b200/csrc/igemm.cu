@@ -466,32 +466,28 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         if (RESB) mbar_wait(smem_u32(bres), 0);
+        const uint64_t a_desc0 = sw128_desc(smem_u32(smem), 16, 1024);
+        const uint64_t bres_desc0 = RESB ? sw128_desc(smem_u32(bres_smem), 16, 1024) : 0;
+        const bool do_mma = !(a.dbg & 2);
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
             tc_fence_after();
             const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
+            // converged warp, one elected lane issues (tc::mma4_elect): operands stay uniform
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(smem_u32(&full[stage]), phase);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint32_t b_addr = RESB ? smem_u32(bres_smem + kb * B_BYTES) : a_addr + A_BYTES;
-#pragma unroll
-                    for (int k = 0; k < ROWB / KSTEP_BYTES; ++k) {
-                        const uint64_t ad = sw128_desc(a_addr + k * KSTEP_BYTES, 16, 1024);
-                        const uint64_t bd = sw128_desc(b_addr + k * KSTEP_BYTES, 16, 1024);
-                        if (!(a.dbg & 2)) mma<T>(dcol, ad, bd, IDESC, (kb | k) != 0);
-                    }
-                    mma_commit(smem_u32(&empty[stage]));
-                }
-                __syncwarp();
+                const uint64_t ad = a_desc0 + static_cast<uint32_t>(stage * (STAGE_BYTES >> 4));
+                const uint64_t bd = RESB ? bres_desc0 + static_cast<uint32_t>(kb * (B_BYTES >> 4))
+                                         : ad + static_cast<uint32_t>(A_BYTES >> 4);
+                if (do_mma) mma4_elect<T>(dcol, ad, bd, IDESC, kb != 0);
+                mma_commit_elect(smem_u32(&empty[stage]));
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) mma_commit(smem_u32(&tfull[acc]));
-            __syncwarp();
+            mma_commit_elect(smem_u32(&tfull[acc]));
             if (++acc == NACC) {
                 acc = 0;
                 acc_phase ^= 1;

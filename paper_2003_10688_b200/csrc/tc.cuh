@@ -107,6 +107,64 @@ __device__ __forceinline__ void mma<float>(uint32_t tmem_d, uint64_t adesc, uint
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
+// The four K=16 steps of one 128-byte K block (descriptor start addresses advance by 32 B = 2
+// units), issued by ONE elected lane of a CONVERGED warp from a single asm statement: with the
+// loop run by the whole warp the operands stay warp-uniform, so ptxas issues back-to-back
+// UTCHMMAs instead of a per-MMA elect/R2UR loop (measured: 48 vs ~110 cycles per N=64 MMA).
+// KIND is "f16" or "tf32"; acc = 0 overwrites the accumulator on the first step.
+template <typename T>
+__device__ __forceinline__ void mma4_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc);
+#define SOLB200_MMA4(KIND)                                                                         \
+    asm volatile(                                                                                  \
+        "{\n.reg .pred p, pa;\n.reg .b64 a1, a2, a3, b1, b2, b3;\n"                               \
+        "elect.sync _|p, 0xffffffff;\n"                                                           \
+        "setp.ne.b32 pa, %4, 0;\n"                                                                \
+        "add.s64 a1, %1, 2;\nadd.s64 a2, %1, 4;\nadd.s64 a3, %1, 6;\n"                           \
+        "add.s64 b1, %2, 2;\nadd.s64 b2, %2, 4;\nadd.s64 b3, %2, 6;\n"                           \
+        "@p tcgen05.mma.cta_group::1.kind::" KIND " [%0], %1, %2, %3, pa;\n"                     \
+        "@p tcgen05.mma.cta_group::1.kind::" KIND " [%0], a1, b1, %3, 1;\n"                      \
+        "@p tcgen05.mma.cta_group::1.kind::" KIND " [%0], a2, b2, %3, 1;\n"                      \
+        "@p tcgen05.mma.cta_group::1.kind::" KIND " [%0], a3, b3, %3, 1;\n"                      \
+        "}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc))
+template <>
+__device__ __forceinline__ void mma4_elect<__nv_bfloat16>(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                          uint32_t acc) {
+    SOLB200_MMA4("f16");
+}
+template <>
+__device__ __forceinline__ void mma4_elect<float>(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    SOLB200_MMA4("tf32");
+}
+#undef SOLB200_MMA4
+
+// One filter row of a 3-tap convolution from shifted operands: taps dkw = 0..2 read A at
+// +dkw rows (8 units of 16 B each) and B at +dkw * BSTR units, four K=16 steps each: twelve
+// bf16 MMAs from one asm statement (immediate offsets -> uniform-register adds only).
+template <int BSTR>
+__device__ __forceinline__ void mma_row3_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+#define SOLB200_STEP(AI, BI) \
+    "add.s64 ra, %1, " #AI ";\nadd.s64 rb, %2, %" #BI ";\n@p tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, 1;\n"
+    asm volatile(
+        "{\n.reg .pred p, pa;\n.reg .b64 ra, rb;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "setp.ne.b32 pa, %4, 0;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pa;\n"
+        SOLB200_STEP(2, 5) SOLB200_STEP(4, 6) SOLB200_STEP(6, 7)
+        SOLB200_STEP(8, 8) SOLB200_STEP(10, 9) SOLB200_STEP(12, 10) SOLB200_STEP(14, 11)
+        SOLB200_STEP(16, 12) SOLB200_STEP(18, 13) SOLB200_STEP(20, 14) SOLB200_STEP(22, 15)
+        "}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc),
+        "n"(2), "n"(4), "n"(6), "n"(BSTR), "n"(BSTR + 2), "n"(BSTR + 4), "n"(BSTR + 6),
+        "n"(2 * BSTR), "n"(2 * BSTR + 2), "n"(2 * BSTR + 4), "n"(2 * BSTR + 6));
+#undef SOLB200_STEP
+}
+
+// tcgen05.commit from one elected lane of a converged warp.
+__device__ __forceinline__ void mma_commit_elect(uint32_t mbar_addr) {
+    asm volatile(
+        "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\n"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(mbar_addr));
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t mbar_addr) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
         mbar_addr));

@@ -1,0 +1,329 @@
+// Tensor-core issue-rate probe: one CTA per SM, one thread issues back-to-back
+// tcgen05.mma (M=128, K=16, bf16 -> f32) from shared-memory (or TMEM) operands for several N;
+// reports cycles per MMA. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+//   -I../../paper_2003_10688_b200/csrc mma_rate.cu -o mma_rate -lcuda
+#include <cstdio>
+#include <cuda_bf16.h>
+#include "tc.cuh"
+
+using namespace solb200;
+using namespace solb200::tc;
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    return x;
+}
+
+// four k16 steps of one 64-element K block in one asm statement, issued by one elected lane
+// of a converged warp (descriptors advance by 32 B = 2 units per step)
+__device__ __forceinline__ void mma4_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p, pa;\n.reg .b64 a1, a2, a3, b1, b2, b3;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "setp.ne.b32 pa, %4, 0;\n"
+        "add.s64 a1, %1, 2;\nadd.s64 a2, %1, 4;\nadd.s64 a3, %1, 6;\n"
+        "add.s64 b1, %2, 2;\nadd.s64 b2, %2, 4;\nadd.s64 b3, %2, 6;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pa;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+        "}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int N, int AMODE, bool MISALIGN = true, bool RANDOM = false>  // AMODE 0: A in smem; 1: A in TMEM; 2: two MMAs share A (N each);
+                             // 3: as 0 while warps 1-3 spin in mbarrier.try_wait on a pending phase
+__global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* A = smem;               // 128 rows x 128 B (mode 14: 232-row halo)
+    uint8_t* B = smem + (AMODE == 14 ? 30720 : 16384);  // N rows x 128 B (x2 for AMODE 2, x9 for 14)
+    __shared__ uint64_t bar, bar2, tfull[4], tempty[4];
+    __shared__ uint32_t slot;
+    if (AMODE == 21) {  // NaN / denormal operands
+        for (int i = threadIdx.x; i < (30720 + 9 * N * 128) / 16; i += blockDim.x)
+            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x7fc17fc1u, 0x00010001u, 0x7f807f80u, 0x80018001u);
+    } else
+    for (int i = threadIdx.x; i < (30720 + 9 * N * 128) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = RANDOM ? make_uint4(hash32(i * 4) & 0xBFFFBFFFu, hash32(i * 4 + 1) & 0xBFFFBFFFu,
+                                                                hash32(i * 4 + 2) & 0xBFFFBFFFu, hash32(i * 4 + 3) & 0xBFFFBFFFu)
+                                                   : make_uint4(0x3f803f80u, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        mbar_init(smem_u32(&bar2), 1);
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(smem_u32(&tfull[i]), 1);
+            mbar_init(smem_u32(&tempty[i]), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    if (threadIdx.x < 32) tmem_alloc<512>(smem_u32(&slot));
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    constexpr uint32_t IDESC = make_idesc(1, N, 128, 0, 0);
+    if (AMODE == 23 && threadIdx.x < 32) {
+        const uint64_t ad = sw128_desc(smem_u32(A), 16, 1024);
+        const uint64_t bd = sw128_desc(smem_u32(B), 16, 1024);
+        const long long t0 = clock64();
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int it = 0; it < iters / 9; ++it) {
+            mbar_wait(smem_u32(&tempty[acc]), aph ^ 1);
+            tc_fence_after();
+            for (int dkh = 0; dkh < 3; ++dkh)
+                mma_row3_elect<N * 8>(tmem + acc * N, ad + dkh * 58 * 8, bd + dkh * 3 * N * 8, IDESC, dkh);
+            mma_commit_elect(smem_u32(&tfull[acc]));
+            if (++acc == 4) { acc = 0; aph ^= 1; }
+        }
+        __syncwarp();
+        if (threadIdx.x == 0) {
+            mma_commit(smem_u32(&bar));
+            mbar_wait(smem_u32(&bar), 0);
+            const long long t1 = clock64();
+            if (blockIdx.x == 0) out[0] = t1 - t0;
+        }
+        __syncwarp();
+    } else if (AMODE == 23 && threadIdx.x >= 128 && threadIdx.x < 256) {
+        const int q = (threadIdx.x / 32) & 3;
+        int acc = 0;
+        uint32_t aph = 0;
+        uint32_t sink = 0;
+        for (int it = 0; it < iters / 9; ++it) {
+            mbar_wait(smem_u32(&tfull[acc]), aph);
+            tc_fence_after();
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * N + c0, v);
+                tmem_wait_ld();
+                for (int j = 0; j < 32; ++j) sink += v[j];
+            }
+            tc_fence_before();
+            mbar_arrive(smem_u32(&tempty[acc]));
+            if (++acc == 4) { acc = 0; aph ^= 1; }
+        }
+        if (sink == 0x1234567u) out[3] = sink;
+    } else if (AMODE == 22 && threadIdx.x < 32) {
+        const uint64_t ad = sw128_desc(smem_u32(A), 16, 1024);
+        const uint64_t bd = sw128_desc(smem_u32(B), 16, 1024);
+        const int kk = static_cast<int>(out[2]);
+        const long long t0 = clock64();
+        for (int it = 0; it < iters / 9; ++it) {
+            uint32_t aoff = 0, boff = 0, accum = 0;
+            for (int dkh = 0; dkh < kk; ++dkh) {
+                for (int dkw = 0; dkw < kk; ++dkw) {
+                    mma4_elect(tmem + (it & 3) * N, ad + aoff, bd + boff, IDESC, accum);
+                    accum = 1;
+                    aoff += 8;
+                    boff += N * 8;
+                }
+                aoff += (58 - kk) * 8;
+            }
+        }
+        __syncwarp();
+        if (threadIdx.x == 0) {
+            mma_commit(smem_u32(&bar));
+            mbar_wait(smem_u32(&bar), 0);
+            const long long t1 = clock64();
+            if (blockIdx.x == 0) out[0] = t1 - t0;
+        }
+        __syncwarp();
+    } else if (threadIdx.x == 0) {
+        const uint64_t ad = sw128_desc(smem_u32(A), 16, 1024);
+        const uint64_t bd = sw128_desc(smem_u32(B), 16, 1024);
+        const uint64_t bd2 = sw128_desc(smem_u32(B + N * 128), 16, 1024);
+        const long long t0 = clock64();
+        if (AMODE == 14) {
+            for (int it = 0; it < iters / 9; ++it) {
+                uint32_t aoff = 0, boff = 0;
+                for (int dkh = 0; dkh < 3; ++dkh) {
+                    for (int dkw = 0; dkw < 3; ++dkw) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            mma<__nv_bfloat16>(tmem + (it & 3) * N, ad + (MISALIGN ? aoff : 0) + 2 * k, bd + boff + 2 * k, IDESC, 1);
+                        aoff += 8;
+                        boff += N * 8;
+                    }
+                    aoff += (58 - 3) * 8;
+                }
+            }
+        } else if (AMODE == 18 || AMODE == 19 || AMODE == 20 || AMODE == 21) {
+            // halo-like with runtime loop bounds (kh = kw = iters % 7 + ... passed via out[2])
+            const int kk = static_cast<int>(out[2]);
+            for (int it = 0; it < iters / 9; ++it) {
+                uint32_t aoff = 0, boff = 0, accum = 0;
+                for (int dkh = 0; dkh < kk; ++dkh) {
+                    for (int dkw = 0; dkw < kk; ++dkw) {
+                        const uint64_t a0 = ad + aoff, b0 = bd + boff;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            mma<__nv_bfloat16>(tmem + (it & 3) * N, a0 + 2 * k, b0 + 2 * k, IDESC, accum);
+                            accum = 1;
+                        }
+                        aoff += 8;
+                        boff += N * 8;
+                    }
+                    aoff += (58 - kk) * 8;
+                }
+            }
+        } else if (AMODE == 16 || AMODE == 17) {
+            // commit to a (never-waited) mbarrier after every 4 (16) or 36 (17) MMAs
+            int cnt = 0;
+            for (int it = 0; it < iters; ++it) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mma<__nv_bfloat16>(tmem, ad + 2 * k, bd + 2 * k, IDESC, 1);
+                if (AMODE == 16 || ++cnt == 9) {
+                    cnt = 0;
+                    mma_commit(smem_u32(&bar2));
+                }
+            }
+        } else
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (AMODE == 0 || AMODE >= 3 && AMODE != 13) {
+                    mma<__nv_bfloat16>(tmem, ad + 2 * k, bd + 2 * k, IDESC, 1);
+                } else if (AMODE == 1 || AMODE == 13) {
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
+                        "r"(tmem + 256 + 8 * k), "l"(bd + 2 * k), "r"(IDESC), "r"(1));
+                } else {
+                    mma<__nv_bfloat16>(tmem, ad + 2 * k, bd + 2 * k, IDESC, 1);
+                    mma<__nv_bfloat16>(tmem + N, ad + 2 * k, bd2 + 2 * k, IDESC, 1);
+                }
+            }
+        }
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        const long long t1 = clock64();
+        if (blockIdx.x == 0) out[0] = t1 - t0;
+        if (AMODE >= 3 && AMODE != 7 && AMODE != 11) mbar_arrive(smem_u32(&bar2));
+    } else if (AMODE == 3 && threadIdx.x % 32 == 0) {
+        mbar_wait(smem_u32(&bar2), 0);
+    } else if (AMODE == 11 && threadIdx.x >= 32) {
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    } else if (AMODE == 15 && threadIdx.x >= 32) {
+        // warps 1-3 keep reading TMEM (columns 256+) like an epilogue draining another stage
+        const int w = threadIdx.x / 32;
+        uint32_t done = 0, acc = 0;
+        while (!done) {
+            uint32_t v[32];
+            tmem_ld32_nowait(tmem + 256 + (static_cast<uint32_t>(w * 32) << 16), v);
+            tmem_wait_ld();
+            for (int j = 0; j < 32; ++j) acc += v[j];
+            asm volatile("{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.b32 %0, 1, 0, P1;\n}\n"
+                         : "=r"(done) : "r"(smem_u32(&bar2)), "r"(0));
+        }
+        if (acc == 0x12345678u) out[1] = acc;
+    } else if ((AMODE == 12 || AMODE == 13) && threadIdx.x >= 32) {
+        // whole warps (not one lane) wait on the mbarrier
+        mbar_wait(smem_u32(&bar2), 0);
+    } else if (AMODE == 7 && threadIdx.x % 32 == 0) {
+        // spin on clock only (no memory traffic) for a fixed long time
+        const long long t0 = clock64();
+        while (clock64() - t0 < 4096LL * 4 * 130) __nanosleep(200);
+    } else if (AMODE == 8 && threadIdx.x == 64) {
+        mbar_wait(smem_u32(&bar2), 0);
+    } else if (AMODE == 9 && threadIdx.x == 0 + 32) {
+        mbar_wait(smem_u32(&bar2), 0);
+    } else if (AMODE >= 4 && AMODE <= 6 && threadIdx.x % 32 == 0) {
+        const uint32_t addr = smem_u32(&bar2);
+        uint32_t done = 0;
+        while (!done) {
+            if (AMODE == 4) {
+                asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\nselp.b32 %0, 1, 0, P1;\n}\n"
+                             : "=r"(done) : "r"(addr), "r"(0), "r"(1000000));
+            } else {
+                asm volatile("{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.b32 %0, 1, 0, P1;\n}\n"
+                             : "=r"(done) : "r"(addr), "r"(0));
+                if (!done) __nanosleep(AMODE == 5 ? 64 : 256);
+            }
+        }
+    }
+    if (AMODE == 11 && threadIdx.x < 32) asm volatile("bar.arrive 1, 128;\n" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+template <int N, int AMODE, bool MISALIGN = true, bool RANDOM = false>
+void run(const char* name) {
+    long long* d;
+    cudaMalloc(&d, 32);
+    const int smem = (AMODE == 19 || AMODE == 20) ? 225 * 1024 : 30720 + 9 * N * 128 + 2048;
+    cudaFuncSetAttribute(rate_kernel<N, AMODE, MISALIGN, RANDOM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int iters = 4096;
+    long long three = 3;
+    cudaMemcpy(d + 2, &three, 8, cudaMemcpyHostToDevice);
+    rate_kernel<N, AMODE, MISALIGN, RANDOM><<<148, AMODE == 20 || AMODE == 23 ? 288 : 128, smem>>>(18, d);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    rate_kernel<N, AMODE, MISALIGN, RANDOM><<<148, AMODE == 20 || AMODE == 23 ? 288 : 128, smem>>>(iters, d);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long cyc;
+    cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+    const double mmas = AMODE == 14 || (AMODE >= 18 && AMODE <= 23) ? (iters / 9) * 36.0 : iters * 4.0 * (AMODE == 2 ? 2 : 1);
+    const double flops = 148.0 * mmas * 2.0 * 128 * N * 16;
+    printf("%-22s N=%3d: %7.1f cycles/MMA  %7.1f TF/s  (%s)\n", name, N, cyc / mmas, flops / (ms * 1e-3) / 1e12,
+           cudaGetErrorString(err));
+    cudaFree(d);
+}
+
+int main() {
+    run<64, 18>("halo-like runtime bounds");
+    run<64, 23>("tile protocol + epilogue");
+    run<128, 23>("tile protocol + epilogue");
+    run<64, 22>("warp-converged elect x4");
+    run<128, 22>("warp-converged elect x4");
+    run<64, 21>("NaN/denormal operands");
+    run<64, 19>("+227KB smem");
+    run<64, 20>("+227KB smem, 288 thr");
+    run<64, 16>("commit every 4 MMAs");
+    run<128, 16>("commit every 4 MMAs");
+    run<256, 16>("commit every 4 MMAs");
+    run<64, 17>("commit every 36 MMAs");
+    run<64, 15>("warps 1-3 tcgen05.ld loop");
+    run<128, 15>("warps 1-3 tcgen05.ld loop");
+    run<64, 14, true, true>("halo-like, random data");
+    run<128, 14, true, true>("halo-like, random data");
+    run<64, 14>("halo-like taps");
+    run<64, 14, false>("halo-like, aligned A");
+    run<128, 14>("halo-like taps");
+    run<32, 0>("A smem");
+    run<64, 0>("A smem");
+    run<128, 0>("A smem");
+    run<192, 0>("A smem");
+    run<256, 0>("A smem");
+    run<64, 1>("A tmem");
+    run<128, 1>("A tmem");
+    run<256, 1>("A tmem");
+    run<64, 2>("A smem, 2 MMAs share A");
+    run<64, 3>("A smem, 3 warps polling");
+    run<128, 3>("A smem, 3 warps polling");
+    run<64, 4>("polling w/ time hint");
+    run<64, 5>("test_wait+nanosleep64");
+    run<64, 6>("test_wait+nanosleep256");
+    run<128, 5>("test_wait+nanosleep64");
+    run<64, 7>("3 warps clock-sleep");
+    run<64, 8>("warp 2 mbar_wait");
+    run<64, 9>("warp 1 mbar_wait");
+    run<64, 11>("warps 1-3 bar.sync");
+    run<64, 12>("warps 1-3 full mbar_wait");
+    run<128, 12>("warps 1-3 full mbar_wait");
+    run<256, 12>("warps 1-3 full mbar_wait");
+    run<64, 13>("A tmem + mbar_wait");
+    run<128, 13>("A tmem + mbar_wait");
+    run<256, 13>("A tmem + mbar_wait");
+    run<128, 2>("A smem, 2 MMAs share A");
+    return 0;
+}

@@ -24,6 +24,8 @@ CASES = [
     (1, 32, 9, 9, 48, 3, 1, 1),
     (16, 64, 28, 28, 64, 3, 1, 1),    # many pixel k-blocks: split wgrad (swapped orientation)
     (8, 64, 28, 28, 256, 1, 1, 0),
+    (3, 64, 56, 56, 64, 3, 1, 1),     # halo-tile kernel (halo.cu), ResNet-50 layer-1 shape
+    (2, 64, 13, 29, 64, 3, 1, 1),     # halo-tile kernel, ragged rows / junk columns
 ]
 
 
@@ -136,3 +138,39 @@ def test_conv_wgrad(gpu, case, dt):
     want = O.conv2d_back_w(quant(dy, dt), quant(x, dt), (k, k), (s, s), (p, p))
     err = O.oracle_err(dw.cpu().numpy(), want)
     assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("case", [(3, 64, 56, 56, 64), (2, 64, 13, 29, 64), (2, 64, 14, 14, 40)])
+def test_halo_conv_matches_im2col(gpu, case):
+    """The row-padded halo-tile conv (halo.cu) accumulates the same k-blocks in the same order
+    as the TMA-im2col kernel, so the two outputs are bit-identical (conv debug flag 512 turns the
+    halo path off)."""
+    import torch
+    from paper_2003_10688_b200 import _lib as L
+    N, Cin, H, W, Cout = case
+    dev = torch.device("cuda:0")
+    st = torch.cuda.current_stream().cuda_stream
+    d = L.ConvDesc(N, Cin, H, W, Cout, H, W, 3, 3, 1, 1, 1, 1, Cin, 1)
+    g = torch.Generator().manual_seed(3)
+    x = (torch.rand(N, H, W, Cin, generator=g) * 2 - 1).to(dev).to(torch.bfloat16)
+    w = ((torch.rand(Cout, Cin, 3, 3, generator=g) * 2 - 1) * 0.1).to(dev)
+    bias = (torch.rand(Cout, generator=g) - 0.5).to(dev)
+    n = C.c_int64()
+    L.check(L.lib().sol_b200_conv_packed_elems(C.byref(d), 0, C.byref(n)))
+    wp = torch.zeros(n.value, dtype=torch.bfloat16, device=dev)
+    L.check(L.lib().sol_b200_conv_pack_weight(C.byref(d), w.data_ptr(), wp.data_ptr(), 0, st))
+    outs = []
+    try:
+        for dbg in (0, 512):
+            L.check(L.lib().sol_b200_set_conv_debug(dbg))
+            y = torch.full((N, H, W, Cout), float("nan"), dtype=torch.bfloat16, device=dev)
+            L.check(L.lib().sol_b200_conv_fprop(C.byref(d), x.data_ptr(), wp.data_ptr(), C.c_void_p(bias.data_ptr()),
+                                                y.data_ptr(), 1, st))
+            torch.cuda.synchronize()
+            outs.append(y.float().cpu())
+    finally:
+        L.check(L.lib().sol_b200_set_conv_debug(0))
+    assert torch.equal(outs[0], outs[1])
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.to(torch.bfloat16).float(), bias, padding=1)
+    err = (outs[0].permute(0, 3, 1, 2) - ref.cpu()).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item()
