@@ -60,6 +60,10 @@ void igemm_launch(const IgemmArgs& a, cudaStream_t stream);
 bool stem_supported(const IgemmArgs& a);
 void stem_launch(const IgemmArgs& a, cudaStream_t stream);
 int stem_kpad(int kh);
+// Stride-2 stem from the NCHW f32 input without an im2col matrix (stem_row.cu): the MMA reads
+// overlapping 64-byte windows of compact bf16 input rows (K-major SWIZZLE_NONE operand).
+bool stem_row_supported(const IgemmArgs& a);
+void stem_row_launch(const IgemmArgs& a, cudaStream_t stream);
 // Stem weight gradient (same halo / im2col machinery): dW canonical [Cout=64][Cin][kh][kw] f32 from
 // dy [N, OH, OW, 64] and x (a.src); `ws` holds stem_wgrad_workspace_floats() partial sums.
 bool stem_wgrad_supported(const IgemmArgs& a, int ld_dy);

@@ -451,6 +451,7 @@ bool stem_supported(const IgemmArgs& a) {
 
 void stem_launch(const IgemmArgs& a, cudaStream_t s) {
     if (!stem_supported(a)) throw std::invalid_argument("stem conv: unsupported shape");
+    if (stem_row_supported(a)) return stem_row_launch(a, s);
     int HH, HWp, nbw, nd;
     stem_geometry(a, HH, HWp, &nbw, &nd);
     static std::once_flag once;

@@ -158,6 +158,20 @@ __device__ __forceinline__ void mma_row3_elect(uint32_t d, uint64_t a, uint64_t 
 #undef SOLB200_STEP
 }
 
+// Two consecutive K=16 bf16 MMAs (one 32-element K slice) for SWIZZLE_NONE operands whose
+// second step starts ASTEP / BSTEP 16-byte units after the first; elected lane, converged warp.
+template <int ASTEP, int BSTEP>
+__device__ __forceinline__ void mma2_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p, pa;\n.reg .b64 a1, b1;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "setp.ne.b32 pa, %4, 0;\n"
+        "add.s64 a1, %1, %5;\nadd.s64 b1, %2, %6;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pa;\n"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+        "}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc), "n"(ASTEP), "n"(BSTEP));
+}
+
 // tcgen05.commit from one elected lane of a converged warp.
 __device__ __forceinline__ void mma_commit_elect(uint32_t mbar_addr) {
     asm volatile(
