@@ -50,6 +50,10 @@ struct IgemmArgs {
     // stem only: `src` is the canonical NCHW f32 input with SC = Cin channels (the layout
     // conversion of the graph input is folded into the stem's halo load)
     int src_nchw_f32 = 0;
+    // stem_row only: fused 3x3 / stride-2 / pad-1 max pool after the epilogue; `out` is then the
+    // pooled tensor [N, OH/2, OW/2, ldo] (OH, OW = the conv's output grid, both even)
+    int pool3s2 = 0;
+    float pool_min_init = -INFINITY;  // the MaxPool2d min_init (0 after the relu-into-pool pass)
 };
 
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).

@@ -239,6 +239,10 @@ public:
                 b_idx_ = (a.has_bias && o.n_params > 1) ? o.params[1] : -1;
                 cin_ = in_.C;
                 cout_ = out_.C;
+                if (op_ == SOL_OP_CONV2D) {  // the conv's own grid (the unit output may be a fused pool's)
+                    conv_oh_ = static_cast<int>((in_.H + 2 * ph_ - kh_) / sh_ + 1);
+                    conv_ow_ = static_cast<int>((in_.W + 2 * pw_ - kw_) / sw_ + 1);
+                }
                 kpad_ = static_cast<int>(round_up(static_cast<int64_t>(kh_) * kw_ * in_.ld, bk));
                 nchw_in_ = d.bindings[o.inputs[0]].is_param == 2;
                 if (nchw_in_ && op_ != SOL_OP_CONV2D) unsupported("canonical NCHW input only for stem convolutions");
@@ -441,6 +445,20 @@ public:
             act_ = d.ops[k].op == SOL_OP_RELU ? 1 : 2;
             ++k;
         }
+        if (k < d.n_ops && d.ops[k].op == SOL_OP_MAXPOOL2D) {
+            // stem + 3x3/2 max pool (plan fusion fuse_stem_pool): the stem kernel pools its own
+            // output rows in shared memory, the full-resolution activation never reaches HBM
+            const sol_attrs& pa = d.ops[k].attrs;
+            if (d.ops[k].inputs[0] != prev_ref(k) || res_idx_ >= 0) unsupported("bad fused max pool");
+            if (pa.kh != 3 || pa.kw != 3 || pa.sh != 2 || pa.sw != 2 || pa.ph != 1 || pa.pw != 1)
+                unsupported("fused max pool must be 3x3 / stride 2 / pad 1");
+            pool_ = true;
+            pool_min_init_ = pa.min_init;
+            algo_flops *= double(conv_oh_) * conv_ow_ / (double(out_.H) * out_.W);  // MACs are on the conv grid
+            if (!stem_ || !stem_row_supported(fprop_args(nullptr, nullptr)))
+                unsupported("fused max pool needs the stride-2 row stem kernel");
+            ++k;
+        }
         if (k != d.n_ops) unsupported("unsupported fused conv epilogue");
         family = op_ == SOL_OP_CONV2D ? (stem_ ? "conv_stem_fused_tcgen05" : "conv_fprop_fused_tcgen05")
                                       : "linear_fused_tcgen05";
@@ -459,12 +477,14 @@ public:
         g.SW = static_cast<int>(in_.W);
         g.SC = static_cast<int>(nchw_in_ ? in_.C : in_.ld);
         g.src_nchw_f32 = nchw_in_ ? 1 : 0;
-        g.OH = static_cast<int>(out_.H);
-        g.OW = static_cast<int>(out_.W);
+        g.OH = conv_oh_ > 0 ? conv_oh_ : static_cast<int>(out_.H);
+        g.OW = conv_ow_ > 0 ? conv_ow_ : static_cast<int>(out_.W);
         g.kh = kh_; g.kw = kw_; g.sh = sh_; g.sw = sw_; g.ph = ph_; g.pw = pw_;
         g.Nout = static_cast<int>(cout_);
         g.K_pad = kpad_;
         g.ldo = static_cast<int>(out_.ld);
+        g.pool3s2 = pool_ ? 1 : 0;
+        g.pool_min_init = pool_min_init_;
         return g;
     }
 
@@ -604,7 +624,9 @@ private:
     Geo in_, out_, x_;
     int64_t cin_ = 0, cout_ = 0;
     int kpad_ = 0;
-    bool stem_ = false, stem_wg_ = false, nchw_in_ = false;
+    bool stem_ = false, stem_wg_ = false, nchw_in_ = false, pool_ = false;
+    int conv_oh_ = 0, conv_ow_ = 0;
+    float pool_min_init_ = -INFINITY;
     std::vector<SubClass> classes_;
     size_t sub_scratch_ = 0;
     int w_idx_ = -1, b_idx_ = -1;

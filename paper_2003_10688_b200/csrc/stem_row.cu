@@ -41,7 +41,9 @@ constexpr int SR_NCMP = 2, SR_NH_MAX = 8, SR_NACC = 4;
 constexpr int OFF_B = 0;
 constexpr int OFF_CMP = OFF_B + SR_B_BYTES;
 constexpr int OFF_STG = OFF_CMP + SR_NCMP * SR_CMP_BYTES;  // epilogue staging, 4 warps x 4 KB
-constexpr int OFF_BAR = OFF_STG + 4 * 4096;
+constexpr int SR_ROW_BYTES = 128 * 128;                    // one conv output row (<= 128 px x 64 ch bf16)
+constexpr int OFF_RING = OFF_STG + 4 * 4096;               // pool mode: last 3 conv rows
+constexpr int OFF_BAR = OFF_RING + 3 * SR_ROW_BYTES;
 constexpr int OFF_HALO = OFF_BAR + 1024;  // ring of NH halo slots (runtime slot size) to the end
 constexpr int SR_SMEM = 227 * 1024;
 
@@ -58,9 +60,31 @@ __device__ __forceinline__ uint64_t plain_desc(uint32_t saddr, uint32_t lbo, uin
     return sw128_desc(saddr, lbo, sbo, 0);  // layout type 0 = SWIZZLE_NONE (K-major core matrices)
 }
 
+// Work order. Plain: tile t = (image, conv row), strided over CTAs. Pool mode: CTAs take bands of
+// BP pooled rows; a band computes conv rows 2*p0-1 .. 2*(p0+BP)-1 in order (one recomputed row).
+struct RowTasks {
+    int N, OH, pool, BP, nbands;
+    __device__ RowTasks(const IgemmArgs& a, int bp) : N(a.N), OH(a.OH), pool(a.pool3s2), BP(bp) {
+        nbands = pool ? (OH / 2 + BP - 1) / BP : 0;
+    }
+    // visits (n, oy, p0) for every conv row this CTA computes, in order
+    template <typename F>
+    __device__ void each(F&& f) const {
+        if (!pool) {
+            for (int t = blockIdx.x; t < N * OH; t += gridDim.x) f(t / OH, t % OH, 0);
+            return;
+        }
+        for (int g = blockIdx.x; g < N * nbands; g += gridDim.x) {
+            const int n = g / nbands, p0 = (g - n * nbands) * BP;
+            const int r0 = max(0, 2 * p0 - 1), r1 = min(OH - 1, 2 * (p0 + BP) - 1);
+            for (int oy = r0; oy <= r1; ++oy) f(n, oy, p0);
+        }
+    }
+};
+
 __global__ void __launch_bounds__(SR_THREADS, 1)
     stem_row_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-                    const __grid_constant__ CUtensorMap tm_o, int nbw, int delta, int slot_bytes, int NH) {
+                    const __grid_constant__ CUtensorMap tm_o, int nbw, int delta, int slot_bytes, int NH, int BP) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -74,7 +98,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + SR_NACC);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tiles = a.N * a.OH;
+    const RowTasks tasks(a, BP);
     const int C = a.SC;
     const uint32_t halo_bytes = static_cast<uint32_t>(C * a.kh * nbw * 4);
 
@@ -112,8 +136,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                 tma_load_2d(smem_u32(smem + OFF_B + j * SR_BN * 16), &tm_w, j * 8, 0, smem_u32(b_full));
             int hb = 0;
             uint32_t hph = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                const int n = t / a.OH, oy = t - n * a.OH;
+            tasks.each([&](int n, int oy, int) {
                 mbar_wait(smem_u32(&halo_empty[hb]), hph ^ 1);
                 mbar_arrive_tx(smem_u32(&halo_full[hb]), halo_bytes);
                 tma_load_4d_f(smem_u32(smem + OFF_HALO + hb * slot_bytes), &tm_x, -a.pw - delta, oy * a.sh - a.ph, 0,
@@ -122,7 +145,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                     hb = 0;
                     hph ^= 1;
                 }
-            }
+            });
         }
     } else if (warp <= 8) {
         // ---------------------------------------------------------------- converters (8 warps)
@@ -133,7 +156,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
         const int pstride = a.kh * nbw;
         int hb = 0, cb = 0;
         uint32_t hph = 0, cph = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        tasks.each([&](int, int, int) {
             mbar_wait(smem_u32(&halo_full[hb]), hph);
             const float* plane = reinterpret_cast<const float*>(smem + OFF_HALO + hb * slot_bytes);
             float f[SR_KH_MAX][4];
@@ -170,7 +193,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                 cb = 0;
                 cph ^= 1;
             }
-        }
+        });
     } else if (warp == 9) {
         // ---------------------------------------------------------------- MMA issuer
         constexpr uint32_t IDESC = make_idesc(1, SR_BN, 128, 0, 0);
@@ -179,7 +202,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
         const uint64_t adesc0 = plain_desc(smem_u32(smem + OFF_CMP), 16, 128);
         int cb = 0, acc = 0;
         uint32_t cph = 0, aph = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        tasks.each([&](int, int, int) {
             mbar_wait(smem_u32(&tempty[acc]), aph ^ 1);
             mbar_wait(smem_u32(&cmp_full[cb]), cph);
             tc_fence_after();
@@ -201,7 +224,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                 acc = 0;
                 aph ^= 1;
             }
-        }
+        });
     } else {
         // ---------------------------------------------------------------- epilogue (warps 10-13)
         const int q = warp & 3;  // TMEM lane quarter = output pixels 32q .. 32q + 31
@@ -210,8 +233,9 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
         const int act = a.relu ? 1 : a.act;
         uint32_t aph = 0;
         int acc = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-            const int n = t / a.OH, oy = t - n * a.OH;
+        const int PH = a.OH / 2, PW = a.OW / 2;
+        uint8_t* ring = smem + OFF_RING;
+        tasks.each([&](int n, int oy, int p0) {
             mbar_wait(smem_u32(&tfull[acc]), aph);
             tc_fence_after();
             uint32_t v[SR_BN];
@@ -225,7 +249,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                 acc = 0;
                 aph ^= 1;
             }
-            if (q * 32 >= a.OW) continue;  // this quarter holds only junk rows
+            if (!a.pool3s2 && q * 32 >= a.OW) return;  // this quarter holds only junk rows
             float f[SR_BN];
 #pragma unroll
             for (int i = 0; i < SR_BN; ++i) f[i] = __uint_as_float(v[i]);
@@ -254,6 +278,59 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                     if (act == 2) f[i] = fminf(f[i], 6.f);
                 }
             }
+            if (a.pool3s2) {
+                // conv row -> ring slot oy % 3 ([px][8 x 16-byte chunks], chunk j at j ^ (px & 7));
+                // after an odd row 2py+1 the 128 epilogue threads max-pool rows 2py-1..2py+1
+                const int ox = q * 32 + lane;
+                uint8_t* slot = ring + (oy % 3) * SR_ROW_BYTES;
+                if (ox < a.OW) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float* src = f + j * 8;
+                        __nv_bfloat162 p0v = __floats2bfloat162_rn(src[0], src[1]);
+                        __nv_bfloat162 p1v = __floats2bfloat162_rn(src[2], src[3]);
+                        __nv_bfloat162 p2v = __floats2bfloat162_rn(src[4], src[5]);
+                        __nv_bfloat162 p3v = __floats2bfloat162_rn(src[6], src[7]);
+                        *reinterpret_cast<uint4*>(slot + ox * 128 + ((j ^ (ox & 7)) << 4)) =
+                            make_uint4(*reinterpret_cast<uint32_t*>(&p0v), *reinterpret_cast<uint32_t*>(&p1v),
+                                       *reinterpret_cast<uint32_t*>(&p2v), *reinterpret_cast<uint32_t*>(&p3v));
+                    }
+                }
+                asm volatile("bar.sync 2, 128;\n" ::: "memory");
+                const int py = (oy - 1) / 2;
+                if ((oy & 1) && py >= p0) {
+                    const int et = tid - 320;  // 0..127
+                    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (static_cast<int64_t>(n) * PH + py) * PW * a.ldo;
+                    for (int item = et; item < PW * 8; item += 128) {
+                        const int px = item >> 3, j = item & 7;
+                        float m[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) m[i] = a.pool_min_init;
+#pragma unroll
+                        for (int dy = -1; dy <= 1; ++dy) {
+                            const int r = 2 * py + dy;
+                            if (r < 0) continue;
+                            const uint8_t* rs = ring + (r % 3) * SR_ROW_BYTES;
+#pragma unroll
+                            for (int dx = -1; dx <= 1; ++dx) {
+                                const int c = 2 * px + dx;
+                                if (c < 0) continue;
+                                const uint4 v = *reinterpret_cast<const uint4*>(rs + c * 128 + ((j ^ (c & 7)) << 4));
+                                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float2 t2 = __bfloat1622float2(h[i]);
+                                    m[2 * i] = fmaxf(m[2 * i], t2.x);
+                                    m[2 * i + 1] = fmaxf(m[2 * i + 1], t2.y);
+                                }
+                            }
+                        }
+                        store16(orow + px * a.ldo + j * 8, m);
+                    }
+                    asm volatile("bar.sync 2, 128;\n" ::: "memory");
+                }
+                return;
+            }
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
             __syncwarp();
 #pragma unroll
@@ -278,7 +355,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
             }
-        }
+        });
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
         __syncwarp();
     }
@@ -348,6 +425,7 @@ bool stem_row_supported(const IgemmArgs& a) {
     if (disabled || !a.src_nchw_f32 || a.mode != IG_FPROP || a.dtype != DT_BF16 || a.out_dtype != DT_BF16) return false;
     if (a.SC < 1 || a.SC > 4 || a.Nout != SR_BN || a.ldo != SR_BN || a.residual != nullptr) return false;
     if (a.sw != 2 || a.kw > 8 || a.kh > SR_KH_MAX || a.K_pad != stem_kpad(a.kh) || a.OW > 124 || a.OW < 1) return false;
+    if (a.pool3s2 && (a.OH % 2 || a.OW % 2 || a.OH < 2)) return false;
     int nbw, delta;
     sr_geometry(a, nbw, delta);
     return nbw <= 256 && a.SC * a.kh * nbw * 4 <= SR_HALO_MAX && a.N > 0 && a.OH > 0;  // one converter per column
@@ -362,12 +440,18 @@ void stem_row_launch(const IgemmArgs& a, cudaStream_t s) {
     });
     const CUtensorMap tx = sr_tmap_x(a, nbw);
     const CUtensorMap tw = sr_tmap_w(a);
-    const CUtensorMap to = sr_tmap_o(a);
-    const int tiles = a.N * a.OH;
+    IgemmArgs ao = a;  // pool mode stores pooled rows directly; the output map is a dummy
+    if (a.pool3s2) ao.OH = ao.OW = 1;
+    const CUtensorMap to = sr_tmap_o(ao);
+    // pool mode: bands of BP pooled rows (~14: one recomputed conv row per 28, CTAs balanced)
+    const int PH = a.OH / 2;
+    const int nb = (PH + 13) / 14;
+    const int BP = a.pool3s2 ? (PH + nb - 1) / nb : 0;
+    const int tiles = a.pool3s2 ? a.N * ((PH + BP - 1) / BP) : a.N * a.OH;
     const int grid = std::min(tiles, num_sms());
     const int slot = (a.SC * a.kh * nbw * 4 + 1023) / 1024 * 1024;
     const int nh = std::min(SR_NH_MAX, (SR_SMEM - 1024 - OFF_HALO) / slot);
-    stem_row_kernel<<<grid, SR_THREADS, SR_SMEM, s>>>(a, tx, tw, to, nbw, delta, slot, nh);
+    stem_row_kernel<<<grid, SR_THREADS, SR_SMEM, s>>>(a, tx, tw, to, nbw, delta, slot, nh, BP);
     SOL_CUDA(cudaGetLastError());
 }
 

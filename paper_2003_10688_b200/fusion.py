@@ -127,3 +127,49 @@ def fuse_bottleneck_tails(g: ModelGraph, units: List[ExecUnit], block: int = 64)
         repl[j] = ExecUnit("dnn", node_ids, v.output, inputs, params)
         drop.add(i)
     return [repl.get(j, w) for j, w in enumerate(units) if j not in drop]
+
+
+def fuse_stem_pool(g: ModelGraph, units: List[ExecUnit], direct_inputs) -> List[ExecUnit]:
+    """Merges the stride-2 stem conv (reading a canonical NCHW graph input, see
+    frontend._direct_stem_inputs) with its single consumer DFP unit
+    [BatchNorm2d(inference)] [-> ReLU] -> MaxPool2d(3x3, stride 2, pad 1) into ONE heavy unit
+    [Conv2d, BN, (ReLU), MaxPool2d]: the stem kernel (stem_row.cu) folds the BN into its epilogue and
+    max-pools its own output rows in shared memory, so the full-resolution activation (4x the pooled
+    tensor) is never written or re-read. MaxPool2d's min_init (0 after the relu-into-pool pass,
+    passes.cpp:76-102) is the pool's initial value, as in the reference lowering."""
+    cons = g.consumers()
+    outputs = set(g.outputs)
+    owner = {nid: i for i, u in enumerate(units) for nid in u.node_ids}
+    drop, repl = set(), {}
+    for i, u in enumerate(units):
+        if u.kind != "dnn" or _ops(g, u) != ["Conv2d"]:
+            continue
+        conv = g.find_node(u.node_ids[0])
+        a = conv.attrs
+        if conv.inputs[0] not in direct_inputs or a.sh != 2 or a.sw != 2 or a.kw > 8 or a.groups > 1:
+            continue
+        _, cout, oh, ow = g.meta_of(conv.id).shape
+        if cout != 64 or oh % 2 or ow % 2 or ow > 124 or u.output in outputs:
+            continue
+        c = cons.get(u.output, [])
+        if len(c) != 1:
+            continue
+        j = owner[c[0]]
+        v = units[j]
+        ops = _ops(g, v)
+        if v.kind != "dfp" or v.node_ids[0] != c[0] or ops not in (["BatchNorm2d", "MaxPool2d"],
+                                                                   ["BatchNorm2d", "ReLU", "MaxPool2d"]):
+            continue
+        nodes = [g.find_node(n) for n in v.node_ids]
+        if nodes[0].attrs.training or nodes[0].inputs[0] != u.output:
+            continue
+        if any(nodes[k].inputs[0] != nodes[k - 1].id for k in range(1, len(nodes))):
+            continue
+        p = nodes[-1].attrs
+        if (p.kh, p.kw, p.sh, p.sw, p.ph, p.pw) != (3, 3, 2, 2, 1, 1):
+            continue
+        inputs = list(u.inputs) + [x for x in v.inputs if x != u.output and x not in u.inputs]
+        params = list(u.params) + [q for q in v.params if q not in u.params]
+        repl[j] = ExecUnit("dnn", list(u.node_ids) + list(v.node_ids), v.output, inputs, params)
+        drop.add(i)
+    return [repl.get(j, w) for j, w in enumerate(units) if j not in drop]
