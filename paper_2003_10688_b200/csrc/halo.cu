@@ -28,7 +28,7 @@ namespace {
 using namespace tc;
 using T_BF16 = __nv_bfloat16;
 
-constexpr int HL_THREADS = 288;  // 4 producer warps (halo cp.async), MMA warp, 4 epilogue warps
+constexpr int HL_THREADS = 416;  // 4 producer warps (1 active), MMA warp, 8 epilogue warps
 constexpr int HL_HALO_MAX = 49152;  // bytes of one halo buffer (all channel blocks)
 
 __device__ __forceinline__ void tma_load_4d_tile(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         }
         for (int s = 0; s < NA; ++s) {
             mbar_init(smem_u32(&tfull[s]), 1);
-            mbar_init(smem_u32(&tempty[s]), 128);
+            mbar_init(smem_u32(&tempty[s]), 256);
         }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&bfull[s]), 1);
@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         }
     } else {
         // ---------------------------------------------------------------- epilogue
+        // two warps per TMEM lane quarter, each taking half of the tile's columns
         const int q = warp & 3;
+        const int half = (warp - 5) >> 2;
         const bool has_bias = a.bias != nullptr, has_fold = a.ep_scale != nullptr, has_res = a.residual != nullptr;
         const int act = a.relu ? 1 : a.act;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
             if ((a.dbg & 64) && blockIdx.x == 0 && q == 0 && lane == 0 && j < 64)
                 reinterpret_cast<long long*>(a.out)[128 + j] = clock64();
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = half * 32; c0 < BN; c0 += 64) {
                 uint32_t v[32];
                 tmem_ld32_nowait(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN + c0), v);
                 tmem_wait_ld();

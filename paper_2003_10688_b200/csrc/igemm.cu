@@ -1096,7 +1096,11 @@ int igemm_block_n(int nout) {
     return 256;
 }
 
-void igemm_launch(const IgemmArgs& a, cudaStream_t s) {
+void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
+    // profiling only: SOL_CONV_DBG ORs debug flags into every plan conv (1 = skip stores, 2 = skip MMA)
+    static const int env_dbg = std::getenv("SOL_CONV_DBG") ? std::atoi(std::getenv("SOL_CONV_DBG")) : 0;
+    IgemmArgs a = a_in;
+    a.dbg |= env_dbg;
     const int vec = a.dtype == DT_BF16 ? 8 : 4;
     const int bk = a.dtype == DT_BF16 ? 64 : 32;
     if (a.SC % vec != 0) throw std::invalid_argument("igemm: channel count must be a multiple of 16 bytes");

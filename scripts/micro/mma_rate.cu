@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out)
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     uint8_t* A = smem;               // 128 rows x 128 B (mode 14: 232-row halo)
-    uint8_t* B = smem + (AMODE == 14 ? 30720 : 16384);  // N rows x 128 B (x2 for AMODE 2, x9 for 14)
+    uint8_t* B = smem + (AMODE >= 30 ? 148480 : (AMODE == 14 ? 30720 : 16384));  // N rows x 128 B (x2 for AMODE 2, x9 for 14)
     __shared__ uint64_t bar, bar2, tfull[4], tempty[4];
     __shared__ uint32_t slot;
     if (AMODE == 21) {  // NaN / denormal operands
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out)
     tc_fence_after();
     const uint32_t tmem = slot;
     constexpr uint32_t IDESC = make_idesc(1, N, 128, 0, 0);
-    if (AMODE == 23 && threadIdx.x < 32) {
+    if ((AMODE == 23 || AMODE >= 30) && threadIdx.x < 32) {
         const uint64_t ad = sw128_desc(smem_u32(A), 16, 1024);
         const uint64_t bd = sw128_desc(smem_u32(B), 16, 1024);
         const long long t0 = clock64();
@@ -72,8 +72,11 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out)
         for (int it = 0; it < iters / 9; ++it) {
             mbar_wait(smem_u32(&tempty[acc]), aph ^ 1);
             tc_fence_after();
+            // 30: A rotates over 5 buffers; 31: + a second commit per tile; 32: both
+            const uint32_t hb_off = (AMODE == 30 || AMODE == 32) ? static_cast<uint32_t>((it % 5) * (29696 >> 4)) : 0u;
             for (int dkh = 0; dkh < 3; ++dkh)
-                mma_row3_elect<N * 8>(tmem + acc * N, ad + dkh * 58 * 8, bd + dkh * 3 * N * 8, IDESC, dkh);
+                mma_row3_elect<N * 8>(tmem + acc * N, ad + hb_off + dkh * 58 * 8, bd + dkh * 3 * N * 8, IDESC, dkh);
+            if (AMODE == 31 || AMODE == 32) mma_commit_elect(smem_u32(&bar2));
             mma_commit_elect(smem_u32(&tfull[acc]));
             if (++acc == 4) { acc = 0; aph ^= 1; }
         }
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out)
             if (blockIdx.x == 0) out[0] = t1 - t0;
         }
         __syncwarp();
-    } else if (AMODE == 23 && threadIdx.x >= 128 && threadIdx.x < 256) {
+    } else if ((AMODE == 23 || AMODE >= 30) && threadIdx.x >= 128 && threadIdx.x < 256) {
         const int q = (threadIdx.x / 32) & 3;
         int acc = 0;
         uint32_t aph = 0;
@@ -255,24 +258,24 @@ template <int N, int AMODE, bool MISALIGN = true, bool RANDOM = false>
 void run(const char* name) {
     long long* d;
     cudaMalloc(&d, 32);
-    const int smem = (AMODE == 19 || AMODE == 20) ? 225 * 1024 : 30720 + 9 * N * 128 + 2048;
+    const int smem = (AMODE == 19 || AMODE == 20 || AMODE >= 30) ? 225 * 1024 : 30720 + 9 * N * 128 + 2048;
     cudaFuncSetAttribute(rate_kernel<N, AMODE, MISALIGN, RANDOM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 4096;
     long long three = 3;
     cudaMemcpy(d + 2, &three, 8, cudaMemcpyHostToDevice);
-    rate_kernel<N, AMODE, MISALIGN, RANDOM><<<148, AMODE == 20 || AMODE == 23 ? 288 : 128, smem>>>(18, d);
+    rate_kernel<N, AMODE, MISALIGN, RANDOM><<<148, AMODE == 20 || AMODE == 23 || AMODE >= 30 ? 288 : 128, smem>>>(18, d);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    rate_kernel<N, AMODE, MISALIGN, RANDOM><<<148, AMODE == 20 || AMODE == 23 ? 288 : 128, smem>>>(iters, d);
+    rate_kernel<N, AMODE, MISALIGN, RANDOM><<<148, AMODE == 20 || AMODE == 23 || AMODE >= 30 ? 288 : 128, smem>>>(iters, d);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     long long cyc;
     cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-    const double mmas = AMODE == 14 || (AMODE >= 18 && AMODE <= 23) ? (iters / 9) * 36.0 : iters * 4.0 * (AMODE == 2 ? 2 : 1);
+    const double mmas = AMODE == 14 || (AMODE >= 18 && AMODE <= 23) || AMODE >= 30 ? (iters / 9) * 36.0 : iters * 4.0 * (AMODE == 2 ? 2 : 1);
     const double flops = 148.0 * mmas * 2.0 * 128 * N * 16;
     printf("%-22s N=%3d: %7.1f cycles/MMA  %7.1f TF/s  (%s)\n", name, N, cyc / mmas, flops / (ms * 1e-3) / 1e12,
            cudaGetErrorString(err));
@@ -282,6 +285,9 @@ void run(const char* name) {
 int main() {
     run<64, 18>("halo-like runtime bounds");
     run<64, 23>("tile protocol + epilogue");
+    run<64, 30>("protocol, A over 5 bufs");
+    run<64, 31>("protocol, 2 commits");
+    run<64, 32>("protocol, 5 bufs + 2 commits");
     run<128, 23>("tile protocol + epilogue");
     run<64, 22>("warp-converged elect x4");
     run<128, 22>("warp-converged elect x4");
