@@ -140,7 +140,8 @@ def test_conv_wgrad(gpu, case, dt):
     assert err <= 1e-2, err
 
 
-@pytest.mark.parametrize("case", [(3, 64, 56, 56, 64), (2, 64, 13, 29, 64), (2, 64, 14, 14, 40)])
+@pytest.mark.parametrize("case", [(3, 64, 56, 56, 64), (2, 64, 13, 29, 64), (2, 64, 14, 14, 40),
+                                  (2, 128, 28, 28, 128), (2, 128, 13, 29, 96)])
 def test_halo_conv_matches_im2col(gpu, case):
     """The row-padded halo-tile conv (halo.cu) accumulates the same k-blocks in the same order
     as the TMA-im2col kernel, so the two outputs are bit-identical (conv debug flag 512 turns the
