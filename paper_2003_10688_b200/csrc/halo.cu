@@ -31,6 +31,7 @@ using T_BF16 = __nv_bfloat16;
 
 constexpr int HL_THREADS = 416;  // 4 producer warps (1 active), MMA warp, 8 epilogue warps
 constexpr int HL_HALO_MAX = 49152;  // bytes of one halo buffer (all channel blocks)
+constexpr int HL_PCACHE = 512;      // channels of cached epilogue parameters (3 x 2 KB after the barriers)
 
 __device__ __forceinline__ void tma_load_4d_tile(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
                                                  uint32_t mbar) {
@@ -59,7 +60,7 @@ __host__ __device__ inline HaloGeo halo_geo(const IgemmArgs& a) {
 
 template <int BN>
 constexpr int hl_stages() {
-    return std::min(12, (227 * 1024 - 2 * HL_HALO_MAX - 2048) / (BN * 128));
+    return std::min(12, (227 * 1024 - 2 * HL_HALO_MAX - 2048 - 12 * HL_PCACHE) / (BN * 128));
 }
 
 // RESB: the whole weight matrix of the (single) N tile stays resident in shared memory, loaded
@@ -271,6 +272,20 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         const __nv_bfloat16* res = static_cast<const __nv_bfloat16*>(a.residual);
         int acc = 0;
         uint32_t acc_phase = 0;
+        // per-channel epilogue parameters cached in shared memory once per CTA (warp-uniform reads
+        // are broadcasts; the global loads' latency sat on every tile's critical path)
+        float* p_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + 1024);
+        float* p_scale = p_bias + HL_PCACHE;
+        float* p_shift = p_scale + HL_PCACHE;
+        const bool cached = a.Nout <= HL_PCACHE;
+        if (cached) {
+            for (int c = tid - 160; c < a.Nout; c += 256) {
+                p_bias[c] = has_bias ? a.bias[c] : 0.f;
+                p_scale[c] = has_fold ? a.ep_scale[c] : 1.f;
+                p_shift[c] = has_fold ? a.ep_shift[c] : 0.f;
+            }
+            asm volatile("bar.sync 3, 256;\n" ::: "memory");
+        }
         const int i = q * 32 + lane;  // tile row (row-padded pixel order)
         const int oyl = i / G.Wp, ox = i - (i / G.Wp) * G.Wp;
         for (int j = 0; j < t_end - t_begin; ++j) {
@@ -299,7 +314,13 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                 // every loop is unrolled so f[] stays in registers (a dynamic index would put it in
                 // local memory); full chunks use float4 parameter loads (the addresses are warp-uniform)
                 if (has_bias) {
-                    if (full) {
+                    if (full && cached) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 bb = *reinterpret_cast<const float4*>(p_bias + n + j);
+                            f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+                        }
+                    } else if (full) {
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
                             const float4 bb = __ldg(reinterpret_cast<const float4*>(a.bias + n + j));
@@ -312,7 +333,17 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                     }
                 }
                 if (has_fold) {
-                    if (full) {
+                    if (full && cached) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 sc = *reinterpret_cast<const float4*>(p_scale + n + j);
+                            const float4 sh = *reinterpret_cast<const float4*>(p_shift + n + j);
+                            f[j] = fmaf(f[j], sc.x, sh.x);
+                            f[j + 1] = fmaf(f[j + 1], sc.y, sh.y);
+                            f[j + 2] = fmaf(f[j + 2], sc.z, sh.z);
+                            f[j + 3] = fmaf(f[j + 3], sc.w, sh.w);
+                        }
+                    } else if (full) {
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
                             const float4 sc = __ldg(reinterpret_cast<const float4*>(a.ep_scale + n + j));
@@ -401,8 +432,8 @@ template <int BN, bool RESB>
 void halo_launch_t(const IgemmArgs& a, cudaStream_t s) {
     const HaloGeo G = halo_geo(a);
     const int bbytes = (RESB ? a.kh * a.kw * G.ncb : hl_stages<BN>()) * BN * 128;
-    const int nh = std::max(2, std::min(HL_NH_MAX, (227 * 1024 - bbytes - 2048) / G.halo_bytes));
-    const int smem = nh * G.halo_bytes + bbytes + 1024 + 1024;
+    const int nh = std::max(2, std::min(HL_NH_MAX, (227 * 1024 - bbytes - 2048 - 12 * HL_PCACHE) / G.halo_bytes));
+    const int smem = nh * G.halo_bytes + bbytes + 1024 + 1024 + 12 * HL_PCACHE;
     static std::once_flag once;
     std::call_once(once, [] {
         SOL_CUDA(cudaFuncSetAttribute(halo_kernel<BN, RESB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
