@@ -211,7 +211,14 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                 uint32_t aoff = 0;  // (dkh * Wp + dkw) * 128 B, in 16-byte units
                 uint32_t boff = 0;
                 uint32_t accum = 0;
-                if (RESB && a.kw == 3 && (G.ncb == 1 || G.ncb == 2)) {
+                if (RESB && a.kh == 3 && a.kw == 3 && G.ncb == 1 && G.Wp == 58 && do_mma) {
+                    // ResNet-50 layer 1 (56x56): row pitch known at compile time, so every
+                    // descriptor is base + immediate and stays in uniform registers
+                    constexpr uint32_t WP8 = 58 * 8, BU = B_BYTES >> 4;
+                    mma_row3_elect<BU>(dcol, adesc0, bdesc0, IDESC, 0);
+                    mma_row3_elect<BU>(dcol, adesc0 + WP8, bdesc0 + 3 * BU, IDESC, 1);
+                    mma_row3_elect<BU>(dcol, adesc0 + 2 * WP8, bdesc0 + 6 * BU, IDESC, 1);
+                } else if (RESB && a.kw == 3 && (G.ncb == 1 || G.ncb == 2)) {
                     // 3x3 fast path: one asm statement per (channel block, filter row)
                     for (int cb = 0; cb < G.ncb; ++cb) {
                         for (int dkh = 0; dkh < a.kh; ++dkh) {

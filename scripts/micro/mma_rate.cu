@@ -74,6 +74,14 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out)
             tc_fence_after();
             // 30: A rotates over 5 buffers; 31: + a second commit per tile; 32: both
             const uint32_t hb_off = (AMODE == 30 || AMODE == 32) ? static_cast<uint32_t>((it % 5) * (29696 >> 4)) : 0u;
+            if (AMODE == 33) {
+                // halo-like codegen: runtime row count / row pitch, per-tile buffer from a runtime index
+                const int kk = static_cast<int>(out[2]);
+                const uint32_t wp8 = static_cast<uint32_t>(out[2]) * 19u + 1u;  // 58 at runtime
+                const uint64_t a0 = ad + static_cast<uint32_t>((it % 5) * (29696 >> 4));
+                for (int dkh = 0; dkh < kk; ++dkh)
+                    mma_row3_elect<N * 8>(tmem + acc * N, a0 + dkh * wp8 * 8, bd + dkh * 3 * N * 8, IDESC, dkh);
+            } else
             for (int dkh = 0; dkh < 3; ++dkh)
                 mma_row3_elect<N * 8>(tmem + acc * N, ad + hb_off + dkh * 58 * 8, bd + dkh * 3 * N * 8, IDESC, dkh);
             if (AMODE == 31 || AMODE == 32) mma_commit_elect(smem_u32(&bar2));
@@ -285,6 +293,8 @@ void run(const char* name) {
 int main() {
     run<64, 18>("halo-like runtime bounds");
     run<64, 23>("tile protocol + epilogue");
+    run<64, 33>("protocol, runtime bounds/base");
+    run<128, 33>("protocol, runtime bounds/base");
     run<64, 30>("protocol, A over 5 bufs");
     run<64, 31>("protocol, 2 commits");
     run<64, 32>("protocol, 5 bufs + 2 commits");
