@@ -789,7 +789,11 @@ void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
             // N tiles of at most 128 (TMEM 2 x 128 columns): with 256-wide tiles (the whole TMEM)
             // the dual GEMM stalled intermittently (~1 in 10^3 full-size launches); at 128 it ran
             // clean through 8k ResNet-50 steps and 80k single-block launches
-            if (a.Nout > 128 && std::getenv("SOL_DUAL_BN256")) return launch_ws_t<T, TO, 256, IG_DUAL>(a, s);
+            // 256-wide single-accumulator tiles halve the A re-reads of the wide (N >= 1024)
+            // stride-2 tails (ResNet-50 l3.0 / l4.0: -8 us each); SOL_DUAL_BN256=0/1 forces off/on
+            static const char* bn256_env = std::getenv("SOL_DUAL_BN256");
+            const bool bn256 = bn256_env ? bn256_env[0] == '1' : a.Nout >= 1024;
+            if (a.Nout > 128 && bn256) return launch_ws_t<T, TO, 256, IG_DUAL>(a, s);
             if (a.Nout > 64) return launch_ws_t<T, TO, 128, IG_DUAL>(a, s);
             return dispatch_ws<T, TO, IG_DUAL>(a, s);
         }
