@@ -131,6 +131,8 @@ typedef struct {
     int64_t launches;     /* kernels launched per run */
     double algo_bytes;    /* algorithmic HBM bytes per run (inputs + output, roofline) */
     double algo_flops;    /* algorithmic FLOPs per run (GEMMs) */
+    int64_t launches_frozen; /* kernels per run once the plan is frozen (weight packing / BN folding
+                                cached: inference) */
 } sol_module_info;
 
 /* rt::TransferStats (include/sol/runtime.hpp:72-82) */

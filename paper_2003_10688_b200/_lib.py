@@ -75,7 +75,8 @@ class UnitDesc(C.Structure):
 
 class ModuleInfo(C.Structure):
     _fields_ = [("family", C.c_char * 32), ("n_args", C.c_int32), ("scratch_bytes", C.c_uint64),
-                ("launches", C.c_int64), ("algo_bytes", C.c_double), ("algo_flops", C.c_double)]
+                ("launches", C.c_int64), ("algo_bytes", C.c_double), ("algo_flops", C.c_double),
+                ("launches_frozen", C.c_int64)]
 
 
 class TransferStats(C.Structure):

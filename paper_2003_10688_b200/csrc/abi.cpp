@@ -120,6 +120,7 @@ static void fill_info(const solb200::Module* m, sol_module_info* info) {
     info->n_args = m->n_args;
     info->scratch_bytes = m->scratch_bytes();
     info->launches = m->launches;
+    info->launches_frozen = m->launches_frozen >= 0 ? m->launches_frozen : m->launches;
     info->algo_bytes = m->algo_bytes;
     info->algo_flops = m->algo_flops;
 }

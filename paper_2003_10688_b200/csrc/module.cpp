@@ -157,6 +157,7 @@ public:
         algo_bytes = (in1_.pixels() * in1_.ld + double(out_.pixels()) * in2_.ld + out_.pixels() * out_.ld) * 2.0 +
                      double(cout_) * (in1_.C + in2_.C) * 2.0;
         launches = 2;
+        launches_frozen = 1;  // the weight fold is cached once the plan is frozen
     }
     void run(void* const* args, int nargs, void*, cudaStream_t s, bool frozen) override {
         if (nargs != n_args) throw std::invalid_argument("dual conv: wrong argument count");
@@ -263,6 +264,7 @@ public:
                 algo_bytes = (in_.pixels() * in_.ld + out_.pixels() * out_.ld) * double(elem_size(dtype_)) +
                              double(cout_) * cin_ * kh_ * kw_ * elem_size(dtype_);
                 launches = 2;
+                launches_frozen = 1;  // packed weights (and folded BN) cached in a frozen plan
                 break;
             }
             case SOL_OP_CONV2DBACKX:
@@ -1400,7 +1402,11 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
         if (!d.bindings[i].is_param) bytes += binding_bytes(d.bindings[i]);
     algo_bytes = bytes;
     launches = 1;
-    for (auto& b : bn_) launches += b.training ? 3 : 1;
+    launches_frozen = 1;  // frozen: inference BN coefficients and depthwise packs are cached
+    for (auto& b : bn_) {
+        launches += b.training ? 3 : 1;
+        if (b.training) launches_frozen += 3;
+    }
     launches += static_cast<int>(dw_.size());
 }
 

@@ -31,6 +31,7 @@ public:
     std::string family;
     int n_args = 0;
     int launches = 1;
+    int launches_frozen = -1;  // per run in a frozen plan (-1: same as launches)
     double algo_bytes = 0.0;
     double algo_flops = 0.0;
     std::vector<size_t> arg_bytes;  // minimum bytes each arg must span (queue bounds checks)

@@ -85,6 +85,11 @@ class UnitModule:
     algo_bytes: float
     algo_flops: float
     launches: int
+    launches_frozen: int = -1  # -1: same as launches
+
+    def __post_init__(self):
+        if self.launches_frozen < 0:
+            self.launches_frozen = self.launches
 
     def info(self):
         return dict(family=self.family, algo_bytes=self.algo_bytes, algo_flops=self.algo_flops)
@@ -159,7 +164,7 @@ def create_module(g: ModelGraph, unit: ExecUnit, dtype: int, nchw_inputs=()) -> 
     info = L.ModuleInfo()
     L.check(L.lib().sol_b200_module_info(h, C.byref(info)))
     return UnitModule(h, info.family.decode(), info.n_args, info.scratch_bytes, info.algo_bytes,
-                      info.algo_flops, info.launches)
+                      info.algo_flops, info.launches, info.launches_frozen)
 
 
 def reorder_module(meta: Meta, dtype: int, inbound: bool) -> UnitModule:
@@ -191,7 +196,7 @@ def reorder_module(meta: Meta, dtype: int, inbound: bool) -> UnitModule:
     info = L.ModuleInfo()
     L.check(L.lib().sol_b200_module_info(h, C.byref(info)))
     return UnitModule(h, info.family.decode(), info.n_args, info.scratch_bytes, info.algo_bytes,
-                      info.algo_flops, info.launches)
+                      info.algo_flops, info.launches, info.launches_frozen)
 
 
 def sgd_multi_module(shapes, lr: float, dtype: int) -> UnitModule:
@@ -225,7 +230,7 @@ def sgd_multi_module(shapes, lr: float, dtype: int) -> UnitModule:
     info = L.ModuleInfo()
     L.check(L.lib().sol_b200_module_info(h, C.byref(info)))
     return UnitModule(h, info.family.decode(), info.n_args, info.scratch_bytes, info.algo_bytes,
-                      info.algo_flops, info.launches)
+                      info.algo_flops, info.launches, info.launches_frozen)
 
 
 def sgd_module(shape, lr: float, dtype: int) -> UnitModule:
@@ -256,4 +261,4 @@ def sgd_module(shape, lr: float, dtype: int) -> UnitModule:
     info = L.ModuleInfo()
     L.check(L.lib().sol_b200_module_info(h, C.byref(info)))
     return UnitModule(h, info.family.decode(), info.n_args, info.scratch_bytes, info.algo_bytes,
-                      info.algo_flops, info.launches)
+                      info.algo_flops, info.launches, info.launches_frozen)

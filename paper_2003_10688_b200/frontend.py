@@ -58,6 +58,7 @@ class StepInfo:
     algo_bytes: float = 0.0
     algo_flops: float = 0.0
     launches: int = 1
+    launches_frozen: int = 1  # once the plan is frozen (inference: cached weight packing)
     node_ids: List[str] = field(default_factory=list)
 
 
@@ -139,6 +140,7 @@ class OptimizedModel:
             L.check(lib.sol_b200_plan_add_step(self.plan, mod.handle, arr, len(ids)))
             info.family = mod.family
             info.algo_bytes, info.algo_flops, info.launches = mod.algo_bytes, mod.algo_flops, mod.launches
+            info.launches_frozen = getattr(mod, "launches_frozen", mod.launches)
             self.steps.append(info)
 
         # parameters: persistent f32 master copies
