@@ -328,6 +328,9 @@ Plan::~Plan() {
         if (kv.second.consumed) cudaEventDestroy(kv.second.consumed);
     }
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
+    if (comm_stream_) cudaStreamSynchronize(comm_stream_);
+    for (cudaEvent_t e : ar_events_) cudaEventDestroy(e);
+    if (comm_stream_) cudaStreamDestroy(comm_stream_);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     steps_.clear();
     if (base_) cudaFree(base_);
@@ -456,7 +459,31 @@ void Plan::run_step(Step& s, cudaStream_t st) {
 
 void Plan::run_steps(cudaStream_t st) {
     static const bool sync_steps = std::getenv("SOL_SYNC_STEPS") != nullptr;  // hang bisection (eager)
+    // all-reduce groups go to the comm stream; the plan stream joins it before the first module step
+    // after the last group (the optimizer reads the reduced gradients)
+    size_t last_ar = steps_.size();
+    for (size_t i = 0; i < steps_.size(); ++i)
+        if (!steps_[i].module) last_ar = i;
+    const bool overlap = comm_ && last_ar < steps_.size() && !sync_steps;
+    int n_groups = 0;
+    if (overlap) {
+        if (!comm_stream_) SOL_CUDA(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+        for (size_t i = 0; i < steps_.size(); ++i)
+            if (!steps_[i].module && (i == 0 || steps_[i - 1].module)) ++n_groups;
+        while (static_cast<int>(ar_events_.size()) < n_groups + 1) {
+            cudaEvent_t e;
+            SOL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ar_events_.push_back(e);
+        }
+    }
+    int group = 0;
+    bool joined = !overlap;
     for (size_t i = 0; i < steps_.size();) {
+        if (!joined && i > last_ar && steps_[i].module) {
+            SOL_CUDA(cudaEventRecord(ar_events_[n_groups], comm_stream_));
+            SOL_CUDA(cudaStreamWaitEvent(st, ar_events_[n_groups], 0));
+            joined = true;
+        }
         if (steps_[i].module || !comm_) {
             if (sync_steps && steps_[i].module) {
                 std::fprintf(stderr, "[sol] step %zu %s\n", i, steps_[i].module->family.c_str());
@@ -470,13 +497,20 @@ void Plan::run_steps(cudaStream_t st) {
         // a run of gradient all-reduces: one NCCL group (aggregated launches); the 1/G mean is
         // ncclAvg when the scale is exactly the replica count, else a scale kernel afterwards
         size_t j = i;
+        cudaStream_t cs = st;
+        if (overlap) {
+            SOL_CUDA(cudaEventRecord(ar_events_[group], st));
+            SOL_CUDA(cudaStreamWaitEvent(comm_stream_, ar_events_[group], 0));
+            cs = comm_stream_;
+            ++group;
+        }
         nccl_check(ncclGroupStart(), "group");
         for (; j < steps_.size() && !steps_[j].module; ++j) {
             Step& s = steps_[j];
             void* buf = base_ + bufs_[s.ar_id].off;
             const bool avg = s.ar_scale == 1.f / static_cast<float>(nranks_);
             nccl_check(ncclAllReduce(buf, buf, s.ar_count, s.ar_dtype == DT_BF16 ? ncclBfloat16 : ncclFloat32,
-                                     avg ? ncclAvg : ncclSum, static_cast<ncclComm_t>(comm_), st),
+                                     avg ? ncclAvg : ncclSum, static_cast<ncclComm_t>(comm_), cs),
                        "allreduce");
         }
         nccl_check(ncclGroupEnd(), "group");
@@ -485,11 +519,15 @@ void Plan::run_steps(cudaStream_t st) {
             if (s.ar_scale == 1.f || s.ar_scale == 1.f / static_cast<float>(nranks_)) continue;
             void* buf = base_ + bufs_[s.ar_id].off;
             const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ceil_div(s.ar_count, 256), 4096));
-            if (s.ar_dtype == DT_BF16) scale_bf16_kernel<<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(buf), s.ar_count, s.ar_scale);
-            else scale_kernel<<<grid, 256, 0, st>>>(static_cast<float*>(buf), s.ar_count, s.ar_scale);
+            if (s.ar_dtype == DT_BF16) scale_bf16_kernel<<<grid, 256, 0, cs>>>(static_cast<__nv_bfloat16*>(buf), s.ar_count, s.ar_scale);
+            else scale_kernel<<<grid, 256, 0, cs>>>(static_cast<float*>(buf), s.ar_count, s.ar_scale);
             SOL_CUDA(cudaGetLastError());
         }
         i = j;
+    }
+    if (!joined) {  // plan ends with an all-reduce group
+        SOL_CUDA(cudaEventRecord(ar_events_[n_groups], comm_stream_));
+        SOL_CUDA(cudaStreamWaitEvent(st, ar_events_[n_groups], 0));
     }
 }
 

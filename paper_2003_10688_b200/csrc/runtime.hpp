@@ -159,6 +159,11 @@ private:
     int nranks_ = 1;
     cudaEvent_t events_[16] = {};
     cudaStream_t copy_stream_ = nullptr;
+    // gradient all-reduce buckets run on comm_stream_, overlapped with the rest of the backward
+    // pass: fork (event on the plan stream) before each bucket, join before the first module step
+    // after the last bucket
+    cudaStream_t comm_stream_ = nullptr;
+    std::vector<cudaEvent_t> ar_events_;
     std::map<int, Staged> staged_;
 };
 

@@ -175,6 +175,38 @@ class OptimizedModel:
                                          name in outputs or o.keep_all)
             return self.buf[name]
 
+        # gradient all-reduce buckets: a bucket is issued right after the unit that
+        # completes its last gradient, so NCCL (on the plan's comm stream) overlaps the remaining
+        # backward units; ~25 MB buckets (SOL_AR_BUCKET_MB)
+        reduce_grads = o.train and (o.world_size > 1 or o.nccl_allreduce)
+        grad_of = {gname: pname for pname, gname in self.param_grads} if reduce_grads else {}
+        bucket_limit = float(os.environ.get("SOL_AR_BUCKET_MB", "25")) * 2 ** 20
+        pending, pending_bytes = [], 0.0
+        self.ar_buckets = 0
+
+        def flush_bucket():
+            nonlocal pending, pending_bytes
+            if not pending:
+                return
+            for gname in pending:
+                n = self.params[grad_of[gname]].size
+                L.check(lib.sol_b200_plan_add_allreduce(self.plan, self.buf[gname], n, L.DT_F32, 1.0 / o.world_size))
+                self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname, algo_bytes=4.0 * n))
+            self.ar_buckets += 1
+            pending, pending_bytes = [], 0.0
+
+        reduced = set()
+
+        def grads_done(names):
+            nonlocal pending_bytes
+            for nme in names:
+                if nme in grad_of and nme not in reduced:
+                    reduced.add(nme)
+                    pending.append(nme)
+                    pending_bytes += 4.0 * self.params[grad_of[nme]].size
+            if pending_bytes >= bucket_limit:
+                flush_bucket()
+
         for u in self.units:
             out_buf(u.output)
             if u.output in absorbed:
@@ -193,6 +225,9 @@ class OptimizedModel:
                 mod.n_args += bin(mask).count("1")
                 ids += [out_buf(x) for x in (gam, bet) if x]
             add_step(mod, ids, StepInfo("unit", "", u.output, node_ids=list(u.node_ids)))
+            grads_done([u.output] + [x for x in siblings.get(u.output, ()) if x])
+        grads_done([gn for gn in grad_of if gn not in reduced])  # (none expected) after every unit
+        flush_bucket()
         # graph outputs: canonical f32 copies for the host
         self.out_canon: Dict[str, int] = {}
         for name in g.outputs:
@@ -205,12 +240,6 @@ class OptimizedModel:
                      StepInfo("reorder", "", name))
         # native training: all-reduce gradients across ranks, then SGD on the device
         if o.train:
-            for pname, gname in self.param_grads:
-                if o.world_size > 1 or o.nccl_allreduce:
-                    L.check(lib.sol_b200_plan_add_allreduce(self.plan, self.buf[gname], self.params[pname].size,
-                                                            L.DT_F32, 1.0 / o.world_size))
-                    self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname,
-                                               algo_bytes=4.0 * self.params[pname].size))
             if o.multi_sgd and self.param_grads:
                 for k in range(0, len(self.param_grads), 512):
                     chunk = self.param_grads[k:k + 512]

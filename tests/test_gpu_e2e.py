@@ -193,11 +193,15 @@ def test_bottleneck_dual_gemm(gpu, stride, conv_bias):
     assert O.oracle_err(got, ref) <= 1e-2
 
 
-def test_nccl_allreduce_plumbing_single_rank(gpu):
-    """The data-parallel training plan (grouped NCCL all-reduce of every gradient, ncclAvg, inside
-    the captured CUDA graph) run with one replica: must reproduce the plain plan bit for bit.
+@pytest.mark.parametrize("bucket_mb", ["25", "0.02"])
+def test_nccl_allreduce_plumbing_single_rank(gpu, monkeypatch, bucket_mb):
+    """The data-parallel training plan (NCCL all-reduce of every gradient in ~bucket_mb buckets,
+    ncclAvg, each bucket issued on the comm stream right after the unit completing its last
+    gradient so it overlaps the rest of the backward pass, joined before SGD; all inside the
+    captured CUDA graph) run with one replica: must reproduce the plain plan bit for bit.
     (Multi-replica runs need one process per GPU; this box has one GPU.)"""
     from paper_2003_10688_b200 import frontend, graph, models
+    monkeypatch.setenv("SOL_AR_BUCKET_MB", bucket_mb)
     batch = 8
     g = models.resnet(18, hw=32, classes=16, width=16, train=True)
     ins = _inputs(graph.infer_shapes(g, batch), batch, seed=4)
@@ -205,6 +209,11 @@ def test_nccl_allreduce_plumbing_single_rank(gpu):
     for force in (False, True):
         m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype="bf16", train=True, lr=0.01,
                                                           nccl_allreduce=force))
+        if force:
+            ar = [i for i, st in enumerate(m.steps) if st.kind == "allreduce"]
+            assert len(ar) == len(m.param_grads)
+            if bucket_mb != "25":  # small buckets interleave with the backward units
+                assert m.ar_buckets > 1 and ar[0] < min(i for i, st in enumerate(m.steps) if st.kind == "sgd") - 10
         losses = [m.train_step(ins) for _ in range(3)]
         res.append((losses, m.host_params()))
     assert res[0][0] == res[1][0]
