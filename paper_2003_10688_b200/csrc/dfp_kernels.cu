@@ -1845,28 +1845,36 @@ __global__ void softmax_back_kernel(const T* __restrict__ d, const T* __restrict
 // dx = A*dy + B*xhat + Cc, xhat = ((x - mean_hi) - mean_lo) * rstd. Each thread owns one channel
 // vector (coefficients in registers) and walks pixels; U pixels of both inputs in flight.
 template <typename T>
-__global__ void __launch_bounds__(THREADS) bnback_apply_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                               int C, int64_t P, const float* __restrict__ coef,
-                                                               const float* __restrict__ xh, T* __restrict__ dx) {
+__global__ void __launch_bounds__(THREADS, 3) bnback_apply_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                                  int C, int64_t P, const float* __restrict__ coef,
+                                                                  const float* __restrict__ xh, T* __restrict__ dx) {
+    // per-channel coefficients staged in shared memory (read back per pixel as 16-byte vectors):
+    // held in registers they took 40 of the kernel's 114 and capped occupancy at 2 blocks/SM,
+    // leaving the loads latency bound
     constexpr int V = VEC<T>;
-    constexpr int U = 4;
+    constexpr int U = 2;
+    __shared__ __align__(16) float sc[5][THREADS * V];  // A, B*rstd, D, mean_hi, mean_lo per channel
     const int cv_total = C / V;
     const int cvb = min(cv_total, THREADS);
     const int rows = THREADS / cvb;
     const int row = threadIdx.x / cvb;
     const int cvi = threadIdx.x - row * cvb;
-    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
-    const int c = (blockIdx.y * cvb + cvi) * V;
-    float A[V], B[V], D[V], mh[V], ml[V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-        const float rstd = __ldg(xh + 2 * C + c + i);
-        A[i] = __ldg(coef + c + i);
-        B[i] = __ldg(coef + C + c + i) * rstd;  // B * xhat = (B * rstd) * ((x - mh) - ml)
-        D[i] = __ldg(coef + 2 * C + c + i);
-        mh[i] = __ldg(xh + c + i);
-        ml[i] = __ldg(xh + C + c + i);
+    const int cbase = blockIdx.y * cvb * V;
+    for (int i = threadIdx.x; i < cvb * V; i += THREADS) {
+        const int ch = cbase + i;
+        if (ch < C) {
+            const float rstd = __ldg(xh + 2 * C + ch);
+            sc[0][i] = __ldg(coef + ch);
+            sc[1][i] = __ldg(coef + C + ch) * rstd;  // B * xhat = (B * rstd) * ((x - mh) - ml)
+            sc[2][i] = __ldg(coef + 2 * C + ch);
+            sc[3][i] = __ldg(xh + ch);
+            sc[4][i] = __ldg(xh + C + ch);
+        }
     }
+    __syncthreads();
+    if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
+    const int c = cbase + cvi * V;
+    const int lc = cvi * V;
     const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
     for (int64_t p0 = static_cast<int64_t>(blockIdx.x) * rows + row; p0 < P; p0 += step * U) {
         uint4 rd[U], rx[U];
@@ -1886,7 +1894,8 @@ __global__ void __launch_bounds__(THREADS) bnback_apply_kernel(const T* __restri
             unpack16(rd[u], dv, static_cast<T*>(nullptr));
             unpack16(rx[u], xv, static_cast<T*>(nullptr));
 #pragma unroll
-            for (int i = 0; i < V; ++i) o[i] = fmaf(dv[i], A[i], fmaf((xv[i] - mh[i]) - ml[i], B[i], D[i]));
+            for (int i = 0; i < V; ++i)
+                o[i] = fmaf(dv[i], sc[0][lc + i], fmaf((xv[i] - sc[3][lc + i]) - sc[4][lc + i], sc[1][lc + i], sc[2][lc + i]));
             store16(dx + p * C + c, o);
         }
     }
