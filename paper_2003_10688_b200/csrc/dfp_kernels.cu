@@ -400,18 +400,60 @@ struct BnRegs {
     }
 };
 
+// BatchNorm coefficients of a block's channel range staged in shared memory (same values and
+// arithmetic as BnRegs, read back per element): keeps them out of the registers of kernels whose
+// occupancy they would cap.
+template <typename T>
+struct BnSmem {
+    static constexpr int V = VEC<T>;
+    static constexpr int NK = sizeof(T) == 2 ? 2 : 4;
+    float* k;  // [NK][n]
+    int n;
+    __device__ void stage(float* buf, int nch, const float* const* P, int b, int c0, int C) {
+        k = buf;
+        n = nch;
+        for (int i = threadIdx.x; i < nch; i += blockDim.x) {
+            const int ch = c0 + i;
+            if (ch >= C) continue;
+            if constexpr (sizeof(T) == 2) {
+                k[i] = __ldg(P[b + 2] + ch);      // scale
+                k[n + i] = __ldg(P[b + 4] + ch);  // shift
+            } else {
+                k[i] = __ldg(P[b] + ch);
+                k[n + i] = __ldg(P[b + 1] + ch);
+                k[2 * n + i] = __ldg(P[b + 2] + ch);
+                k[3 * n + i] = __ldg(P[b + 3] + ch);
+            }
+        }
+    }
+    __device__ __forceinline__ void apply(float* v, int lc) const {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            if constexpr (sizeof(T) == 2) v[i] = fmaf(v[i], k[lc + i], k[n + lc + i]);
+            else v[i] = fmaf((v[i] - k[lc + i]) - k[n + lc + i], k[2 * n + lc + i], k[3 * n + lc + i]);
+        }
+    }
+};
+
 // y = act( bn0(x0) [+ bn1(x1)] )
 template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
-__global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
+__global__ void __launch_bounds__(THREADS, 3) chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs) {
     constexpr int V = VEC<T>;
-    constexpr int U = 4;
+    constexpr int U = ADD ? 2 : 4;  // two-input chains: fewer loads per thread, 3 blocks per SM
+    constexpr int NK = sizeof(T) == 2 ? 2 : 4;
+    __shared__ __align__(16) float bn_s[(BN0 ? 1 : 0) + (BN1 ? 1 : 0) > 0 ? ((BN0 ? 1 : 0) + (BN1 ? 1 : 0)) * NK * THREADS * V : 1];
     const int cv_total = a.C / V;
     const int cvb = min(cv_total, THREADS);
     const int rows = THREADS / cvb;
     const int row = threadIdx.x / cvb;
     const int cvi = threadIdx.x - row * cvb;
+    BnSmem<T> b0, b1;
+    if (BN0) b0.stage(bn_s, cvb * V, a.P, cs.bn0, blockIdx.y * cvb * V, a.C);
+    if (BN1) b1.stage(bn_s + (BN0 ? NK * THREADS * V : 0), cvb * V, a.P, cs.bn1, blockIdx.y * cvb * V, a.C);
+    if (BN0 || BN1) __syncthreads();
     if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
     const int c = (blockIdx.y * cvb + cvi) * V;
+    const int lc = cvi * V;
     const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
     const T* x0;
     int ld0;
@@ -430,9 +472,6 @@ __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ 
     const int ld1 = ADD ? a.in_ld[cs.s1] : 0;
     T* out = static_cast<T*>(a.out) + a.out_coff + c;
     T* out2 = a.out2 ? static_cast<T*>(a.out2) + a.out_coff + c : nullptr;
-    BnRegs<T> b0, b1;
-    if (BN0) b0.load(a.P, cs.bn0, c);
-    if (BN1) b1.load(a.P, cs.bn1, c);
     const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
     for (int64_t p0 = static_cast<int64_t>(blockIdx.x) * rows + row; p0 < P; p0 += step * U) {
         uint4 r0[U], r1[U];
@@ -450,11 +489,11 @@ __global__ void __launch_bounds__(THREADS) chain_kernel(const __grid_constant__ 
             if (p >= P) break;
             float v[V];
             unpack16(r0[u], v, static_cast<T*>(nullptr));
-            if (BN0) b0.apply(v);
+            if (BN0) b0.apply(v, lc);
             if (ADD) {
                 float w[V];
                 unpack16(r1[u], w, static_cast<T*>(nullptr));
-                if (BN1) b1.apply(w);
+                if (BN1) b1.apply(w, lc);
 #pragma unroll
                 for (int i = 0; i < V; ++i) v[i] += w[i];
             }
