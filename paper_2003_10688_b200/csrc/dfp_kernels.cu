@@ -1267,7 +1267,7 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
     constexpr int V = VEC<T>;
     constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
     constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
-    constexpr int UN = NI == 2 ? 4 : 8;  // 8 16-byte loads in flight per thread
+    constexpr int UN = NI == 2 ? 6 : 12;  // 12 16-byte loads in flight per thread
     __shared__ double red[THREADS * V];
     const int cv_total = C / V;
     const int cvb = min(cv_total, THREADS);
@@ -1305,11 +1305,14 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
                     if (NI == 2) r1[u] = __ldg(reinterpret_cast<const uint4*>(x1 + p * ld1 + c));
                 }
             }
+            // bf16 plans (f32 thread accumulator) add straight into acc; f32 plans sum each group
+            // of UN pixels in f32 and fold it into the f64 accumulator
+            constexpr bool DIRECT = sizeof(T) == 2;
             float f[NS][V];
 #pragma unroll
             for (int k = 0; k < NS; ++k)
 #pragma unroll
-                for (int i = 0; i < V; ++i) f[k][i] = 0.f;
+                for (int i = 0; i < V; ++i) f[k][i] = DIRECT ? static_cast<float>(acc[k][i]) : 0.f;
 #pragma unroll
             for (int u = 0; u < UN; ++u) {
                 if (pb + static_cast<int64_t>(u) * rows >= p1) break;
@@ -1334,7 +1337,10 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
 #pragma unroll
             for (int k = 0; k < NS; ++k)
 #pragma unroll
-                for (int i = 0; i < V; ++i) acc[k][i] += static_cast<Acc>(f[k][i]);
+                for (int i = 0; i < V; ++i) {
+                    if (DIRECT) acc[k][i] = static_cast<Acc>(f[k][i]);
+                    else acc[k][i] += static_cast<Acc>(f[k][i]);
+                }
         }
     }
     // combine the pixel lanes of each channel vector: warp shuffles across the rows that share a
