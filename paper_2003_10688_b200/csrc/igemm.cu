@@ -10,6 +10,7 @@
 //   * the epilogue moves TMEM -> registers with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31,
 //     i.e. output rows), adds the bias and stores NHWC rows.
 #include "igemm.cuh"
+#include "pack.cuh"
 #include "tc.cuh"
 
 #include <algorithm>
@@ -225,6 +226,24 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc<TCOLS>(tmem_d);
+    }
+}
+
+// split-K reduction straight into the canonical layout: canonical i = ((co*Cin + ci)*KH + kh)*KW + kw
+// reads packed j = co*KH*KW*ld + (kh*KW + kw)*ld + ci of every split
+__global__ void wgrad_reduce_canon_kernel(const float* __restrict__ ws, float* __restrict__ w, int64_t n, int splits,
+                                          int Cout, int Cin, int KH, int KW, int ld) {
+    const int64_t total = static_cast<int64_t>(Cout) * Cin * KH * KW;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int kw = static_cast<int>(i % KW);
+        const int kh = static_cast<int>((i / KW) % KH);
+        const int ci = static_cast<int>((i / (KW * KH)) % Cin);
+        const int co = static_cast<int>(i / (static_cast<int64_t>(KW) * KH * Cin));
+        const int64_t j = static_cast<int64_t>(co) * KH * KW * ld + (kh * KW + kw) * ld + ci;
+        float acc = 0.f;
+        for (int sp = 0; sp < splits; ++sp) acc += __ldg(ws + sp * n + j);
+        w[i] = acc;
     }
 }
 
@@ -1166,12 +1185,21 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
             default: launch_wgrad_t<float, 128>(a, p.ncol, p.splits, p.kb_per_split, s); break;
         }
     }
-    if (p.splits > 1) {
+    if (p.splits > 1 && a.dw_canon) {
+        const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
+        const int64_t total = static_cast<int64_t>(a.Cout) * a.canon_cin * a.kh * a.kw;
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8L * num_sms())));
+        wgrad_reduce_canon_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw_canon, n, p.splits, a.Cout, a.canon_cin,
+                                                       a.kh, a.kw, a.SC);
+        SOL_CUDA(cudaGetLastError());
+    } else if (p.splits > 1) {
         const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
         const int threads = 256;
         wgrad_reduce_kernel<<<static_cast<unsigned>(ceil_div(ceil_div(n, 4), threads)), threads, 0, s>>>(
             a.workspace, a.dw, n, p.splits);
         SOL_CUDA(cudaGetLastError());
+    } else if (a.dw_canon) {
+        unpack_conv_grad(a.dw, a.dw_canon, a.Cout, a.canon_cin, a.kh, a.kw, a.SC, s);
     }
 }
 

@@ -91,6 +91,10 @@ struct WgradArgs {
     int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
     int ld_dy = 0;
     float* workspace = nullptr;  // split-K partials (size from wgrad_workspace_floats)
+    // optional canonical output dW[co][ci][kh][kw] (ci < canon_cin): the split-K reduction writes
+    // it directly (one pass instead of reduce + unpack); without splits dw is unpacked into it
+    float* dw_canon = nullptr;
+    int canon_cin = 0;
 };
 void wgrad_launch(const WgradArgs& a, cudaStream_t stream);
 size_t wgrad_workspace_floats(const WgradArgs& a);

@@ -611,9 +611,9 @@ public:
                 float* packed = static_cast<float*>(scratch);
                 float* ws = ws_floats_ ? packed + round_up(static_cast<int64_t>(packed_floats_), 64) : nullptr;
                 WgradArgs w = wargs(args[0], args[1], packed, ws);
+                w.dw_canon = static_cast<float*>(out);  // reduce (or unpack) straight to canonical dW
+                w.canon_cin = static_cast<int>(cin_);
                 wgrad_launch(w, s);
-                unpack_conv_grad(packed, static_cast<float*>(out), static_cast<int>(cout_), static_cast<int>(cin_),
-                                 kh_, kw_, static_cast<int>(x_.ld), s);
                 break;
             }
         }
