@@ -1786,6 +1786,9 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
             const int cvb = std::min(cv_total, THREADS);
             dim3 grid(static_cast<unsigned>(a.reduce_blocks), static_cast<unsigned>(ceil_div(cv_total, cvb)));
             if (launch_reduce_fast<T>(a, grid, s)) break;
+            for (int k = 0; k < a.pre.n; ++k)
+                if (a.pre.ins[k].op == PW_PARAM && a.P[a.pre.ins[k].arg] == nullptr)
+                    throw std::invalid_argument("dfp: in-place BN shift needs the fast row reduction");
             chan_reduce_kernel<T><<<grid, THREADS, 0, s>>>(a);
             break;
         }
@@ -2015,7 +2018,12 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalizeArgs a) {
         const double d = s1 / m;
         double var = s2 / m - d * d;
         if (var < 0) var = 0;
-        const double mean = static_cast<double>(a.shift[c]) + d;
+        // the shift is x's first pixel, read in place when no shift array is given
+        const double shift = a.shift ? static_cast<double>(a.shift[c])
+                                     : (a.shift_dtype == DT_BF16
+                                            ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.shift_x)[c]))
+                                            : static_cast<double>(static_cast<const float*>(a.shift_x)[c]));
+        const double mean = shift + d;
         const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
         if (a.stats_out) {
             a.stats_out[c] = static_cast<float>(mean);

@@ -302,7 +302,7 @@ public:
                 algo_flops = 2.0 * in_.pixels() * cout_ * kh_ * kw_ * cin_;
                 algo_bytes = (in_.pixels() * in_.ld + x_.pixels() * x_.ld) * double(elem_size(dtype_)) +
                              double(cout_) * cin_ * kh_ * kw_ * 4.0;
-                launches = ws_floats_ ? 3 : 2;
+                launches = 2;  // wgrad + (split-K reduce | unpack) into the canonical layout
                 break;
             }
             default:
@@ -1404,8 +1404,8 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
     launches = 1;
     launches_frozen = 1;  // frozen: inference BN coefficients and depthwise packs are cached
     for (auto& b : bn_) {
-        launches += b.training ? 3 : 1;
-        if (b.training) launches_frozen += 3;
+        launches += b.training ? 2 : 1;  // training: row reduction + finalize
+        if (b.training) launches_frozen += 2;
     }
     launches += static_cast<int>(dw_.size());
 }
@@ -1422,7 +1422,7 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
             continue;
         }
         double* partial = static_cast<double*>(scratch);
-        bn_shift(dtype_, args[b.x_binding], b.x_ld, b.C, b.shift, s);
+        // shift = x's first pixel, read in place by the reduction and the finalize (no copy launch)
         DfpArgs a;
         a.family = FAM_CHAN_REDUCE;
         a.dtype = dtype_;
@@ -1433,7 +1433,7 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
         a.n_in = 1;
         a.in[0] = args[b.x_binding];
         a.in_ld[0] = b.x_ld;
-        a.P[0] = b.shift;
+        a.P[0] = nullptr;  // in-place shift: the fast row reduction reads x's first pixel
         push(a.pre, PW_LD, 0, 0);                 // r0 = x
         push(a.pre, PW_PARAM, 1, 0, 0, 0);        // r1 = shift
         push(a.pre, PW_SCALE, 1, 0, 0, 0, -1.f);  // r1 = -shift
@@ -1449,7 +1449,9 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
         f.partial = partial;
         f.count = static_cast<double>(b.pixels);
         f.eps = b.eps;
-        f.shift = b.shift;
+        f.shift = nullptr;
+        f.shift_x = args[b.x_binding];
+        f.shift_dtype = dtype_;
         f.gamma = static_cast<const float*>(args[b.g]);
         f.beta = static_cast<const float*>(args[b.b]);
         f.stats_out = b.stats;
