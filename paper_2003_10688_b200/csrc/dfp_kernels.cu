@@ -4,6 +4,7 @@
 #include "dfp.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -1672,6 +1673,203 @@ bool launch_maxpool_back_fast(const DfpArgs& a, cudaStream_t s) {
     return true;
 }
 
+// MaxPool2dBack for the 3x3 / stride 2 / pad 1 window (the ResNet stem pool) in ONE pass: a block
+// owns a band of 2R dx rows of one image; it first computes the first-max tap of the R+1 window
+// rows covering the band into shared memory (same scan order and min_init rule as
+// maxpool_argmax_kernel), then gathers exactly like maxpool_back_fast_kernel (same window order,
+// so the sums are bit-identical). The argmax never round-trips through HBM and x's band is read
+// while it is still in L2 for the mask.
+constexpr int kBandSmemCap = 36 * 1024;
+
+template <typename T, bool ADD, bool MASK>
+__global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __grid_constant__ DfpArgs a,
+                                                                    PoolBackSpec ps, int R) {
+    constexpr int V = VEC<T>;
+    extern __shared__ __align__(16) uint8_t am_s[];
+    const int cv = a.C / V;
+    const int bands = (a.OH + R - 1) / R;
+    const int n = blockIdx.x / bands;
+    const int oh0 = (blockIdx.x - n * bands) * R;
+    const int nwr = min(R + 1, a.OH - oh0);
+    const T* x = static_cast<const T*>(a.in[a.pool_x]);
+    const int ldx = a.in_ld[a.pool_x];
+    // phase 1: first-max tap of windows (oh0 .. oh0+nwr-1, all ow)
+    const int wins = nwr * a.OW * cv;
+    for (int i = threadIdx.x; i < wins; i += THREADS) {
+        const int wv = i % cv;
+        const int t = i / cv;
+        const int ow = t % a.OW;
+        const int oh = oh0 + t / a.OW;
+        const int c = wv * V;
+        // the 9 taps stay as raw 16-byte vectors (36 registers) until compared
+        uint4 raw[9];
+        bool inb[9];
+#pragma unroll
+        for (int kh = 0; kh < 3; ++kh) {
+            const int hh = oh * 2 - 1 + kh;
+#pragma unroll
+            for (int kw = 0; kw < 3; ++kw) {
+                const int ww = ow * 2 - 1 + kw;
+                inb[kh * 3 + kw] = hh >= 0 && hh < a.H && ww >= 0 && ww < a.W;
+                if (inb[kh * 3 + kw])
+                    raw[kh * 3 + kw] = __ldg(reinterpret_cast<const uint4*>(
+                        x + ((static_cast<int64_t>(n) * a.H + hh) * a.W + ww) * ldx + c));
+            }
+        }
+        float best[V];
+        uint8_t bidx[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            best[e] = -INFINITY;
+            bidx[e] = 255;
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            if (!inb[k]) continue;
+            float xv[V];
+            unpack16(raw[k], xv, static_cast<T*>(nullptr));
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                if (xv[e] > best[e]) {
+                    best[e] = xv[e];
+                    bidx[e] = static_cast<uint8_t>(k);
+                }
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+            if (!(best[e] > a.min_init)) bidx[e] = 255;
+        uint8_t* dst = am_s + (static_cast<int>(t) * a.C + c);
+        if constexpr (V == 8) {
+            uint2 r;
+            memcpy(&r, bidx, 8);
+            *reinterpret_cast<uint2*>(dst) = r;
+        } else {
+            uint32_t r;
+            memcpy(&r, bidx, 4);
+            *reinterpret_cast<uint32_t*>(dst) = r;
+        }
+    }
+    __syncthreads();
+    // phase 2: dx rows 2*oh0 .. 2*oh0 + 2R - 1 by gather, one 2x2 pixel quad per item: quad
+    // (qh, qw) is covered only by windows (qh|qh+1, qw|qw+1), so its 4 window gradients, 4 argmax
+    // vectors and 4 mask vectors are loaded together (independent loads in flight) and each
+    // pixel sums its taps in maxpool_back_fast_kernel's (oh, ow) order — bit-identical sums.
+    const int qrows = min(R, a.OH - oh0);
+    const int items = qrows * a.OW * cv;
+    const T* d0 = static_cast<const T*>(a.in[ps.s0]);
+    const T* d1 = ADD ? static_cast<const T*>(a.in[ps.s1]) : nullptr;
+    const T* xm = MASK ? static_cast<const T*>(a.in[ps.sm]) : nullptr;
+    const int ld0 = a.in_ld[ps.s0], ld1 = ADD ? a.in_ld[ps.s1] : 0, ldm = MASK ? a.in_ld[ps.sm] : 0;
+    T* out = static_cast<T*>(a.out);
+    for (int i = threadIdx.x; i < items; i += THREADS) {
+        const int wv = i % cv;
+        const int t = i / cv;
+        const int qw = t % a.OW;
+        const int qh = oh0 + t / a.OW;
+        const int c = wv * V;
+        const bool has_r = qw + 1 < a.OW, has_d = qh + 1 < a.OH;  // windows (., qw+1), (qh+1, .)
+        const bool px_r = 2 * qw + 1 < a.W, px_d = 2 * qh + 1 < a.H;
+        uint4 g0[4], g1[4];
+        uint2 am[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int oh = qh + (w >> 1), ow = qw + (w & 1);
+            const bool ok = (w == 0) || (w == 1 && has_r) || (w == 2 && has_d) || (w == 3 && has_r && has_d);
+            g0[w] = make_uint4(0, 0, 0, 0);
+            g1[w] = make_uint4(0, 0, 0, 0);
+            am[w] = make_uint2(0xffffffffu, 0xffffffffu);
+            if (ok) {
+                const int64_t opix = (static_cast<int64_t>(n) * a.OH + oh) * a.OW + ow;
+                g0[w] = __ldg(reinterpret_cast<const uint4*>(d0 + opix * ld0 + c));
+                if (ADD) g1[w] = __ldg(reinterpret_cast<const uint4*>(d1 + opix * ld1 + c));
+                const uint8_t* ap = am_s + (((oh - oh0) * a.OW + ow) * a.C + c);
+                if constexpr (V == 8) am[w] = *reinterpret_cast<const uint2*>(ap);
+                else am[w].x = *reinterpret_cast<const uint32_t*>(ap);
+            }
+        }
+        uint4 mraw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool ok = (q == 0) || (q == 1 && px_r) || (q == 2 && px_d) || (q == 3 && px_r && px_d);
+            if (MASK && ok) {
+                const int64_t p = (static_cast<int64_t>(n) * a.H + 2 * qh + (q >> 1)) * a.W + 2 * qw + (q & 1);
+                mraw[q] = __ldg(reinterpret_cast<const uint4*>(xm + p * ldm + c));
+            }
+        }
+        // taps: pixel q of the quad takes window w's tap (dkh, dkw) = (1 + dy - 2*wy, 1 + dx - 2*wx)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int dy = q >> 1, dx = q & 1;
+            const bool ok = (q == 0) || (q == 1 && px_r) || (q == 2 && px_d) || (q == 3 && px_r && px_d);
+            if (!ok) continue;
+            float acc[V];
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int wy = w >> 1, wx = w & 1;
+                if (wy > dy || wx > dx) continue;  // window (qh+1, .) / (., qw+1) covers only odd rows / cols
+                const uint32_t me = static_cast<uint32_t>((1 + dy - 2 * wy) * 3 + (1 + dx - 2 * wx));
+                float g[V];
+                unpack16(g0[w], g, static_cast<T*>(nullptr));
+                if (ADD) {
+                    float h[V];
+                    unpack16(g1[w], h, static_cast<T*>(nullptr));
+#pragma unroll
+                    for (int e = 0; e < V; ++e) g[e] += h[e];
+                }
+#pragma unroll
+                for (int e = 0; e < V; ++e)
+                    if ((((e < 4 ? am[w].x : am[w].y) >> (8 * (e & 3))) & 0xffu) == me) acc[e] += g[e];
+            }
+            if (MASK) {
+                float m[V];
+                unpack16(mraw[q], m, static_cast<T*>(nullptr));
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc[e] = m[e] > 0.f ? acc[e] : 0.f;
+            }
+            const int64_t p = (static_cast<int64_t>(n) * a.H + 2 * qh + dy) * a.W + 2 * qw + dx;
+            store16(out + p * a.out_ld + c, acc);
+        }
+    }
+}
+
+template <typename T>
+bool launch_maxpool_back_band(const DfpArgs& a, cudaStream_t s) {
+    if (std::getenv("SOL_NO_POOLBACK_BAND") != nullptr) return false;  // read per compile/capture
+    if (a.kh != 3 || a.kw != 3 || a.sh != 2 || a.sw != 2 || a.ph != 1 || a.pw != 1) return false;
+    if (a.OH != (a.H - 1) / 2 + 1 || a.OW != (a.W - 1) / 2 + 1) return false;
+    const PoolBackSpec ps = match_pool_back(a.pre, a.post);
+    if (!ps.ok || a.out_coff != 0 || a.in_kind[a.pool_x] != IN_PIX || a.in_coff[a.pool_x] != 0) return false;
+    for (int sl : {ps.s0, ps.s1, ps.sm})
+        if (sl >= 0 && (a.in_kind[sl] != IN_PIX || a.in_coff[sl] != 0)) return false;
+    const int64_t row_bytes = static_cast<int64_t>(a.OW) * a.C;
+    const int rmax = static_cast<int>(std::min<int64_t>(16, kBandSmemCap / row_bytes - 1));
+    if (rmax < 1) return false;
+    const bool add = ps.s1 >= 0, mask = ps.sm >= 0;
+    auto kern = add ? (mask ? maxpool_back_band_kernel<T, true, true> : maxpool_back_band_kernel<T, true, false>)
+                    : (mask ? maxpool_back_band_kernel<T, false, true> : maxpool_back_band_kernel<T, false, false>);
+    // band height: minimise (waves of resident blocks) x (window rows per block) — with N*bands
+    // just above a multiple of the resident count the last wave would run nearly empty
+    int R = 1;
+    int64_t best = -1;
+    for (int r = 1; r <= rmax; ++r) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, static_cast<size_t>((r + 1) * row_bytes));
+        const int64_t resident = static_cast<int64_t>(std::max(occ, 1)) * num_sms();
+        const int64_t blocks = static_cast<int64_t>(a.N) * ((a.OH + r - 1) / r);
+        const int64_t cost = ceil_div(blocks, resident) * (r + 1);
+        if (best < 0 || cost < best) {
+            best = cost;
+            R = r;
+        }
+    }
+    const int64_t blocks = static_cast<int64_t>(a.N) * ((a.OH + R - 1) / R);
+    if (blocks >= (int64_t(1) << 31)) return false;
+    kern<<<dim3(static_cast<unsigned>(blocks)), THREADS, static_cast<size_t>((R + 1) * row_bytes), s>>>(a, ps, R);
+    return true;
+}
+
 template <typename T, bool IS_MAX>
 __global__ void __launch_bounds__(THREADS) pool_back_kernel(const __grid_constant__ DfpArgs a) {
     constexpr int V = VEC<T>;
@@ -1794,6 +1992,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
         }
         case FAM_MAXPOOL_BACK: {
             if (a.argmax == nullptr || a.kh * a.kw > 254) throw std::invalid_argument("dfp: maxpool backward needs argmax scratch");
+            if (launch_maxpool_back_band<T>(a, s)) break;
             const int64_t windows = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
             maxpool_argmax_kernel<T><<<grid_for(windows, THREADS), THREADS, 0, s>>>(a);
             if (launch_maxpool_back_fast<T>(a, s)) break;

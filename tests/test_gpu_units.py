@@ -173,3 +173,33 @@ def test_stem_wgrad(gpu, hw):
     assert fam == "conv_stem_wgrad_tcgen05"
     err = O.oracle_err(got, local[u.output])
     assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_maxpool_back_band_stem_scale(gpu, monkeypatch, dtype):
+    """The ResNet stem's MaxPool2dBack (+ReluBack) unit at 224x224 (112x112 -> 56x56, 3x3/2/1):
+    the one-pass band kernel matches the oracle and is bit-identical to the two-pass
+    argmax + gather path (SOL_NO_POOLBACK_BAND=1). Inputs on a coarse grid so windows hold ties
+    (first-max routing, reference.cpp:294-327) and ReLU zeros (min_init routes nothing)."""
+    from paper_2003_10688_b200 import models
+    from paper_2003_10688_b200 import autodiff, graph, partition, passes
+    batch = 2
+    g = models.resnet(18, hw=224, classes=16, width=16, train=True)
+    gi = graph.infer_shapes(g, batch)
+    gi = graph.infer_shapes(autodiff.build_training_graph(gi).graph, batch)
+    gp = passes.run_pipeline(gi)
+    units = [u for u in partition.partition(gp)
+             if any(gp.find_node(nid).op == "MaxPool2dBack" for nid in u.node_ids)]
+    assert len(units) == 1
+    u = units[0]
+    rng = np.random.default_rng(5)
+    env = {}
+    for nm in u.inputs:
+        shape = gp.meta_of(nm).shape
+        env[nm] = (rng.integers(-3, 5, shape) / 4.0).astype(np.float32)
+    _check_units(gp, [u], env, dtype, gpu)
+    fam, band = run_unit(gp, u, env, dtype, gpu)
+    assert fam == "dfp_maxpool_back"
+    monkeypatch.setenv("SOL_NO_POOLBACK_BAND", "1")
+    _, two_pass = run_unit(gp, u, env, dtype, gpu)
+    assert np.array_equal(band, two_pass)
