@@ -2161,7 +2161,29 @@ __global__ void __launch_bounds__(128) finalize_kernel(const FinalizeArgs a) {
     const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
     double q[4] = {0.0, 0.0, 0.0, 0.0};
     const double* base = a.partial + static_cast<int64_t>(c) * a.blocks * ns;
-    for (int b = threadIdx.x; b < a.blocks; b += 128) {
+    // the first 8 partials of every thread are loaded together (16-byte loads; a dependent
+    // load-add chain made this launch latency bound at ~7 us), then summed in block order
+    constexpr int J = 8;
+    double2 lo[J], hi[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int b = threadIdx.x + 128 * j;
+        lo[j] = make_double2(0.0, 0.0);
+        hi[j] = make_double2(0.0, 0.0);
+        if (b < a.blocks) {
+            const double2* src = reinterpret_cast<const double2*>(base + static_cast<int64_t>(b) * ns);
+            lo[j] = src[0];
+            if (ns == 4) hi[j] = src[1];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        q[0] += lo[j].x;
+        q[1] += lo[j].y;
+        q[2] += hi[j].x;
+        q[3] += hi[j].y;
+    }
+    for (int b = threadIdx.x + 128 * J; b < a.blocks; b += 128) {
         const double* src = base + static_cast<int64_t>(b) * ns;
         q[0] += src[0];
         q[1] += src[1];
@@ -2336,8 +2358,9 @@ int dfp_reduce_blocks(int64_t pixels, int C) {
     const int64_t cvec = std::max<int64_t>(1, C / 8);
     const int64_t gy = ceil_div(cvec, 256);
     const int64_t want = ceil_div(pixels * cvec, static_cast<int64_t>(256) * 32 * gy);
-    const int64_t wave = std::max<int64_t>(1, 2 * num_sms() / gy);
-    const int64_t blocks = want <= wave / 2 ? want : std::min<int64_t>(2, ceil_div(want, wave)) * wave;
+    static const int64_t per_sm = std::getenv("SOL_REDUCE_PER_SM") ? std::atoi(std::getenv("SOL_REDUCE_PER_SM")) : 2;
+    const int64_t wave = std::max<int64_t>(1, per_sm * num_sms() / gy);
+    const int64_t blocks = std::min(want, wave);
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, pixels)));
 }
 
