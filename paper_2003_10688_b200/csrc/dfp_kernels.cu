@@ -359,6 +359,12 @@ __device__ __forceinline__ void bn_apply(float* v, const float* const* P, int b,
 // Row-walking geometry shared by the channel-resident kernels: each thread owns one 16-byte
 // channel vector (per-channel coefficients stay in registers) and walks pixels; block = cvb
 // channel vectors x rows pixel lanes, grid = (pixel blocks, channel-vector blocks).
+// Cap on the pixel blocks of the row-walking kernels per SM (SOL_ROW_BLOCKS_PER_SM overrides).
+inline int64_t row_blocks_per_sm() {
+    static const int64_t k = std::getenv("SOL_ROW_BLOCKS_PER_SM") ? std::atoi(std::getenv("SOL_ROW_BLOCKS_PER_SM")) : 6;
+    return k;
+}
+
 struct RowGeo {
     dim3 grid;
 };
@@ -369,7 +375,7 @@ inline RowGeo row_geo(int C, int V, int64_t pixels, int per_thread = 4) {
     const int rows = THREADS / cvb;
     const int gy = static_cast<int>(ceil_div(cv_total, cvb));
     const int64_t want = ceil_div(pixels, static_cast<int64_t>(rows) * per_thread);
-    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 32LL * num_sms() / gy)));
+    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, row_blocks_per_sm() * num_sms() / gy)));
     return RowGeo{dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy))};
 }
 
@@ -2412,7 +2418,7 @@ void bn_back_apply(int dtype, const void* dy, const void* x, int C, int64_t pixe
     const int gy = static_cast<int>(ceil_div(cv_total, cvb));
     // ~4 waves of 8 blocks per SM, each thread covering >= 4 pixels
     const int64_t want = ceil_div(pixels, static_cast<int64_t>(rows) * 4);
-    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 32LL * num_sms() / gy)));
+    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, row_blocks_per_sm() * num_sms() / gy)));
     dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
     if (dtype == DT_BF16)
         bnback_apply_kernel<__nv_bfloat16><<<grid, THREADS, 0, s>>>(

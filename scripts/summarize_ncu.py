@@ -58,8 +58,25 @@ def traffic_json(path, out):
                    "note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per conv launch, one inference step"}, f)
 
 
+def family_traffic_table(path, peak_gbs=6551.4):
+    """Per-kernel totals of an ncu time + DRAM metrics CSV: DRAM GB/s against the measured HBM
+    copy peak (MEASURED_PEAKS.json); cold-cache, serialised launches."""
+    L = by_launch(path)
+    agg = OrderedDict()
+    for d in L.values():
+        a = agg.setdefault(short(d["name"]), [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += d["gpu__time_duration.sum"]
+        a[2] += d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+    tot = sum(a[1] for a in agg.values())
+    print(f"{len(L)} launches, {tot/1e6:.3f} ms total (serialised, cold-cache under ncu)\n")
+    print("| kernel | launches | total ms | DRAM MB | DRAM GB/s | of HBM peak |\n|---|---:|---:|---:|---:|---:|")
+    for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"| `{k}` | {n} | {t/1e6:.3f} | {b/1e6:.0f} | {b/t:.0f} | {100*b/t/peak_gbs:.0f}% |")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "traffic-json":
         traffic_json(sys.argv[2], sys.argv[3])
     else:
-        {"launches": launch_table, "traffic": traffic_table}[sys.argv[1]](sys.argv[2])
+        {"launches": launch_table, "traffic": traffic_table, "family-traffic": family_traffic_table}[sys.argv[1]](sys.argv[2])
