@@ -2382,13 +2382,19 @@ void transpose(const void* in, void* out, int N, int R, int C, int ld_in, int r_
 
 int dfp_reduce_blocks(int64_t pixels, int C) {
     // ~32 16-byte vectors per thread (256 threads) over the pixel range, grid.y covers channel
-    // vector blocks of 256; whole waves of two resident blocks per SM, at most two waves
+    // vector blocks of 256; at most one wave of two resident blocks per SM (a second wave cost
+    // more in per-block combination than it hid)
     const int64_t cvec = std::max<int64_t>(1, C / 8);
     const int64_t gy = ceil_div(cvec, 256);
     const int64_t want = ceil_div(pixels * cvec, static_cast<int64_t>(256) * 32 * gy);
     static const int64_t per_sm = std::getenv("SOL_REDUCE_PER_SM") ? std::atoi(std::getenv("SOL_REDUCE_PER_SM")) : 2;
     const int64_t wave = std::max<int64_t>(1, per_sm * num_sms() / gy);
-    const int64_t blocks = std::min(want, wave);
+    // small tensors (layers 3/4): a full wave as long as every thread keeps >= 4 pixels — sizing
+    // by ~32 vectors per thread alone left 49..196 blocks, i.e. idle SMs
+    const int64_t rows = 256 / std::min<int64_t>(cvec, 256);
+    static const bool old_sizing = std::getenv("SOL_REDUCE_OLD_SIZING") != nullptr;
+    const int64_t fill = old_sizing ? want : std::max(want, ceil_div(pixels, rows * 4));
+    const int64_t blocks = std::min(fill, wave);
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, pixels)));
 }
 
