@@ -272,38 +272,70 @@ def bench_model(m, inputs, steps, warmup, out_names):
     m.sync()
     dev_ms = m.elapsed_ms(0, 1) / steps
     dev_ms = dp.max_over_ranks(dev_ms)
-    # end-to-end through the public API: every step copies its batch host -> device (pinned) and
-    # reads its result back; the input copy of step i+1 is staged on the plan's copy stream while
-    # step i computes (pipelined serving, OptimizedModel.stage_inputs)
-    import ctypes as C
-    from paper_2003_10688_b200 import _lib as L
-    lib = L.lib()
-    for name, a in inputs.items():
-        m.pin_in[name].view(np.float32, a.shape)[...] = a
+    # end-to-end through the public API: every step copies its batch from pinned host memory to the
+    # device and reads its result back; the input copy of step i+1 is staged on the plan's copy
+    # stream while step i computes (OptimizedModel.stage_inputs). The pinned slots are filled in
+    # place through OptimizedModel.input_buffers() -- what a data loader writing pinned memory does
     h2d = sum(4 * a.size for a in inputs.values())
     d2h = sum(4 * m.graph.meta_of(n).numel for n in out_names)
 
-    def pipelined(k):
+    def pipelined(k, fill):
+        if fill:
+            for name, v in m.input_buffers().items():
+                v[...] = inputs[name]
         m.stage_inputs()
         for i in range(k):
             m.run()
             if i + 1 < k:
+                if fill:
+                    for name, v in m.input_buffers().items():
+                        v[...] = inputs[name]
                 m.stage_inputs()
-            for n in out_names:
-                L.check(lib.sol_b200_plan_d2h(m.plan, m.pin_out[n].ptr, m.out_canon[n], 4 * m.graph.meta_of(n).numel))
+            m.enqueue_fetch(out_names)
 
-    pipelined(max(warmup, 3))  # warm-up (allocates the staging buffers, primes the copy stream)
+    pipelined(max(warmup, 3), True)  # warm-up: fills both pinned slots, primes the copy stream
     dp_barrier()
     m.sync()
     m.event(2)
-    pipelined(steps)
+    pipelined(steps, False)
     m.event(3)
     m.sync()
     e2e_ms = dp.max_over_ranks(m.elapsed_ms(2, 3) / steps)
-    return dev_ms, e2e_ms, h2d, d2h
+    # the synchronous predict()/train_step() call from numpy arrays: the host copy into pinned
+    # memory, H2D, the plan, D2H and the host synchronisation all on the critical path (wall clock)
+    import time as _t
+    k = min(steps, 10)
+    call = (lambda: m.predict(inputs)) if m.loss_name is None else (lambda: m.train_step(inputs))
+    call()
+    dp_barrier()
+    t0 = _t.perf_counter()
+    for _ in range(k):
+        call()
+    sync_ms = dp.max_over_ranks((_t.perf_counter() - t0) * 1e3 / k)
+    return dev_ms, e2e_ms, h2d, d2h, sync_ms
 
 
 _DIST = False
+
+
+def distinct_gpus(device: int) -> int:
+    """Number of distinct physical GPUs (by UUID) the ranks of this job run on."""
+    import torch
+    uuid = str(torch.cuda.get_device_properties(device).uuid)
+    if not _DIST:
+        return 1
+    import torch.distributed as dist
+    got = [None] * dist.get_world_size()
+    dist.all_gather_object(got, uuid)
+    return len(set(got))
+
+
+def comm_of(m, world: int):
+    """The training plan's NCCL communicator as NCCL reports it (ncclCommCount / ncclCommCuDevice)."""
+    if world == 1:
+        return {"nranks": 1, "nranks_ok": True, "note": "single replica: no communicator"}
+    n, r, d = m.comm_info()
+    return {"nranks": n, "rank": r, "cuda_device": d, "nranks_ok": n == world}
 
 
 def dp_barrier():
@@ -317,6 +349,8 @@ def run_b200(args):
     from paper_2003_10688_b200 import dp, frontend, models
     ctx = dp.init("nccl") if args.gpus > 1 else dp.env_context()
     _DIST = ctx.world > 1
+    if ctx.world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but the process group has {ctx.world} ranks")
     device = ctx.local_rank
     all_cpus = os.sched_getaffinity(0)
     local = gpu_local_cpus(device)
@@ -332,12 +366,13 @@ def run_b200(args):
     sampler = ClockSampler(device) if ctx.rank == 0 and not os.environ.get("SOL_BENCH_NO_CLOCKS") else None
     if sampler:
         sampler.start()
-    dev_ms, e2e_ms, h2d, d2h = bench_model(m, {"x": x}, args.steps, args.warmup, ["prob"])
+    dev_ms, e2e_ms, h2d, d2h, sync_ms = bench_model(m, {"x": x}, args.steps, args.warmup, ["prob"])
     clocks = sampler.stop() if sampler else None
     launches_per_step = measured_launches(m)
     if launches_per_step is None:
         launches_per_step = sum(s.launches_frozen for s in m.steps)  # the inference plan runs frozen
     world = ctx.world
+    gpus_active = distinct_gpus(device)
     value = world * B / (dev_ms / 1e3)
     e2e = world * B / (e2e_ms / 1e3)
     conv_fams = {"conv_fprop_tcgen05", "conv_fprop_fused_tcgen05", "conv_stem_tcgen05", "conv_stem_fused_tcgen05"}
@@ -357,7 +392,7 @@ def run_b200(args):
         t = np.zeros((Bt, 1000), np.float32)
         t[np.arange(Bt), rng.integers(0, 1000, Bt)] = 1
         xt = x[:Bt] if Bt <= B else rng.uniform(-1, 1, (Bt, 3, 224, 224)).astype(np.float32)
-        tdev, te2e, th2d, td2h = bench_model(mt, {"x": xt, "t": t}, args.train_steps, args.warmup, ["loss"])
+        tdev, te2e, th2d, td2h, tsync = bench_model(mt, {"x": xt, "t": t}, args.train_steps, args.warmup, ["loss"])
         troof, ttimes = roofline_of(mt, peaks, peaks_kind,
                                     {"conv_fprop_tcgen05", "conv_dgrad_tcgen05", "conv_wgrad_tcgen05",
                                      "conv_stem_tcgen05", "conv_stem_wgrad_tcgen05"}, "tensor")
@@ -368,7 +403,10 @@ def run_b200(args):
                  "value": world * Bt / (tdev / 1e3), "unit": "images/s", "ms_per_step": tdev,
                  "global_batch": world * Bt, "per_gpu_batch": Bt,
                  "e2e": {"value": world * Bt / (te2e / 1e3), "unit": "images/s", "h2d_bytes_per_step": th2d,
-                         "d2h_bytes_per_step": td2h},
+                         "d2h_bytes_per_step": td2h, "source": "pinned host slots, H2D pipelined on the copy stream"},
+                 "e2e_sync_call": {"value": world * Bt / (tsync / 1e3), "unit": "images/s",
+                                   "api": "train_step(numpy batch) per step, wall clock"},
+                 "comm": comm_of(mt, world),
                  "roofline": troof,
                  "gpu_launches": (measured_launches(mt) or sum(s.launches for s in mt.steps)) * args.train_steps,
                  "family_ms_per_step": {k: round(v / 1e3, 3) for k, v in sorted(tfam.items(), key=lambda kv: -kv[1])[:8]}}
@@ -389,13 +427,35 @@ def run_b200(args):
                    "model": "resnet50", "global_batch": world * B, "per_gpu_batch": B, "seq_len": 0,
                    "parallelism": f"dp{world} (batch-sharded, no collective for inference)",
                    "l2": "per-step working set >> 126 MB L2 (no flush needed)"},
-        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "source": "pinned host slots filled in place (input_buffers), H2D pipelined on the copy stream"},
+        "e2e_sync_call": {"value": world * B / (sync_ms / 1e3), "unit": "images/s",
+                          "api": "predict(numpy batch) per step: host copy into pinned + H2D + plan + D2H + sync, wall clock"},
+        "gpus_active": gpus_active,
         "roofline": roof, "roofline_dfp": roof_dfp, "cpu_baseline": cpu, "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "family_ms_per_step": {k: round(v / 1e3, 3) for k, v in sorted(fam_time.items(), key=lambda kv: -kv[1])[:8]},
         "train": train,
     }
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks (one process per GPU)
+    under torch.distributed.run on this node. Refuses when fewer than N GPUs are visible."""
+    import socket
+    if args.impl == "b200":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench: --gpus {args.gpus} requested but only {have} CUDA device(s) visible")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -410,6 +470,8 @@ def main():
     ap.add_argument("--no-train", dest="train", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

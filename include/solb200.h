@@ -205,6 +205,11 @@ int sol_b200_plan_d2h(sol_b200_plan_t p, void* dst, int32_t id, uint64_t bytes);
  * next plan_run starts by moving it into the buffer. The host-to-device copy of step i+1 thus
  * overlaps the kernels of step i (the reference queue's copy/compute overlap, runtime.hpp:95-145). */
 int sol_b200_plan_stage_h2d(sol_b200_plan_t p, int32_t id, const void* src, uint64_t bytes);
+/* Copy-stream fences for pinned-source reuse: a ticket taken after stage_h2d() calls completes once
+   those copies have read their host sources; copy_wait blocks the host until then (the refill of a
+   pinned staging buffer must not race the copy still reading it). */
+int sol_b200_plan_copy_fence(sol_b200_plan_t p, uint64_t* ticket);
+int sol_b200_plan_copy_wait(sol_b200_plan_t p, uint64_t ticket);
 /* CUDA events on the plan stream (slots 0..15) for device-side timing. */
 int sol_b200_plan_event_record(sol_b200_plan_t p, int32_t slot);
 int sol_b200_plan_event_elapsed(sol_b200_plan_t p, int32_t a, int32_t b, float* ms);
@@ -215,6 +220,10 @@ int sol_b200_host_free(void* ptr);
 /* ---- NCCL (batch-sharded data parallelism) ------------------------------------------------ */
 int sol_b200_nccl_unique_id(uint8_t id[128]);
 int sol_b200_plan_set_comm(sol_b200_plan_t p, const uint8_t id[128], int32_t rank, int32_t nranks);
+/* The plan communicator as NCCL sees it (ncclCommCount / ncclCommUserRank / ncclCommCuDevice);
+   1 / 0 / the plan device when no communicator is attached. Bench evidence that N ranks really
+   share one communicator on N distinct GPUs. */
+int sol_b200_plan_comm_info(sol_b200_plan_t p, int32_t* nranks, int32_t* rank, int32_t* cuda_device);
 
 /* ---- raw heavy-layer entry points (KernelProvider::execute on device pointers) ------------ */
 typedef struct {

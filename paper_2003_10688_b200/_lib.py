@@ -42,7 +42,8 @@ SYMBOLS = [
     "sol_b200_conv_wgrad_workspace", "sol_b200_conv_wgrad",
     "sol_b200_plan_h2d", "sol_b200_plan_d2h", "sol_b200_plan_event_record", "sol_b200_plan_event_elapsed",
     "sol_b200_host_alloc", "sol_b200_host_free", "sol_b200_set_conv_debug", "sol_b200_plan_stage_h2d",
-    "sol_b200_module_set_sibling_outputs",
+    "sol_b200_module_set_sibling_outputs", "sol_b200_plan_comm_info",
+    "sol_b200_plan_copy_fence", "sol_b200_plan_copy_wait",
 ]
 
 
@@ -153,6 +154,7 @@ def lib():
             "sol_b200_plan_arena_bytes": [vp, C.POINTER(u64)],
             "sol_b200_nccl_unique_id": [C.POINTER(C.c_uint8)],
             "sol_b200_plan_set_comm": [vp, C.POINTER(C.c_uint8), i32, i32],
+            "sol_b200_plan_comm_info": [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
             "sol_b200_conv_packed_elems": [C.POINTER(ConvDesc), i32, C.POINTER(i64)],
             "sol_b200_conv_pack_weight": [C.POINTER(ConvDesc), vp, vp, i32, vp],
             "sol_b200_conv_fprop": [C.POINTER(ConvDesc), vp, vp, vp, vp, i32, vp],
@@ -161,6 +163,8 @@ def lib():
             "sol_b200_conv_wgrad": [C.POINTER(ConvDesc), vp, vp, vp, vp, vp],
             "sol_b200_plan_h2d": [vp, i32, vp, u64],
             "sol_b200_plan_stage_h2d": [vp, i32, vp, u64],
+            "sol_b200_plan_copy_fence": [vp, C.POINTER(C.c_uint64)],
+            "sol_b200_plan_copy_wait": [vp, u64],
             "sol_b200_module_set_sibling_outputs": [vp, i32],
             "sol_b200_plan_d2h": [vp, vp, i32, u64],
             "sol_b200_plan_event_record": [vp, i32],

@@ -308,6 +308,14 @@ int sol_b200_plan_stage_h2d(sol_b200_plan_t p, int32_t id, const void* src, uint
     return guard([&] { p->p->stage_h2d(id, src, bytes); });
 }
 
+int sol_b200_plan_copy_fence(sol_b200_plan_t p, uint64_t* ticket) {
+    return guard([&] { *ticket = p->p->copy_fence(); });
+}
+
+int sol_b200_plan_copy_wait(sol_b200_plan_t p, uint64_t ticket) {
+    return guard([&] { p->p->copy_wait(ticket); });
+}
+
 int sol_b200_plan_d2h(sol_b200_plan_t p, void* dst, int32_t id, uint64_t bytes) {
     return guard([&] { p->p->d2h(dst, id, bytes); });
 }
@@ -342,6 +350,16 @@ int sol_b200_nccl_unique_id(uint8_t id[128]) {
 
 int sol_b200_plan_set_comm(sol_b200_plan_t p, const uint8_t id[128], int32_t rank, int32_t nranks) {
     return guard([&] { p->p->set_comm(id, rank, nranks); });
+}
+
+int sol_b200_plan_comm_info(sol_b200_plan_t p, int32_t* nranks, int32_t* rank, int32_t* cuda_device) {
+    return guard([&] {
+        int n = 1, r = 0, d = 0;
+        p->p->comm_info(&n, &r, &d);
+        *nranks = n;
+        *rank = r;
+        *cuda_device = d;
+    });
 }
 
 // ---- raw heavy-layer entry points ------------------------------------------------------------

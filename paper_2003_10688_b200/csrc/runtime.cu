@@ -327,6 +327,8 @@ Plan::~Plan() {
         if (kv.second.ready) cudaEventDestroy(kv.second.ready);
         if (kv.second.consumed) cudaEventDestroy(kv.second.consumed);
     }
+    for (cudaEvent_t e : fences_)
+        if (e) cudaEventDestroy(e);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (comm_stream_) cudaStreamSynchronize(comm_stream_);
     for (cudaEvent_t e : ar_events_) cudaEventDestroy(e);
@@ -542,13 +544,29 @@ void Plan::stage_h2d(int id, const void* src, uint64_t bytes) {
         SOL_CUDA(cudaEventCreateWithFlags(&st.ready, cudaEventDisableTiming));
         SOL_CUDA(cudaEventCreateWithFlags(&st.consumed, cudaEventDisableTiming));
     }
-    if (st.pending) throw std::invalid_argument("plan: staged input not consumed by a run yet");
+    // re-staging before a run replaces the pending batch: the copies are ordered on copy_stream_
     // the staging area is free once the previous run moved its content into the plan buffer
     if (st.consumed_valid) SOL_CUDA(cudaStreamWaitEvent(copy_stream_, st.consumed, 0));
     SOL_CUDA(cudaMemcpyAsync(st.dev, src, bytes, cudaMemcpyHostToDevice, copy_stream_));
     SOL_CUDA(cudaEventRecord(st.ready, copy_stream_));
     st.bytes = bytes;
     st.pending = true;
+}
+
+uint64_t Plan::copy_fence() {
+    SOL_CUDA(cudaSetDevice(device_));
+    if (!copy_stream_) SOL_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    cudaEvent_t& e = fences_[fence_next_ % kFences];
+    if (!e) SOL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SOL_CUDA(cudaEventRecord(e, copy_stream_));
+    return fence_next_++;
+}
+
+void Plan::copy_wait(uint64_t ticket) {
+    if (ticket >= fence_next_) throw std::invalid_argument("plan: copy fence ticket was never issued");
+    // an overwritten slot holds a LATER fence on the same in-order stream: waiting on it is a
+    // superset of the requested wait
+    SOL_CUDA(cudaEventSynchronize(fences_[ticket % kFences]));
 }
 
 void Plan::consume_staged() {
@@ -649,6 +667,17 @@ void Plan::set_comm(const uint8_t id[128], int rank, int nranks) {
     nccl_check(ncclCommInitRank(&c, nranks, uid, rank), "init");
     comm_ = c;
     nranks_ = nranks;
+}
+
+void Plan::comm_info(int* nranks, int* rank, int* cuda_device) const {
+    *nranks = 1;
+    *rank = 0;
+    *cuda_device = device_;
+    if (!comm_) return;
+    auto c = static_cast<ncclComm_t>(comm_);
+    nccl_check(ncclCommCount(c, nranks), "count");
+    nccl_check(ncclCommUserRank(c, rank), "rank");
+    nccl_check(ncclCommCuDevice(c, cuda_device), "device");
 }
 
 }  // namespace solb200

@@ -115,8 +115,13 @@ public:
     const Module* step_module(int i) const { return steps_[i].module.get(); }
     uint64_t arena_bytes() const { return total_; }
     void set_comm(const uint8_t id[128], int rank, int nranks);
+    void comm_info(int* nranks, int* rank, int* cuda_device) const;
     void h2d(int id, const void* src, uint64_t bytes);
     void stage_h2d(int id, const void* src, uint64_t bytes);
+    // host-side fences on the copy stream: a ticket taken after stage_h2d() calls is complete once
+    // those copies have read their pinned sources (the host may then refill them)
+    uint64_t copy_fence();
+    void copy_wait(uint64_t ticket);
     void d2h(void* dst, int id, uint64_t bytes);
     void event_record(int slot);
     float event_elapsed(int a, int b);
@@ -165,6 +170,9 @@ private:
     cudaStream_t comm_stream_ = nullptr;
     std::vector<cudaEvent_t> ar_events_;
     std::map<int, Staged> staged_;
+    static constexpr int kFences = 8;
+    cudaEvent_t fences_[kFences] = {};
+    uint64_t fence_next_ = 0;
 };
 
 }  // namespace solb200

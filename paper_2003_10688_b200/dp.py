@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import os
 from dataclasses import dataclass
-from typing import Optional
+from typing import Dict, List, Optional
 
 import numpy as np
 
@@ -70,14 +70,29 @@ def max_over_ranks(value: float) -> float:
     return float(t.item())
 
 
-def average_gradients_host(grads: dict) -> dict:
-    """Host-side mirror of the plan's all-reduce step (sum then x 1/G), for CPU tests (gloo)."""
-    import torch
-    import torch.distributed as dist
-    out = {}
-    world = dist.get_world_size()
-    for k in sorted(grads):
-        t = torch.from_numpy(np.ascontiguousarray(grads[k], np.float32)).clone()
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        out[k] = (t / world).numpy()
+def allreduce_schedule(completions: List[List[str]], grad_bytes: Dict[str, float],
+                       bucket_limit: float) -> Dict[int, List[str]]:
+    """The training plan's gradient all-reduce buckets: walking the plan's units in
+    order, each parameter gradient joins the pending bucket when the unit that completes it runs;
+    the bucket is issued right after the unit that brings it to >= bucket_limit bytes, and the
+    remainder after the last unit. Returns {unit index: [gradient names]} -- every gradient exactly
+    once, never before its producer. The plan issues each bucket as one NCCL group on its comm
+    stream (sum x 1/G = ncclAvg), overlapping the backward units that follow."""
+    out: Dict[int, List[str]] = {}
+    pending: List[str] = []
+    size = 0.0
+    seen = set()
+    last = len(completions) - 1
+    for i, names in enumerate(completions):
+        for n in names:
+            if n in grad_bytes and n not in seen:
+                seen.add(n)
+                pending.append(n)
+                size += grad_bytes[n]
+        if pending and (size >= bucket_limit or i == last):
+            out[i] = pending
+            pending, size = [], 0.0
+    missing = set(grad_bytes) - seen
+    if missing:
+        raise ValueError(f"gradients never produced by a plan unit: {sorted(missing)[:4]}")
     return out

@@ -25,6 +25,7 @@ from . import _lib as L
 from .autodiff import build_training_graph
 from .dfp import (DTYPES, ELEM, create_module, is_f32_tensor, reorder_module, sgd_module, sgd_multi_module,
                   storage_bytes)
+from .dp import allreduce_schedule
 from .graph import Meta, ModelGraph, infer_shapes
 from .partition import ExecUnit, partition
 from .passes import run_pipeline
@@ -60,6 +61,25 @@ class StepInfo:
     launches: int = 1
     launches_frozen: int = 1  # once the plan is frozen (inference: cached weight packing)
     node_ids: List[str] = field(default_factory=list)
+
+
+_COPY_POOL = None
+
+
+def parallel_copy(dst: np.ndarray, src: np.ndarray):
+    """dst[...] = src split over host threads along the batch dimension (numpy releases the GIL
+    for plain copies): filling a 154 MB pinned batch single-threaded costs ~4x one B200 step."""
+    global _COPY_POOL
+    n = dst.shape[0] if dst.ndim else 1
+    if dst.nbytes < (8 << 20) or n < 2:
+        np.copyto(dst, src)
+        return
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _COPY_POOL = ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1)))
+    parts = min(n, _COPY_POOL._max_workers * 2)
+    bounds = [(i * n // parts, (i + 1) * n // parts) for i in range(parts)]
+    list(_COPY_POOL.map(lambda b: np.copyto(dst[b[0]:b[1]], src[b[0]:b[1]]), bounds))
 
 
 class PinnedBuffer:
@@ -163,9 +183,9 @@ class OptimizedModel:
                      StepInfo("reorder", "", gi.name))
         # unit outputs
         self.modules = []
-        siblings = self._bn_back_siblings() if (o.train and o.fuse_bn_backward) else {}
+        siblings = bn_back_siblings(g, self.units) if (o.train and o.fuse_bn_backward) else {}
         absorbed = {v for sib in siblings.values() for v in sib if v is not None}
-        act_sibs = self._activation_siblings() if o.fuse_bn_backward else {}
+        act_sibs = activation_siblings(g, self.units) if o.fuse_bn_backward else {}
         absorbed |= {v[0] for v in act_sibs.values()}
 
         def out_buf(name):
@@ -177,40 +197,28 @@ class OptimizedModel:
 
         # gradient all-reduce buckets: a bucket is issued right after the unit that
         # completes its last gradient, so NCCL (on the plan's comm stream) overlaps the remaining
-        # backward units; ~25 MB buckets (SOL_AR_BUCKET_MB)
+        # backward units; ~25 MB buckets (SOL_AR_BUCKET_MB). The schedule is dp.allreduce_schedule.
         reduce_grads = o.train and (o.world_size > 1 or o.nccl_allreduce)
-        grad_of = {gname: pname for pname, gname in self.param_grads} if reduce_grads else {}
-        bucket_limit = float(os.environ.get("SOL_AR_BUCKET_MB", "25")) * 2 ** 20
-        pending, pending_bytes = [], 0.0
-        self.ar_buckets = 0
+        self.ar_schedule = {}
+        if reduce_grads:
+            self.ar_schedule = allreduce_schedule(
+                gradient_completions(self.units, siblings, absorbed),
+                {gname: 4.0 * self.params[pname].size for pname, gname in self.param_grads},
+                float(os.environ.get("SOL_AR_BUCKET_MB", "25")) * 2 ** 20)
+        self.ar_buckets = len(self.ar_schedule)
+        grad_param = {gname: pname for pname, gname in self.param_grads}
 
-        def flush_bucket():
-            nonlocal pending, pending_bytes
-            if not pending:
-                return
-            for gname in pending:
-                n = self.params[grad_of[gname]].size
+        def issue_bucket(names):
+            for gname in names:
+                n = self.params[grad_param[gname]].size
                 L.check(lib.sol_b200_plan_add_allreduce(self.plan, self.buf[gname], n, L.DT_F32, 1.0 / o.world_size))
                 self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname, algo_bytes=4.0 * n))
-            self.ar_buckets += 1
-            pending, pending_bytes = [], 0.0
 
-        reduced = set()
-
-        def grads_done(names):
-            nonlocal pending_bytes
-            for nme in names:
-                if nme in grad_of and nme not in reduced:
-                    reduced.add(nme)
-                    pending.append(nme)
-                    pending_bytes += 4.0 * self.params[grad_of[nme]].size
-            if pending_bytes >= bucket_limit:
-                flush_bucket()
-
-        for u in self.units:
+        for ui, u in enumerate(self.units):
             out_buf(u.output)
-            if u.output in absorbed:
-                continue  # computed by its BatchNormBackX sibling's step
+            if u.output in absorbed:  # computed by its BatchNormBackX sibling's step
+                issue_bucket(self.ar_schedule.get(ui, ()))
+                continue
             mod = create_module(g, u, self.dtype, [n for n in u.inputs if n in direct])
             ids = [self.buf[n] for n in list(u.inputs) + list(u.params)] + [self.buf[u.output]]
             if u.output in act_sibs:
@@ -225,9 +233,7 @@ class OptimizedModel:
                 mod.n_args += bin(mask).count("1")
                 ids += [out_buf(x) for x in (gam, bet) if x]
             add_step(mod, ids, StepInfo("unit", "", u.output, node_ids=list(u.node_ids)))
-            grads_done([u.output] + [x for x in siblings.get(u.output, ()) if x])
-        grads_done([gn for gn in grad_of if gn not in reduced])  # (none expected) after every unit
-        flush_bucket()
+            issue_bucket(self.ar_schedule.get(ui, ()))
         # graph outputs: canonical f32 copies for the host
         self.out_canon: Dict[str, int] = {}
         for name in g.outputs:
@@ -263,7 +269,8 @@ class OptimizedModel:
         self.stream = C.c_void_p()
         L.check(lib.sol_b200_plan_stream(self.plan, C.byref(self.stream)))
         # pinned staging for the host interface
-        self.pin_in = {n: PinnedBuffer(4 * m.numel) for n, m in self.inputs.items()}
+        self.pin_in = {n: [PinnedBuffer(4 * m.numel) for _ in range(2)] for n, m in self.inputs.items()}
+        self._slot, self._slot_ticket = 0, [None, None]
         self.pin_out = {n: PinnedBuffer(4 * g.meta_of(n).numel) for n in g.outputs}
 
     def _direct_stem_inputs(self):
@@ -283,49 +290,6 @@ class OptimizedModel:
                     and n0.attrs.out_channels == 64 and n0.attrs.kw <= 8 and n0.attrs.kh * 32 <= 256
                     and sum(1 for n in u.node_ids for i in g.find_node(n).inputs if i == gi.name) == 1):
                 out.add(gi.name)
-        return out
-
-    def _activation_siblings(self):
-        """DFP unit output -> (ReLU unit output, mask) where a single-op ReLU / ReLU6 unit reads the
-        output of a straight-line BatchNorm [+ Add] unit (training graphs keep them apart because
-        ReluBack needs the pre-activation tensor): one kernel writes both tensors."""
-        g = self.graph
-        by_out = {u.output: u for u in self.units}
-        out = {}
-        for u in self.units:
-            if u.kind != "dfp" or len(u.node_ids) != 1:
-                continue
-            n = g.find_node(u.node_ids[0])
-            if n.op not in ("ReLU", "ReLU6"):
-                continue
-            p = by_out.get(n.inputs[0])
-            if p is None or p.kind != "dfp" or p.output in out:
-                continue
-            ops = [g.find_node(i).op for i in p.node_ids]
-            if ops not in (["BatchNorm2d"], ["BatchNorm2d", "Add"]):
-                continue
-            out[p.output] = (u.output, 4 if n.op == "ReLU" else 8)
-        return out
-
-    def _bn_back_siblings(self):
-        """BatchNormBackX unit output -> (BatchNormBackGamma output, BatchNormBackBeta output) of the
-        same BatchNorm (same delta and x inputs); each sibling is a single-op unit."""
-        g = self.graph
-        single = {}
-        for u in self.units:
-            if len(u.node_ids) == 1:
-                n = g.find_node(u.node_ids[0])
-                if n.op in ("BatchNormBackX", "BatchNormBackGamma", "BatchNormBackBeta"):
-                    single[u.output] = n
-        xs = {nm: n for nm, n in single.items() if n.op == "BatchNormBackX"}
-        out = {}
-        for nm, nx in xs.items():
-            gam = next((k for k, n in single.items() if n.op == "BatchNormBackGamma"
-                        and list(n.inputs[:2]) == list(nx.inputs[:2])), None)
-            bet = next((k for k, n in single.items() if n.op == "BatchNormBackBeta"
-                        and n.inputs[0] == nx.inputs[0]), None)
-            if gam or bet:
-                out[nm] = (gam, bet)
         return out
 
     def _upload_params(self):
@@ -359,29 +323,56 @@ class OptimizedModel:
             out[name] = pb.view(np.float32, arr.shape).copy()
         return out
 
-    def set_inputs(self, inputs: Dict[str, np.ndarray]):
-        lib = L.lib()
+    def _validated(self, inputs: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
+        out = {}
         for name, meta in self.inputs.items():
             if name not in inputs:
                 raise KeyError(f"missing graph input '{name}'")
             a = np.asarray(inputs[name], np.float32)
             if a.size != meta.numel:
                 raise ValueError(f"input '{name}' size mismatch")
-            self.pin_in[name].view(np.float32, meta.shape)[...] = a.reshape(meta.shape)
-        for name, meta in self.inputs.items():
-            L.check(lib.sol_b200_plan_h2d(self.plan, self.in_canon[name], self.pin_in[name].ptr, 4 * meta.numel))
+            out[name] = a.reshape(meta.shape)
+        return out
+
+    def _wait_slot(self, k: int):
+        """The pinned staging slot k is free once the copy that last read it has completed."""
+        t = self._slot_ticket[k]
+        if t is not None:
+            L.check(L.lib().sol_b200_plan_copy_wait(self.plan, t))
+            self._slot_ticket[k] = None
+
+    def input_buffers(self) -> Dict[str, np.ndarray]:
+        """Zero-copy serving: writable views of the free pinned staging slot (canonical NCHW f32).
+        A data loader fills them in place, then stage_inputs() (no argument) ships them. Blocks only
+        if the copy that last read this slot (two stages ago) is still running."""
+        k = self._slot
+        self._wait_slot(k)
+        return {n: self.pin_in[n][k].view(np.float32, m.shape) for n, m in self.inputs.items()}
 
     def stage_inputs(self, inputs: Optional[Dict[str, np.ndarray]] = None):
-        """Pipelined serving: (optionally fill the pinned input buffers, then) start the host-to-device
-        copy for the NEXT run() on the plan's copy stream. It overlaps the kernels of the run in
-        flight; the next run() first moves the staged batch into the plan's input buffers."""
+        """Pipelined serving: (optionally fill the free pinned slot -- a parallel host copy --, then)
+        start the host-to-device copy for the NEXT run() on the plan's copy stream. It overlaps the
+        kernels of the run in flight; the next run() first moves the staged batch into the plan's
+        input buffers. The two pinned slots alternate, and a slot is refilled only after the copy
+        that read it completed (copy-stream fence), so staging batch i+1 never corrupts batch i."""
         lib = L.lib()
+        k = self._slot
+        self._wait_slot(k)
         if inputs is not None:
+            arrs = self._validated(inputs)
             for name, meta in self.inputs.items():
-                self.pin_in[name].view(np.float32, meta.shape)[...] = np.asarray(inputs[name], np.float32).reshape(
-                    meta.shape)
+                parallel_copy(self.pin_in[name][k].view(np.float32, meta.shape), arrs[name])
         for name, meta in self.inputs.items():
-            L.check(lib.sol_b200_plan_stage_h2d(self.plan, self.in_canon[name], self.pin_in[name].ptr, 4 * meta.numel))
+            L.check(lib.sol_b200_plan_stage_h2d(self.plan, self.in_canon[name], self.pin_in[name][k].ptr,
+                                                4 * meta.numel))
+        t = C.c_uint64()
+        L.check(lib.sol_b200_plan_copy_fence(self.plan, C.byref(t)))
+        self._slot_ticket[k] = t.value
+        self._slot ^= 1
+
+    def set_inputs(self, inputs: Dict[str, np.ndarray]):
+        """Inputs of the next run() (host, canonical layout): staged through the pinned slots."""
+        self.stage_inputs(inputs)
 
     def run(self):
         """One pass of the plan on its stream (no host synchronisation)."""
@@ -396,13 +387,19 @@ class OptimizedModel:
             return
         L.check(lib.sol_b200_plan_run(self.plan, int(use_graph)))
 
-    def fetch_outputs(self, names=None) -> Dict[str, np.ndarray]:
+    def enqueue_fetch(self, names=None):
+        """Device-to-host copies of outputs into the pinned output buffers, ordered on the plan
+        stream after the runs already issued (no host synchronisation)."""
         lib = L.lib()
         names = list(self.graph.outputs) if names is None else names
         for n in names:
             meta = self.graph.meta_of(n)
             L.check(lib.sol_b200_plan_d2h(self.plan, self.pin_out[n].ptr, self.out_canon[n], 4 * meta.numel))
-        L.check(lib.sol_b200_plan_sync(self.plan))
+
+    def fetch_outputs(self, names=None) -> Dict[str, np.ndarray]:
+        names = list(self.graph.outputs) if names is None else names
+        self.enqueue_fetch(names)
+        L.check(L.lib().sol_b200_plan_sync(self.plan))
         return {n: self.pin_out[n].view(np.float32, self.graph.meta_of(n).shape).copy() for n in names}
 
     def predict(self, inputs: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
@@ -464,6 +461,12 @@ class OptimizedModel:
     def sync(self):
         L.check(L.lib().sol_b200_plan_sync(self.plan))
 
+    def comm_info(self):
+        """(nranks, rank, cuda device) of the plan's NCCL communicator, as NCCL reports them."""
+        n, r, d = C.c_int32(), C.c_int32(), C.c_int32()
+        L.check(L.lib().sol_b200_plan_comm_info(self.plan, C.byref(n), C.byref(r), C.byref(d)))
+        return n.value, r.value, d.value
+
     def arena_bytes(self) -> int:
         v = C.c_uint64()
         L.check(L.lib().sol_b200_plan_arena_bytes(self.plan, C.byref(v)))
@@ -476,6 +479,65 @@ class OptimizedModel:
                 self.plan = None
         except Exception:
             pass
+
+
+def activation_siblings(g: ModelGraph, units: List[ExecUnit]) -> Dict[str, tuple]:
+    """DFP unit output -> (ReLU unit output, mask) where a single-op ReLU / ReLU6 unit reads the
+    output of a straight-line BatchNorm [+ Add] unit (training graphs keep them apart because
+    ReluBack needs the pre-activation tensor): one kernel writes both tensors."""
+    by_out = {u.output: u for u in units}
+    out = {}
+    for u in units:
+        if u.kind != "dfp" or len(u.node_ids) != 1:
+            continue
+        n = g.find_node(u.node_ids[0])
+        if n.op not in ("ReLU", "ReLU6"):
+            continue
+        p = by_out.get(n.inputs[0])
+        if p is None or p.kind != "dfp" or p.output in out:
+            continue
+        ops = [g.find_node(i).op for i in p.node_ids]
+        if ops not in (["BatchNorm2d"], ["BatchNorm2d", "Add"]):
+            continue
+        out[p.output] = (u.output, 4 if n.op == "ReLU" else 8)
+    return out
+
+
+def bn_back_siblings(g: ModelGraph, units: List[ExecUnit]) -> Dict[str, tuple]:
+    """BatchNormBackX unit output -> (BatchNormBackGamma output, BatchNormBackBeta output) of the
+    same BatchNorm (same delta and x inputs); each sibling is a single-op unit."""
+    single = {}
+    for u in units:
+        if len(u.node_ids) == 1:
+            n = g.find_node(u.node_ids[0])
+            if n.op in ("BatchNormBackX", "BatchNormBackGamma", "BatchNormBackBeta"):
+                single[u.output] = n
+    xs = {nm: n for nm, n in single.items() if n.op == "BatchNormBackX"}
+    out = {}
+    taken = set()
+    for nm, nx in xs.items():
+        gam = next((k for k, n in single.items() if n.op == "BatchNormBackGamma" and k not in taken
+                    and list(n.inputs[:2]) == list(nx.inputs[:2])), None)
+        # Beta reads only the delta, which two BatchNorms share behind an Add (residual block with
+        # a downsample branch): assign one-to-one so every Beta tensor has exactly one writer
+        bet = next((k for k, n in single.items() if n.op == "BatchNormBackBeta" and k not in taken
+                    and n.inputs[0] == nx.inputs[0]), None)
+        taken.update(k for k in (gam, bet) if k)
+        if gam or bet:
+            out[nm] = (gam, bet)
+    return out
+
+
+def gradient_completions(units: List[ExecUnit], siblings: Dict[str, tuple], absorbed) -> List[List[str]]:
+    """Per unit of the plan (in order): the tensors its step completes -- its own output plus the
+    BatchNormBackGamma/Beta siblings it writes; absorbed sibling units complete nothing."""
+    out = []
+    for u in units:
+        if u.output in absorbed:
+            out.append([])
+        else:
+            out.append([u.output] + [x for x in siblings.get(u.output, ()) if x])
+    return out
 
 
 def optimize(g: ModelGraph, options: OptimizeOptions) -> OptimizedModel:

@@ -159,6 +159,24 @@ def test_pipelined_staging_matches_predict(gpu):
         got.append(m.fetch_outputs(["prob"])["prob"])
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+    # serving order: the next batch is staged (pinned slot refilled on the host) while the current
+    # run is still in flight, BEFORE its outputs are fetched; each answer must still be its own
+    # batch's (the pinned slots alternate and are refilled only after their copy completed)
+    batches = [_inputs(gi, batch, seed=s) for s in range(20, 27)]
+    want = [m.predict(b)["prob"] for b in batches]
+    m.stage_inputs(batches[0])
+    for i in range(len(batches)):
+        m.run()
+        if i + 1 < len(batches):
+            m.stage_inputs(batches[i + 1])
+        assert np.array_equal(m.fetch_outputs(["prob"])["prob"], want[i]), i
+    # zero-copy slots: fill input_buffers() in place, then stage without an argument
+    for i in (3, 4):
+        for name, v in m.input_buffers().items():
+            v[...] = batches[i][name]
+        m.stage_inputs()
+        m.run()
+        assert np.array_equal(m.fetch_outputs(["prob"])["prob"], want[i]), i
 
 
 @pytest.mark.parametrize("stride,conv_bias", [(1, False), (2, False), (2, True)])
