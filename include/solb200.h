@@ -139,6 +139,10 @@ typedef struct {
 typedef struct {
     uint64_t h2d_bytes, d2h_bytes, h2d_ops, d2h_ops, packed_transfers, launches;
     double device_time_us;
+    /* allocator evidence (B200): pinned host slabs ever allocated for copy staging (a reusable
+       pool: constant once warm) and device arena slabs (the arena grows stream-ordered instead of
+       failing when full) */
+    uint64_t pinned_slabs, device_slabs;
 } sol_transfer_stats;
 
 const char* sol_b200_last_error(void);

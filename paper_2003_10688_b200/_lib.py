@@ -83,7 +83,7 @@ class ModuleInfo(C.Structure):
 class TransferStats(C.Structure):
     _fields_ = [("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("h2d_ops", C.c_uint64),
                 ("d2h_ops", C.c_uint64), ("packed_transfers", C.c_uint64), ("launches", C.c_uint64),
-                ("device_time_us", C.c_double)]
+                ("device_time_us", C.c_double), ("pinned_slabs", C.c_uint64), ("device_slabs", C.c_uint64)]
 
 
 class ConvDesc(C.Structure):

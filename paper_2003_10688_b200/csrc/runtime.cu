@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <tuple>
 
 #include "../../include/solb200.h"
 
@@ -32,9 +33,10 @@ Arena::~Arena() {
     if (base_) cudaFree(base_);
 }
 
-void Arena::init(size_t bytes) {
+void Arena::init(size_t bytes, cudaStream_t stream) {
     cap_ = round_up(static_cast<int64_t>(std::max<size_t>(bytes, kAlign)), kAlign);
-    SOL_CUDA(cudaMalloc(&base_, cap_));
+    if (stream) SOL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base_), cap_, stream));
+    else SOL_CUDA(cudaMalloc(&base_, cap_));
     free_.clear();
     live_.clear();
     free_[0] = cap_;
@@ -107,18 +109,44 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ staging, int n) {
 
 }  // namespace
 
+PinnedPool::~PinnedPool() {
+    for (auto& s : slabs_) cudaFreeHost(s.p);
+}
+
+void* PinnedPool::get(size_t bytes) {
+    bytes = static_cast<size_t>(round_up(static_cast<int64_t>(std::max<size_t>(bytes, 16)), 64));
+    for (; cur_ < slabs_.size(); ++cur_) {
+        Slab& s = slabs_[cur_];
+        if (s.cap - s.used >= bytes) {
+            void* p = s.p + s.used;
+            s.used += bytes;
+            return p;
+        }
+    }
+    const size_t cap = std::max<size_t>({bytes, slabs_.empty() ? size_t(1) << 20 : 2 * slabs_.back().cap});
+    Slab s{nullptr, cap, bytes};
+    SOL_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s.p), cap));
+    slabs_.push_back(s);
+    cur_ = slabs_.size() - 1;
+    return s.p;
+}
+
+void PinnedPool::reset() {
+    for (auto& s : slabs_) s.used = 0;
+    cur_ = 0;
+}
+
 Queue::Queue(int device, size_t arena_bytes, bool coalesce) : device_(device), coalesce_(coalesce) {
     SOL_CUDA(cudaSetDevice(device));
     SOL_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    arena_.init(arena_bytes ? arena_bytes : (256ull << 20));
+    slabs_.push_back(std::make_unique<Arena>());
+    slabs_.back()->init(arena_bytes ? arena_bytes : (256ull << 20));
     SOL_CUDA(cudaEventCreate(&ev_start_));
     SOL_CUDA(cudaEventCreate(&ev_end_));
 }
 
 Queue::~Queue() {
     cudaStreamSynchronize(stream_);
-    for (void* p : pinned_live_) cudaFreeHost(p);
-    for (auto& d : d2h_) cudaFreeHost(d.pinned);
     if (ev_start_) cudaEventDestroy(ev_start_);
     if (ev_end_) cudaEventDestroy(ev_end_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -148,16 +176,33 @@ uint8_t* Queue::resolve(uint64_t vptr, uint64_t bytes) {
         defer(SOL_E_OUT_OF_BOUNDS, "access beyond allocation " + std::to_string(ref));
         return nullptr;
     }
-    return arena_.base() + it->second.off + off;
+    return arena_ptr(it->second.slab, it->second.off) + off;
+}
+
+std::pair<int, int64_t> Queue::arena_alloc(size_t bytes) {
+    for (size_t i = 0; i < slabs_.size(); ++i) {
+        const int64_t off = slabs_[i]->alloc(bytes);
+        if (off >= 0) return {static_cast<int>(i), off};
+    }
+    // grow: a new slab from the stream-ordered allocator (never blocks the launch stream)
+    size_t biggest = 0;
+    for (auto& a : slabs_) biggest = std::max(biggest, a->capacity());
+    slabs_.push_back(std::make_unique<Arena>());
+    slabs_.back()->init(std::max(2 * biggest, bytes + kAlign), stream_);
+    const int64_t off = slabs_.back()->alloc(bytes);
+    if (off < 0) throw CudaError(static_cast<int>(cudaErrorMemoryAllocation), "device arena growth failed");
+    return {static_cast<int>(slabs_.size() - 1), off};
 }
 
 uint64_t Queue::malloc_async(uint64_t bytes) {
     if (bytes == 0 || bytes > 0xffffffffull) throw std::invalid_argument("malloc_async: bytes must be in (0, 2^32)");
     if (next_ref_ > 0xffffffffull) throw std::overflow_error("virtual pointer refs exhausted");
     const uint32_t ref = static_cast<uint32_t>(next_ref_++);
-    const int64_t off = arena_.alloc(bytes);
-    if (off < 0) throw CudaError(static_cast<int>(cudaErrorMemoryAllocation), "device arena exhausted");
-    allocs_[ref] = {off, bytes};
+    const auto [slab, off] = arena_alloc(bytes);
+    allocs_[ref] = {slab, off, bytes};
+    // fresh allocations read as zeros (the reference's allocs_[ref].resize(bytes), runtime.cpp:187);
+    // stream-ordered, so the host never waits
+    SOL_CUDA(cudaMemsetAsync(arena_ptr(slab, off), 0, bytes, stream_));
     freed_.erase(ref);
     return static_cast<uint64_t>(ref) << 32;
 }
@@ -172,17 +217,12 @@ void Queue::free_async(uint64_t vptr) {
         return;
     }
     close_copy_run();  // pending copies into this block must land before reuse
-    arena_.free(it->second.off);
+    slabs_[it->second.slab]->free(it->second.off);
     allocs_.erase(it);
     freed_[ref] = true;
 }
 
-void* Queue::staging(size_t bytes) {
-    void* p = nullptr;
-    SOL_CUDA(cudaMallocHost(&p, std::max<size_t>(bytes, 16)));
-    pinned_live_.push_back(p);
-    return p;
-}
+void* Queue::staging(size_t bytes) { return pinned_.get(bytes); }
 
 void Queue::memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes) {
     if (failed() || bytes == 0) return;
@@ -191,6 +231,13 @@ void Queue::memcpy_h2d(uint64_t dst, const void* src, uint64_t bytes) {
     mark_start();
     stats_.h2d_bytes += bytes;
     stats_.h2d_ops += 1;
+    // one packed transfer scatters its copies concurrently: a copy overlapping one already in the
+    // open run closes the run first, so the later copy still lands last (program order)
+    for (const PendingCopy& c : run_)
+        if (d < c.dst + c.bytes && c.dst < d + bytes) {
+            close_copy_run();
+            break;
+        }
     // snapshot now (reference: "H2D snapshots the host range at enqueue time")
     const uint64_t off = round_up(static_cast<int64_t>(run_payload_.size()), 16);
     run_payload_.resize(off + bytes);
@@ -210,14 +257,13 @@ void Queue::close_copy_run() {
         for (size_t i = 0; i < run_.size(); ++i)
             tab[i] = {reinterpret_cast<uint64_t>(run_[i].dst), tab_bytes + run_[i].off, run_[i].bytes};
         std::memcpy(host + tab_bytes, run_payload_.data(), total);
-        const int64_t doff = arena_.alloc(tab_bytes + total);
-        if (doff < 0) throw CudaError(static_cast<int>(cudaErrorMemoryAllocation), "device arena exhausted (staging)");
-        uint8_t* dev = arena_.base() + doff;
+        const auto [dslab, doff] = arena_alloc(tab_bytes + total);
+        uint8_t* dev = arena_ptr(dslab, doff);
         SOL_CUDA(cudaMemcpyAsync(dev, host, tab_bytes + total, cudaMemcpyHostToDevice, stream_));
         const int n = static_cast<int>(run_.size());
         scatter_kernel<<<std::min(n, 1024), 256, 0, stream_>>>(dev, n);
         SOL_CUDA(cudaGetLastError());
-        arena_.free(doff);  // stream-ordered: later users run after the scatter
+        slabs_[dslab]->free(doff);  // stream-ordered: later users run after the scatter
         stats_.packed_transfers += 1;
     } else {
         uint8_t* host = static_cast<uint8_t*>(staging(total));
@@ -235,8 +281,7 @@ void Queue::memcpy_d2h(void* dst, uint64_t src, uint64_t bytes) {
     if (!s) return;
     close_copy_run();
     mark_start();
-    void* pinned = nullptr;
-    SOL_CUDA(cudaMallocHost(&pinned, bytes));
+    void* pinned = staging(bytes);
     SOL_CUDA(cudaMemcpyAsync(pinned, s, bytes, cudaMemcpyDeviceToHost, stream_));
     d2h_.push_back({dst, pinned, bytes});
     stats_.d2h_bytes += bytes;
@@ -257,13 +302,12 @@ void Queue::launch(Module* m, const uint64_t* args, int nargs) {
     }
     const size_t need = m->scratch_bytes();
     if (need > scratch_bytes_) {
-        if (scratch_off_ >= 0) arena_.free(scratch_off_);
-        scratch_off_ = arena_.alloc(need);
-        if (scratch_off_ < 0) throw CudaError(static_cast<int>(cudaErrorMemoryAllocation), "arena exhausted (scratch)");
+        if (scratch_off_ >= 0) slabs_[scratch_slab_]->free(scratch_off_);
+        std::tie(scratch_slab_, scratch_off_) = arena_alloc(need);
         scratch_bytes_ = need;
     }
     mark_start();
-    m->run(ptrs.data(), nargs, scratch_off_ >= 0 ? arena_.base() + scratch_off_ : nullptr, stream_, false);
+    m->run(ptrs.data(), nargs, scratch_off_ >= 0 ? arena_ptr(scratch_slab_, scratch_off_) : nullptr, stream_, false);
     stats_.launches += 1;
 }
 
@@ -279,13 +323,9 @@ int Queue::synchronize(std::string* msg) {
         if (cudaEventElapsedTime(&ms, ev_start_, ev_end_) == cudaSuccess) stats_.device_time_us += ms * 1000.0;
         timing_ = false;
     }
-    for (auto& d : d2h_) {
-        std::memcpy(d.user, d.pinned, d.bytes);
-        cudaFreeHost(d.pinned);
-    }
+    for (auto& d : d2h_) std::memcpy(d.user, d.pinned, d.bytes);
     d2h_.clear();
-    for (void* p : pinned_live_) cudaFreeHost(p);
-    pinned_live_.clear();
+    pinned_.reset();  // the stream is idle: every staging slab is free again
     if (msg) *msg = err_.msg;
     return err_.code;
 }

@@ -18,7 +18,8 @@ class Arena {
 public:
     Arena() = default;
     ~Arena();
-    void init(size_t bytes);
+    // stream != nullptr: the slab comes from cudaMallocAsync on that stream (stream-ordered growth)
+    void init(size_t bytes, cudaStream_t stream = nullptr);
     // returns offset or -1 when full
     int64_t alloc(size_t bytes);
     void free(int64_t off);
@@ -31,6 +32,25 @@ private:
     size_t cap_ = 0, used_ = 0;
     std::map<int64_t, size_t> free_;   // offset -> size
     std::map<int64_t, size_t> live_;   // offset -> size
+};
+
+// Reusable page-locked staging for the queue's copies: slabs grow geometrically and are recycled
+// after every synchronize (the stream is idle then), so steady-state copies never call
+// cudaMallocHost (a slow, implicitly synchronising call).
+class PinnedPool {
+public:
+    ~PinnedPool();
+    void* get(size_t bytes);
+    void reset();
+    uint64_t slabs() const { return slabs_.size(); }
+
+private:
+    struct Slab {
+        uint8_t* p;
+        size_t cap, used;
+    };
+    std::vector<Slab> slabs_;
+    size_t cur_ = 0;
 };
 
 struct QueueErr {
@@ -50,14 +70,23 @@ public:
     void launch(Module* m, const uint64_t* args, int nargs);
     void barrier();
     int synchronize(std::string* msg);
-    sol_transfer_stats stats() const { return stats_; }
+    sol_transfer_stats stats() const {
+        sol_transfer_stats s = stats_;
+        s.pinned_slabs = pinned_.slabs();
+        s.device_slabs = slabs_.size();
+        return s;
+    }
     cudaStream_t stream() const { return stream_; }
 
 private:
     struct Alloc {
+        int slab;
         int64_t off;
         uint64_t bytes;
     };
+    // first fit over the arena slabs; a full arena grows by a new stream-ordered slab
+    std::pair<int, int64_t> arena_alloc(size_t bytes);
+    uint8_t* arena_ptr(int slab, int64_t off) const { return slabs_[slab]->base() + off; }
     // resolves to a device pointer; on failure records the deferred error and returns nullptr
     uint8_t* resolve(uint64_t vptr, uint64_t bytes);
     bool failed() const { return err_.code != 0; }
@@ -68,7 +97,8 @@ private:
 
     int device_;
     cudaStream_t stream_ = nullptr;
-    Arena arena_;
+    std::vector<std::unique_ptr<Arena>> slabs_;
+    PinnedPool pinned_;
     bool coalesce_;
     std::map<uint32_t, Alloc> allocs_;
     std::map<uint32_t, bool> freed_;
@@ -83,14 +113,13 @@ private:
     };
     std::vector<PendingCopy> run_;
     std::vector<uint8_t> run_payload_;
-    // pinned staging buffers released at synchronize
-    std::vector<void*> pinned_live_;
     struct D2H {
         void* user;
         void* pinned;
         uint64_t bytes;
     };
     std::vector<D2H> d2h_;
+    int scratch_slab_ = -1;
     int64_t scratch_off_ = -1;
     size_t scratch_bytes_ = 0;
     cudaEvent_t ev_start_ = nullptr, ev_end_ = nullptr;
