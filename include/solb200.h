@@ -158,6 +158,16 @@ int sol_b200_module_info(sol_b200_module_t m, sol_module_info* info);
  * single reduction pass; their buffers follow the output in the run arguments (n_args grows).
  * Returns SOL_E_UNSUPPORTED for modules that cannot. */
 int sol_b200_module_set_sibling_outputs(sol_b200_module_t m, int32_t mask);
+/* Module options. SOL_MODOPT_UPDATE_BN_RUNNING_STATS (value 0/1, default 0): a training
+ * BatchNorm2d unit also applies autodiff::update_bn_running_stats (autodiff.cpp:356-384: momentum,
+ * unbiased variance) to its running_mean / running_var parameters, in place, from the batch
+ * statistics it computes anyway. Off by default so module_run keeps interpret's purity contract;
+ * training plans turn it on. SOL_E_UNSUPPORTED when the option does not apply to the module. */
+/* SOL_MODOPT_TILE_N (conv / linear forward and the dual GEMM): the tcgen05 tile configuration,
+ * chosen by autotune: 0 = built-in heuristic (incl. the halo kernel for 64-channel 3x3 convs),
+ * 64 / 128 / 256 = N-tile width on the im2col / TMA path, 65 = 64-wide with resident weights. */
+enum { SOL_MODOPT_UPDATE_BN_RUNNING_STATS = 1, SOL_MODOPT_TILE_N = 2 };
+int sol_b200_module_set_option(sol_b200_module_t m, int32_t key, int32_t value);
 /* Raw-pointer launch on a CUDA stream (cudaStream_t passed as void*): args = bindings in order,
  * then the output; scratch must hold info.scratch_bytes. `frozen_params` lets a module cache
  * parameter-derived constants (BN coefficients, packed weights) across runs. */
@@ -228,6 +238,16 @@ int sol_b200_plan_set_comm(sol_b200_plan_t p, const uint8_t id[128], int32_t ran
    1 / 0 / the plan device when no communicator is attached. Bench evidence that N ranks really
    share one communicator on N distinct GPUs. */
 int sol_b200_plan_comm_info(sol_b200_plan_t p, int32_t* nranks, int32_t* rank, int32_t* cuda_device);
+
+/* ---- runtime knobs (fe::OptimizedModel::train_step(batch, lr, mode), autotune) ------------ */
+/* Sets the learning rate every SgdUpdate step of the plan reads at run time (a stream-ordered
+   device write, so captured graph replays see it); *n_steps = how many steps took it. */
+int sol_b200_plan_set_lr(sol_b200_plan_t p, float lr, int32_t* n_steps);
+/* Median device time (us) of module step `step` run alone `reps` times (after one warm-up run),
+   on the plan's buffers as they are: the measurement behind autotune (dnn.cpp:214-290). */
+int sol_b200_plan_time_step(sol_b200_plan_t p, int32_t step, int32_t reps, double* us);
+/* sol_b200_module_set_option on the module a plan step owns (the plan owns added modules). */
+int sol_b200_plan_step_set_option(sol_b200_plan_t p, int32_t step, int32_t key, int32_t value);
 
 /* ---- raw heavy-layer entry points (KernelProvider::execute on device pointers) ------------ */
 typedef struct {

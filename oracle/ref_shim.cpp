@@ -135,6 +135,15 @@ int solref_run_reference(void* h) {
     });
 }
 
+// autodiff::update_bn_running_stats (autodiff.cpp:356-384) on the session parameters from the last
+// run's environment (call solref_run_reference first).
+int solref_update_bn_running_stats(void* h) {
+    return guarded([&] {
+        auto* s = static_cast<Session*>(h);
+        autodiff::update_bn_running_stats(s->g, s->g.params, s->env);
+    });
+}
+
 // The reference's compiled f32 CPU path: partition -> DFP kernels via lower_group/run_kernel,
 // heavy layers via the builtin providers' heuristic choice. Runs on the current session graph
 // (call solref_pipeline first to apply the reference passes).

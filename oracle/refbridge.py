@@ -48,7 +48,7 @@ def lib():
         L.solref_load.restype = ctypes.c_void_p
         L.solref_load.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_int]
         L.solref_free.argtypes = [ctypes.c_void_p]
-        for f in ("solref_pipeline", "solref_run_reference", "solref_run_compiled"):
+        for f in ("solref_pipeline", "solref_run_reference", "solref_run_compiled", "solref_update_bn_running_stats"):
             getattr(L, f).argtypes = [ctypes.c_void_p]
         L.solref_set_input.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64]
         L.solref_set_param.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64]
@@ -110,6 +110,9 @@ class RefSession:
 
     def run_compiled(self):
         _check(lib().solref_run_compiled(self.h))
+
+    def update_bn_running_stats(self):
+        _check(lib().solref_update_bn_running_stats(self.h))
 
     def get(self, name: str, shape=None) -> np.ndarray:
         n = lib().solref_numel(self.h, name.encode())

@@ -445,3 +445,24 @@ def run_graph(g, inputs: Dict[str, np.ndarray], store_f32: bool = True) -> Dict[
         out = eval_node(n, [env[i] for i in n.inputs], params, g)
         env[n.id] = np.asarray(out, np.float32).astype(np.float64) if store_f32 else np.asarray(out)
     return env
+
+
+def update_bn_running_stats(g, params: Dict[str, np.ndarray], env: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
+    """autodiff.cpp:356-384: for every training BatchNorm2d, running_mean <- (1-m) rm + m mean and
+    running_var <- (1-m) rv + m var_biased * count/(count-1), statistics of the BN input in f64 over
+    all non-channel positions. Returns the updated parameter dict (inputs untouched)."""
+    out = dict(params)
+    for n in g.nodes:
+        if n.op != "BatchNorm2d" or not n.attrs.training:
+            continue
+        x = np.asarray(env[n.inputs[0]], np.float64)
+        axes = (0,) + tuple(range(2, x.ndim))
+        count = x.size // x.shape[1]
+        mean = x.mean(axis=axes)
+        var = ((x - mean.reshape((1, -1) + (1,) * (x.ndim - 2))) ** 2).sum(axis=axes)
+        unbias = count / (count - 1) if count > 1 else 1.0
+        mom = n.attrs.momentum
+        rm, rv = n.params[2], n.params[3]
+        out[rm] = ((1 - mom) * np.asarray(params[rm], np.float64) + mom * mean).astype(np.float32)
+        out[rv] = ((1 - mom) * np.asarray(params[rv], np.float64) + mom * (var / count) * unbias).astype(np.float32)
+    return out

@@ -22,6 +22,9 @@ SOL_E_OUT_OF_REFS = 14
 SOL_E_NCCL = 50
 SOL_E_CUDA = 100
 
+MODOPT_UPDATE_BN_RUNNING_STATS = 1
+MODOPT_TILE_N = 2
+
 DT_F32 = 0
 DT_BF16 = 1
 MAX_OP_IN = 40
@@ -43,7 +46,8 @@ SYMBOLS = [
     "sol_b200_plan_h2d", "sol_b200_plan_d2h", "sol_b200_plan_event_record", "sol_b200_plan_event_elapsed",
     "sol_b200_host_alloc", "sol_b200_host_free", "sol_b200_set_conv_debug", "sol_b200_plan_stage_h2d",
     "sol_b200_module_set_sibling_outputs", "sol_b200_plan_comm_info",
-    "sol_b200_plan_copy_fence", "sol_b200_plan_copy_wait",
+    "sol_b200_plan_copy_fence", "sol_b200_plan_copy_wait", "sol_b200_module_set_option",
+    "sol_b200_plan_set_lr", "sol_b200_plan_time_step", "sol_b200_plan_step_set_option",
 ]
 
 
@@ -166,6 +170,10 @@ def lib():
             "sol_b200_plan_copy_fence": [vp, C.POINTER(C.c_uint64)],
             "sol_b200_plan_copy_wait": [vp, u64],
             "sol_b200_module_set_sibling_outputs": [vp, i32],
+            "sol_b200_module_set_option": [vp, i32, i32],
+            "sol_b200_plan_set_lr": [vp, C.c_float, C.POINTER(i32)],
+            "sol_b200_plan_time_step": [vp, i32, i32, C.POINTER(C.c_double)],
+            "sol_b200_plan_step_set_option": [vp, i32, i32, i32],
             "sol_b200_plan_d2h": [vp, vp, i32, u64],
             "sol_b200_plan_event_record": [vp, i32],
             "sol_b200_plan_event_elapsed": [vp, i32, i32, C.POINTER(C.c_float)],

@@ -132,6 +132,13 @@ int sol_b200_module_info(sol_b200_module_t m, sol_module_info* info) {
     });
 }
 
+int sol_b200_module_set_option(sol_b200_module_t m, int32_t key, int32_t value) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null module");
+        if (!m->m->set_option(key, value)) throw solb200::UnsupportedError("module option does not apply");
+    });
+}
+
 int sol_b200_module_set_sibling_outputs(sol_b200_module_t m, int32_t mask) {
     return guard([&] {
         if (!m) throw std::invalid_argument("null module");
@@ -350,6 +357,23 @@ int sol_b200_nccl_unique_id(uint8_t id[128]) {
 
 int sol_b200_plan_set_comm(sol_b200_plan_t p, const uint8_t id[128], int32_t rank, int32_t nranks) {
     return guard([&] { p->p->set_comm(id, rank, nranks); });
+}
+
+int sol_b200_plan_set_lr(sol_b200_plan_t p, float lr, int32_t* n_steps) {
+    return guard([&] {
+        const int n = p->p->set_lr(lr);
+        if (n_steps) *n_steps = n;
+    });
+}
+
+int sol_b200_plan_time_step(sol_b200_plan_t p, int32_t step, int32_t reps, double* us) {
+    return guard([&] { *us = p->p->time_step(step, reps); });
+}
+
+int sol_b200_plan_step_set_option(sol_b200_plan_t p, int32_t step, int32_t key, int32_t value) {
+    return guard([&] {
+        if (!p->p->step_set_option(step, key, value)) throw solb200::UnsupportedError("module option does not apply");
+    });
 }
 
 int sol_b200_plan_comm_info(sol_b200_plan_t p, int32_t* nranks, int32_t* rank, int32_t* cuda_device) {

@@ -166,12 +166,15 @@ void bn_infer_coef(const float* gamma, const float* beta, const float* mean, con
 void bn_shift(int dtype, const void* x, int ld, int C, float* shift, cudaStream_t s);
 
 // w -= lr * g over n f32 elements (SgdUpdate, reference.cpp:580-584); optional bf16 mirror.
-void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror_bf16, cudaStream_t s);
+// lr_dev (optional): the learning rate read from device memory at run time (plan_set_lr), else lr
+void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror_bf16, cudaStream_t s,
+                const float* lr_dev = nullptr);
 // One launch updating many parameters: w_i -= lr * g_i for i < count (multi-tensor SGD).
 constexpr int SGD_MULTI_MAX = 512;
 struct SgdMultiArgs {
     int count = 0;
     float lr = 0.f;
+    const float* lr_dev = nullptr;  // when set, the learning rate is read from device memory
     float* w[SGD_MULTI_MAX];
     const float* g[SGD_MULTI_MAX];
     int64_t n[SGD_MULTI_MAX];

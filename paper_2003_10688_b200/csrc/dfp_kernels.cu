@@ -2332,7 +2332,8 @@ __global__ void bn_shift_kernel(const T* x, int ld, int C, float* shift) {
 }
 
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, int64_t n, float lr,
-                           __nv_bfloat16* mirror) {
+                           __nv_bfloat16* mirror, const float* lr_dev) {
+    if (lr_dev) lr = *lr_dev;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const float v = w[i] - lr * g[i];
@@ -2513,17 +2514,18 @@ __global__ void __launch_bounds__(256) sgd_multi_kernel(const __grid_constant__ 
     float* w = a.w[t];
     const float* g = a.g[t];
     const int64_t n = a.n[t];
+    const float lr = a.lr_dev ? *a.lr_dev : a.lr;
     if (base + 4 <= n && (reinterpret_cast<uintptr_t>(w + base) & 15) == 0 &&
         (reinterpret_cast<uintptr_t>(g + base) & 15) == 0) {
         float4 wv = *reinterpret_cast<float4*>(w + base);
         const float4 gv = __ldg(reinterpret_cast<const float4*>(g + base));
-        wv.x -= a.lr * gv.x;
-        wv.y -= a.lr * gv.y;
-        wv.z -= a.lr * gv.z;
-        wv.w -= a.lr * gv.w;
+        wv.x -= lr * gv.x;
+        wv.y -= lr * gv.y;
+        wv.z -= lr * gv.z;
+        wv.w -= lr * gv.w;
         *reinterpret_cast<float4*>(w + base) = wv;
     } else {
-        for (int64_t i = base; i < base + 4 && i < n; ++i) w[i] = w[i] - a.lr * g[i];
+        for (int64_t i = base; i < base + 4 && i < n; ++i) w[i] = w[i] - lr * g[i];
     }
 }
 
@@ -2562,8 +2564,8 @@ void subpixel_interleave(int dtype, const InterleaveArgs& a, cudaStream_t s) {
     SOL_CUDA(cudaGetLastError());
 }
 
-void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror, cudaStream_t s) {
-    sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, g, n, lr, static_cast<__nv_bfloat16*>(mirror));
+void sgd_update(float* w, const float* g, int64_t n, float lr, void* mirror, cudaStream_t s, const float* lr_dev) {
+    sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, g, n, lr, static_cast<__nv_bfloat16*>(mirror), lr_dev);
     SOL_CUDA(cudaGetLastError());
 }
 

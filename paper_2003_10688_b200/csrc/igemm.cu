@@ -777,6 +777,17 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
 
 template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
+    if (a.tile_n) {  // autotuned choice
+        if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
+            if (a.tile_n == 65 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX) return launch_ws_t<T, TO, 64, MODE, true>(a, s);
+        }
+        switch (a.tile_n) {
+            case 64: case 65: return launch_ws_t<T, TO, 64, MODE>(a, s);
+            case 128: return launch_ws_t<T, TO, 128, MODE>(a, s);
+            case 256: return launch_ws_t<T, TO, 256, MODE>(a, s);
+            default: throw std::invalid_argument("igemm: tile_n must be 0, 64, 65, 128 or 256");
+        }
+    }
     if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
         const int bn = igemm_block_n(a.Nout);
         static const bool no_resb = std::getenv("SOL_NO_RESB") != nullptr;
@@ -811,7 +822,7 @@ void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
             // 256-wide single-accumulator tiles halve the A re-reads of the wide (N >= 1024)
             // stride-2 tails (ResNet-50 l3.0 / l4.0: -8 us each); SOL_DUAL_BN256=0/1 forces off/on
             static const char* bn256_env = std::getenv("SOL_DUAL_BN256");
-            const bool bn256 = bn256_env ? bn256_env[0] == '1' : a.Nout >= 1024;
+            const bool bn256 = a.tile_n ? a.tile_n == 256 : (bn256_env ? bn256_env[0] == '1' : a.Nout >= 1024);
             if (a.Nout > 128 && bn256) return launch_ws_t<T, TO, 256, IG_DUAL>(a, s);
             if (a.Nout > 64) return launch_ws_t<T, TO, 128, IG_DUAL>(a, s);
             return dispatch_ws<T, TO, IG_DUAL>(a, s);
@@ -1135,7 +1146,7 @@ void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.src2 && (a.SC % 64 || a.SC2 % 64 || a.K1 != a.SC || a.K_pad != a.SC + a.SC2 || a.mode != IG_FPROP))
         throw std::invalid_argument("igemm: dual GEMM needs two 1x1 convs over 128-byte channel blocks");
-    if (!a.src2 && halo_supported(a)) return halo_launch(a, s);
+    if (!a.src2 && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
         else dispatch_mode<__nv_bfloat16, float>(a, s);

@@ -54,6 +54,9 @@ struct IgemmArgs {
     // pooled tensor [N, OH/2, OW/2, ldo] (OH, OW = the conv's output grid, both even)
     int pool3s2 = 0;
     float pool_min_init = -INFINITY;  // the MaxPool2d min_init (0 after the relu-into-pool pass)
+    // autotune override (SOL_MODOPT_TILE_N): 0 = heuristic; 64 / 128 / 256 = that N-tile width;
+    // 65 = 64-wide with the weights resident in shared memory (RESB)
+    int tile_n = 0;
 };
 
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).

@@ -193,10 +193,17 @@ public:
         g.SW2 = static_cast<int>(in2_.W);
         g.SC2 = static_cast<int>(in2_.C);
         g.s2 = s2_;
+        g.tile_n = tile_n_;
         igemm_launch(g, s);
+    }
+    bool set_option(int key, int value) override {
+        if (key != SOL_MODOPT_TILE_N || (value != 0 && value != 128 && value != 256)) return false;
+        tile_n_ = value;
+        return true;
     }
 
 private:
+    int tile_n_ = 0;
     int dtype_, act_ = 0, i1_ = -1, i2_ = -1, s2_ = 1, cout_ = 0;
     Geo in1_, in2_, out_;
     int w1_ = -1, cb1_ = -1, w2_ = -1, cb2_ = -1, bn1_[4] = {}, bn2_[4] = {};
@@ -559,6 +566,7 @@ public:
                     g.ld_res = static_cast<int>(out_.ld);
                 }
                 g.act = act_;
+                g.tile_n = tile_n_;
                 if (stem_) stem_launch(g, s);
                 else igemm_launch(g, s);
                 break;
@@ -618,8 +626,16 @@ public:
             }
         }
     }
+    bool set_option(int key, int value) override {
+        if (key != SOL_MODOPT_TILE_N || stem_ || (op_ != SOL_OP_CONV2D && op_ != SOL_OP_LINEAR)) return false;
+        if (value != 0 && value != 64 && value != 65 && value != 128 && value != 256) return false;
+        if (value == 65 && dtype_ != DT_BF16) return false;
+        tile_n_ = value;
+        return true;
+    }
 
 private:
+    int tile_n_ = 0;  // autotuned tcgen05 tile (SOL_MODOPT_TILE_N)
     int dtype_;
     int op_;
     int kh_, kw_, sh_, sw_, ph_, pw_;
@@ -746,18 +762,26 @@ public:
         lr_ = d.ops[0].attrs.lr;
         n_ = param_numel(d.bindings[d.ops[0].inputs[0]]);
         algo_bytes = 12.0 * n_;
+        lr_dev_ = static_cast<float*>(dev_alloc(4));
+        SOL_CUDA(cudaMemcpy(lr_dev_, &lr_, 4, cudaMemcpyHostToDevice));
+    }
+    bool set_lr(float lr, cudaStream_t s) override {
+        lr_ = lr;
+        SOL_CUDA(cudaMemcpyAsync(lr_dev_, &lr_, 4, cudaMemcpyHostToDevice, s));
+        return true;
     }
     void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
         if (nargs != n_args) throw std::invalid_argument("sgd: wrong argument count");
         float* w = static_cast<float*>(args[0]);
         float* o = static_cast<float*>(args[2]);
         if (o != w) SOL_CUDA(cudaMemcpyAsync(o, w, n_ * 4, cudaMemcpyDeviceToDevice, s));
-        sgd_update(o, static_cast<const float*>(args[1]), n_, lr_, nullptr, s);
+        sgd_update(o, static_cast<const float*>(args[1]), n_, lr_, nullptr, s, lr_dev_);
     }
 
 private:
     float lr_;
     int64_t n_;
+    float* lr_dev_ = nullptr;
 };
 
 // Many SgdUpdate ops in one unit (plan-level multi-tensor update): bindings are (param, grad)
@@ -782,6 +806,14 @@ public:
             algo_bytes += 12.0 * a_.n[i];
         }
         a_.block0[d.n_ops] = blocks;
+        lr_dev_ = static_cast<float*>(dev_alloc(4));
+        SOL_CUDA(cudaMemcpy(lr_dev_, &a_.lr, 4, cudaMemcpyHostToDevice));
+        a_.lr_dev = lr_dev_;
+    }
+    bool set_lr(float lr, cudaStream_t s) override {
+        a_.lr = lr;
+        SOL_CUDA(cudaMemcpyAsync(lr_dev_, &a_.lr, 4, cudaMemcpyHostToDevice, s));
+        return true;
     }
     void run(void* const* args, int nargs, void*, cudaStream_t s, bool) override {
         if (nargs != n_args) throw std::invalid_argument("sgd: wrong argument count");
@@ -795,6 +827,7 @@ public:
 
 private:
     SgdMultiArgs a_;
+    float* lr_dev_ = nullptr;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -972,8 +1005,17 @@ public:
         arg_bytes.push_back(arg_bytes.back());
         return true;
     }
+    bool set_option(int key, int value) override {
+        if (key != SOL_MODOPT_UPDATE_BN_RUNNING_STATS) return false;
+        bool any = false;
+        for (const auto& b : bn_) any |= b.training && b.m >= 0 && b.v >= 0;
+        if (!any) return false;
+        update_running_ = value != 0;
+        return true;
+    }
 
 private:
+    bool update_running_ = false;  // training BN: update running_mean / running_var in place
     struct SlotSrc {
         int binding;
     };
@@ -982,6 +1024,7 @@ private:
         int x_binding;      // training: the BN input (boundary binding)
         int g, b, m, v;     // param bindings
         float eps;
+        float momentum;     // training: running-statistics update (autodiff.cpp:356-384)
         int C;
         float* coef;        // [3C] (mean, scale, beta) -> P[3i], P[3i+1], P[3i+2]
         float* shift;
@@ -1232,6 +1275,7 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
         b.m = o.n_params > 2 ? o.params[2] : -1;
         b.v = o.n_params > 3 ? o.params[3] : -1;
         b.eps = o.attrs.eps;
+        b.momentum = o.attrs.momentum;
         const Geo xg = geo_ref(o.inputs[0]);
         b.C = static_cast<int>(xg.C);
         b.coef = static_cast<float*>(dev_alloc(5 * b.C * 4));
@@ -1456,6 +1500,13 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
         f.beta = static_cast<const float*>(args[b.b]);
         f.stats_out = b.stats;
         f.coef = b.coef;
+        // update_bn_running_stats (autodiff.cpp:356-384): momentum, unbiased variance, in place on
+        // the running_mean / running_var parameters, from the same f64 batch statistics
+        if (b.m >= 0 && b.v >= 0 && update_running_) {
+            f.running_mean = static_cast<float*>(args[b.m]);
+            f.running_var = static_cast<float*>(args[b.v]);
+            f.momentum = b.momentum;
+        }
         dfp_finalize(f, s);
     }
     for (auto& w : dw_) {

@@ -27,6 +27,10 @@ public:
     // Extra outputs written by this module on behalf of sibling units (mask bits; see
     // sol_b200_module_set_sibling_outputs). Returns false if the module cannot produce them.
     virtual bool set_sibling_outputs(int mask) { return mask == 0; }
+    // Module options (SOL_MODOPT_*); returns false when the option does not apply to the module.
+    virtual bool set_option(int key, int value) { return false; }
+    // Runtime learning rate of SgdUpdate modules (stream-ordered device write; graph replays read it).
+    virtual bool set_lr(float lr, cudaStream_t s) { return false; }
 
     std::string family;
     int n_args = 0;

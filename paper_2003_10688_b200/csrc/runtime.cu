@@ -709,6 +709,48 @@ void Plan::set_comm(const uint8_t id[128], int rank, int nranks) {
     nranks_ = nranks;
 }
 
+int Plan::set_lr(float lr) {
+    SOL_CUDA(cudaSetDevice(device_));
+    int n = 0;
+    for (auto& s : steps_)
+        if (s.module && s.module->set_lr(lr, stream_)) ++n;
+    return n;
+}
+
+double Plan::time_step(int i, int reps) {
+    if (!finalized_) finalize();
+    if (i < 0 || i >= static_cast<int>(steps_.size()) || !steps_[i].module) throw std::invalid_argument("time_step: not a module step");
+    SOL_CUDA(cudaSetDevice(device_));
+    cudaEvent_t a, b;
+    SOL_CUDA(cudaEventCreate(&a));
+    SOL_CUDA(cudaEventCreate(&b));
+    std::vector<float> t;
+    run_step(steps_[i], stream_);  // warm-up (first-run caches)
+    for (int r = 0; r < std::max(reps, 1); ++r) {
+        SOL_CUDA(cudaEventRecord(a, stream_));
+        run_step(steps_[i], stream_);
+        SOL_CUDA(cudaEventRecord(b, stream_));
+        SOL_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        SOL_CUDA(cudaEventElapsedTime(&ms, a, b));
+        t.push_back(ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(t.begin(), t.end());
+    return 1000.0 * t[t.size() / 2];
+}
+
+bool Plan::step_set_option(int i, int key, int value) {
+    if (i < 0 || i >= static_cast<int>(steps_.size()) || !steps_[i].module) throw std::invalid_argument("not a module step");
+    const bool ok = steps_[i].module->set_option(key, value);
+    if (ok && graph_exec_) {  // a captured graph holds the old launch configuration
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+    }
+    return ok;
+}
+
 void Plan::comm_info(int* nranks, int* rank, int* cuda_device) const {
     *nranks = 1;
     *rank = 0;

@@ -145,6 +145,9 @@ public:
     uint64_t arena_bytes() const { return total_; }
     void set_comm(const uint8_t id[128], int rank, int nranks);
     void comm_info(int* nranks, int* rank, int* cuda_device) const;
+    int set_lr(float lr);  // SgdUpdate steps' runtime learning rate; returns how many steps took it
+    double time_step(int i, int reps);  // median device time (us) of step i run alone, eagerly
+    bool step_set_option(int i, int key, int value);
     void h2d(int id, const void* src, uint64_t bytes);
     void stage_h2d(int id, const void* src, uint64_t bytes);
     // host-side fences on the copy stream: a ticket taken after stage_h2d() calls is complete once

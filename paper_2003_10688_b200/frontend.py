@@ -14,8 +14,14 @@ tensor-core GEMMs); parameters are f32 master copies in the reference's canonica
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
+import enum
+import hashlib
+import json
 import os
+import threading
 import time
+import weakref
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional
 
@@ -49,6 +55,18 @@ class OptimizeOptions:
     fuse_bn_backward: bool = True  # training: BatchNormBackX also writes its Gamma/Beta siblings
     multi_sgd: bool = True         # training: every SgdUpdate in one multi-tensor launch
     nccl_allreduce: bool = False   # test hook: run the NCCL gradient all-reduce even with one replica
+    update_bn_stats: bool = True   # training: update BN running_mean / running_var on the device
+                                   # (autodiff::update_bn_running_stats, autodiff.cpp:356-384)
+    autotune: bool = False         # measure the tcgen05 tile configs of every conv/linear (dnn.cpp:214-290)
+    tune_budget: int = 5           # measured runs per candidate (median; one warm-up besides)
+    tune_cache_path: Optional[str] = None  # persistent TuneCache JSON (None: process-wide, in memory)
+    cache: bool = True             # optimize() returns the live model compiled for the same graph+options
+
+    def fingerprint(self) -> str:
+        """fe::OptimizeOptions::fingerprint (frontend.hpp:35): every field that changes the plan."""
+        d = {k: v for k, v in self.__dict__.items() if k not in ("nccl_id", "tune_cache_path", "cache")}
+        d["env"] = sorted((k, v) for k, v in os.environ.items() if k.startswith("SOL_"))
+        return json.dumps(d, sort_keys=True, default=str)
 
 
 @dataclass
@@ -105,7 +123,12 @@ class PinnedBuffer:
             pass
 
 
-class OptimizedModel:
+class DevicePlan:
+    """One compiled plan on one device (fe::DevicePlan / Step, frontend.hpp:41-61): the compiled
+    graph, its units, one plan buffer per tensor, one step per unit module, optionally the gradient
+    all-reduce buckets and the SGD step; executed by libsolb200 (eagerly, or replayed as a CUDA
+    graph). OptimizedModel owns one per mode (forward, training)."""
+
     def __init__(self, g: ModelGraph, options: OptimizeOptions):
         t0 = time.perf_counter()
         self.options = options
@@ -137,6 +160,8 @@ class OptimizedModel:
                 self.units = fuse_stem_pool(cg, self.units, self._direct_stem_inputs())
         self.params: Dict[str, np.ndarray] = {k: np.asarray(v, np.float32).copy() for k, v in g.params.items()}
         self._build_plan()
+        self.lr = options.lr
+        self.tuner_runs, self.tune_cache_hits, self.tuned = 0, 0, {}
         self.compile_ms = (time.perf_counter() - t0) * 1e3
 
     # ------------------------------------------------------------------------------------------
@@ -220,6 +245,9 @@ class OptimizedModel:
                 issue_bucket(self.ar_schedule.get(ui, ()))
                 continue
             mod = create_module(g, u, self.dtype, [n for n in u.inputs if n in direct])
+            if o.train and o.update_bn_stats and any(
+                    g.find_node(n).op == "BatchNorm2d" and g.find_node(n).attrs.training for n in u.node_ids):
+                L.check(lib.sol_b200_module_set_option(mod.handle, L.MODOPT_UPDATE_BN_RUNNING_STATS, 1))
             ids = [self.buf[n] for n in list(u.inputs) + list(u.params)] + [self.buf[u.output]]
             if u.output in act_sibs:
                 relu_out, mask = act_sibs[u.output]
@@ -292,36 +320,59 @@ class OptimizedModel:
                 out.add(gi.name)
         return out
 
-    def _upload_params(self):
+    def _upload_params(self, names=None):
+        """Host master parameters -> plan buffers (one pinned staging area, one sync). Frozen
+        parameter caches (packed weights, folded BN) are rebuilt by the next (eager) run."""
         lib = L.lib()
-        for name, arr in self.params.items():
-            pb = PinnedBuffer(arr.nbytes)
-            pb.view(np.float32, arr.shape)[...] = arr
-            L.check(lib.sol_b200_plan_h2d(self.plan, self.buf[name], pb.ptr, arr.nbytes))
-            L.check(lib.sol_b200_plan_sync(self.plan))
+        names = list(self.params) if names is None else list(names)
+        total = sum(self.params[n].nbytes for n in names)
+        pb = PinnedBuffer(max(total, 16))
+        off = 0
+        for name in names:
+            arr = self.params[name]
+            pb.u8[off:off + arr.nbytes] = np.ascontiguousarray(arr, np.float32).view(np.uint8).ravel()
+            L.check(lib.sol_b200_plan_h2d(self.plan, self.buf[name], pb.ptr.value + off, arr.nbytes))
+            off += arr.nbytes
+        L.check(lib.sol_b200_plan_sync(self.plan))
         L.check(lib.sol_b200_plan_set_frozen(self.plan, 0))
         self._frozen = False
+        self._ran = False
+
+    def download_params(self, names=None) -> Dict[str, np.ndarray]:
+        """Plan parameter buffers -> host arrays (one pinned staging area, one sync)."""
+        lib = L.lib()
+        names = list(self.params) if names is None else list(names)
+        total = sum(self.params[n].nbytes for n in names)
+        pb = PinnedBuffer(max(total, 16))
+        offs, off = {}, 0
+        for name in names:
+            arr = self.params[name]
+            L.check(lib.sol_b200_plan_d2h(self.plan, pb.ptr.value + off, self.buf[name], arr.nbytes))
+            offs[name] = off
+            off += arr.nbytes
+        L.check(lib.sol_b200_plan_sync(self.plan))
+        return {n: pb.u8[offs[n]:offs[n] + self.params[n].nbytes].view(np.float32).reshape(self.params[n].shape).copy()
+                for n in names}
+
+    def set_lr(self, lr: float) -> int:
+        """Runtime learning rate of the plan's SgdUpdate steps (stream-ordered device write)."""
+        n = C.c_int32()
+        L.check(L.lib().sol_b200_plan_set_lr(self.plan, float(lr), C.byref(n)))
+        self.lr = float(lr)
+        return n.value
 
     # ------------------------------------------------------------------------------------------
     def load_state(self, params: Dict[str, np.ndarray]):
-        """Replaces the master parameters (frontend.hpp:115); device caches are rebuilt."""
+        """Replaces this plan's parameters; device caches are rebuilt."""
         for k, v in params.items():
             if k not in self.params or self.params[k].shape != np.shape(v):
                 raise ValueError(f"parameter {k} mismatch")
             self.params[k] = np.asarray(v, np.float32).copy()
-        self._upload_params()
-        self._ran = False
+        self._upload_params(params.keys())
 
     def host_params(self) -> Dict[str, np.ndarray]:
-        """Pulls device parameters back (frontend.hpp:127-128: sync_host_params)."""
-        lib = L.lib()
-        out = {}
-        for name, arr in self.params.items():
-            pb = PinnedBuffer(arr.nbytes)
-            L.check(lib.sol_b200_plan_d2h(self.plan, pb.ptr, self.buf[name], arr.nbytes))
-            L.check(lib.sol_b200_plan_sync(self.plan))
-            out[name] = pb.view(np.float32, arr.shape).copy()
-        return out
+        """This plan's device parameters, pulled back."""
+        return self.download_params()
 
     def _validated(self, inputs: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
         out = {}
@@ -384,6 +435,8 @@ class OptimizedModel:
             self._ran = True
             if not self.options.train:
                 L.check(lib.sol_b200_plan_set_frozen(self.plan, 1))
+            if self.options.autotune and not self.tuned:
+                autotune(self)
             return
         L.check(lib.sol_b200_plan_run(self.plan, int(use_graph)))
 
@@ -540,9 +593,436 @@ def gradient_completions(units: List[ExecUnit], siblings: Dict[str, tuple], abso
     return out
 
 
+# ------------------------------------------------------------------------------------------------
+# autotune over B200 tile configurations (dnn::TuneCache / autotune, dnn.hpp:99-131, dnn.cpp:117-290)
+# ------------------------------------------------------------------------------------------------
+
+TUNE_VERSION = 1
+TILE_CANDIDATES = {"conv": (0, 64, 65, 128, 256), "dual": (0, 128, 256)}
+
+
+class TuneCache:
+    """dnn::TuneCache (dnn.hpp:104-121): winners keyed by layer hyperparameters (never node ids),
+    concurrent readers / exclusive writers, persisted as versioned JSON. A value is
+    {"choice": {"tile_n": T}, "micros": t}."""
+
+    def __init__(self):
+        self._mu = threading.Lock()
+        self._entries: Dict[str, dict] = {}
+
+    @staticmethod
+    def key(g: ModelGraph, unit: ExecUnit, dtype: int, device: str) -> str:
+        parts = [device, f"dt{dtype}"]
+        for nid in unit.node_ids:
+            n = g.find_node(nid)
+            a = n.attrs
+            parts.append(f"{n.op}:{a.out_channels},{a.out_features},{a.kh},{a.kw},{a.sh},{a.sw},{a.ph},{a.pw},"
+                         f"{a.groups},{int(a.has_bias)}")
+        for nm in unit.inputs:
+            parts.append("x" + "x".join(str(v) for v in g.meta_of(nm).shape))
+        return "|".join(parts)
+
+    def find(self, key: str) -> Optional[dict]:
+        with self._mu:
+            e = self._entries.get(key)
+            return dict(e) if e else None
+
+    def put(self, key: str, entry: dict):
+        with self._mu:
+            self._entries[key] = dict(entry)
+
+    def size(self) -> int:
+        with self._mu:
+            return len(self._entries)
+
+    def load(self, path: str):
+        """A missing file leaves the cache empty; another format version is ignored."""
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except FileNotFoundError:
+            return
+        if d.get("version") != TUNE_VERSION:
+            return
+        with self._mu:
+            self._entries.update(d.get("entries", {}))
+
+    def save(self, path: str):
+        with self._mu:
+            d = {"version": TUNE_VERSION, "entries": dict(sorted(self._entries.items()))}
+        tmp = path + ".tmp"
+        with open(tmp, "w") as f:
+            json.dump(d, f, indent=1)
+        os.replace(tmp, path)
+
+
+_TUNE_CACHE = TuneCache()
+
+
+def _device_name(dev: int) -> str:
+    try:
+        import torch
+        return torch.cuda.get_device_name(dev)
+    except Exception:
+        return "cuda"
+
+
+def autotune(plan: "DevicePlan", cache: Optional[TuneCache] = None) -> Dict[int, dict]:
+    """For every conv / linear forward step (and dual-GEMM tail) of a plan that has run once: time
+    each B200 tile configuration (SOL_MODOPT_TILE_N) with the step alone on the plan's own buffers,
+    keep the median of `tune_budget` runs, select the fastest, memoise it under the layer's
+    hyperparameter key (dnn.cpp:214-290). Cache hits skip the measurement."""
+    o = plan.options
+    lib = L.lib()
+    cache = cache or _TUNE_CACHE
+    if o.tune_cache_path:
+        cache.load(o.tune_cache_path)
+    dev = _device_name(o.device)
+    heavy_units = {u.output: u for u in plan.units if u.kind == "dnn"}
+    out = {}
+    for i, st in enumerate(plan.steps):
+        if st.kind != "unit" or st.output not in heavy_units:
+            continue
+        u = heavy_units[st.output]
+        fam = st.family
+        if not (fam.startswith("conv_fprop") or fam.startswith("linear")):
+            continue
+        cands = TILE_CANDIDATES["dual" if len(u.node_ids) >= 5 and fam == "conv_fprop_fused_tcgen05"
+                                and sum(plan.graph.find_node(n).op == "Conv2d" for n in u.node_ids) == 2
+                                else "conv"]
+        key = TuneCache.key(plan.graph, u, plan.dtype, dev)
+        hit = cache.find(key)
+        if hit is not None:
+            rc = lib.sol_b200_plan_step_set_option(plan.plan, i, L.MODOPT_TILE_N, int(hit["choice"]["tile_n"]))
+            if rc == L.SOL_OK:
+                plan.tune_cache_hits += 1
+                out[i] = hit
+                continue
+        times = {}
+        for t in cands:
+            if lib.sol_b200_plan_step_set_option(plan.plan, i, L.MODOPT_TILE_N, t) != L.SOL_OK:
+                continue
+            us = C.c_double()
+            L.check(lib.sol_b200_plan_time_step(plan.plan, i, max(1, o.tune_budget), C.byref(us)))
+            plan.tuner_runs += max(1, o.tune_budget) + 1
+            times[t] = us.value
+        if not times:
+            continue
+        best = min(times, key=lambda t: (times[t], t != 0))  # ties keep the heuristic
+        L.check(lib.sol_b200_plan_step_set_option(plan.plan, i, L.MODOPT_TILE_N, best))
+        entry = {"choice": {"tile_n": best}, "micros": times[best], "candidates": {str(k): v for k, v in times.items()}}
+        cache.put(key, entry)
+        out[i] = entry
+    if o.tune_cache_path:
+        cache.save(o.tune_cache_path)
+    plan.tuned = out or {"none": True}
+    return out
+
+
+# ------------------------------------------------------------------------------------------------
+# the network API: fe::OptimizedModel (frontend.hpp:104-165)
+# ------------------------------------------------------------------------------------------------
+
+class TrainMode(enum.Enum):
+    """fe::TrainMode (frontend.hpp:38)."""
+    TRANSPARENT = 0  # forward + backward on the device, gradients round-trip, SGD on the host
+    NATIVE = 1       # the whole step, SGD included, on the device
+
+
+@dataclass
+class CompileSummary:
+    """fe::CompileSummary (frontend.hpp:63-69)."""
+    units: int = 0
+    dfp_units: int = 0
+    dnn_units: int = 0
+    kernels: int = 0
+    reorders: int = 0
+    tuner_runs: int = 0
+    tune_cache_hits: int = 0
+    compile_ms: float = 0.0
+    cached: bool = False
+
+
+class OptimizedModel:
+    """fe::OptimizedModel over the B200 backend: a host master copy of the parameters, a forward
+    plan and (for training models) a training plan, each with its parameter context -- the version
+    of the host parameters its device buffers hold (ParamContext, frontend.hpp:137-145): a plan is
+    re-uploaded only when the host parameters moved past it. After native training steps the
+    training plan's device parameters are authoritative until sync_host_params() pulls them.
+
+    Attribute access not defined here goes to the primary plan (the training plan of a training
+    model, else the forward plan): run / stage_inputs / profile / steps / units / graph ..."""
+
+    def __init__(self, g: ModelGraph, options: OptimizeOptions):
+        t0 = time.perf_counter()
+        self.__dict__["_plans"] = {}
+        self.base = g
+        self.options = options
+        self.params: Dict[str, np.ndarray] = {k: np.asarray(v, np.float32).copy() for k, v in g.params.items()}
+        self.param_version = 1
+        self._ctx: Dict[bool, int] = {}         # plan (training?) -> parameter version it holds
+        self._device_authoritative = False      # the training plan holds newer parameters
+        self._mu = threading.RLock()
+        self._primary = bool(options.train)
+        self._plan(self._primary)
+        self.summary = self._summarize((time.perf_counter() - t0) * 1e3)
+
+    def __getattr__(self, name):
+        plans = self.__dict__.get("_plans")
+        if not plans:
+            raise AttributeError(name)
+        return getattr(plans[self.__dict__["_primary"]], name)
+
+    # -- plans and parameter contexts ----------------------------------------------------------
+    def _plan(self, training: bool) -> DevicePlan:
+        if training not in self._plans:
+            if training and not self.options.train:
+                raise RuntimeError("model was not compiled for training")
+            opts = dataclasses.replace(self.options, train=training)
+            if not training:
+                opts.world_size, opts.nccl_allreduce = 1, False
+            p = DevicePlan(self.base if training else forward_graph(self.base), opts)
+            self._plans[training] = p
+            # a new plan holds the base graph's parameters: version 1 (ensure_context uploads newer)
+            self._ctx[training] = 1
+        return self._plans[training]
+
+    def plan(self, training: bool = False) -> DevicePlan:
+        """The device plan for inference or training (frontend.hpp:112), compiled on first use."""
+        with self._mu:
+            return self._plan(training)
+
+    def _ensure_context(self, training: bool) -> DevicePlan:
+        """ensure_context (frontend.hpp:145): the plan holds the current parameters."""
+        p = self._plan(training)
+        if self._device_authoritative and not training:
+            self.sync_host_params()
+        if self._ctx.get(training) != self.param_version:
+            p.params = {k: v.copy() for k, v in self.params.items()}
+            p._upload_params()
+            self._ctx[training] = self.param_version
+        return p
+
+    # -- API ------------------------------------------------------------------------------------
+    def load_state(self, params: Dict[str, np.ndarray]):
+        """Replaces the host master parameters; every device context invalidates (frontend.hpp:115)."""
+        with self._mu:
+            for k, v in params.items():
+                if k not in self.params or self.params[k].shape != np.shape(v):
+                    raise ValueError(f"parameter {k} mismatch")
+            for k, v in params.items():
+                self.params[k] = np.asarray(v, np.float32).copy()
+            self._device_authoritative = False
+            self.param_version += 1
+            self._ensure_context(self._primary)
+
+    def predict(self, inputs: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
+        """Inference (frontend.hpp:119): host inputs in, canonical host outputs back. A training
+        model runs its forward plan, synchronised with the latest trained parameters."""
+        with self._mu:
+            return self._ensure_context(False).predict(inputs)
+
+    def train_step(self, batch: Dict[str, np.ndarray], lr: Optional[float] = None,
+                   mode: TrainMode = TrainMode.NATIVE) -> float:
+        """One SGD step, returns the loss (frontend.hpp:121-123). NATIVE: forward, backward,
+        gradient all-reduce, SGD and the BN running statistics all on the device. TRANSPARENT:
+        the device computes loss and gradients (its SGD runs with lr 0), the gradients come back
+        and the host applies theta - lr * g in f32 (autodiff::sgd_step, autodiff.cpp:331-354)."""
+        if not self.options.train:
+            raise RuntimeError("model was not compiled for training")
+        lr = self.options.lr if lr is None else float(lr)
+        with self._mu:
+            p = self._ensure_context(True)
+            if mode == TrainMode.NATIVE:
+                if p.lr != lr:
+                    p.set_lr(lr)
+                loss = p.train_step(batch)
+                self.param_version += 1
+                self._ctx[True] = self.param_version
+                self._device_authoritative = True
+                return loss
+            if p.lr != 0.0:
+                p.set_lr(0.0)
+            loss = p.train_step(batch)
+            grads = p.gradients()
+            self._device_authoritative = True
+            self.sync_host_params()  # running statistics (and the unchanged weights)
+            lr32 = np.float32(lr)
+            for name, gr in grads.items():
+                self.params[name] = (self.params[name] - lr32 * gr.astype(np.float32)).astype(np.float32)
+            self.param_version += 1
+            p.params = {k: v.copy() for k, v in self.params.items()}
+            p._upload_params(grads.keys())
+            self._ctx[True] = self.param_version
+            return loss
+
+    def sync_host_params(self):
+        """Pulls the device-resident parameters into the host master copy after native training
+        (frontend.hpp:127); a no-op when the host copy is current."""
+        with self._mu:
+            if not self._device_authoritative:
+                return
+            got = self._plans[True].download_params()
+            for k, v in got.items():
+                self.params[k] = v
+            self._plans[True].params = {k: v.copy() for k, v in got.items()}
+            self._device_authoritative = False
+            self._ctx[True] = self.param_version
+
+    def host_params(self) -> Dict[str, np.ndarray]:
+        """The host master parameters, synchronised first (frontend.hpp:128)."""
+        with self._mu:
+            self.sync_host_params()
+            return {k: v.copy() for k, v in self.params.items()}
+
+    def gradients(self) -> Dict[str, np.ndarray]:
+        return self._plan(True).gradients()
+
+    def export_bundle(self, directory: str, force: bool = False) -> str:
+        """frontend.hpp:131: manifest + weights (SOLW) of a self-contained deployment bundle; returns
+        the manifest path. run_bundle() replays it bit-identically to this model's predict()."""
+        from .graph import model_to_json, weights_to_bytes
+        man = os.path.join(directory, "manifest.json")
+        if os.path.exists(man) and not force:
+            raise FileExistsError(f"{man} exists (force=True overwrites)")
+        os.makedirs(directory, exist_ok=True)
+        with self._mu:
+            self.sync_host_params()
+            fwd = self._plan(False)
+            params = {k: v.copy() for k, v in self.params.items()}
+        g = forward_graph(self.base)
+        g2 = ModelGraph(graph_inputs=g.graph_inputs, nodes=g.nodes, outputs=g.outputs, params=params)
+        with open(os.path.join(directory, "weights.solw"), "wb") as f:
+            f.write(weights_to_bytes(params))
+        opts = {k: v for k, v in dataclasses.asdict(self.options).items()
+                if k not in ("nccl_id", "world_size", "rank", "nccl_allreduce", "train", "device", "tune_cache_path",
+                             "cache", "autotune")}
+        manifest = {
+            "format": "solb200-bundle", "version": 1,
+            "library_sha256": library_sha256(),
+            "model": json.loads(model_to_json(g2)),
+            "weights": "weights.solw",
+            "options": opts,
+            "env": {k: v for k, v in os.environ.items() if k.startswith("SOL_")},
+            "plan": {"units": [[u.kind, list(u.node_ids), u.output] for u in fwd.units],
+                     "steps": [[st.kind, st.family, st.output] for st in fwd.steps],
+                     "tiles": {str(k): v["choice"]["tile_n"] for k, v in fwd.tuned.items() if k != "none"}},
+            "inputs": {n: list(m.shape) for n, m in fwd.inputs.items()},
+            "outputs": list(fwd.graph.outputs),
+        }
+        with open(man, "w") as f:
+            json.dump(manifest, f, indent=1)
+        return man
+
+    def _summarize(self, ms: float) -> CompileSummary:
+        p = self._plans[self._primary]
+        return CompileSummary(units=len(p.units), dfp_units=sum(u.kind == "dfp" for u in p.units),
+                              dnn_units=sum(u.kind == "dnn" for u in p.units),
+                              kernels=sum(st.launches for st in p.steps if st.kind != "allreduce"),
+                              reorders=sum(st.kind == "reorder" for st in p.steps),
+                              tuner_runs=p.tuner_runs, tune_cache_hits=p.tune_cache_hits, compile_ms=ms)
+
+
+def forward_graph(g: ModelGraph) -> ModelGraph:
+    """The inference graph of a training model: a CrossEntropyLoss output is replaced by its
+    prediction input, and graph inputs only the loss read (the labels) are dropped."""
+    losses = [n for n in g.nodes if n.op == "CrossEntropyLoss" and n.id in g.outputs]
+    if not losses:
+        return g
+    drop = {n.id for n in losses}
+    outs = []
+    for o in g.outputs:
+        if o in drop:
+            p = g.find_node(o).inputs[0]
+            if p not in outs:
+                outs.append(p)
+        elif o not in outs:
+            outs.append(o)
+    nodes = [n for n in g.nodes if n.id not in drop]
+    used = {i for n in nodes for i in n.inputs} | set(outs)
+    return ModelGraph([gi for gi in g.graph_inputs if gi.name in used], nodes, outs, g.params)
+
+
+def library_sha256() -> str:
+    h = hashlib.sha256()
+    with open(L.LIB_PATH, "rb") as f:
+        for chunk in iter(lambda: f.read(1 << 20), b""):
+            h.update(chunk)
+    return h.hexdigest()
+
+
+def run_bundle(directory: str, inputs: Dict[str, np.ndarray], device: int = 0,
+               allow_other_library: bool = False) -> Dict[str, np.ndarray]:
+    """fe::run_bundle (frontend.hpp:180): replays an exported bundle -- the same plan (verified
+    unit by unit and step by step against the manifest) with the same kernels (library hash) and
+    tile choices -- so the outputs are bit-identical to the exporting model's predict()."""
+    from .graph import model_from_json
+    with open(os.path.join(directory, "manifest.json")) as f:
+        man = json.load(f)
+    if man.get("format") != "solb200-bundle" or man.get("version") != 1:
+        raise ValueError("not a solb200 bundle (format / version)")
+    if man["library_sha256"] != library_sha256() and not allow_other_library:
+        raise RuntimeError("bundle was exported with another libsolb200 build (bit-identity not guaranteed)")
+    with open(os.path.join(directory, man["weights"]), "rb") as f:
+        g = model_from_json(json.dumps(man["model"]), f.read())
+    saved = {k: os.environ.get(k) for k in man.get("env", {})}
+    os.environ.update(man.get("env", {}))
+    try:
+        kw = dict(man["options"], device=device, train=False, cache=False, autotune=False)
+        opts = OptimizeOptions(**kw)
+        m = optimize(g, opts)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    fwd = m.plan(False)
+    units = [[u.kind, list(u.node_ids), u.output] for u in fwd.units]
+    steps = [[st.kind, st.family, st.output] for st in fwd.steps]
+    if units != man["plan"]["units"] or steps != man["plan"]["steps"]:
+        raise RuntimeError("bundle plan mismatch: the rebuilt plan differs from the exported one")
+    for k, t in man["plan"].get("tiles", {}).items():
+        L.check(L.lib().sol_b200_plan_step_set_option(fwd.plan, int(k), L.MODOPT_TILE_N, int(t)))
+    return m.predict(inputs)
+
+
+# compiled-model cache: (graph structure, options) -> live model (fe::Engine model cache,
+# frontend.hpp:93-94); weak, so a model no caller holds releases its device memory
+_MODEL_CACHE: "weakref.WeakValueDictionary[str, OptimizedModel]" = weakref.WeakValueDictionary()
+_CACHE_MU = threading.Lock()
+
+
+def _structure_key(g: ModelGraph, options: OptimizeOptions) -> str:
+    from .graph import model_to_json
+    h = hashlib.sha256(model_to_json(g).encode())
+    for k in sorted(g.params):
+        h.update(k.encode())
+        h.update(str(np.shape(g.params[k])).encode())
+    h.update(options.fingerprint().encode())
+    return h.hexdigest()
+
+
 def optimize(g: ModelGraph, options: OptimizeOptions) -> OptimizedModel:
-    """fe::optimize_graph (frontend.hpp:173-174)."""
-    return OptimizedModel(g, options)
+    """fe::optimize_graph (frontend.hpp:173-180): infer_shapes -> [build_training_graph] ->
+    run_pipeline -> partition -> module compile -> plan. Results are cached on (structure,
+    options): a repeated call returns the live cached model with `g`'s weights loaded
+    (summary.cached = True)."""
+    if not options.cache or options.world_size > 1:
+        return OptimizedModel(g, options)
+    key = _structure_key(g, options)
+    with _CACHE_MU:
+        m = _MODEL_CACHE.get(key)
+    if m is not None:
+        t0 = time.perf_counter()
+        if any(not np.array_equal(m.params[k], v) for k, v in g.params.items()):
+            m.load_state(g.params)
+        m.summary = dataclasses.replace(m.summary, cached=True, compile_ms=(time.perf_counter() - t0) * 1e3)
+        return m
+    m = OptimizedModel(g, options)
+    with _CACHE_MU:
+        _MODEL_CACHE[key] = m
+    return m
 
 
 def nccl_unique_id() -> bytes:

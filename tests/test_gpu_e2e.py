@@ -281,3 +281,38 @@ def test_stem_conv_pool_fusion(gpu, monkeypatch, hw):
     assert O.oracle_err(got, want) <= 1e-2
     if hw <= 64:  # the f64 oracle at 224x224 takes minutes; the unfused plan is oracle-checked elsewhere
         assert O.oracle_err(got, O.run_graph(gi, ins)["prob"]) <= 1e-2
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_train_step_updates_bn_running_stats(gpu, dtype):
+    """Native training applies update_bn_running_stats (autodiff.cpp:356-384) on the device: after
+    one step every running_mean / running_var equals the oracle's update computed from the plan's
+    own BatchNorm input tensors (f64 statistics, momentum 0.1, unbiased variance); a second step
+    applies it again; inference after training uses the updated statistics."""
+    import torch
+    from paper_2003_10688_b200 import dfp, frontend, graph, models
+    from tests.gpu_util import from_device
+    batch = 8
+    g = models.resnet(18, hw=32, classes=16, width=16, train=True)
+    m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype=dtype, train=True, lr=0.0, keep_all=True))
+    gi = graph.infer_shapes(g, batch)
+    ins = _inputs(gi, batch, seed=19)
+
+    def get(nm):
+        raw = m.read_tensor(nm)
+        f32 = dtype == "f32" or dfp.is_f32_tensor(m.graph, nm)
+        t = torch.from_numpy(raw.view(np.float32).copy() if f32 else raw.view(np.int16).copy())
+        return from_device(t if f32 else t.view(torch.bfloat16), m.graph.meta_of(nm)).astype(np.float64)
+
+    params = {k: v.copy() for k, v in g.params.items()}
+    for step in range(2):
+        m.train_step(ins)
+        env = {n.inputs[0]: get(n.inputs[0]) for n in m.graph.nodes if n.op == "BatchNorm2d" and n.attrs.training}
+        params = O.update_bn_running_stats(m.graph, params, env)
+        got = m.host_params()
+        names = [k for k in params if k.endswith(("running_mean", "running_var"))]
+        assert len(names) == 2 * sum(1 for n in m.graph.nodes if n.op == "BatchNorm2d")
+        for k in names:
+            np.testing.assert_allclose(got[k], params[k], rtol=2e-5, atol=1e-6, err_msg=f"step {step} {k}")
+        for k in names:
+            params[k] = got[k]  # the next step starts from the device's values

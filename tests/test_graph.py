@@ -136,3 +136,42 @@ def test_conv_epilogue_fusion():
             ops = [cg.find_node(n).op for n in u.node_ids]
             assert ops[0] in ("Conv2d", "Linear") and ops[1] == "BatchNorm2d"
             assert set(ops[2:]) <= {"Add", "ReLU", "ReLU6"}
+
+
+def test_tune_cache_roundtrip_and_version(tmp_path):
+    """dnn::TuneCache semantics (dnn.hpp:104-121): keyed by hyperparameters, persisted as
+    versioned JSON; a missing file is an empty cache, another version is ignored."""
+    import json
+    from paper_2003_10688_b200 import frontend, graph, models, partition
+    g = graph.infer_shapes(models.resnet(18, hw=32, classes=10, width=8), 2)
+    units = [u for u in partition.partition(g) if u.kind == "dnn"]
+    keys = {frontend.TuneCache.key(g, u, 1, "B200") for u in units}
+    assert len(keys) < len(units)  # repeated layer shapes share one key (no node ids in it)
+    c = frontend.TuneCache()
+    c.load(str(tmp_path / "missing.json"))
+    assert c.size() == 0
+    for i, k in enumerate(sorted(keys)):
+        c.put(k, {"choice": {"tile_n": 128}, "micros": float(i)})
+    p = str(tmp_path / "t.json")
+    c.save(p)
+    d = frontend.TuneCache()
+    d.load(p)
+    assert d.size() == len(keys) and d.find(sorted(keys)[1])["micros"] == 1.0
+    j = json.load(open(p))
+    j["version"] = 99
+    json.dump(j, open(p, "w"))
+    e = frontend.TuneCache()
+    e.load(p)
+    assert e.size() == 0
+
+
+def test_options_fingerprint_tracks_plan_fields(monkeypatch):
+    from paper_2003_10688_b200 import frontend
+    monkeypatch.delenv("SOL_NO_DUAL", raising=False)
+    a = frontend.OptimizeOptions(batch=4)
+    fp0 = a.fingerprint()
+    assert fp0 == frontend.OptimizeOptions(batch=4).fingerprint()
+    assert fp0 != frontend.OptimizeOptions(batch=8).fingerprint()
+    assert fp0 == frontend.OptimizeOptions(batch=4, tune_cache_path="/x").fingerprint()
+    monkeypatch.setenv("SOL_NO_DUAL", "1")  # plan-changing switches are part of the key
+    assert fp0 != a.fingerprint() and "SOL_NO_DUAL" in a.fingerprint()
