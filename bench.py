@@ -195,7 +195,20 @@ def run_reference_arm(args):
 # B200 arm
 # ------------------------------------------------------------------------------------------------
 
-def roofline_of(m, peaks, peaks_kind, families, bound):
+def conv_traffic_profile(key):
+    """ncu DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant conv
+    kernel, from the committed capture for THIS workload (profiles/conv_traffic_latest.json holds
+    one entry per workload key); None when no capture exists for it."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "conv_traffic_latest.json")) as f:
+            tj = json.load(f)
+    except Exception:
+        return None
+    e = tj.get(key) if isinstance(tj.get(key), dict) else (tj if tj.get("workload") == key else None)
+    return e.get("mean_dram_bytes_per_launch") if e else None
+
+
+def roofline_of(m, peaks, peaks_kind, families, bound, traffic=None):
     """Achieved throughput of one kernel family measured live with CUDA events around every plan
     step (one eager profiled pass): algorithmic FLOPs (or bytes) per launch / launch time."""
     times = m.profile()
@@ -213,14 +226,6 @@ def roofline_of(m, peaks, peaks_kind, families, bound):
     hbm_peak = peaks["hbm_gbs"] * 1e9
     sol_t = sum(max(st.algo_flops / tc_peak, st.algo_bytes / hbm_peak) for st, t in zip(info, times)
                 if st.family in families)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "conv_traffic_latest.json")) as f:
-            tj = json.load(f)
-        if bound == "tensor":
-            traffic = tj.get("mean_dram_bytes_per_launch")
-    except Exception:
-        pass
     if bound == "tensor":
         achieved = tot_w / (tot_t * 1e-6) / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
@@ -376,7 +381,8 @@ def run_b200(args):
     value = world * B / (dev_ms / 1e3)
     e2e = world * B / (e2e_ms / 1e3)
     conv_fams = {"conv_fprop_tcgen05", "conv_fprop_fused_tcgen05", "conv_stem_tcgen05", "conv_stem_fused_tcgen05"}
-    roof, times = roofline_of(m, peaks, peaks_kind, conv_fams, "tensor")
+    roof, times = roofline_of(m, peaks, peaks_kind, conv_fams, "tensor",
+                              traffic=conv_traffic_profile("resnet50_infer_b256_bf16"))
     dfp_fams = {s.family for s in m.steps if s.family.startswith("dfp_")}
     roof_dfp, _ = roofline_of(m, peaks, peaks_kind, dfp_fams, "hbm")
     fam_time = {}
@@ -412,6 +418,7 @@ def run_b200(args):
                  "family_ms_per_step": {k: round(v / 1e3, 3) for k, v in sorted(tfam.items(), key=lambda kv: -kv[1])[:8]}}
     if ctx.rank != 0:
         return
+    others = other_configs(args, peaks, peaks_kind, device) if (world == 1 and args.configs) else None
     os.sched_setaffinity(0, all_cpus)  # the CPU baseline uses every host core
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -436,6 +443,7 @@ def run_b200(args):
         "gpu_launches": launches_per_step * args.steps,
         "family_ms_per_step": {k: round(v / 1e3, 3) for k, v in sorted(fam_time.items(), key=lambda kv: -kv[1])[:8]},
         "train": train,
+        "other_configs": others,
     }
     print(json.dumps(line), flush=True)
 
@@ -458,6 +466,83 @@ def spawn_ranks(args):
     os.execv(sys.executable, cmd)
 
 
+OTHER_CONFIGS = [
+    # BASELINE.json configs beyond the headline (configs[2] inference, configs[3] training)
+    ("configs[0] small CNN f32 inference B=32 32x32", "small_cnn", 32, "f32", 32),
+    ("configs[1] ResNet-18 f32 (TF32 tensor cores) inference B=64 224x224", "resnet18", 64, "f32", 224),
+    ("configs[4] DenseNet-121 bf16 inference B=128/GPU 224x224", "densenet121", 128, "bf16", 224),
+    ("configs[4] MobileNet-V2 bf16 inference B=128/GPU 224x224", "mobilenet_v2", 128, "bf16", 224),
+    ("configs[4] DenseNet-121 bf16 inference B=16/GPU (global 128 on 8 GPUs)", "densenet121", 16, "bf16", 224),
+    ("configs[4] MobileNet-V2 bf16 inference B=16/GPU (global 128 on 8 GPUs)", "mobilenet_v2", 16, "bf16", 224),
+]
+
+
+def tf32_peak_tflops():
+    """Dense TF32 tensor-core peak measured here (cuBLAS via torch.matmul, 8192^3, best of 5): the
+    roofline denominator for the f32/TF32 configs (MEASURED_PEAKS.json has bf16 only)."""
+    import torch
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(2):
+            a @ b
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        return best
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+
+
+def other_configs(args, peaks, peaks_kind, device):
+    """Every other BASELINE config at full size on this GPU: device-timed images/s (inputs resident,
+    CUDA events on the plan stream) and the conv / DFP rooflines of each plan."""
+    from paper_2003_10688_b200 import frontend, models
+    out = []
+    tf32 = tf32_peak_tflops()
+    for name, model, B, dt, hw in OTHER_CONFIGS:
+        t0 = time.time()
+        try:
+            g = models.MODELS[model](hw=hw) if model == "small_cnn" else models.MODELS[model]()
+            m = frontend.optimize(g, frontend.OptimizeOptions(batch=B, dtype=dt, device=device, fuse_epilogue=True))
+            x = np.random.default_rng(7).uniform(-1, 1, (B, 3, hw, hw)).astype(np.float32)
+            m.set_inputs({"x": x})
+            for _ in range(max(args.warmup, 3)):
+                m.run()
+            m.sync()
+            k = max(3, min(args.steps, 10))
+            m.event(0)
+            for _ in range(k):
+                m.run()
+            m.event(1)
+            m.sync()
+            ms = m.elapsed_ms(0, 1) / k
+            pk = dict(peaks)
+            if dt == "f32":
+                pk["bf16_tflops_sustained"] = tf32  # TF32 tensor cores
+            conv = {f for f in (st.family for st in m.steps) if f.startswith(("conv_", "linear"))}
+            roof, _ = roofline_of(m, pk, peaks_kind if dt == "bf16" else "measured here (TF32 cuBLAS 8192^3)",
+                                  conv, "tensor")
+            dfp = {st.family for st in m.steps if st.family.startswith("dfp_")}
+            roof_d, _ = roofline_of(m, pk, peaks_kind, dfp, "hbm") if dfp else (None, None)
+            out.append({"workload": name, "value": B / (ms / 1e3), "unit": "images/s", "ms_per_step": ms,
+                        "per_gpu_batch": B, "dtype": dt if dt == "bf16" else "f32 (TF32 tensor cores)",
+                        "roofline_conv": roof, "roofline_dfp": roof_d, "units": len(m.units),
+                        "compile_s": round(time.time() - t0, 1)})
+            del m
+        except Exception as e:  # reported, never silently dropped
+            out.append({"workload": name, "error": f"{type(e).__name__}: {e}"})
+    return {"tf32_peak_tflops_measured": tf32, "configs": out}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -469,6 +554,8 @@ def main():
     ap.add_argument("--train-steps", type=int, default=10)
     ap.add_argument("--no-train", dest="train", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the other BASELINE configs (small CNN, ResNet-18 TF32, DenseNet-121, MobileNet-V2)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args)

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 
 namespace solb200 {
@@ -859,6 +860,118 @@ __global__ void __launch_bounds__(THREADS) pool3s2_row_kernel(const __grid_const
     }
 }
 
+// 3x3 / stride-2 pooling by bands of whole input rows staged in shared memory with 1-D bulk TMA
+// copies (cp.async.bulk + mbarrier): one block = one image's band of R output rows = 2R+1 input
+// rows (the stem pool: 5 x 14 KB). The copy engine keeps every SM's band loads in flight at once
+// (the thread-per-output-row kernel above is latency bound at ~52% of HBM); each output vector
+// then reads its 3x3 window from shared memory (a warp touches 4 x 128 B per wavefront).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <typename T, bool IS_MAX, bool BN0, int ACT>
+__global__ void __launch_bounds__(THREADS) pool3s2_bulk_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs,
+                                                                int R) {
+    // persistent: the block walks bands (image, R output rows) with stride gridDim.x through a
+    // 2-stage ring -- the bulk copies of band i+2 are in flight while band i is pooled
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    constexpr int V = VEC<T>;
+    const int cv = a.C / V;
+    const int bands = (a.OH + R - 1) / R;
+    const int64_t total = static_cast<int64_t>(a.N) * bands;
+    const int ldx = a.in_ld[cs.s0];
+    const int64_t row_elems = static_cast<int64_t>(a.W) * ldx;
+    const uint32_t row_bytes = static_cast<uint32_t>(row_elems * sizeof(T));
+    const uint32_t stage_bytes = static_cast<uint32_t>(2 * R + 1) * row_bytes;
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    const uint32_t tile_s = bar0 + 128;
+    T* out = static_cast<T*>(a.out) + a.out_coff;
+    auto geo = [&](int64_t band, int& n, int& oh0, int& nr, int& h0, int& r_lo, int& r_hi) {
+        n = static_cast<int>(band / bands);
+        oh0 = static_cast<int>(band % bands) * R;
+        nr = min(R, a.OH - oh0);
+        h0 = oh0 * 2 - a.ph;
+        r_lo = max(0, -h0);
+        r_hi = min(2 * nr + 1, a.H - h0);
+    };
+    auto issue = [&](int64_t band, int stage) {
+        int n, oh0, nr, h0, r_lo, r_hi;
+        geo(band, n, oh0, nr, h0, r_lo, r_hi);
+        const uint32_t bar = bar0 + 8 * stage;
+        asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+                     "r"(static_cast<uint32_t>(r_hi - r_lo) * row_bytes));
+        const T* src = static_cast<const T*>(a.in[cs.s0]) + (static_cast<int64_t>(n) * a.H + h0) * row_elems;
+        for (int r = r_lo; r < r_hi; ++r)
+            bulk_g2s(tile_s + stage * stage_bytes + r * row_bytes, src + r * row_elems, row_bytes, bar);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < 2; ++st) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8 * st));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        for (int st = 0; st < 2; ++st)
+            if (blockIdx.x + st * static_cast<int64_t>(gridDim.x) < total) issue(blockIdx.x + st * static_cast<int64_t>(gridDim.x), st);
+    }
+    __syncthreads();
+    int i = 0;
+    for (int64_t band = blockIdx.x; band < total; band += gridDim.x, ++i) {
+        const int stage = i & 1;
+        const uint32_t bar = bar0 + 8 * stage;
+        const uint32_t parity = (i >> 1) & 1;
+        asm volatile(
+            "{\n.reg .pred P1;\nWAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(bar), "r"(parity));
+        int n, oh0, nr, h0, r_lo, r_hi;
+        geo(band, n, oh0, nr, h0, r_lo, r_hi);
+        const T* tile = reinterpret_cast<const T*>(smem_raw + 128 + stage * stage_bytes);
+        const int items = nr * a.OW * cv;
+        for (int it = threadIdx.x; it < items; it += blockDim.x) {
+            const int cvec = it % cv;
+            const int rest = it / cv;
+            const int ow = rest % a.OW, r = rest / a.OW;
+            const int c = cvec * V;
+            BnRegs<T> bn;
+            if (BN0) bn.load(a.P, cs.bn0, c);
+            float m[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) m[q] = IS_MAX ? -INFINITY : 0.f;
+            int cnt = 0;
+#pragma unroll
+            for (int kr = 0; kr < 3; ++kr) {
+                const int rr = 2 * r + kr;
+                if (rr < r_lo || rr >= r_hi) continue;
+#pragma unroll
+                for (int kc = 0; kc < 3; ++kc) {
+                    const int iw = ow * 2 - a.pw + kc;
+                    if (iw < 0 || iw >= a.W) continue;
+                    ++cnt;
+                    float e[V];
+                    unpack16(*reinterpret_cast<const uint4*>(tile + rr * row_elems + static_cast<int64_t>(iw) * ldx + c),
+                             e, static_cast<T*>(nullptr));
+                    if (BN0) bn.apply(e);
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        if (ACT >= 1) e[q] = fmaxf(e[q], 0.f);
+                        if (ACT == 2) e[q] = fminf(e[q], 6.f);
+                        m[q] = IS_MAX ? fmaxf(m[q], e[q]) : m[q] + e[q];
+                    }
+                }
+            }
+            float o[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                if (IS_MAX) o[q] = fmaxf(m[q], a.min_init);
+                else o[q] = m[q] / static_cast<float>(a.count_padding ? 9 : cnt);
+            }
+            store16(out + ((static_cast<int64_t>(n) * a.OH + oh0 + r) * a.OW + ow) * a.out_ld + c, o);
+        }
+        __syncthreads();  // every thread is done with this stage: refill it
+        if (threadIdx.x == 0 && band + 2 * static_cast<int64_t>(gridDim.x) < total)
+            issue(band + 2 * static_cast<int64_t>(gridDim.x), stage);
+    }
+}
+
 // Global average pool over a straight-line source chain; warps stride over pixels so every
 // thread keeps several independent 16-byte loads in flight.
 template <typename T, bool BN0, bool ADD, bool BN1, int ACT>
@@ -963,8 +1076,39 @@ bool launch_pool_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
     (void)grid;
     const bool k3 = a.kh == 3 && a.kw == 3;
     if (k3 && a.sh == 2 && a.sw == 2 && a.ph <= 1 && a.pw <= 1) {
-        const unsigned gr = grid_for(static_cast<int64_t>(a.N) * a.OH * (a.C / VEC<T>), THREADS);
         const bool bb = c.bn0 >= 0;
+        // bands of input rows staged by bulk copies when R = 2 output rows fit 3 blocks per SM
+        static const int band_env = std::getenv("SOL_POOL_BAND") ? std::atoi(std::getenv("SOL_POOL_BAND")) : 1;
+        // blocks per SM of the persistent 2-stage ring; 0 (default, measured fastest on B200: 126 vs
+        // 150 us for the ResNet-50 stem pool) = one band per block, one stage, ~5 resident blocks
+        static const int bps_env = std::getenv("SOL_POOL_BPS") ? std::atoi(std::getenv("SOL_POOL_BPS")) : 0;
+        const int64_t row_bytes = static_cast<int64_t>(a.W) * a.in_ld[c.s0] * static_cast<int64_t>(sizeof(T));
+        const int R = band_env;
+        const int64_t bands = static_cast<int64_t>(a.N) * ((a.OH + R - 1) / R);
+        const unsigned gb = static_cast<unsigned>(
+            bps_env > 0 ? std::min<int64_t>(bands, static_cast<int64_t>(num_sms()) * bps_env) : bands);
+        const size_t smem = 128 + (gb < bands ? 2 : 1) * static_cast<size_t>(2 * R + 1) * row_bytes;
+        if (R > 0 && row_bytes % 16 == 0 && smem <= 227 * 1024 && (a.C / VEC<T>) <= THREADS) {
+#define SOL_PB(MX, B, A)                                                                                         \
+    do {                                                                                                         \
+        static std::once_flag once;                                                                              \
+        std::call_once(once, [] {                                                                                \
+            SOL_CUDA(cudaFuncSetAttribute(pool3s2_bulk_kernel<T, MX, B, A>,                                      \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));             \
+        });                                                                                                      \
+        pool3s2_bulk_kernel<T, MX, B, A><<<gb, THREADS, smem, s>>>(a, c, R);                                     \
+    } while (0)
+            if (a.pool_max) {
+                if (bb) { if (c.act == 0) SOL_PB(true, true, 0); else if (c.act == 1) SOL_PB(true, true, 1); else SOL_PB(true, true, 2); }
+                else { if (c.act == 0) SOL_PB(true, false, 0); else if (c.act == 1) SOL_PB(true, false, 1); else SOL_PB(true, false, 2); }
+            } else {
+                if (bb) { if (c.act == 0) SOL_PB(false, true, 0); else if (c.act == 1) SOL_PB(false, true, 1); else SOL_PB(false, true, 2); }
+                else { if (c.act == 0) SOL_PB(false, false, 0); else if (c.act == 1) SOL_PB(false, false, 1); else SOL_PB(false, false, 2); }
+            }
+#undef SOL_PB
+            return true;
+        }
+        const unsigned gr = grid_for(static_cast<int64_t>(a.N) * a.OH * (a.C / VEC<T>), THREADS);
 #define SOL_P3(MX, B, A) pool3s2_row_kernel<T, MX, B, A><<<gr, THREADS, 0, s>>>(a, c)
         if (a.pool_max) {
             if (bb) { if (c.act == 0) SOL_P3(true, true, 0); else if (c.act == 1) SOL_P3(true, true, 1); else SOL_P3(true, true, 2); }

@@ -379,3 +379,38 @@ def test_bench_train_plan_units_match_oracle(gpu, bench_train):
     print(f"full-size training plan: {checked} distinct units checked of {len(m.units)}")
     assert checked > 50
     assert not bad, bad
+
+
+# ------------------------------------------------------------------------------------------------
+# the other BASELINE configs at full size (bench.py other_configs): predict() on the full batch,
+# images checked against the oracle (eval BatchNorm: images are independent)
+# ------------------------------------------------------------------------------------------------
+
+CONFIGS = [("small_cnn", 32, "f32", 32, 8), ("resnet18", 64, "f32", 224, 3),
+           ("densenet121", 128, "bf16", 224, 2), ("mobilenet_v2", 128, "bf16", 224, 2)]
+
+
+@pytest.mark.parametrize("model,batch,dtype,hw,check", CONFIGS, ids=[c[0] + "-" + c[2] for c in CONFIGS])
+def test_baseline_config_full_size(gpu, model, batch, dtype, hw, check):
+    """ResNet-18 f32/TF32 B=64 and the small CNN against the REFERENCE's compiled path; DenseNet-121
+    and MobileNet-V2 (Concat / ReLU6: not in the reference IR, parity unpinned) against the numpy
+    oracle restatement. Bars: oracle_err <= 1e-2 on the probabilities (TF32 / bf16 tensor cores),
+    top-1 agreement on every clear row and at least one clear row."""
+    from paper_2003_10688_b200 import frontend, graph, models
+    g = models.MODELS[model](hw=hw) if model == "small_cnn" else models.MODELS[model]()
+    m = frontend.optimize(g, frontend.OptimizeOptions(batch=batch, dtype=dtype, fuse_epilogue=True, cache=False))
+    x = np.random.default_rng(7).uniform(-1, 1, (batch, 3, hw, hw)).astype(np.float32)
+    prob = m.predict({"x": x})["prob"]
+    assert np.all(np.isfinite(prob))
+    idx = np.linspace(0, batch - 1, check).astype(int)
+    if model in ("small_cnn", "resnet18"):
+        want = _reference_compiled(g, x[idx], os.cpu_count() or 1)
+    else:
+        want = O.run_graph(graph.infer_shapes(g, len(idx)), {"x": x[idx]})["prob"]
+    got = prob[idx]
+    err = O.oracle_err(got, want)
+    clear = _clear_rows(want)
+    print(f"{model} {dtype} B={batch}: oracle_err {err:.3e}, clear rows {int(clear.sum())}/{len(idx)}")
+    assert err <= TOL, err
+    assert clear.sum() > 0
+    assert np.all(np.argmax(got, 1)[clear] == np.argmax(want, 1)[clear])
