@@ -103,7 +103,12 @@ struct DfpArgs {
 };
 
 void dfp_launch(const DfpArgs& a, cudaStream_t s);
-int dfp_reduce_blocks(int64_t pixels, int C);  // partial blocks used by FAM_CHAN_REDUCE
+int dfp_reduce_blocks(int64_t pixels, int C, int dtype);  // partial blocks used by FAM_CHAN_REDUCE
+struct ReduceGeo {
+    int blocks;  // pixel blocks (the partials' block dimension)
+    int cvb;     // channel vectors per block (grid.y = ceil(C / V / cvb))
+};
+ReduceGeo reduce_geo(int64_t pixels, int C, int V);
 
 // Small fixed-function kernels (rows of [N, C], BN finalisation, SGD, layout conversion).
 void softmax_rows(int dtype, const void* x, void* y, int rows, int cols, int ld, cudaStream_t s);
@@ -149,13 +154,17 @@ struct FinalizeArgs {
     int shift_dtype = DT_BF16;
 };
 void dfp_finalize(const FinalizeArgs& a, cudaStream_t s);
+// A FAM_CHAN_REDUCE launch followed by its finalisation: one cooperative kernel when the reduction
+// has a fast path and its grid is co-resident, else the two launches.
+void dfp_reduce_finalize(const DfpArgs& a, const FinalizeArgs& f, cudaStream_t s);
 
 // BatchNorm backward in two HBM passes (training; autodiff BNBackX/Gamma/Beta,
 // dfp_lower.cpp:709-753, 806-851): one reduction over (dy, x) producing, per channel and block,
 // [sum dy, sum dy*(x - shift), sum (x - shift), sum (x - shift)^2] (f64 partials [blocks][C][4]),
 // then (after FIN_BN_BACK4) dx = A*dy + B*xhat + Cc with xhat = ((x - mean_hi) - mean_lo) * rstd.
-void bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
-                    double* partial, int blocks, cudaStream_t s);
+// (returns true when the finalisation `fin` ran fused in the same cooperative launch)
+bool bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
+                    double* partial, int blocks, cudaStream_t s, const FinalizeArgs* fin = nullptr);
 void bn_back_apply(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* coef,
                    const float* xhat, void* dx, cudaStream_t s);
 

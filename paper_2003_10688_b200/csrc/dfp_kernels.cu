@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace solb200 {
@@ -1408,20 +1410,188 @@ __global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__
 // input in flight (raw 16-byte registers), sums them in f32 and folds every UN pixels into the
 // thread accumulator: f64 for f32 plans (the 1e-5 bar), f32 for bf16 plans (8 channels per
 // thread; the block and grid combination is f64 either way).
+// Finalises channel c with a whole block (the first 128 threads reduce, in the fixed order of the
+// stand-alone launch, so fused and separate finalisation are bit-identical).
+__device__ __forceinline__ void finalize_channel(const FinalizeArgs& a, const int c, double (*wsum)[4]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
+    double q[4] = {0.0, 0.0, 0.0, 0.0};
+    if (threadIdx.x < 128) {
+        const double* base = a.partial + static_cast<int64_t>(c) * a.blocks * ns;
+        // the first 8 partials of every thread are loaded together (16-byte loads; a dependent
+        // load-add chain made this launch latency bound at ~7 us), then summed in block order
+        constexpr int J = 8;
+        double2 lo[J], hi[J];
+    #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int b = threadIdx.x + 128 * j;
+            lo[j] = make_double2(0.0, 0.0);
+            hi[j] = make_double2(0.0, 0.0);
+            if (b < a.blocks) {
+                const double2* src = reinterpret_cast<const double2*>(base + static_cast<int64_t>(b) * ns);
+                lo[j] = src[0];
+                if (ns == 4) hi[j] = src[1];
+            }
+        }
+    #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            q[0] += lo[j].x;
+            q[1] += lo[j].y;
+            q[2] += hi[j].x;
+            q[3] += hi[j].y;
+        }
+        for (int b = threadIdx.x + 128 * J; b < a.blocks; b += 128) {
+            const double* src = base + static_cast<int64_t>(b) * ns;
+            q[0] += src[0];
+            q[1] += src[1];
+            if (ns == 4) {
+                q[2] += src[2];
+                q[3] += src[3];
+            }
+        }
+    #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+    #pragma unroll
+            for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
+            if (lane == 0) wsum[w][k] = q[k];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) [&] {  // a lambda: the BN_BACK4 branch returns early
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
+    if (a.mode == FIN_BN_BACK4) {
+        const double sd = q[0], sdx = q[1], sx = q[2], sxx = q[3];
+        const double m = a.count;
+        const double d = sx / m;  // mean - shift
+        double var = sxx / m - d * d;
+        if (var < 0) var = 0;
+        const double shift = a.shift ? a.shift[c]
+                                     : (a.shift_dtype == DT_BF16
+                                            ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.shift_x)[c]))
+                                            : static_cast<double>(static_cast<const float*>(a.shift_x)[c]));
+        const double mean = shift + d;
+        const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
+        const double s1 = sd;                    // sum dy                 (dbeta)
+        const double s2 = rstd * (sdx - d * sd);  // sum dy * xhat         (dgamma)
+        if (a.out0) a.out0[c] = static_cast<float>(s1);
+        if (a.out1) a.out1[c] = static_cast<float>(s2);
+        if (a.coef) {
+            const double gr = static_cast<double>(a.gamma[c]) * rstd;
+            a.coef[c] = static_cast<float>(gr);
+            a.coef[a.C + c] = static_cast<float>(-gr * s2 / m);
+            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
+        }
+        if (a.xhat) {
+            const float hi = static_cast<float>(mean);
+            a.xhat[c] = hi;
+            a.xhat[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
+            a.xhat[2 * a.C + c] = static_cast<float>(rstd);
+        }
+        return;
+    }
+    const double s1 = q[0], s2 = q[1];
+    const double m = a.count;
+    if (a.mode == FIN_BN_STATS) {
+        // sums over (x - shift): mean = shift + s1/m, var = s2/m - (s1/m)^2 (biased)
+        const double d = s1 / m;
+        double var = s2 / m - d * d;
+        if (var < 0) var = 0;
+        // the shift is x's first pixel, read in place when no shift array is given
+        const double shift = a.shift ? static_cast<double>(a.shift[c])
+                                     : (a.shift_dtype == DT_BF16
+                                            ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.shift_x)[c]))
+                                            : static_cast<double>(static_cast<const float*>(a.shift_x)[c]));
+        const double mean = shift + d;
+        const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
+        if (a.stats_out) {
+            a.stats_out[c] = static_cast<float>(mean);
+            a.stats_out[a.C + c] = static_cast<float>(rstd);
+        }
+        if (a.coef) {
+            const float hi = static_cast<float>(mean);
+            a.coef[c] = hi;
+            a.coef[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
+            a.coef[2 * a.C + c] = static_cast<float>(static_cast<double>(a.gamma[c]) * rstd);
+            a.coef[3 * a.C + c] = a.beta[c];
+            a.coef[4 * a.C + c] = static_cast<float>(a.beta[c] - mean * static_cast<double>(a.gamma[c]) * rstd);
+        }
+        if (a.running_mean) {
+            const double unbias = m > 1 ? m / (m - 1) : 1.0;
+            const double mom = a.momentum;
+            a.running_mean[c] = static_cast<float>((1 - mom) * a.running_mean[c] + mom * mean);
+            a.running_var[c] = static_cast<float>((1 - mom) * a.running_var[c] + mom * var * unbias);
+        }
+    } else if (a.mode == FIN_SUMS) {
+        if (a.out0) a.out0[c] = static_cast<float>(s1);
+        if (a.out1) a.out1[c] = static_cast<float>(s2);
+    } else {
+        // s1 = sum dy (dbeta), s2 = sum dy * xhat (dgamma); dx = g*r*(dy - s1/m - xhat*s2/m)
+        if (a.out0) a.out0[c] = static_cast<float>(s1);
+        if (a.out1) a.out1[c] = static_cast<float>(s2);
+        if (a.coef) {
+            const double g = a.gamma[c];
+            const double rstd = a.stats[a.C + c];
+            const double gr = g * rstd;
+            // dx = gr*dy - gr*xhat*s2/m - gr*s1/m, with xhat = (x - mean)*rstd formed accurately
+            // by the apply program (mean split hi/lo) so no |mean| >> std cancellation occurs
+            a.coef[c] = static_cast<float>(gr);
+            a.coef[a.C + c] = static_cast<float>(-gr * s2 / m);
+            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
+        }
+    }
+    }();
+    __syncthreads();
+}
+
 enum RRMode { RR_BNBACK = 0, RR_STATS = 1, RR_SUM = 2 };
+
+// Cooperative launch (all blocks co-resident: grid.sync() is legal) of a one-wave reduction whose
+// finalisation runs in the same kernel after the grid barrier: saves the stand-alone finalize
+// launch (~100 per ResNet-50 training step, ~7 us each). false when the grid does not fit.
+template <typename K, typename... Args>
+bool launch_coop(K kernel, dim3 grid, size_t smem, cudaStream_t s, Args... args) {
+    static const bool off = std::getenv("SOL_NO_COOP_FINALIZE") != nullptr;
+    if (off) return false;
+    int per_sm = 0;
+    SOL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, THREADS, smem));
+    if (static_cast<int64_t>(per_sm) * num_sms() < static_cast<int64_t>(grid.x) * grid.y * grid.z) return false;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SOL_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+    return true;
+}
+
+// after every block wrote its partials: grid barrier, then block b finalises channels b, b + nb, ..
+__device__ __forceinline__ void fused_finalize(const FinalizeArgs& fin, double (*wsum)[4]) {
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    const int nb = gridDim.x * gridDim.y;
+    for (int c = blockIdx.y * gridDim.x + blockIdx.x; c < fin.C; c += nb) finalize_channel(fin, c, wsum);
+}
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restrict__ x0, const T* __restrict__ x1,
                                                                int C, int ld0, int ld1, int64_t P,
                                                                const float* __restrict__ shift,
-                                                               double* __restrict__ partial) {
+                                                               double* __restrict__ partial, int cvb_arg,
+                                                               const __grid_constant__ FinalizeArgs fin, int do_fin) {
+    __shared__ double fin_wsum[4][4];
     constexpr int V = VEC<T>;
     constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
     constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
     constexpr int UN = NI == 2 ? 6 : 12;  // 12 16-byte loads in flight per thread
     __shared__ double red[THREADS * V];
     const int cv_total = C / V;
-    const int cvb = min(cv_total, THREADS);
+    const int cvb = cvb_arg;  // channel vectors per block (grid.y = channel slices)
     const int rows = THREADS / cvb;
     const int tid = threadIdx.x;
     const int row = tid / cvb;
@@ -1530,28 +1700,236 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
         }
         __syncthreads();
     }
+    if (do_fin) fused_finalize(fin, fin_wsum);
 }
 
-// Matches the reduction programs emitted by module.cpp; returns false for anything else.
+// The same reductions fed by 1-D bulk copies: a block's pixel range [p0, p1) is one contiguous
+// byte range per input, streamed through a STAGES-deep shared-memory ring by one thread
+// (cp.async.bulk + mbarrier, ~16 KB per input per stage) -- the copy engine keeps ~96 KB per
+// block in flight whatever the warps do, where the register-staged loop above tops out at ~50%
+// of HBM. Threads then walk the staged pixels exactly as above (cvb channel vectors x rows pixel
+// lanes, all channels in one block). Same partials layout ([C][blocks][NS]), same finalize.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(THREADS, 2) rowreduce_bulk_kernel(const T* __restrict__ x0,
+                                                                     const T* __restrict__ x1, int C, int ld0,
+                                                                     int ld1, int64_t P,
+                                                                     const float* __restrict__ shift,
+                                                                     double* __restrict__ partial, int chunk_px,
+                                                                     int stages, const __grid_constant__ FinalizeArgs fin,
+                                                                     int do_fin) {
+    __shared__ double fin_wsum[4][4];
+    constexpr int V = VEC<T>;
+    constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
+    constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ double red[THREADS * V];
+    const int cv_total = C / V;
+    const int cvb = cv_total;  // the whole channel range in one block (host checks cv_total <= THREADS)
+    const int rows = THREADS / cvb;
+    const int tid = threadIdx.x;
+    const int row = tid / cvb;
+    const int cvi = tid - row * cvb;
+    const int c = cvi * V;
+    const int64_t per = ceil_div(P, static_cast<int64_t>(gridDim.x));
+    const int64_t p0 = blockIdx.x * per;
+    const int64_t p1 = min(P, p0 + per);
+    const int64_t npx = p1 > p0 ? p1 - p0 : 0;
+    const int nchunks = static_cast<int>(ceil_div(npx, static_cast<int64_t>(chunk_px)));
+    const uint32_t rb0 = static_cast<uint32_t>(ld0 * sizeof(T)), rb1 = static_cast<uint32_t>(ld1 * sizeof(T));
+    const uint32_t sb0 = chunk_px * rb0, sb1 = NI == 2 ? chunk_px * rb1 : 0;
+    const uint32_t bar0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    const uint32_t ring = bar0 + 128;
+    auto issue = [&](int ch, int st) {
+        const int64_t q0 = p0 + static_cast<int64_t>(ch) * chunk_px;
+        const int64_t left = p1 - q0;
+        const uint32_t n = static_cast<uint32_t>(left < chunk_px ? left : chunk_px);
+        const uint32_t bar = bar0 + 8 * st;
+        asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+                     "r"(n * (rb0 + (NI == 2 ? rb1 : 0))));
+        const uint32_t dst = ring + st * (sb0 + sb1);
+        bulk_g2s(dst, x0 + q0 * ld0, n * rb0, bar);
+        if (NI == 2) bulk_g2s(dst + sb0, x1 + q0 * ld1, n * rb1, bar);
+    };
+    if (tid == 0) {
+        for (int st = 0; st < stages; ++st) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8 * st));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+        for (int st = 0; st < stages && st < nchunks; ++st) issue(st, st);
+    }
+    __syncthreads();
+    using Acc = typename std::conditional<sizeof(T) == 2, float, double>::type;
+    Acc acc[NS][V];
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[k][i] = Acc(0);
+    const bool active = row < rows;
+    float q[V];
+    {
+        const T* xs = MODE == RR_BNBACK ? x1 : x0;
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+            q[i] = MODE == RR_SUM ? 0.f : (shift ? __ldg(shift + c + i) : to_f32(xs[c + i]));
+    }
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int st = ch % stages;
+        const uint32_t parity = static_cast<uint32_t>(ch / stages) & 1u;
+        asm volatile(
+            "{\n.reg .pred P1;\nWAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(bar0 + 8 * st), "r"(parity));
+        const int64_t left = p1 - (p0 + static_cast<int64_t>(ch) * chunk_px);
+        const int n = static_cast<int>(left < chunk_px ? left : chunk_px);
+        const uint8_t* base = smem_raw + 128 + st * (sb0 + sb1);
+        if (active) {
+            constexpr bool DIRECT = sizeof(T) == 2;
+            float f[NS][V];
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+#pragma unroll
+                for (int i = 0; i < V; ++i) f[k][i] = DIRECT ? static_cast<float>(acc[k][i]) : 0.f;
+            for (int px = row; px < n; px += rows) {
+                float v0[V], v1[V];
+                unpack16(*reinterpret_cast<const uint4*>(base + px * rb0 + c * sizeof(T)), v0, static_cast<T*>(nullptr));
+                if (NI == 2)
+                    unpack16(*reinterpret_cast<const uint4*>(base + sb0 + px * rb1 + c * sizeof(T)), v1,
+                             static_cast<T*>(nullptr));
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (MODE == RR_BNBACK) {
+                        const float xs = v1[i] - q[i];
+                        f[0][i] += v0[i];
+                        f[1][i] = fmaf(v0[i], xs, f[1][i]);
+                        f[2][i] += xs;
+                        f[3][i] = fmaf(xs, xs, f[3][i]);
+                    } else {
+                        const float xs = v0[i] - q[i];
+                        f[0][i] += xs;
+                        f[1][i] = fmaf(xs, xs, f[1][i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    if (DIRECT) acc[k][i] = static_cast<Acc>(f[k][i]);
+                    else acc[k][i] += static_cast<Acc>(f[k][i]);
+                }
+        }
+        __syncthreads();  // the stage is consumed: refill it
+        if (tid == 0 && ch + stages < nchunks) issue(ch + stages, st);
+    }
+    // combine the pixel lanes (as in rowreduce_kernel)
+    const int lane = tid & 31;
+    const bool pow2 = (cvb & (cvb - 1)) == 0;
+    const int rows_w = (pow2 && cvb < 32) ? 32 / cvb : 1;
+    const int groups = rows / rows_w;
+    const int grp = row / rows_w;
+    const bool lead = row < rows && (rows_w == 1 || lane < cvb);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        double t[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            t[i] = static_cast<double>(acc[k][i]);
+            if (rows_w > 1)
+                for (int off = cvb; off < 32; off <<= 1) t[i] += __shfl_xor_sync(0xffffffffu, t[i], off);
+        }
+        if (lead && row % rows_w == 0) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) red[(grp * cvb + cvi) * V + i] = t[i];
+        }
+        __syncthreads();
+        if (tid < cvb) {
+            double u[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) u[i] = 0.0;
+            for (int g2 = 0; g2 < groups; ++g2)
+#pragma unroll
+                for (int i = 0; i < V; ++i) u[i] += red[(g2 * cvb + tid) * V + i];
+            const int64_t c0 = static_cast<int64_t>(tid) * V;
+#pragma unroll
+            for (int i = 0; i < V; ++i) partial[((c0 + i) * gridDim.x + blockIdx.x) * NS + k] = u[i];
+        }
+        __syncthreads();
+    }
+    if (do_fin) fused_finalize(fin, fin_wsum);
+}
+
+// Bulk-fed reduction launch (true) when the channels fit one block and rows are 16-byte aligned.
+template <typename T, int MODE>
+bool launch_rowreduce_bulk(const T* x0, const T* x1, int C, int ld0, int ld1, int64_t P, const float* shift,
+                           double* partial, unsigned blocks, cudaStream_t s, const FinalizeArgs* fin,
+                           bool* fused) {
+    static const bool off = std::getenv("SOL_NO_BULK_REDUCE") != nullptr;
+    constexpr int V = VEC<T>;
+    constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
+    if (off || C % V || C / V > THREADS || (ld0 * sizeof(T)) % 16 || (NI == 2 && (ld1 * sizeof(T)) % 16)) return false;
+    if ((reinterpret_cast<uintptr_t>(x0) & 15) || (NI == 2 && (reinterpret_cast<uintptr_t>(x1) & 15))) return false;
+    const int row_bytes = ld0 * static_cast<int>(sizeof(T)) + (NI == 2 ? ld1 * static_cast<int>(sizeof(T)) : 0);
+    static const int kb = std::getenv("SOL_BULK_KB") ? std::atoi(std::getenv("SOL_BULK_KB")) : 96;
+    const int chunk_px = std::max(8, (16384 * NI) / row_bytes);
+    const int stages = std::max(2, std::min(8, (kb * 1024) / (chunk_px * row_bytes)));
+    const size_t smem = 128 + static_cast<size_t>(stages) * chunk_px * row_bytes;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        SOL_CUDA(cudaFuncSetAttribute(rowreduce_bulk_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      110 * 1024));
+    });
+    if (smem > 110 * 1024) return false;
+    if (fin && launch_coop(rowreduce_bulk_kernel<T, MODE>, dim3(blocks), smem, s, x0, x1, C, ld0, ld1, P, shift,
+                           partial, chunk_px, stages, *fin, 1)) {
+        *fused = true;
+        return true;
+    }
+    rowreduce_bulk_kernel<T, MODE><<<blocks, THREADS, smem, s>>>(x0, x1, C, ld0, ld1, P, shift, partial, chunk_px,
+                                                                 stages, FinalizeArgs{}, 0);
+    SOL_CUDA(cudaGetLastError());
+    return true;
+}
+
+// Matches the reduction programs emitted by module.cpp; returns false for anything else. With a
+// finalisation `fin`, tries the cooperative fused launch and reports it in *fused.
+template <typename T, int MODE>
+void launch_rowreduce(const T* x0, const T* x1, int C, int ld0, int ld1, int64_t P, const float* shift,
+                      double* partial, const ReduceGeo& rg, cudaStream_t s, const FinalizeArgs* fin, bool* fused) {
+    const dim3 grid(static_cast<unsigned>(rg.blocks), static_cast<unsigned>(ceil_div(C / VEC<T>, rg.cvb)));
+    *fused = false;
+    if (grid.y == 1 && launch_rowreduce_bulk<T, MODE>(x0, x1, C, ld0, ld1, P, shift, partial, grid.x, s, fin, fused))
+        return;
+    if (fin && launch_coop(rowreduce_kernel<T, MODE>, grid, 0, s, x0, x1, C, ld0, ld1, P, shift, partial, rg.cvb, *fin,
+                           1)) {
+        *fused = true;
+        return;
+    }
+    rowreduce_kernel<T, MODE><<<grid, THREADS, 0, s>>>(x0, x1, C, ld0, ld1, P, shift, partial, rg.cvb, FinalizeArgs{},
+                                                       0);
+    SOL_CUDA(cudaGetLastError());
+}
+
 template <typename T>
-bool launch_reduce_fast(const DfpArgs& a, dim3 grid, cudaStream_t s) {
+bool launch_reduce_fast(const DfpArgs& a, dim3 grid, cudaStream_t s, const FinalizeArgs* fin = nullptr,
+                        bool* fused = nullptr) {
+    const int64_t P = static_cast<int64_t>(a.N) * a.H * a.W;
+    const ReduceGeo rg = reduce_geo(P, a.C, VEC<T>);
+    if (static_cast<int>(grid.x) != rg.blocks) return false;
+    bool dummy = false;
+    if (!fused) fused = &dummy;
     const Program& p = a.pre;
     auto is = [&](int k, PwOp op, int dst) { return k < p.n && p.ins[k].op == op && p.ins[k].dst == dst; };
     if (p.n == 5 && is(0, PW_LD, 0) && is(1, PW_PARAM, 1) && is(2, PW_SCALE, 1) && p.ins[2].imm == -1.f &&
         is(3, PW_ADD, 0) && p.ins[3].a == 0 && p.ins[3].b == 1 && is(4, PW_MOV, 1) && p.ins[4].a == 0) {
         const int sl = p.ins[0].a;
         if (a.in_kind[sl] != IN_PIX) return false;
-        rowreduce_kernel<T, RR_STATS><<<grid, THREADS, 0, s>>>(static_cast<const T*>(a.in[sl]), nullptr, a.C,
-                                                               a.in_ld[sl], 0, static_cast<int64_t>(a.N) * a.H * a.W,
-                                                               a.P[p.ins[1].arg], a.partial);
+        launch_rowreduce<T, RR_STATS>(static_cast<const T*>(a.in[sl]), nullptr, a.C, a.in_ld[sl], 0, P,
+                                      a.P[p.ins[1].arg], a.partial, rg, s, fin, fused);
         return true;
     }
     if (p.n == 2 && is(0, PW_LD, 0) && is(1, PW_MOV, 1) && p.ins[1].a == 0) {
         const int sl = p.ins[0].a;
         if (a.in_kind[sl] != IN_PIX) return false;
-        rowreduce_kernel<T, RR_SUM><<<grid, THREADS, 0, s>>>(static_cast<const T*>(a.in[sl]), nullptr, a.C,
-                                                             a.in_ld[sl], 0, static_cast<int64_t>(a.N) * a.H * a.W,
-                                                             nullptr, a.partial);
+        launch_rowreduce<T, RR_SUM>(static_cast<const T*>(a.in[sl]), nullptr, a.C, a.in_ld[sl], 0, P, nullptr,
+                                    a.partial, rg, s, fin, fused);
         return true;
     }
     return false;
@@ -2328,132 +2706,7 @@ __global__ void __launch_bounds__(THREADS, 3) bnback_apply_kernel(const T* __res
 // a fixed-order shuffle + shared-memory tree combines them (deterministic), thread 0 finalises.
 __global__ void __launch_bounds__(128) finalize_kernel(const FinalizeArgs a) {
     __shared__ double wsum[4][4];
-    const int c = blockIdx.x;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
-    double q[4] = {0.0, 0.0, 0.0, 0.0};
-    const double* base = a.partial + static_cast<int64_t>(c) * a.blocks * ns;
-    // the first 8 partials of every thread are loaded together (16-byte loads; a dependent
-    // load-add chain made this launch latency bound at ~7 us), then summed in block order
-    constexpr int J = 8;
-    double2 lo[J], hi[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-        const int b = threadIdx.x + 128 * j;
-        lo[j] = make_double2(0.0, 0.0);
-        hi[j] = make_double2(0.0, 0.0);
-        if (b < a.blocks) {
-            const double2* src = reinterpret_cast<const double2*>(base + static_cast<int64_t>(b) * ns);
-            lo[j] = src[0];
-            if (ns == 4) hi[j] = src[1];
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-        q[0] += lo[j].x;
-        q[1] += lo[j].y;
-        q[2] += hi[j].x;
-        q[3] += hi[j].y;
-    }
-    for (int b = threadIdx.x + 128 * J; b < a.blocks; b += 128) {
-        const double* src = base + static_cast<int64_t>(b) * ns;
-        q[0] += src[0];
-        q[1] += src[1];
-        if (ns == 4) {
-            q[2] += src[2];
-            q[3] += src[3];
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
-        if (lane == 0) wsum[w][k] = q[k];
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
-    if (a.mode == FIN_BN_BACK4) {
-        const double sd = q[0], sdx = q[1], sx = q[2], sxx = q[3];
-        const double m = a.count;
-        const double d = sx / m;  // mean - shift
-        double var = sxx / m - d * d;
-        if (var < 0) var = 0;
-        const double shift = a.shift ? a.shift[c]
-                                     : (a.shift_dtype == DT_BF16
-                                            ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.shift_x)[c]))
-                                            : static_cast<double>(static_cast<const float*>(a.shift_x)[c]));
-        const double mean = shift + d;
-        const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
-        const double s1 = sd;                    // sum dy                 (dbeta)
-        const double s2 = rstd * (sdx - d * sd);  // sum dy * xhat         (dgamma)
-        if (a.out0) a.out0[c] = static_cast<float>(s1);
-        if (a.out1) a.out1[c] = static_cast<float>(s2);
-        if (a.coef) {
-            const double gr = static_cast<double>(a.gamma[c]) * rstd;
-            a.coef[c] = static_cast<float>(gr);
-            a.coef[a.C + c] = static_cast<float>(-gr * s2 / m);
-            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
-        }
-        if (a.xhat) {
-            const float hi = static_cast<float>(mean);
-            a.xhat[c] = hi;
-            a.xhat[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
-            a.xhat[2 * a.C + c] = static_cast<float>(rstd);
-        }
-        return;
-    }
-    const double s1 = q[0], s2 = q[1];
-    const double m = a.count;
-    if (a.mode == FIN_BN_STATS) {
-        // sums over (x - shift): mean = shift + s1/m, var = s2/m - (s1/m)^2 (biased)
-        const double d = s1 / m;
-        double var = s2 / m - d * d;
-        if (var < 0) var = 0;
-        // the shift is x's first pixel, read in place when no shift array is given
-        const double shift = a.shift ? static_cast<double>(a.shift[c])
-                                     : (a.shift_dtype == DT_BF16
-                                            ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.shift_x)[c]))
-                                            : static_cast<double>(static_cast<const float*>(a.shift_x)[c]));
-        const double mean = shift + d;
-        const double rstd = 1.0 / sqrt(var + static_cast<double>(a.eps));
-        if (a.stats_out) {
-            a.stats_out[c] = static_cast<float>(mean);
-            a.stats_out[a.C + c] = static_cast<float>(rstd);
-        }
-        if (a.coef) {
-            const float hi = static_cast<float>(mean);
-            a.coef[c] = hi;
-            a.coef[a.C + c] = static_cast<float>(mean - static_cast<double>(hi));
-            a.coef[2 * a.C + c] = static_cast<float>(static_cast<double>(a.gamma[c]) * rstd);
-            a.coef[3 * a.C + c] = a.beta[c];
-            a.coef[4 * a.C + c] = static_cast<float>(a.beta[c] - mean * static_cast<double>(a.gamma[c]) * rstd);
-        }
-        if (a.running_mean) {
-            const double unbias = m > 1 ? m / (m - 1) : 1.0;
-            const double mom = a.momentum;
-            a.running_mean[c] = static_cast<float>((1 - mom) * a.running_mean[c] + mom * mean);
-            a.running_var[c] = static_cast<float>((1 - mom) * a.running_var[c] + mom * var * unbias);
-        }
-    } else if (a.mode == FIN_SUMS) {
-        if (a.out0) a.out0[c] = static_cast<float>(s1);
-        if (a.out1) a.out1[c] = static_cast<float>(s2);
-    } else {
-        // s1 = sum dy (dbeta), s2 = sum dy * xhat (dgamma); dx = g*r*(dy - s1/m - xhat*s2/m)
-        if (a.out0) a.out0[c] = static_cast<float>(s1);
-        if (a.out1) a.out1[c] = static_cast<float>(s2);
-        if (a.coef) {
-            const double g = a.gamma[c];
-            const double rstd = a.stats[a.C + c];
-            const double gr = g * rstd;
-            // dx = gr*dy - gr*xhat*s2/m - gr*s1/m, with xhat = (x - mean)*rstd formed accurately
-            // by the apply program (mean split hi/lo) so no |mean| >> std cancellation occurs
-            a.coef[c] = static_cast<float>(gr);
-            a.coef[a.C + c] = static_cast<float>(-gr * s2 / m);
-            a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
-        }
-    }
+    finalize_channel(a, blockIdx.x, wsum);
 }
 
 __global__ void bn_infer_coef_kernel(const float* g, const float* b, const float* mu, const float* var,
@@ -2525,39 +2778,68 @@ void transpose(const void* in, void* out, int N, int R, int C, int ld_in, int r_
 
 }  // namespace
 
-int dfp_reduce_blocks(int64_t pixels, int C) {
-    // ~32 16-byte vectors per thread (256 threads) over the pixel range, grid.y covers channel
-    // vector blocks of 256; at most one wave of two resident blocks per SM (a second wave cost
-    // more in per-block combination than it hid)
-    const int64_t cvec = std::max<int64_t>(1, C / 8);
-    const int64_t gy = ceil_div(cvec, 256);
-    const int64_t want = ceil_div(pixels * cvec, static_cast<int64_t>(256) * 32 * gy);
+ReduceGeo reduce_geo(int64_t pixels, int C, int V) {
+    // (pixel blocks, channel vectors per block) of the per-channel reductions. One wave of ~2
+    // blocks per SM; the per-block partial sums ([C][blocks][<= 4] doubles, re-read by the
+    // finalisation) must stay small next to the tensor itself, so tensors with few pixels and many
+    // channels (ResNet-50 layers 3-4: 6272 pixels x 2048 channels) split their channels over
+    // grid.y instead of multiplying pixel blocks (one wave of 296 pixel blocks made the partials
+    // 75% of the layer-4 tensor's bytes)
+    const int64_t cvec = std::max<int64_t>(1, C / V);
     static const int64_t per_sm = std::getenv("SOL_REDUCE_PER_SM") ? std::atoi(std::getenv("SOL_REDUCE_PER_SM")) : 2;
-    const int64_t wave = std::max<int64_t>(1, per_sm * num_sms() / gy);
-    // small tensors (layers 3/4): a full wave as long as every thread keeps >= 4 pixels — sizing
-    // by ~32 vectors per thread alone left 49..196 blocks, i.e. idle SMs
-    const int64_t rows = 256 / std::min<int64_t>(cvec, 256);
-    static const bool old_sizing = std::getenv("SOL_REDUCE_OLD_SIZING") != nullptr;
-    const int64_t fill = old_sizing ? want : std::max(want, ceil_div(pixels, rows * 4));
-    const int64_t blocks = std::min(fill, wave);
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, pixels)));
+    const int64_t wave = std::max<int64_t>(1, per_sm * num_sms());
+    int64_t cvb = std::min<int64_t>(cvec, THREADS);
+    for (;;) {
+        const int64_t gy = ceil_div(cvec, cvb);
+        const int64_t rows = THREADS / cvb;
+        // pixel blocks: fill the wave, each thread >= 4 pixels, partials <= ~6% of the tensor
+        int64_t bx = std::max<int64_t>(1, wave / gy);
+        bx = std::min(bx, std::max<int64_t>(1, ceil_div(pixels, rows * 4)));
+        // partials (<= 32 B per channel and block) within 1/16 of a bf16 tensor's 2 B per channel and pixel
+        const bool small_partials = bx * 256 <= pixels;
+        if (small_partials || cvb <= 8 || cvb % 2) {
+            return ReduceGeo{static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(bx, pixels))), static_cast<int>(cvb)};
+        }
+        cvb /= 2;
+    }
 }
 
-void bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
-                    double* partial, int blocks, cudaStream_t s) {
+int dfp_reduce_blocks(int64_t pixels, int C, int dtype) {
+    return reduce_geo(pixels, C, dtype == DT_BF16 ? 8 : 4).blocks;
+}
+
+bool bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
+                    double* partial, int blocks, cudaStream_t s, const FinalizeArgs* fin) {
     const int V = dtype == DT_BF16 ? 8 : 4;
     if (C % V != 0) throw std::invalid_argument("bn_back_reduce: channel count must be a multiple of 16 bytes");
-    const int cv_total = C / V;
-    const int cvb = std::min(cv_total, THREADS);
-    dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ceil_div(cv_total, cvb)));
+    const ReduceGeo rg = reduce_geo(pixels, C, V);
+    if (rg.blocks != blocks) throw std::invalid_argument("bn_back_reduce: partial blocks differ from the geometry");
+    bool fused = false;
     if (dtype == DT_BF16)
-        rowreduce_kernel<__nv_bfloat16, RR_BNBACK><<<grid, THREADS, 0, s>>>(
-            static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), C, C, C, pixels, shift, partial);
+        launch_rowreduce<__nv_bfloat16, RR_BNBACK>(static_cast<const __nv_bfloat16*>(dy),
+                                                   static_cast<const __nv_bfloat16*>(x), C, C, C, pixels, shift,
+                                                   partial, rg, s, fin, &fused);
     else
-        rowreduce_kernel<float, RR_BNBACK><<<grid, THREADS, 0, s>>>(static_cast<const float*>(dy),
-                                                                   static_cast<const float*>(x), C, C, C, pixels, shift,
-                                                                   partial);
-    SOL_CUDA(cudaGetLastError());
+        launch_rowreduce<float, RR_BNBACK>(static_cast<const float*>(dy), static_cast<const float*>(x), C, C, C,
+                                           pixels, shift, partial, rg, s, fin, &fused);
+    return fused;
+}
+
+void dfp_reduce_finalize(const DfpArgs& a, const FinalizeArgs& f, cudaStream_t s) {
+    if (a.family == FAM_CHAN_REDUCE) {
+        const int V = a.dtype == DT_BF16 ? 8 : 4;
+        const dim3 grid(static_cast<unsigned>(a.reduce_blocks), 1);
+        bool fused = false;
+        const bool done = a.dtype == DT_BF16 ? launch_reduce_fast<__nv_bfloat16>(a, grid, s, &f, &fused)
+                                             : launch_reduce_fast<float>(a, grid, s, &f, &fused);
+        (void)V;
+        if (done) {
+            if (!fused) dfp_finalize(f, s);
+            return;
+        }
+    }
+    dfp_launch(a, s);
+    dfp_finalize(f, s);
 }
 
 void bn_back_apply(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* coef,

@@ -865,7 +865,7 @@ public:
         delta_ = geo_b(d.bindings[o.inputs[0]]);
         C_ = static_cast<int>(delta_.ld);       // reduce over the stored (padded) width
         Creal_ = static_cast<int>(delta_.C);
-        blocks_ = dfp_reduce_blocks(delta_.pixels(), C_);
+        blocks_ = dfp_reduce_blocks(delta_.pixels(), C_, dtype_);
         const bool needs_x = op_ == SOL_OP_BATCHNORMBACKX || op_ == SOL_OP_BATCHNORMBACKGAMMA;
         if (needs_x && !training_) unsupported("BatchNorm backward in inference mode");
         if (needs_x && C_ != Creal_) unsupported("BatchNorm backward over padded channel storage");
@@ -936,7 +936,6 @@ public:
             DfpArgs a = base(args, partial);
             a.pre = prog_load(0);
             push(a.pre, PW_MOV, 1, 0);
-            dfp_launch(a, s);
             FinalizeArgs f;
             f.mode = FIN_SUMS;
             f.C = Creal_;
@@ -944,12 +943,11 @@ public:
             f.blocks = blocks_;
             f.partial = partial;
             f.out0 = out;
-            dfp_finalize(f, s);
+            dfp_reduce_finalize(a, f, s);
             return;
         }
         // BNBackX / BNBackGamma: one pass over (dy, x) gives the x statistics and both sums
         // shifted sums about x's first pixel, read in place by the reduction and the finalisation
-        bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), nullptr, partial, blocks_, s);
         FinalizeArgs f;
         f.mode = FIN_BN_BACK4;
         f.C = C_;
@@ -962,15 +960,17 @@ public:
         f.shift_dtype = dtype_;
         if (op_ == SOL_OP_BATCHNORMBACKGAMMA) {
             f.out1 = out;
-            dfp_finalize(f, s);
-            return;
+        } else {
+            f.gamma = static_cast<const float*>(args[gamma_idx_]);
+            f.coef = coef_;
+            f.xhat = xhat_;
+            f.out1 = sib_gamma;
+            f.out0 = sib_beta;
         }
-        f.gamma = static_cast<const float*>(args[gamma_idx_]);
-        f.coef = coef_;
-        f.xhat = xhat_;
-        f.out1 = sib_gamma;
-        f.out0 = sib_beta;
-        dfp_finalize(f, s);
+        // one pass over (dy, x) + the finalisation, fused in one cooperative launch when possible
+        if (!bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), nullptr, partial, blocks_, s, &f))
+            dfp_finalize(f, s);
+        if (op_ == SOL_OP_BATCHNORMBACKGAMMA) return;
         bn_back_apply(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), coef_, xhat_, out, s);
     }
 
@@ -1291,7 +1291,7 @@ DfpModule::DfpModule(const sol_unit_desc& d) : d_(d), dtype_(d.dtype) {
             b.xW = static_cast<int>(xg.W);
             if (xg.ld != xg.C) unsupported("training BatchNorm2d over padded storage");
             stats_scratch_ = std::max(stats_scratch_,
-                                      static_cast<size_t>(dfp_reduce_blocks(b.pixels, b.C)) * b.C * 2 * 8 + 256);
+                                      static_cast<size_t>(dfp_reduce_blocks(b.pixels, b.C, dtype_)) * b.C * 2 * 8 + 256);
         }
         bn_of_op_[k] = static_cast<int>(bn_.size());
         if (5 * static_cast<int>(bn_.size()) + 4 >= DFP_MAX_P) unsupported("too many BatchNorms in one unit");
@@ -1484,8 +1484,7 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
         push(a.pre, PW_ADD, 0, 0, 1);             // r0 = x - shift
         push(a.pre, PW_MOV, 1, 0);                // r1 = r0
         a.partial = partial;
-        a.reduce_blocks = dfp_reduce_blocks(b.pixels, b.C);
-        dfp_launch(a, s);
+        a.reduce_blocks = dfp_reduce_blocks(b.pixels, b.C, dtype_);
         FinalizeArgs f;
         f.mode = FIN_BN_STATS;
         f.C = b.C;
@@ -1507,7 +1506,7 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
             f.running_var = static_cast<float*>(args[b.v]);
             f.momentum = b.momentum;
         }
-        dfp_finalize(f, s);
+        dfp_reduce_finalize(a, f, s);  // statistics + finalisation (one cooperative launch when possible)
     }
     for (auto& w : dw_) {
         if (!(frozen && coef_ready_))
