@@ -55,6 +55,8 @@ class OptimizeOptions:
     fuse_bn_backward: bool = True  # training: BatchNormBackX also writes its Gamma/Beta siblings
     multi_sgd: bool = True         # training: every SgdUpdate in one multi-tensor launch
     nccl_allreduce: bool = False   # test hook: run the NCCL gradient all-reduce even with one replica
+    relu_mask_from_output: bool = True  # training: ReluBack masks read the ReLU output (passes.py), so
+                                        # BN+ReLU fuse and the pre-activation is never stored
     update_bn_stats: bool = True   # training: update BN running_mean / running_var on the device
                                    # (autodiff::update_bn_running_stats, autodiff.cpp:356-384)
     autotune: bool = False         # measure the tcgen05 tile configs of every conv/linear (dnn.cpp:214-290)
@@ -143,6 +145,9 @@ class DevicePlan:
         else:
             cg = gi
             self.loss_name = None
+        if options.train and options.relu_mask_from_output:
+            from .passes import relu_mask_from_output
+            cg = infer_shapes(relu_mask_from_output(cg), options.batch)
         if options.passes:
             cg = run_pipeline(cg)
         self.graph = cg

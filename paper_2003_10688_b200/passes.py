@@ -109,3 +109,24 @@ def run_pipeline(g: ModelGraph) -> ModelGraph:
         cur = fuse_relu_pool(reorder_commuting(cur))
         if _fingerprint(cur) == before:
             return cur
+
+
+def relu_mask_from_output(g: ModelGraph) -> ModelGraph:
+    """Training-graph rewrite beyond the reference pass set (plan option `relu_mask_from_output`):
+    ReluBack(delta, x) -> ReluBack(delta, relu(x)) and ReLU6Back(delta, x) -> ReLU6Back(delta,
+    relu6(x)). Exact: x > 0 <=> relu(x) > 0 and 0 < x < 6 <=> 0 < relu6(x) < 6 (also after bf16
+    rounding, which preserves sign and order). The pre-activation then has the activation as its
+    only consumer, so partition() fuses BN [+ Add] + ReLU into one unit that never writes the
+    pre-activation tensor (one full activation write per BN saved in the forward pass)."""
+    g = g.copy()
+    by_input = {}
+    for n in g.nodes:
+        if n.op in ("ReLU", "ReLU6") and n.inputs:
+            by_input.setdefault((n.op, n.inputs[0]), n.id)
+    for n in g.nodes:
+        if n.op in ("ReluBack", "ReLU6Back") and len(n.inputs) == 2:
+            fwd = by_input.get(("ReLU" if n.op == "ReluBack" else "ReLU6", n.inputs[1]))
+            if fwd is not None:
+                n.inputs = [n.inputs[0], fwd]
+    g.reindex()
+    return g
