@@ -391,7 +391,7 @@ public:
             if (!c.th) continue;
             void* dst = static_cast<uint8_t*>(scratch) + c.scratch_off;
             il.cls[ci] = dst;
-            if (!(frozen && packed_valid_))
+            if (!prepacked_ && !(frozen && packed_valid_))
                 pack_dgrad_class(static_cast<const float*>(args[w_idx_]), c.packed, dtype_, static_cast<int>(cout_),
                                  static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), c.kpad, c.th, c.tw, c.kh0,
                                  c.kw0, sh_, sw_, s);
@@ -536,10 +536,14 @@ public:
     void run(void* const* args, int nargs, void* scratch, cudaStream_t s, bool frozen) override {
         if (nargs != n_args) throw std::invalid_argument("heavy module: wrong argument count");
         void* out = args[nargs - 1];
+        struct ClearPrepack {
+            bool& f;
+            ~ClearPrepack() { f = false; }
+        } clear_prepack{prepacked_};
         switch (op_) {
             case SOL_OP_CONV2D:
             case SOL_OP_LINEAR: {
-                if (!(frozen && packed_valid_)) {
+                if (!prepacked_ && !(frozen && packed_valid_)) {
                     if (stem_)
                         pack_stem_weight(static_cast<const float*>(args[w_idx_]), packed_, static_cast<int>(cout_),
                                          static_cast<int>(cin_), kh_, kw_, kpad_, s);
@@ -580,7 +584,7 @@ public:
                 // stride 1: dx = conv(dy, mirrored transposed taps, padding k-1-p), which runs on the
                 // forward kernels' TMA (1x1) / TMA-im2col (k x k) operand paths
                 const bool as_fprop = sh_ == 1 && sw_ == 1 && ph_ <= kh_ - 1 && pw_ <= kw_ - 1;
-                if (!(frozen && packed_valid_)) {
+                if (!prepacked_ && !(frozen && packed_valid_)) {
                     pack_conv_weight_t(static_cast<const float*>(args[w_idx_]), packed_, dtype_,
                                        static_cast<int>(cout_), static_cast<int>(cin_), kh_, kw_,
                                        static_cast<int>(in_.ld), kpad_, s, as_fprop);
@@ -626,6 +630,36 @@ public:
             }
         }
     }
+    // Packs this step's weights now (the plan batches every module's packing of a run into one
+    // launch before the first step, pack.cuh); run() then skips its own packing once.
+    bool prepack(void* const* args, cudaStream_t s, bool frozen) override {
+        if (frozen && packed_valid_) return false;
+        if (op_ == SOL_OP_CONV2D || op_ == SOL_OP_LINEAR) {
+            if (stem_)
+                pack_stem_weight(static_cast<const float*>(args[w_idx_]), packed_, static_cast<int>(cout_),
+                                 static_cast<int>(cin_), kh_, kw_, kpad_, s);
+            else
+                pack_conv_weight(static_cast<const float*>(args[w_idx_]), packed_, dtype_, static_cast<int>(cout_),
+                                 static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), kpad_, s);
+        } else if (op_ == SOL_OP_CONV2DBACKX || op_ == SOL_OP_LINEARBACKX) {
+            if (!classes_.empty()) {
+                for (auto& c : classes_)
+                    if (c.th)
+                        pack_dgrad_class(static_cast<const float*>(args[w_idx_]), c.packed, dtype_,
+                                         static_cast<int>(cout_), static_cast<int>(cin_), kh_, kw_,
+                                         static_cast<int>(in_.ld), c.kpad, c.th, c.tw, c.kh0, c.kw0, sh_, sw_, s);
+            } else {
+                const bool as_fprop = sh_ == 1 && sw_ == 1 && ph_ <= kh_ - 1 && pw_ <= kw_ - 1;
+                pack_conv_weight_t(static_cast<const float*>(args[w_idx_]), packed_, dtype_, static_cast<int>(cout_),
+                                   static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), kpad_, s, as_fprop);
+            }
+        } else {
+            return false;
+        }
+        packed_valid_ = true;
+        prepacked_ = true;
+        return true;
+    }
     bool set_option(int key, int value) override {
         if (key != SOL_MODOPT_TILE_N || stem_ || (op_ != SOL_OP_CONV2D && op_ != SOL_OP_LINEAR)) return false;
         if (value != 0 && value != 64 && value != 65 && value != 128 && value != 256) return false;
@@ -635,6 +669,7 @@ public:
     }
 
 private:
+    bool prepacked_ = false;  // prepack() ran for the current run
     int tile_n_ = 0;  // autotuned tcgen05 tile (SOL_MODOPT_TILE_N)
     int dtype_;
     int op_;

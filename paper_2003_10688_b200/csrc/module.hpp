@@ -31,6 +31,9 @@ public:
     virtual bool set_option(int key, int value) { return false; }
     // Runtime learning rate of SgdUpdate modules (stream-ordered device write; graph replays read it).
     virtual bool set_lr(float lr, cudaStream_t s) { return false; }
+    // Weight packing of this run issued ahead of the plan's steps (inside a pack batch, pack.cuh);
+    // false when the module packs nothing this run.
+    virtual bool prepack(void* const* args, cudaStream_t s, bool frozen) { return false; }
 
     std::string family;
     int n_args = 0;

@@ -28,5 +28,9 @@ void pack_conv_weight_t(const float* w, void* packed, int dtype, int Cout, int C
                         int kpad, cudaStream_t s, bool flip = false);
 void unpack_conv_grad(const float* packed, float* w, int Cout, int Cin, int kh, int kw, int ld, cudaStream_t s);
 void pack_dw_weight(const float* w, float* packed, int C, int kh, int kw, cudaStream_t s);
+// Batched packing: between begin and end, pack_conv_weight / _t / pack_stem_weight /
+// pack_dgrad_class record jobs instead of launching; end() issues them as one launch on `s`.
+void pack_batch_begin();
+void pack_batch_end(cudaStream_t s);
 
 }  // namespace solb200

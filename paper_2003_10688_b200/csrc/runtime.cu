@@ -8,6 +8,7 @@
 //   * adjacent H2D copies coalesce: a run of >= 64 KiB becomes one packed transfer (:144-155) —
 //     here a real one: one pinned->device DMA of the whole run plus one scatter kernel.
 #include "runtime.hpp"
+#include "pack.cuh"
 
 #include <cstdio>
 #include <cstdlib>
@@ -516,6 +517,27 @@ void Plan::run_steps(cudaStream_t st) {
             cudaEvent_t e;
             SOL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             ar_events_.push_back(e);
+        }
+    }
+    // every weight packing of this run (training: the master weights SGD updated last run) in one
+    // launch ahead of the steps, instead of one small pack launch per conv step
+    {
+        static const bool no_batch = std::getenv("SOL_NO_PACK_BATCH") != nullptr;
+        if (!no_batch) {
+            pack_batch_begin();
+            try {
+                std::vector<void*> big;
+                for (auto& s : steps_) {
+                    if (!s.module) continue;
+                    big.resize(s.ids.size());
+                    for (size_t k = 0; k < s.ids.size(); ++k) big[k] = base_ + bufs_[s.ids[k]].off;
+                    s.module->prepack(big.data(), st, frozen_);
+                }
+            } catch (...) {
+                pack_batch_end(st);
+                throw;
+            }
+            pack_batch_end(st);
         }
     }
     int group = 0;
