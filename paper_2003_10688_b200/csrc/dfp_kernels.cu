@@ -1273,27 +1273,35 @@ PostSpec match_post(const Program& p) {
 // thread = one channel vector with the 9 taps, bias and both BN coefficient sets in registers,
 // walking output pixels with all nine 16-byte window loads in flight.
 template <typename T, bool BN0, int ACT0, bool BN1, int ACT1>
-__global__ void __launch_bounds__(THREADS, 1) dwconv3_chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs,
+__global__ void __launch_bounds__(THREADS, 3) dwconv3_chain_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs,
                                                                    PostSpec ps) {
+    // the 3x3 taps of the block's channel slice live in shared memory (72 registers per thread
+    // for a full bf16 vector otherwise): three resident blocks per SM instead of one (MobileNet-V2
+    // depthwise units were at ~10% of HBM with one)
     constexpr int V = VEC<T>;
+    __shared__ __align__(16) float wsh[9][1024];  // [tap][channel of the slice] (host: slice <= 1024 channels)
     const int cv_total = a.C / V;
     const int cvb = min(cv_total, THREADS);
     const int rows = THREADS / cvb;
     const int row = threadIdx.x / cvb;
     const int cvi = threadIdx.x - row * cvb;
+    const int cslice = blockIdx.y * cvb * V;
+    const int nch = min(cvb * V, a.C - cslice);
+    for (int i = threadIdx.x; i < 9 * nch; i += blockDim.x) {
+        const int k = i / nch, cc = i - k * nch;
+        wsh[k][cc] = __ldg(a.dw_w + k * a.C + cslice + cc);
+    }
+    __syncthreads();
     if (row >= rows || blockIdx.y * cvb + cvi >= cv_total) return;
     const int c = (blockIdx.y * cvb + cvi) * V;
+    const int cl = cvi * V;
     const T* x = static_cast<const T*>(a.in[cs.s0]) + c;
     const int ldx = a.in_ld[cs.s0];
     T* out = static_cast<T*>(a.out) + a.out_coff + c;
     BnRegs<T> b0, b1;
     if (BN0) b0.load(a.P, cs.bn0, c);
     if (BN1) b1.load(a.P, ps.bn, c);
-    float w[9][V], bias[V];
-#pragma unroll
-    for (int k = 0; k < 9; ++k)
-#pragma unroll
-        for (int i = 0; i < V; ++i) w[k][i] = __ldg(a.dw_w + k * a.C + c + i);
+    float bias[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) bias[i] = a.dw_b ? __ldg(a.dw_b + c + i) : 0.f;
     const int64_t P = static_cast<int64_t>(a.N) * a.OH * a.OW;
@@ -1319,14 +1327,22 @@ __global__ void __launch_bounds__(THREADS, 1) dwconv3_chain_kernel(const __grid_
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
             if (!ok[k]) continue;
-            float v[V];
+            float v[V], wk[V];
+#pragma unroll
+            for (int i = 0; i < V; i += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(&wsh[k][cl + i]);
+                wk[i] = w4.x;
+                wk[i + 1] = w4.y;
+                wk[i + 2] = w4.z;
+                wk[i + 3] = w4.w;
+            }
             unpack16(r[k], v, static_cast<T*>(nullptr));
             if (BN0) b0.apply(v);
 #pragma unroll
             for (int i = 0; i < V; ++i) {
                 if (ACT0 >= 1) v[i] = fmaxf(v[i], 0.f);
                 if (ACT0 == 2) v[i] = fminf(v[i], 6.f);
-                acc[i] = fmaf(v[i], w[k][i], acc[i]);
+                acc[i] = fmaf(v[i], wk[i], acc[i]);
             }
         }
         if (BN1) b1.apply(acc);
@@ -1339,12 +1355,167 @@ __global__ void __launch_bounds__(THREADS, 1) dwconv3_chain_kernel(const __grid_
     }
 }
 
+// Depthwise 3x3 (pad 1, stride 1 or 2) from a shared-memory tile: one block = TH output rows of
+// one image x a CS-channel slice. The input rows it needs are loaded once (16-byte vectors), the
+// BatchNorm + activation prologue is applied once per input element while staging (f32 in shared
+// memory) -- the register kernel above re-applied it for each of the 9 taps and re-read every
+// input 9 times through L1 -- and each output vector then reads its 9 taps from shared memory.
+template <typename T, bool BN0, int ACT0, bool BN1, int ACT1>
+__global__ void __launch_bounds__(THREADS, 2) dwconv3_tile_kernel(const __grid_constant__ DfpArgs a, ChainSpec cs,
+                                                                 PostSpec ps, int TH, int CS) {
+    extern __shared__ __align__(16) float smem_f[];  // taps [9][CS] | tile [rows][cols][CS] (f32)
+    constexpr int V = VEC<T>;
+    const int S = a.sh;
+    const int bands = (a.OH + TH - 1) / TH;
+    const int n = blockIdx.x / bands;
+    const int oh0 = (blockIdx.x - n * bands) * TH;
+    const int nr = min(TH, a.OH - oh0);
+    const int c0 = blockIdx.y * CS;
+    const int cs_n = min(CS, a.C - c0);  // channels of this slice (multiple of V)
+    const int cvs = cs_n / V;
+    const int prow = blockDim.x / cvs;   // pixel lanes; thread -> fixed channel vector
+    const int lanep = threadIdx.x / cvs, cv = threadIdx.x - lanep * cvs;
+    const int rows = (nr - 1) * S + 3, cols = (a.OW - 1) * S + 3;
+    const int h0 = oh0 * S - a.ph, w0 = -a.pw;
+    float* taps = smem_f;
+    float* tile = smem_f + 9 * CS;
+    for (int i = threadIdx.x; i < 9 * cs_n; i += blockDim.x) {
+        const int k = i / cs_n, cc = i - k * cs_n;
+        taps[k * CS + cc] = __ldg(a.dw_w + k * a.C + c0 + cc);
+    }
+    const bool active = lanep < prow;
+    const int c = c0 + cv * V;
+    const T* x = static_cast<const T*>(a.in[cs.s0]);
+    const int ldx = a.in_ld[cs.s0];
+    BnRegs<T> b0, b1;
+    if (BN0 && active) b0.load(a.P, cs.bn0, c);
+    if (BN1 && active) b1.load(a.P, ps.bn, c);
+    // stage: BN0 + ACT0 applied once per element; outside the image: zero (the conv's padding)
+    if (active) {
+        const int npix = rows * cols;
+        const T* xb = x + static_cast<int64_t>(n) * a.H * a.W * ldx + c;
+        constexpr int U = 6;  // loads in flight per thread (a dependent load per iteration was latency bound)
+        for (int p0 = lanep; p0 < npix; p0 += prow * U) {
+            uint4 raw[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int pix = p0 + u * prow;
+                const int r = pix / cols, cc = pix - r * cols;
+                const int ih = h0 + r, iw = w0 + cc;
+                ok[u] = pix < npix && ih >= 0 && ih < a.H && iw >= 0 && iw < a.W;
+                if (ok[u]) raw[u] = __ldg(reinterpret_cast<const uint4*>(xb + (static_cast<int64_t>(ih) * a.W + iw) * ldx));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int pix = p0 + u * prow;
+                if (pix >= npix) break;
+                float v[V];
+                if (ok[u]) {
+                    unpack16(raw[u], v, static_cast<T*>(nullptr));
+                    if (BN0) b0.apply(v);
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        if (ACT0 >= 1) v[q] = fmaxf(v[q], 0.f);
+                        if (ACT0 == 2) v[q] = fminf(v[q], 6.f);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) v[q] = 0.f;
+                }
+                float* dst = tile + static_cast<int64_t>(pix) * CS + cv * V;
+#pragma unroll
+                for (int q = 0; q < V; q += 4)
+                    *reinterpret_cast<float4*>(dst + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+            }
+        }
+    }
+    __syncthreads();
+    if (!active) return;
+    float bias[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) bias[q] = a.dw_b ? __ldg(a.dw_b + c + q) : 0.f;
+    T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    const int nout = nr * a.OW;
+    for (int pix = lanep; pix < nout; pix += prow) {
+        const int r = pix / a.OW, ow = pix - r * a.OW;
+        float acc[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = bias[q];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const int kr = k / 3, kc = k - kr * 3;
+            const float* src = tile + (static_cast<int64_t>(r * S + kr) * cols + ow * S + kc) * CS + cv * V;
+            const float* wv = taps + k * CS + cv * V;
+#pragma unroll
+            for (int q = 0; q < V; q += 4) {
+                const float4 t4 = *reinterpret_cast<const float4*>(src + q);
+                const float4 w4 = *reinterpret_cast<const float4*>(wv + q);
+                acc[q] = fmaf(t4.x, w4.x, acc[q]);
+                acc[q + 1] = fmaf(t4.y, w4.y, acc[q + 1]);
+                acc[q + 2] = fmaf(t4.z, w4.z, acc[q + 2]);
+                acc[q + 3] = fmaf(t4.w, w4.w, acc[q + 3]);
+            }
+        }
+        if (BN1) b1.apply(acc);
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            if (ACT1 >= 1) acc[q] = fmaxf(acc[q], 0.f);
+            if (ACT1 == 2) acc[q] = fminf(acc[q], 6.f);
+        }
+        store16(out + ((static_cast<int64_t>(n) * a.OH + oh0 + r) * a.OW + ow) * a.out_ld, acc);
+    }
+}
+
+template <typename T>
+bool launch_dwconv3_tile(const DfpArgs& a, const ChainSpec& c, const PostSpec& ps, cudaStream_t s) {
+    static const bool off = std::getenv("SOL_NO_DW_TILE") != nullptr;
+    constexpr int V = VEC<T>;
+    if (off || a.ph != 1 || a.pw != 1 || a.sh != 1 || a.sw != 1 || a.C % V) return false;  // stride 1 only
+    // channel slice: up to 64 channels; band height: the f32 tile within ~100 KB
+    const int CS = std::min(a.C, 64);
+    int TH = 8;
+    auto bytes = [&](int th) {
+        return static_cast<size_t>(((std::min(th, a.OH) - 1) * a.sh + 3)) * ((a.OW - 1) * a.sh + 3) * CS * 4 +
+               static_cast<size_t>(9) * CS * 4;
+    };
+    static const size_t cap = (std::getenv("SOL_DW_TILE_KB") ? std::atoi(std::getenv("SOL_DW_TILE_KB")) : 100) * 1024;
+    while (TH > 1 && bytes(TH) > cap) TH /= 2;
+    if (bytes(TH) > 110 * 1024) return false;
+    const size_t smem = bytes(TH);
+    const dim3 grid(static_cast<unsigned>(a.N * ((a.OH + TH - 1) / TH)), static_cast<unsigned>((a.C + CS - 1) / CS));
+    const bool b0 = c.bn0 >= 0, b1 = ps.bn >= 0;
+#define SOL_DT(B0, A0, B1, A1)                                                                                     \
+    do {                                                                                                           \
+        static std::once_flag once;                                                                                \
+        std::call_once(once, [] {                                                                                  \
+            SOL_CUDA(cudaFuncSetAttribute(dwconv3_tile_kernel<T, B0, A0, B1, A1>,                                  \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));               \
+        });                                                                                                        \
+        dwconv3_tile_kernel<T, B0, A0, B1, A1><<<grid, THREADS, smem, s>>>(a, c, ps, TH, CS);                     \
+    } while (0)
+#define SOL_DT_A1(B0, A0, B1) \
+    do { if (ps.act == 0) SOL_DT(B0, A0, B1, 0); else if (ps.act == 1) SOL_DT(B0, A0, B1, 1); else SOL_DT(B0, A0, B1, 2); } while (0)
+#define SOL_DT_B1(B0, A0) do { if (b1) SOL_DT_A1(B0, A0, true); else SOL_DT_A1(B0, A0, false); } while (0)
+#define SOL_DT_A0(B0) do { if (c.act == 0) SOL_DT_B1(B0, 0); else if (c.act == 1) SOL_DT_B1(B0, 1); else SOL_DT_B1(B0, 2); } while (0)
+    if (b0) SOL_DT_A0(true);
+    else SOL_DT_A0(false);
+#undef SOL_DT_A0
+#undef SOL_DT_B1
+#undef SOL_DT_A1
+#undef SOL_DT
+    SOL_CUDA(cudaGetLastError());
+    return true;
+}
+
 template <typename T>
 bool launch_dwconv3_chain(const DfpArgs& a, cudaStream_t s) {
     if (a.kh != 3 || a.kw != 3) return false;
     const ChainSpec c = match_chain(a.pre);
     const PostSpec ps = match_post(a.post);
     if (!c.ok || c.add || !ps.ok || a.in_kind[c.s0] != IN_PIX || a.in_coff[c.s0] != 0) return false;
+    if (launch_dwconv3_tile<T>(a, c, ps, s)) return true;
+    if (std::min(a.C / VEC<T>, THREADS) * VEC<T> > 1024) return false;  // the kernel's shared tap table
     const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW, 2).grid;
     const bool b0 = c.bn0 >= 0, b1 = ps.bn >= 0;
 #define SOL_DW(B0, A0, B1, A1) dwconv3_chain_kernel<T, B0, A0, B1, A1><<<grid, THREADS, 0, s>>>(a, c, ps)
