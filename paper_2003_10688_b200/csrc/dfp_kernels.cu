@@ -1224,28 +1224,43 @@ __global__ void __launch_bounds__(THREADS) pool_kernel(const __grid_constant__ D
 
 template <typename T>
 __global__ void __launch_bounds__(THREADS) gap_kernel(const __grid_constant__ DfpArgs a) {
+    // generic source programs (e.g. DenseNet's Concat + BN + ReLU + GAP): 8 lanes of a warp share
+    // one (image, channel vector) and stride its pixels, then combine by shuffles in a fixed order
+    // (one thread walking all pixels was latency bound: DenseNet-121's final unit took 124 us)
     constexpr int V = VEC<T>;
+    constexpr int G = 8;
     const int cv = a.C / V;
     const int64_t total = static_cast<int64_t>(a.N) * cv;
     const int hw = a.H * a.W;
-    for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
-         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int n = static_cast<int>(v / cv);
-        const int c = static_cast<int>(v - static_cast<int64_t>(n) * cv) * V;
+    const int g = threadIdx.x & (G - 1);
+    const int64_t per_iter = static_cast<int64_t>(gridDim.x) * (blockDim.x / G);
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * (blockDim.x / G); base < total; base += per_iter) {
+        const int64_t v = base + threadIdx.x / G;
+        const bool active = v < total;  // the shuffles below stay warp-uniform
+        const int n = active ? static_cast<int>(v / cv) : 0;
+        const int c = active ? static_cast<int>(v - static_cast<int64_t>(n) * cv) * V : 0;
         float acc[V];
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = 0.f;
-        for (int p = 0; p < hw; ++p) {
-            float r[NREG][V];
-            run_prog<T>(a.pre, a, static_cast<int64_t>(n) * hw + p, n, c, r);
+        if (active) {
+            for (int p = g; p < hw; p += G) {
+                float r[NREG][V];
+                run_prog<T>(a.pre, a, static_cast<int64_t>(n) * hw + p, n, c, r);
 #pragma unroll
-            for (int i = 0; i < V; ++i) acc[i] += r[0][i];
+                for (int i = 0; i < V; ++i) acc[i] += r[0][i];
+            }
         }
-        float r[NREG][V];
 #pragma unroll
-        for (int i = 0; i < V; ++i) r[0][i] = acc[i] / static_cast<float>(hw);
-        run_prog<T>(a.post, a, n, n, c, r);
-        store_out<T>(a, n, c, r[0]);
+        for (int i = 0; i < V; ++i)
+#pragma unroll
+            for (int off = G / 2; off > 0; off >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+        if (active && g == 0) {
+            float r[NREG][V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) r[0][i] = acc[i] / static_cast<float>(hw);
+            run_prog<T>(a.post, a, n, n, c, r);
+            store_out<T>(a, n, c, r[0]);
+        }
     }
 }
 
@@ -2669,7 +2684,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
         case FAM_GAP: {
             const int64_t work = static_cast<int64_t>(a.N) * (a.C / V);
             if (launch_gap_chain<T>(a, s, grid_for(work, THREADS))) break;
-            gap_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);
+            gap_kernel<T><<<grid_for(work * 8, THREADS), THREADS, 0, s>>>(a);
             break;
         }
         case FAM_DWCONV: {
