@@ -175,3 +175,31 @@ def test_options_fingerprint_tracks_plan_fields(monkeypatch):
     assert fp0 == frontend.OptimizeOptions(batch=4, tune_cache_path="/x").fingerprint()
     monkeypatch.setenv("SOL_NO_DUAL", "1")  # plan-changing switches are part of the key
     assert fp0 != a.fingerprint() and "SOL_NO_DUAL" in a.fingerprint()
+
+
+def test_relu_mask_from_output_is_exact_and_fuses():
+    """The training rewrite ReluBack(d, x) -> ReluBack(d, relu(x)) (and ReLU6Back) leaves every
+    oracle gradient bit-identical and lets partition() fuse BN [+ Add] + ReLU (fewer units)."""
+    import numpy as np
+    from oracle import sol_oracle as O
+    from paper_2003_10688_b200 import autodiff, graph, models, partition, passes
+    for g in (models.resnet(18, hw=16, classes=10, width=8, train=True),
+              models.mobilenet_v2(hw=32, classes=10, width_mult=0.5, train=True)):
+        hw = g.graph_inputs[0].meta.shape[2]
+        gi = graph.infer_shapes(g, 2)
+        tg = autodiff.build_training_graph(gi)
+        a = graph.infer_shapes(tg.graph, 2)
+        b = graph.infer_shapes(passes.relu_mask_from_output(a), 2)
+        assert any(n.op in ("ReluBack", "ReLU6Back") for n in b.nodes)
+        for n in b.nodes:
+            if n.op in ("ReluBack", "ReLU6Back"):
+                assert b.find_node(n.inputs[1]).op in ("ReLU", "ReLU6")
+        assert len(partition.partition(passes.run_pipeline(b))) < len(partition.partition(passes.run_pipeline(a)))
+        rng = np.random.default_rng(1)
+        ins = {"x": rng.uniform(-1, 1, (2, 3, hw, hw)).astype(np.float32)}
+        t = np.zeros((2, 10), np.float32)
+        t[np.arange(2), [3, 7]] = 1
+        ins["t"] = t
+        ea, eb = O.run_graph(a, ins), O.run_graph(b, ins)
+        for _, gn in tg.param_grads:
+            assert np.array_equal(ea[gn], eb[gn]), gn
