@@ -412,6 +412,7 @@ public:
             g.Nout = static_cast<int>(cin_);
             g.K_pad = c.kpad;
             g.ldo = static_cast<int>(out_.ld);
+            g.tile_n = tile_n_;
             igemm_launch(g, s);
         }
         packed_valid_ = true;
@@ -609,6 +610,7 @@ public:
                 g.Nout = static_cast<int>(cin_);
                 g.K_pad = kpad_;
                 g.ldo = static_cast<int>(out_.ld);
+                g.tile_n = tile_n_;
                 igemm_launch(g, s);
                 break;
             }
@@ -661,7 +663,9 @@ public:
         return true;
     }
     bool set_option(int key, int value) override {
-        if (key != SOL_MODOPT_TILE_N || stem_ || (op_ != SOL_OP_CONV2D && op_ != SOL_OP_LINEAR)) return false;
+        if (key != SOL_MODOPT_TILE_N || stem_ ||
+            (op_ != SOL_OP_CONV2D && op_ != SOL_OP_LINEAR && op_ != SOL_OP_CONV2DBACKX && op_ != SOL_OP_LINEARBACKX))
+            return false;
         if (value != 0 && value != 64 && value != 65 && value != 128 && value != 256) return false;
         if (value == 65 && dtype_ != DT_BF16) return false;
         tile_n_ = value;

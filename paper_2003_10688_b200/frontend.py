@@ -690,7 +690,9 @@ def autotune(plan: "DevicePlan", cache: Optional[TuneCache] = None) -> Dict[int,
             continue
         u = heavy_units[st.output]
         fam = st.family
-        if not (fam.startswith("conv_fprop") or fam.startswith("linear")):
+        if not (fam.startswith("conv_fprop") or fam.startswith("linear") or fam == "conv_dgrad_tcgen05"):
+            continue
+        if fam.startswith("linear") and ("wgrad" in fam):
             continue
         cands = TILE_CANDIDATES["dual" if len(u.node_ids) >= 5 and fam == "conv_fprop_fused_tcgen05"
                                 and sum(plan.graph.find_node(n).op == "Conv2d" for n in u.node_ids) == 2
