@@ -1598,54 +1598,8 @@ __global__ void __launch_bounds__(THREADS) dwconv_kernel(const __grid_constant__
 // thread; the block and grid combination is f64 either way).
 // Finalises channel c with a whole block (the first 128 threads reduce, in the fixed order of the
 // stand-alone launch, so fused and separate finalisation are bit-identical).
-__device__ __forceinline__ void finalize_channel(const FinalizeArgs& a, const int c, double (*wsum)[4]) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
-    double q[4] = {0.0, 0.0, 0.0, 0.0};
-    if (threadIdx.x < 128) {
-        const double* base = a.partial + static_cast<int64_t>(c) * a.blocks * ns;
-        // the first 8 partials of every thread are loaded together (16-byte loads; a dependent
-        // load-add chain made this launch latency bound at ~7 us), then summed in block order
-        constexpr int J = 8;
-        double2 lo[J], hi[J];
-    #pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int b = threadIdx.x + 128 * j;
-            lo[j] = make_double2(0.0, 0.0);
-            hi[j] = make_double2(0.0, 0.0);
-            if (b < a.blocks) {
-                const double2* src = reinterpret_cast<const double2*>(base + static_cast<int64_t>(b) * ns);
-                lo[j] = src[0];
-                if (ns == 4) hi[j] = src[1];
-            }
-        }
-    #pragma unroll
-        for (int j = 0; j < J; ++j) {
-            q[0] += lo[j].x;
-            q[1] += lo[j].y;
-            q[2] += hi[j].x;
-            q[3] += hi[j].y;
-        }
-        for (int b = threadIdx.x + 128 * J; b < a.blocks; b += 128) {
-            const double* src = base + static_cast<int64_t>(b) * ns;
-            q[0] += src[0];
-            q[1] += src[1];
-            if (ns == 4) {
-                q[2] += src[2];
-                q[3] += src[3];
-            }
-        }
-    #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-    #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
-            if (lane == 0) wsum[w][k] = q[k];
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) [&] {  // a lambda: the BN_BACK4 branch returns early
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
+// The per-channel finalisation arithmetic on the channel's combined sums q[0..3] (f64).
+__device__ void finalize_math(const FinalizeArgs& a, const int c, const double* q) {
     if (a.mode == FIN_BN_BACK4) {
         const double sd = q[0], sdx = q[1], sx = q[2], sxx = q[3];
         const double m = a.count;
@@ -1726,7 +1680,58 @@ __device__ __forceinline__ void finalize_channel(const FinalizeArgs& a, const in
             a.coef[2 * a.C + c] = static_cast<float>(-gr * s1 / m);
         }
     }
-    }();
+}
+
+__device__ __forceinline__ void finalize_channel(const FinalizeArgs& a, const int c, double (*wsum)[4]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ns = a.mode == FIN_BN_BACK4 ? 4 : 2;
+    double q[4] = {0.0, 0.0, 0.0, 0.0};
+    if (threadIdx.x < 128) {
+        const double* base = a.partial + static_cast<int64_t>(c) * a.blocks * ns;
+        // the first 8 partials of every thread are loaded together (16-byte loads; a dependent
+        // load-add chain made this launch latency bound at ~7 us), then summed in block order
+        constexpr int J = 8;
+        double2 lo[J], hi[J];
+    #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int b = threadIdx.x + 128 * j;
+            lo[j] = make_double2(0.0, 0.0);
+            hi[j] = make_double2(0.0, 0.0);
+            if (b < a.blocks) {
+                const double2* src = reinterpret_cast<const double2*>(base + static_cast<int64_t>(b) * ns);
+                lo[j] = src[0];
+                if (ns == 4) hi[j] = src[1];
+            }
+        }
+    #pragma unroll
+        for (int j = 0; j < J; ++j) {
+            q[0] += lo[j].x;
+            q[1] += lo[j].y;
+            q[2] += hi[j].x;
+            q[3] += hi[j].y;
+        }
+        for (int b = threadIdx.x + 128 * J; b < a.blocks; b += 128) {
+            const double* src = base + static_cast<int64_t>(b) * ns;
+            q[0] += src[0];
+            q[1] += src[1];
+            if (ns == 4) {
+                q[2] += src[2];
+                q[3] += src[3];
+            }
+        }
+    #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+    #pragma unroll
+            for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
+            if (lane == 0) wsum[w][k] = q[k];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
+        finalize_math(a, c, q);
+    }
     __syncthreads();
 }
 
@@ -1756,12 +1761,35 @@ bool launch_coop(K kernel, dim3 grid, size_t smem, cudaStream_t s, Args... args)
     return true;
 }
 
-// after every block wrote its partials: grid barrier, then block b finalises channels b, b + nb, ..
+// after every block wrote its partials: grid barrier, then every warp of the grid finalises
+// channels (lanes stride the channel's partials in a fixed order, a fixed shuffle tree combines
+// them): ~one channel per warp, where a channel per block serialised 2048-channel layers
 __device__ __forceinline__ void fused_finalize(const FinalizeArgs& fin, double (*wsum)[4]) {
+    (void)wsum;
     __threadfence();
     cooperative_groups::this_grid().sync();
-    const int nb = gridDim.x * gridDim.y;
-    for (int c = blockIdx.y * gridDim.x + blockIdx.x; c < fin.C; c += nb) finalize_channel(fin, c, wsum);
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int nw = gridDim.x * gridDim.y * wpb;
+    const int ns = fin.mode == FIN_BN_BACK4 ? 4 : 2;
+    for (int c = (blockIdx.y * gridDim.x + blockIdx.x) * wpb + (threadIdx.x >> 5); c < fin.C; c += nw) {
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* base = fin.partial + static_cast<int64_t>(c) * fin.blocks * ns;
+        for (int b = lane; b < fin.blocks; b += 32) {
+            const double* src = base + static_cast<int64_t>(b) * ns;
+            q[0] += src[0];
+            q[1] += src[1];
+            if (ns == 4) {
+                q[2] += src[2];
+                q[3] += src[3];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
+        if (lane == 0) finalize_math(fin, c, q);
+    }
 }
 
 template <typename T, int MODE>
