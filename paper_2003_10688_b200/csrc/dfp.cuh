@@ -162,9 +162,11 @@ void dfp_reduce_finalize(const DfpArgs& a, const FinalizeArgs& f, cudaStream_t s
 // dfp_lower.cpp:709-753, 806-851): one reduction over (dy, x) producing, per channel and block,
 // [sum dy, sum dy*(x - shift), sum (x - shift), sum (x - shift)^2] (f64 partials [blocks][C][4]),
 // then (after FIN_BN_BACK4) dx = A*dy + B*xhat + Cc with xhat = ((x - mean_hi) - mean_lo) * rstd.
-// (returns true when the finalisation `fin` ran fused in the same cooperative launch)
-bool bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
-                    double* partial, int blocks, cudaStream_t s, const FinalizeArgs* fin = nullptr);
+// Returns 0 (reduction only), 1 (+ the finalisation `fin`, fused in one cooperative launch) or
+// 2 (+ also the BatchNormBackX apply into `apply_out`, over each block's own rows, same launch).
+int bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
+                   double* partial, int blocks, cudaStream_t s, const FinalizeArgs* fin = nullptr,
+                   void* apply_out = nullptr);
 void bn_back_apply(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* coef,
                    const float* xhat, void* dx, cudaStream_t s);
 

@@ -1737,6 +1737,52 @@ __device__ __forceinline__ void finalize_channel(const FinalizeArgs& a, const in
 
 enum RRMode { RR_BNBACK = 0, RR_STATS = 1, RR_SUM = 2 };
 
+// BatchNormBackX apply for the pixel range a reduction block owned (after the grid-wide
+// finalisation): dx = A dy + B rstd ((x - mean_hi) - mean_lo) + D, the same arithmetic as
+// bnback_apply_kernel; the block re-reads the (dy, x) rows it just reduced, mostly from L2.
+template <typename T>
+__device__ __forceinline__ void bnback_apply_range(const T* __restrict__ dy, const T* __restrict__ x, int C,
+                                                   int64_t p0, int64_t p1, int row, int rows, int c,
+                                                   const FinalizeArgs& fin, T* __restrict__ dx, bool act) {
+    constexpr int V = VEC<T>;
+    __threadfence();
+    cooperative_groups::this_grid().sync();  // every channel's coefficients are final
+    if (!act) return;
+    float A[V], Bs[V], D[V], mh[V], ml[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const float rstd = fin.xhat[2 * C + c + i];
+        A[i] = fin.coef[c + i];
+        Bs[i] = fin.coef[C + c + i] * rstd;
+        D[i] = fin.coef[2 * C + c + i];
+        mh[i] = fin.xhat[c + i];
+        ml[i] = fin.xhat[C + c + i];
+    }
+    constexpr int U = 4;
+    for (int64_t pb = p0 + row; pb < p1; pb += static_cast<int64_t>(rows) * U) {
+        uint4 rd[U], rx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = pb + static_cast<int64_t>(u) * rows;
+            if (p < p1) {
+                rd[u] = __ldg(reinterpret_cast<const uint4*>(dy + p * C + c));
+                rx[u] = __ldg(reinterpret_cast<const uint4*>(x + p * C + c));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = pb + static_cast<int64_t>(u) * rows;
+            if (p >= p1) break;
+            float dv[V], xv[V], o[V];
+            unpack16(rd[u], dv, static_cast<T*>(nullptr));
+            unpack16(rx[u], xv, static_cast<T*>(nullptr));
+#pragma unroll
+            for (int i = 0; i < V; ++i) o[i] = fmaf(dv[i], A[i], fmaf((xv[i] - mh[i]) - ml[i], Bs[i], D[i]));
+            store16(dx + p * C + c, o);
+        }
+    }
+}
+
 // Cooperative launch (all blocks co-resident: grid.sync() is legal) of a one-wave reduction whose
 // finalisation runs in the same kernel after the grid barrier: saves the stand-alone finalize
 // launch (~100 per ResNet-50 training step, ~7 us each). false when the grid does not fit.
@@ -1797,7 +1843,8 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
                                                                int C, int ld0, int ld1, int64_t P,
                                                                const float* __restrict__ shift,
                                                                double* __restrict__ partial, int cvb_arg,
-                                                               const __grid_constant__ FinalizeArgs fin, int do_fin) {
+                                                               const __grid_constant__ FinalizeArgs fin, int do_fin,
+                                                               T* __restrict__ apply_out) {
     __shared__ double fin_wsum[4][4];
     constexpr int V = VEC<T>;
     constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
@@ -1915,6 +1962,13 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_kernel(const T* __restri
         __syncthreads();
     }
     if (do_fin) fused_finalize(fin, fin_wsum);
+    if constexpr (MODE == RR_BNBACK) {
+        // fused BatchNormBackX apply over this block's own rows (cooperative launch, do_fin == 2)
+        if (do_fin == 2) {
+            const bool act = row < rows && (blockIdx.y * cvb + cvi) < cv_total;
+            bnback_apply_range<T>(x0, x1, C, p0, p1, row, rows, c, fin, apply_out, act);
+        }
+    }
 }
 
 // The same reductions fed by 1-D bulk copies: a block's pixel range [p0, p1) is one contiguous
@@ -1930,7 +1984,7 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_bulk_kernel(const T* __r
                                                                      const float* __restrict__ shift,
                                                                      double* __restrict__ partial, int chunk_px,
                                                                      int stages, const __grid_constant__ FinalizeArgs fin,
-                                                                     int do_fin) {
+                                                                     int do_fin, T* __restrict__ apply_out) {
     __shared__ double fin_wsum[4][4];
     constexpr int V = VEC<T>;
     constexpr int NS = MODE == RR_BNBACK ? 4 : 2;
@@ -2068,13 +2122,16 @@ __global__ void __launch_bounds__(THREADS, 2) rowreduce_bulk_kernel(const T* __r
         __syncthreads();
     }
     if (do_fin) fused_finalize(fin, fin_wsum);
+    if constexpr (MODE == RR_BNBACK) {
+        if (do_fin == 2) bnback_apply_range<T>(x0, x1, C, p0, p1, row, rows, c, fin, apply_out, active);
+    }
 }
 
 // Bulk-fed reduction launch (true) when the channels fit one block and rows are 16-byte aligned.
 template <typename T, int MODE>
 bool launch_rowreduce_bulk(const T* x0, const T* x1, int C, int ld0, int ld1, int64_t P, const float* shift,
                            double* partial, unsigned blocks, cudaStream_t s, const FinalizeArgs* fin,
-                           bool* fused) {
+                           bool* fused, T* apply_out = nullptr) {
     static const bool off = std::getenv("SOL_NO_BULK_REDUCE") != nullptr;
     constexpr int V = VEC<T>;
     constexpr int NI = MODE == RR_BNBACK ? 2 : 1;
@@ -2092,12 +2149,12 @@ bool launch_rowreduce_bulk(const T* x0, const T* x1, int C, int ld0, int ld1, in
     });
     if (smem > 110 * 1024) return false;
     if (fin && launch_coop(rowreduce_bulk_kernel<T, MODE>, dim3(blocks), smem, s, x0, x1, C, ld0, ld1, P, shift,
-                           partial, chunk_px, stages, *fin, 1)) {
+                           partial, chunk_px, stages, *fin, apply_out ? 2 : 1, apply_out)) {
         *fused = true;
         return true;
     }
     rowreduce_bulk_kernel<T, MODE><<<blocks, THREADS, smem, s>>>(x0, x1, C, ld0, ld1, P, shift, partial, chunk_px,
-                                                                 stages, FinalizeArgs{}, 0);
+                                                                 stages, FinalizeArgs{}, 0, static_cast<T*>(nullptr));
     SOL_CUDA(cudaGetLastError());
     return true;
 }
@@ -2106,18 +2163,20 @@ bool launch_rowreduce_bulk(const T* x0, const T* x1, int C, int ld0, int ld1, in
 // finalisation `fin`, tries the cooperative fused launch and reports it in *fused.
 template <typename T, int MODE>
 void launch_rowreduce(const T* x0, const T* x1, int C, int ld0, int ld1, int64_t P, const float* shift,
-                      double* partial, const ReduceGeo& rg, cudaStream_t s, const FinalizeArgs* fin, bool* fused) {
+                      double* partial, const ReduceGeo& rg, cudaStream_t s, const FinalizeArgs* fin, bool* fused,
+                      T* apply_out = nullptr) {
     const dim3 grid(static_cast<unsigned>(rg.blocks), static_cast<unsigned>(ceil_div(C / VEC<T>, rg.cvb)));
     *fused = false;
-    if (grid.y == 1 && launch_rowreduce_bulk<T, MODE>(x0, x1, C, ld0, ld1, P, shift, partial, grid.x, s, fin, fused))
+    if (grid.y == 1 &&
+        launch_rowreduce_bulk<T, MODE>(x0, x1, C, ld0, ld1, P, shift, partial, grid.x, s, fin, fused, apply_out))
         return;
     if (fin && launch_coop(rowreduce_kernel<T, MODE>, grid, 0, s, x0, x1, C, ld0, ld1, P, shift, partial, rg.cvb, *fin,
-                           1)) {
+                           apply_out ? 2 : 1, apply_out)) {
         *fused = true;
         return;
     }
     rowreduce_kernel<T, MODE><<<grid, THREADS, 0, s>>>(x0, x1, C, ld0, ld1, P, shift, partial, rg.cvb, FinalizeArgs{},
-                                                       0);
+                                                       0, static_cast<T*>(nullptr));
     SOL_CUDA(cudaGetLastError());
 }
 
@@ -3022,8 +3081,8 @@ int dfp_reduce_blocks(int64_t pixels, int C, int dtype) {
     return reduce_geo(pixels, C, dtype == DT_BF16 ? 8 : 4).blocks;
 }
 
-bool bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
-                    double* partial, int blocks, cudaStream_t s, const FinalizeArgs* fin) {
+int bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pixels, const float* shift,
+                   double* partial, int blocks, cudaStream_t s, const FinalizeArgs* fin, void* apply_out) {
     const int V = dtype == DT_BF16 ? 8 : 4;
     if (C % V != 0) throw std::invalid_argument("bn_back_reduce: channel count must be a multiple of 16 bytes");
     const ReduceGeo rg = reduce_geo(pixels, C, V);
@@ -3032,11 +3091,11 @@ bool bn_back_reduce(int dtype, const void* dy, const void* x, int C, int64_t pix
     if (dtype == DT_BF16)
         launch_rowreduce<__nv_bfloat16, RR_BNBACK>(static_cast<const __nv_bfloat16*>(dy),
                                                    static_cast<const __nv_bfloat16*>(x), C, C, C, pixels, shift,
-                                                   partial, rg, s, fin, &fused);
+                                                   partial, rg, s, fin, &fused, static_cast<__nv_bfloat16*>(apply_out));
     else
         launch_rowreduce<float, RR_BNBACK>(static_cast<const float*>(dy), static_cast<const float*>(x), C, C, C,
-                                           pixels, shift, partial, rg, s, fin, &fused);
-    return fused;
+                                           pixels, shift, partial, rg, s, fin, &fused, static_cast<float*>(apply_out));
+    return fused ? (apply_out ? 2 : 1) : 0;
 }
 
 void dfp_reduce_finalize(const DfpArgs& a, const FinalizeArgs& f, cudaStream_t s) {

@@ -1006,10 +1006,17 @@ public:
             f.out1 = sib_gamma;
             f.out0 = sib_beta;
         }
-        // one pass over (dy, x) + the finalisation, fused in one cooperative launch when possible
-        if (!bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), nullptr, partial, blocks_, s, &f))
-            dfp_finalize(f, s);
-        if (op_ == SOL_OP_BATCHNORMBACKGAMMA) return;
+        // one pass over (dy, x) + the finalisation [+ the dx apply over each block's own rows], fused
+        // in one cooperative launch when the grid is co-resident
+        // opt-in (SOL_BNBACK_FUSED_APPLY=1): measured slower on B200 (14.84 vs 14.30 ms per ResNet-50
+        // training step): the one-wave reduction grid applies at lower occupancy than the dedicated
+        // apply kernel, and the second grid barrier costs more than the saved launch
+        static const bool fuse_apply = std::getenv("SOL_BNBACK_FUSED_APPLY") != nullptr;
+        void* apply_out = (op_ == SOL_OP_BATCHNORMBACKGAMMA || !fuse_apply) ? nullptr : out;
+        const int fused = bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), nullptr, partial, blocks_,
+                                         s, &f, apply_out);
+        if (fused == 0) dfp_finalize(f, s);
+        if (op_ == SOL_OP_BATCHNORMBACKGAMMA || fused == 2) return;
         bn_back_apply(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), coef_, xhat_, out, s);
     }
 
