@@ -3,6 +3,7 @@
 // reports cycles per MMA. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
 //   -I../../paper_2003_10688_b200/csrc mma_rate.cu -o mma_rate -lcuda
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include "tc.cuh"
 
@@ -262,8 +263,12 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters, long long* out)
     }
 }
 
+// one probe per process when an index is given (a faulting probe poisons the context)
+static int g_sel = -1, g_idx = -1;
+
 template <int N, int AMODE, bool MISALIGN = true, bool RANDOM = false>
 void run(const char* name) {
+    if (++g_idx != g_sel && g_sel >= 0) return;
     long long* d;
     cudaMalloc(&d, 32);
     const int smem = (AMODE == 19 || AMODE == 20 || AMODE >= 30) ? 225 * 1024 : 30720 + 9 * N * 128 + 2048;
@@ -290,7 +295,8 @@ void run(const char* name) {
     cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) g_sel = atoi(argv[1]);
     run<64, 18>("halo-like runtime bounds");
     run<64, 23>("tile protocol + epilogue");
     run<64, 33>("protocol, runtime bounds/base");
