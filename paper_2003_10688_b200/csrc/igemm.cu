@@ -231,8 +231,11 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
 
 // split-K reduction straight into the canonical layout: canonical i = ((co*Cin + ci)*KH + kh)*KW + kw
 // reads packed j = co*KH*KW*ld + (kh*KW + kw)*ld + ci of every split
+// splits = partials per column group; column group g (packed columns [g * cpg, (g + 1) * cpg))
+// sums partials [g * splits, (g + 1) * splits) -- one group (cpg = all columns) except for the
+// halo wgrad, whose CTAs each own one filter row
 __global__ void wgrad_reduce_canon_kernel(const float* __restrict__ ws, float* __restrict__ w, int64_t n, int splits,
-                                          int Cout, int Cin, int KH, int KW, int ld) {
+                                          int Cout, int Cin, int KH, int KW, int ld, int cpg) {
     const int64_t total = static_cast<int64_t>(Cout) * Cin * KH * KW;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -240,28 +243,32 @@ __global__ void wgrad_reduce_canon_kernel(const float* __restrict__ ws, float* _
         const int kh = static_cast<int>((i / KW) % KH);
         const int ci = static_cast<int>((i / (KW * KH)) % Cin);
         const int co = static_cast<int>(i / (static_cast<int64_t>(KW) * KH * Cin));
-        const int64_t j = static_cast<int64_t>(co) * KH * KW * ld + (kh * KW + kw) * ld + ci;
+        const int pcol = (kh * KW + kw) * ld + ci;
+        const int64_t j = static_cast<int64_t>(co) * KH * KW * ld + pcol;
+        const int sp0 = pcol / cpg * splits;
         float acc = 0.f;
-        for (int sp = 0; sp < splits; ++sp) acc += __ldg(ws + sp * n + j);
+        for (int sp = sp0; sp < sp0 + splits; ++sp) acc += __ldg(ws + sp * n + j);
         w[i] = acc;
     }
 }
 
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dw, int64_t n,
-                                    int splits) {
+                                    int splits, int ncol, int cpg) {
     const int64_t i4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
     if (i4 >= n) return;
-    if (i4 + 4 <= n) {
+    if (i4 + 4 <= n && ncol % 4 == 0 && cpg % 4 == 0) {
+        const int s0 = static_cast<int>(i4 % ncol) / cpg * splits;
         float4 acc = make_float4(0, 0, 0, 0);
-        for (int s = 0; s < splits; ++s) {
+        for (int s = s0; s < s0 + splits; ++s) {
             float4 v = __ldg(reinterpret_cast<const float4*>(ws + s * n + i4));
             acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
         *reinterpret_cast<float4*>(dw + i4) = acc;
     } else {
-        for (int64_t i = i4; i < n; ++i) {
+        for (int64_t i = i4; i < n && i < i4 + 4; ++i) {
+            const int s0 = static_cast<int>(i % ncol) / cpg * splits;
             float acc = 0.f;
-            for (int s = 0; s < splits; ++s) acc += ws[s * n + i];
+            for (int s = s0; s < s0 + splits; ++s) acc += ws[s * n + i];
             dw[i] = acc;
         }
     }
@@ -1069,7 +1076,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 
 struct WgradPlan {
     int ncol, bn, splits, kb_per_split;
-    bool fast = false, swap = false;
+    bool fast = false, swap = false, halo = false;
+    int spg = 0, cpg = 0;  // reduction: partials per column group, columns per group (0: one group)
     int m_tiles = 1, n_tiles = 1;
 };
 
@@ -1077,6 +1085,13 @@ WgradPlan plan_wgrad(const WgradArgs& a) {
     WgradPlan p;
     p.ncol = a.kh * a.kw * a.SC;
     const int total_kb = static_cast<int>(ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, 64));
+    if (wgrad_halo_supported(a)) {  // one partial per CTA (wgrad_halo.cu)
+        p.halo = true;
+        p.bn = 64;
+        p.splits = wgrad_halo_splits(a, &p.spg, &p.cpg);
+        p.kb_per_split = 0;
+        return p;
+    }
     if (a.dtype == DT_BF16 && a.SC % 64 == 0 && (a.ld_dy * 2) % 16 == 0) {
         p.fast = true;
         p.swap = a.Cout < 128 && p.ncol > a.Cout;
@@ -1174,7 +1189,9 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
     WgradPlan p = plan_wgrad(a);
     if (p.splits <= 1) a.workspace = nullptr;
     else if (a.workspace == nullptr) throw std::invalid_argument("wgrad: workspace required");
-    if (p.fast) {
+    if (p.halo) {
+        wgrad_halo_launch(a, s);
+    } else if (p.fast) {
         if (p.swap) {
             switch (p.bn) {
                 case 64: launch_wgrad_ws<64, true>(a, p, s); break;
@@ -1205,14 +1222,14 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
         const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
         const int64_t total = static_cast<int64_t>(a.Cout) * a.canon_cin * a.kh * a.kw;
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8L * num_sms())));
-        wgrad_reduce_canon_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw_canon, n, p.splits, a.Cout, a.canon_cin,
-                                                       a.kh, a.kw, a.SC);
+        wgrad_reduce_canon_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw_canon, n, p.spg ? p.spg : p.splits, a.Cout,
+                                                       a.canon_cin, a.kh, a.kw, a.SC, p.cpg ? p.cpg : p.ncol);
         SOL_CUDA(cudaGetLastError());
     } else if (p.splits > 1) {
         const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
         const int threads = 256;
         wgrad_reduce_kernel<<<static_cast<unsigned>(ceil_div(ceil_div(n, 4), threads)), threads, 0, s>>>(
-            a.workspace, a.dw, n, p.splits);
+            a.workspace, a.dw, n, p.spg ? p.spg : p.splits, p.ncol, p.cpg ? p.cpg : p.ncol);
         SOL_CUDA(cudaGetLastError());
     } else if (a.dw_canon) {
         unpack_conv_grad(a.dw, a.dw_canon, a.Cout, a.canon_cin, a.kh, a.kw, a.SC, s);

@@ -100,6 +100,10 @@ struct WgradArgs {
     int canon_cin = 0;
 };
 void wgrad_launch(const WgradArgs& a, cudaStream_t stream);
+// halo weight gradient (wgrad_halo.cu): stride-1 3x3, 64 -> 64 or 128 -> 128 channels, bf16
+bool wgrad_halo_supported(const WgradArgs& a);
+int wgrad_halo_splits(const WgradArgs& a, int* splits_per_group = nullptr, int* cols_per_group = nullptr);
+void wgrad_halo_launch(const WgradArgs& a, cudaStream_t stream);
 size_t wgrad_workspace_floats(const WgradArgs& a);
 
 }  // namespace solb200

@@ -26,6 +26,8 @@ CASES = [
     (8, 64, 28, 28, 256, 1, 1, 0),
     (3, 64, 56, 56, 64, 3, 1, 1),     # halo-tile kernel (halo.cu), ResNet-50 layer-1 shape
     (2, 64, 13, 29, 64, 3, 1, 1),     # halo-tile kernel, ragged rows / junk columns
+    (2, 128, 28, 28, 128, 3, 1, 1),   # ResNet-50 layer-2 shape: halo fprop, halo wgrad by filter row
+    (3, 128, 11, 19, 128, 3, 1, 1),   # halo wgrad (128 channels), ragged rows / junk columns
 ]
 
 
