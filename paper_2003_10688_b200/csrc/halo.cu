@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
         const int q = warp & 3;
         const int half = (warp - 5) >> 2;
         const bool has_bias = a.bias != nullptr, has_fold = a.ep_scale != nullptr, has_res = a.residual != nullptr;
+        const bool res_mask = a.res_mode == 1;
         const int act = a.relu ? 1 : a.act;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
         const __nv_bfloat16* res = static_cast<const __nv_bfloat16*>(a.residual);
@@ -374,12 +375,15 @@ __global__ void __launch_bounds__(HL_THREADS, 1)
                             float r8[8];
                             load16(rp + j, r8);
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) f[j + k] += r8[k];
+                            for (int k = 0; k < 8; ++k) f[j + k] = res_mask ? (r8[k] > 0.f ? f[j + k] : 0.f) : f[j + k] + r8[k];
                         }
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (n + j < a.Nout) f[j] += __bfloat162float(rp[j]);
+                            if (n + j < a.Nout) {
+                                const float r = __bfloat162float(rp[j]);
+                                f[j] = res_mask ? (r > 0.f ? f[j] : 0.f) : f[j] + r;
+                            }
                     }
                 }
                 if (act != 0) {

@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const bool has_bias = a.bias != nullptr;
         const bool has_fold = a.ep_scale != nullptr;
         const bool has_res = a.residual != nullptr;
+        const bool res_mask = a.res_mode == 1;
         const int act = a.relu ? 1 : a.act;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -643,7 +644,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                             rr[3] = __uint_as_float(r3);
                         }
 #pragma unroll
-                        for (int k = 0; k < static_cast<int>(16 / sizeof(TO)); ++k) f[j * (16 / sizeof(TO)) + k] += rr[k];
+                        for (int k = 0; k < static_cast<int>(16 / sizeof(TO)); ++k) {
+                            float& fv = f[j * (16 / sizeof(TO)) + k];
+                            fv = res_mask ? (rr[k] > 0.f ? fv : 0.f) : fv + rr[k];
+                        }
                     }
                 }
                 if (act != 0) {

@@ -42,6 +42,9 @@ struct IgemmArgs {
     const void* residual = nullptr;  // same dtype as the output, row stride ld_res
     int ld_res = 0;
     int act = 0;                     // 0 none, 1 relu, 2 relu6 (applied after the residual add)
+    // 1: the residual is a ReLU OUTPUT used as a backward mask instead of an addend:
+    //    y = residual > 0 ? acc : 0 (ReluBack(delta, relu(x)) fused into the dgrad epilogue)
+    int res_mode = 0;
     // dual GEMM (inference bottleneck-block fusion): K = [0, K1) reads A from `src` as a 1x1
     // stride-1 conv, K = [K1, K_pad) reads a second 1x1 conv with stride s2 over src2
     // [N, SH2, SW2, SC2] on the same output grid; B packs both weight matrices side by side.

@@ -424,6 +424,21 @@ public:
     // The plan compiler only forms such units when the conv output has no other consumer.
     void parse_epilogue(const sol_unit_desc& d) {
         if (d.n_ops == 1) return;
+        if (op_ == SOL_OP_CONV2DBACKX) {
+            // training plan fusion (fusion.fuse_dgrad_relu_back): ReluBack(dx, relu_out) with the mask
+            // read from the ReLU output (passes.relu_mask_from_output) applied in the GEMM epilogue
+            const sol_unit_op& r = d.ops[1];
+            if (d.n_ops != 2 || r.op != SOL_OP_RELUBACK || r.n_inputs != 2 || r.inputs[0] != -1 || r.inputs[1] < 0)
+                unsupported("dgrad epilogue fusion: only ReluBack(dx, relu output)");
+            if (!classes_.empty()) unsupported("strided dgrad (sub-pixel classes) has no fused ReluBack");
+            res_idx_ = r.inputs[1];
+            const Geo m = geo_b(d.bindings[res_idx_]);
+            if (m.ld != out_.ld || m.pixels() != out_.pixels()) unsupported("ReLU output layout mismatch");
+            res_mode_ = 1;
+            algo_bytes += double(m.pixels()) * m.ld * elem_size(dtype_);  // the mask read
+            family = "conv_dgrad_fused_tcgen05";
+            return;
+        }
         if (op_ != SOL_OP_CONV2D && op_ != SOL_OP_LINEAR) unsupported("epilogue fusion only after fprop");
         int k = 1;
         auto prev_ref = [&](int kk) { return -kk; };  // output of member op kk-1 is ref -(kk-1)-1 = -kk
@@ -611,6 +626,11 @@ public:
                 g.K_pad = kpad_;
                 g.ldo = static_cast<int>(out_.ld);
                 g.tile_n = tile_n_;
+                if (res_idx_ >= 0) {  // fused ReluBack: mask = relu output > 0
+                    g.residual = args[res_idx_];
+                    g.ld_res = static_cast<int>(out_.ld);
+                    g.res_mode = res_mode_;
+                }
                 igemm_launch(g, s);
                 break;
             }
@@ -696,6 +716,7 @@ private:
     int bn_g_ = -1, bn_b_ = -1, bn_m_ = -1, bn_v_ = -1;
     float bn_eps_ = 1e-5f;
     int res_idx_ = -1;
+    int res_mode_ = 0;  // 1: the residual binding is a ReLU output used as a backward mask
     int act_ = 0;
 };
 
@@ -1592,6 +1613,7 @@ std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
     const sol_unit_op& o0 = d.ops[0];
     if (d.kind == 1 && d.n_ops >= 5 && o0.op == SOL_OP_CONV2D && d.ops[2].op == SOL_OP_CONV2D)
         return std::make_unique<DualConvModule>(d);
+    if (d.kind == 1 && d.n_ops == 2 && o0.op == SOL_OP_CONV2DBACKX) return std::make_unique<HeavyModule>(d);
     if (d.kind == 1 && d.n_ops > 1 && (o0.op == SOL_OP_CONV2D || o0.op == SOL_OP_LINEAR)) {
         // heavy node + fused epilogue chain (plan-level fusion, see HeavyModule::parse_epilogue)
         const Geo g = geo_b(d.bindings[o0.inputs[0]]);

@@ -57,6 +57,8 @@ class OptimizeOptions:
     nccl_allreduce: bool = False   # test hook: run the NCCL gradient all-reduce even with one replica
     relu_mask_from_output: bool = True  # training: ReluBack masks read the ReLU output (passes.py), so
                                         # BN+ReLU fuse and the pre-activation is never stored
+    fuse_relu_back: bool = True    # training: a stride-1 Conv2dBackX applies the following ReluBack
+                                   # mask (read from the ReLU output) in its GEMM epilogue
     update_bn_stats: bool = True   # training: update BN running_mean / running_var on the device
                                    # (autodiff::update_bn_running_stats, autodiff.cpp:356-384)
     autotune: bool = False         # measure the tcgen05 tile configs of every conv/linear (dnn.cpp:214-290)
@@ -152,6 +154,9 @@ class DevicePlan:
             cg = run_pipeline(cg)
         self.graph = cg
         self.units: List[ExecUnit] = partition(cg)
+        if options.train and options.relu_mask_from_output and options.fuse_relu_back:
+            from .fusion import fuse_dgrad_relu_back
+            self.units = fuse_dgrad_relu_back(cg, self.units)
         if options.fuse_epilogue and not options.train:
             from .fusion import fuse_bottleneck_tails, fuse_conv_epilogues
             self.units = fuse_conv_epilogues(cg, self.units)
@@ -690,7 +695,7 @@ def autotune(plan: "DevicePlan", cache: Optional[TuneCache] = None) -> Dict[int,
             continue
         u = heavy_units[st.output]
         fam = st.family
-        if not (fam.startswith("conv_fprop") or fam.startswith("linear") or fam == "conv_dgrad_tcgen05"):
+        if not (fam.startswith("conv_fprop") or fam.startswith("linear") or fam.startswith("conv_dgrad")):
             continue
         if fam.startswith("linear") and ("wgrad" in fam):
             continue

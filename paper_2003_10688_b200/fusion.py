@@ -173,3 +173,54 @@ def fuse_stem_pool(g: ModelGraph, units: List[ExecUnit], direct_inputs) -> List[
         repl[j] = ExecUnit("dnn", list(u.node_ids) + list(v.node_ids), v.output, inputs, params)
         drop.add(i)
     return [repl.get(j, w) for j, w in enumerate(units) if j not in drop]
+
+
+def fuse_dgrad_relu_back(g: ModelGraph, units: List[ExecUnit]) -> List[ExecUnit]:
+    """Training plans: a stride-1 Conv2dBackX unit whose output feeds exactly one ReluBack unit
+    ReluBack(dx, relu_out) (the mask read from the ReLU output, passes.relu_mask_from_output) is
+    merged with it: the dgrad GEMM epilogue writes relu_out > 0 ? dx : 0, which is bit-for-bit the
+    ReluBack unit's output (the mask does not round), and dx never round-trips through HBM (one
+    write and two reads of an activation-sized tensor per inner ReLU saved). The merged unit runs
+    at the ReluBack's position. Strided dgrads (sub-pixel classes + interleave) and grouped convs
+    keep the separate unit."""
+    cons = g.consumers()
+    outputs = set(g.outputs)
+    owner = {}
+    for i, u in enumerate(units):
+        for nid in u.node_ids:
+            owner[nid] = i
+    merged_into = {}
+    for i, u in enumerate(units):
+        if u.kind != "dnn" or len(u.node_ids) != 1:
+            continue
+        n = g.find_node(u.output)
+        a = n.attrs
+        if n.op != "Conv2dBackX" or a.groups > 1 or max(a.sh, 1) != 1 or max(a.sw, 1) != 1:
+            continue
+        c = cons.get(u.output, [])
+        if len(c) != 1 or u.output in outputs:
+            continue
+        j = owner[c[0]]
+        v = units[j]
+        if v.kind != "dfp" or len(v.node_ids) != 1 or j in merged_into.values():
+            continue
+        r = g.find_node(v.node_ids[0])
+        if r.op != "ReluBack" or len(r.inputs) != 2 or r.inputs[0] != u.output or r.inputs[1] == u.output:
+            continue
+        if g.find_node(r.inputs[1]) is None or g.find_node(r.inputs[1]).op != "ReLU":
+            continue  # the mask must be a ReLU output (relu_mask_from_output)
+        merged_into[i] = j
+    out = []
+    absorbed = set(merged_into)
+    for j, v in enumerate(units):
+        if j in absorbed:
+            continue
+        src = [i for i, jj in merged_into.items() if jj == j]
+        if not src:
+            out.append(v)
+            continue
+        u = units[src[0]]
+        inputs = list(u.inputs) + [x for x in v.inputs if x != u.output and x not in u.inputs]
+        out.append(ExecUnit("dnn", list(u.node_ids) + list(v.node_ids), v.output, inputs, list(u.params)))
+    return out
+

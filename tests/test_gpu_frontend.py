@@ -152,3 +152,23 @@ def test_export_and_run_bundle_bit_identical(gpu, tmp_path):
     got = frontend.run_bundle(d, x)["prob"]
     assert man.endswith("manifest.json")
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_fused_dgrad_relu_back_is_exact(gpu, dtype):
+    """fusion.fuse_dgrad_relu_back: the stride-1 dgrads apply the ReluBack mask in their GEMM
+    epilogue; the step (loss, every gradient) is bit-identical to the unfused plan's."""
+    from paper_2003_10688_b200 import frontend, graph
+    g = _model(True)
+    ins = _inputs(graph.infer_shapes(g, 8), 8, seed=9)
+    a = frontend.optimize(g, _opts(dtype=dtype, train=True, lr=0.05))
+    b = frontend.optimize(g, _opts(dtype=dtype, train=True, lr=0.05, fuse_relu_back=False))
+    fused = [u for u in a.units if u.kind == "dnn" and [a.graph.find_node(n).op for n in u.node_ids] ==
+             ["Conv2dBackX", "ReluBack"]]
+    assert fused and len(a.units) == len(b.units) - len(fused)
+    assert any(st.family == "conv_dgrad_fused_tcgen05" for st in a.steps)
+    assert a.train_step(ins) == b.train_step(ins)
+    ga, gb = a.gradients(), b.gradients()
+    assert ga.keys() == gb.keys()
+    for k in ga:
+        assert np.array_equal(ga[k], gb[k]), k
