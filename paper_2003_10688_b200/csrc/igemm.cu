@@ -309,7 +309,8 @@ template <typename T, typename TO, int BN, int MODE, bool RESB = false>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
-                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
+                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2,
+                    const __grid_constant__ CUtensorMap tmap_m) {
     constexpr int VEC = 16 / sizeof(T);
     constexpr int BK = ROWB / sizeof(T);
     constexpr int A_BYTES = BM * ROWB;
@@ -533,6 +534,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const bool has_fold = a.ep_scale != nullptr;
         const bool has_res = a.residual != nullptr;
         const bool res_mask = a.res_mode == 1;
+        const bool has_m2 = a.mask != nullptr;  // host guarantees one chunk per warp (SLOTS == 1)
         const int act = a.relu ? 1 : a.act;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -555,6 +557,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                         mbar_arrive_tx(smem_u32(&rbar[(warp - 4) * 2 + bi]), 4096);
                         tma_load_2d(smem_u32(stage_buf + bi * 4096), &tmap_r, n0 + cc, m0 + q * 32,
                                     smem_u32(&rbar[(warp - 4) * 2 + bi]));
+                        if (has_m2) {  // the mask box goes to the other buffer
+                            mbar_arrive_tx(smem_u32(&rbar[(warp - 4) * 2 + (bi ^ 1)]), 4096);
+                            tma_load_2d(smem_u32(stage_buf + (bi ^ 1) * 4096), &tmap_m, n0 + cc, m0 + q * 32,
+                                        smem_u32(&rbar[(warp - 4) * 2 + (bi ^ 1)]));
+                        }
                     }
                 }
                 __syncwarp();
@@ -622,6 +629,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     }
                     mbar_wait(smem_u32(&rbar[(warp - 4) * 2 + buf]), (rphase >> buf) & 1);
                     rphase ^= 1u << buf;
+                    if (has_m2) {
+                        mbar_wait(smem_u32(&rbar[(warp - 4) * 2 + (buf ^ 1)]), (rphase >> (buf ^ 1)) & 1);
+                        rphase ^= 1u << (buf ^ 1);
+                    }
+                    uint8_t* mb = stage_buf + (buf ^ 1) * 4096;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const uint32_t addr = smem_u32(sb + lane * 128 + ((j ^ (lane & 7)) << 4));
@@ -643,10 +655,34 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                             rr[2] = __uint_as_float(r2);
                             rr[3] = __uint_as_float(r3);
                         }
+                        float mm[16 / sizeof(TO)];
+                        if (has_m2) {
+                            uint32_t m0r, m1r, m2r, m3r;
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                                         : "=r"(m0r), "=r"(m1r), "=r"(m2r), "=r"(m3r)
+                                         : "r"(smem_u32(mb + lane * 128 + ((j ^ (lane & 7)) << 4))));
+                            if constexpr (sizeof(TO) == 2) {
+                                const uint32_t w[4] = {m0r, m1r, m2r, m3r};
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    mm[2 * k] = __uint_as_float(w[k] << 16);
+                                    mm[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+                                }
+                            } else {
+                                mm[0] = __uint_as_float(m0r);
+                                mm[1] = __uint_as_float(m1r);
+                                mm[2] = __uint_as_float(m2r);
+                                mm[3] = __uint_as_float(m3r);
+                            }
+                        }
 #pragma unroll
                         for (int k = 0; k < static_cast<int>(16 / sizeof(TO)); ++k) {
                             float& fv = f[j * (16 / sizeof(TO)) + k];
+                            // Add + ReluBack: the unfused plan adds the stored (rounded) dgrad output
+                            if constexpr (sizeof(TO) == 2)
+                                if (has_m2) fv = __bfloat162float(__float2bfloat16_rn(fv));
                             fv = res_mask ? (rr[k] > 0.f ? fv : 0.f) : fv + rr[k];
+                            if (has_m2) fv = mm[k] > 0.f ? fv : 0.f;
                         }
                     }
                 }
@@ -780,15 +816,20 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     const int grid = std::min(tiles, num_sms());
     const int dto = sizeof(TO) == 2 ? DT_BF16 : DT_F32;
     CUtensorMap tc = make_tmap_2d(a.out, dto, a.ldo, static_cast<uint64_t>(M), a.ldo, 32);
-    CUtensorMap tr = tc;
+    CUtensorMap tr = tc, tm = tc;
     if (a.residual) tr = make_tmap_2d(a.residual, dto, a.Nout, static_cast<uint64_t>(M), a.ld_res, 32);
-    igemm_ws_kernel<T, TO, BN, MODE, RESB><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2);
+    if (a.mask) {
+        constexpr int CW = 128 / static_cast<int>(sizeof(TO));
+        if ((BN / CW + 1) / 2 > 1 || !a.residual) throw std::logic_error("igemm: epilogue mask needs one chunk per warp");
+        tm = make_tmap_2d(a.mask, dto, a.Nout, static_cast<uint64_t>(M), a.ld_res, 32);
+    }
+    igemm_ws_kernel<T, TO, BN, MODE, RESB><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2, tm);
     SOL_CUDA(cudaGetLastError());
 }
 
 template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
-    if (a.tile_n) {  // autotuned choice
+    if (a.tile_n && !(a.mask && a.tile_n > (sizeof(TO) == 2 ? 128 : 64))) {  // autotuned choice
         if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
             if (a.tile_n == 65 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX) return launch_ws_t<T, TO, 64, MODE, true>(a, s);
         }
@@ -806,6 +847,7 @@ void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
             return launch_ws_t<T, TO, 64, MODE, true>(a, s);
     }
     int bn_sel = igemm_block_n(a.Nout);
+    if (a.mask) bn_sel = std::min(bn_sel, sizeof(TO) == 2 ? 128 : 64);  // one epilogue chunk per warp
     // small-M GEMMs (the classifier: M = batch): narrower N tiles put more SMs on the long K loop
     const int64_t m_tiles = ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, BM);
     if (bn_sel > 64 && m_tiles * ceil_div(a.Nout, bn_sel) < num_sms() / 4) bn_sel = 64;
@@ -1170,7 +1212,7 @@ void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.src2 && (a.SC % 64 || a.SC2 % 64 || a.K1 != a.SC || a.K_pad != a.SC + a.SC2 || a.mode != IG_FPROP))
         throw std::invalid_argument("igemm: dual GEMM needs two 1x1 convs over 128-byte channel blocks");
-    if (!a.src2 && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
+    if (!a.src2 && !a.mask && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
         else dispatch_mode<__nv_bfloat16, float>(a, s);

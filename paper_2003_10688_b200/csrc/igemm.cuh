@@ -45,6 +45,10 @@ struct IgemmArgs {
     // 1: the residual is a ReLU OUTPUT used as a backward mask instead of an addend:
     //    y = residual > 0 ? acc : 0 (ReluBack(delta, relu(x)) fused into the dgrad epilogue)
     int res_mode = 0;
+    // optional second epilogue input: y = mask > 0 ? acc + residual : 0 (Add + ReluBack fused into
+    // a dgrad epilogue; mask = the ReLU output, same layout as the residual; N tiles of one chunk
+    // per epilogue warp so both boxes fit the warp's two staging buffers)
+    const void* mask = nullptr;
     // dual GEMM (inference bottleneck-block fusion): K = [0, K1) reads A from `src` as a 1x1
     // stride-1 conv, K = [K1, K_pad) reads a second 1x1 conv with stride s2 over src2
     // [N, SH2, SW2, SC2] on the same output grid; B packs both weight matrices side by side.

@@ -425,17 +425,34 @@ public:
     void parse_epilogue(const sol_unit_desc& d) {
         if (d.n_ops == 1) return;
         if (op_ == SOL_OP_CONV2DBACKX) {
-            // training plan fusion (fusion.fuse_dgrad_relu_back): ReluBack(dx, relu_out) with the mask
-            // read from the ReLU output (passes.relu_mask_from_output) applied in the GEMM epilogue
-            const sol_unit_op& r = d.ops[1];
-            if (d.n_ops != 2 || r.op != SOL_OP_RELUBACK || r.n_inputs != 2 || r.inputs[0] != -1 || r.inputs[1] < 0)
-                unsupported("dgrad epilogue fusion: only ReluBack(dx, relu output)");
-            if (!classes_.empty()) unsupported("strided dgrad (sub-pixel classes) has no fused ReluBack");
-            res_idx_ = r.inputs[1];
-            const Geo m = geo_b(d.bindings[res_idx_]);
-            if (m.ld != out_.ld || m.pixels() != out_.pixels()) unsupported("ReLU output layout mismatch");
-            res_mode_ = 1;
-            algo_bytes += double(m.pixels()) * m.ld * elem_size(dtype_);  // the mask read
+            // training plan fusion (fusion.fuse_dgrad_relu_back), applied in the GEMM epilogue with
+            // the mask read from the ReLU output (passes.relu_mask_from_output):
+            //   [Conv2dBackX, ReluBack(dx, relu_out)]                 -> relu_out > 0 ? dx : 0
+            //   [Conv2dBackX, Add(dx, g), ReluBack(sum, relu_out)]    -> relu_out > 0 ? dx + g : 0
+            if (!classes_.empty()) unsupported("strided dgrad (sub-pixel classes) has no fused epilogue");
+            auto check_layout = [&](int idx) {
+                const Geo m = geo_b(d.bindings[idx]);
+                if (m.ld != out_.ld || m.pixels() != out_.pixels()) unsupported("fused dgrad input layout mismatch");
+                algo_bytes += double(m.pixels()) * m.ld * elem_size(dtype_);
+            };
+            const sol_unit_op& r = d.ops[d.n_ops - 1];
+            if (r.op != SOL_OP_RELUBACK || r.n_inputs != 2 || r.inputs[0] != -(d.n_ops - 1) || r.inputs[1] < 0)
+                unsupported("dgrad epilogue fusion ends in ReluBack(chain, relu output)");
+            if (d.n_ops == 2) {
+                res_idx_ = r.inputs[1];
+                res_mode_ = 1;
+                check_layout(res_idx_);
+            } else if (d.n_ops == 3 && d.ops[1].op == SOL_OP_ADD) {
+                const int x0 = d.ops[1].inputs[0], x1 = d.ops[1].inputs[1];
+                if (x0 == -1 && x1 >= 0) res_idx_ = x1;
+                else if (x1 == -1 && x0 >= 0) res_idx_ = x0;
+                else unsupported("fused Add must combine dx with a unit input");
+                mask_idx_ = r.inputs[1];
+                check_layout(res_idx_);
+                check_layout(mask_idx_);
+            } else {
+                unsupported("unsupported fused dgrad epilogue");
+            }
             family = "conv_dgrad_fused_tcgen05";
             return;
         }
@@ -626,10 +643,11 @@ public:
                 g.K_pad = kpad_;
                 g.ldo = static_cast<int>(out_.ld);
                 g.tile_n = tile_n_;
-                if (res_idx_ >= 0) {  // fused ReluBack: mask = relu output > 0
+                if (res_idx_ >= 0) {  // fused [Add +] ReluBack: mask = relu output > 0
                     g.residual = args[res_idx_];
                     g.ld_res = static_cast<int>(out_.ld);
                     g.res_mode = res_mode_;
+                    if (mask_idx_ >= 0) g.mask = args[mask_idx_];
                 }
                 igemm_launch(g, s);
                 break;
@@ -717,6 +735,7 @@ private:
     float bn_eps_ = 1e-5f;
     int res_idx_ = -1;
     int res_mode_ = 0;  // 1: the residual binding is a ReLU output used as a backward mask
+    int mask_idx_ = -1;  // fused Add + ReluBack: the ReLU output binding (residual = the added gradient)
     int act_ = 0;
 };
 
@@ -1613,7 +1632,7 @@ std::unique_ptr<Module> compile_unit(const sol_unit_desc& d) {
     const sol_unit_op& o0 = d.ops[0];
     if (d.kind == 1 && d.n_ops >= 5 && o0.op == SOL_OP_CONV2D && d.ops[2].op == SOL_OP_CONV2D)
         return std::make_unique<DualConvModule>(d);
-    if (d.kind == 1 && d.n_ops == 2 && o0.op == SOL_OP_CONV2DBACKX) return std::make_unique<HeavyModule>(d);
+    if (d.kind == 1 && (d.n_ops == 2 || d.n_ops == 3) && o0.op == SOL_OP_CONV2DBACKX) return std::make_unique<HeavyModule>(d);
     if (d.kind == 1 && d.n_ops > 1 && (o0.op == SOL_OP_CONV2D || o0.op == SOL_OP_LINEAR)) {
         // heavy node + fused epilogue chain (plan-level fusion, see HeavyModule::parse_epilogue)
         const Geo g = geo_b(d.bindings[o0.inputs[0]]);

@@ -176,13 +176,16 @@ def fuse_stem_pool(g: ModelGraph, units: List[ExecUnit], direct_inputs) -> List[
 
 
 def fuse_dgrad_relu_back(g: ModelGraph, units: List[ExecUnit]) -> List[ExecUnit]:
-    """Training plans: a stride-1 Conv2dBackX unit whose output feeds exactly one ReluBack unit
-    ReluBack(dx, relu_out) (the mask read from the ReLU output, passes.relu_mask_from_output) is
-    merged with it: the dgrad GEMM epilogue writes relu_out > 0 ? dx : 0, which is bit-for-bit the
-    ReluBack unit's output (the mask does not round), and dx never round-trips through HBM (one
-    write and two reads of an activation-sized tensor per inner ReLU saved). The merged unit runs
-    at the ReluBack's position. Strided dgrads (sub-pixel classes + interleave) and grouped convs
-    keep the separate unit."""
+    """Training plans: a stride-1 Conv2dBackX unit whose output feeds exactly one unit
+      ReluBack(dx, relu_out)                  (inner ReLUs), or
+      Add(dx, g) -> ReluBack(sum, relu_out)   (block outputs: dx from the next block's conv1,
+                                               g the skip-path gradient)
+    with the mask read from the ReLU output (passes.relu_mask_from_output) is merged with it: the
+    dgrad GEMM epilogue writes relu_out > 0 ? [bf16(dx) + g | dx] : 0, bit-for-bit the separate
+    unit's output (the epilogue rounds dx to the stored precision before the add, as the unfused
+    plan does), and dx never round-trips through HBM (a write and two reads of an activation-sized
+    tensor per ReLU saved). The merged unit runs at the consumer's position. Strided dgrads
+    (sub-pixel classes + interleave) and grouped convs keep the separate unit."""
     cons = g.consumers()
     outputs = set(g.outputs)
     owner = {}
@@ -202,13 +205,24 @@ def fuse_dgrad_relu_back(g: ModelGraph, units: List[ExecUnit]) -> List[ExecUnit]
             continue
         j = owner[c[0]]
         v = units[j]
-        if v.kind != "dfp" or len(v.node_ids) != 1 or j in merged_into.values():
+        if v.kind != "dfp" or len(v.node_ids) > 2 or j in merged_into.values():
             continue
-        r = g.find_node(v.node_ids[0])
-        if r.op != "ReluBack" or len(r.inputs) != 2 or r.inputs[0] != u.output or r.inputs[1] == u.output:
+        vn = [g.find_node(n) for n in v.node_ids]
+        r = vn[-1]
+        if r.op != "ReluBack" or len(r.inputs) != 2 or len(vn) > 2:
             continue
         if g.find_node(r.inputs[1]) is None or g.find_node(r.inputs[1]).op != "ReLU":
             continue  # the mask must be a ReLU output (relu_mask_from_output)
+        if len(vn) == 1:  # ReluBack(dx, relu_out)
+            if r.inputs[0] != u.output or r.inputs[1] == u.output:
+                continue
+        else:  # Add(dx, g) -> ReluBack(sum, relu_out): the block-output gradient
+            ad = vn[0]
+            if ad.op != "Add" or len(ad.inputs) != 2 or u.output not in ad.inputs or r.inputs[0] != ad.id:
+                continue
+            other = ad.inputs[1] if ad.inputs[0] == u.output else ad.inputs[0]
+            if other == u.output or other not in v.inputs or r.inputs[1] == u.output:
+                continue
         merged_into[i] = j
     out = []
     absorbed = set(merged_into)

@@ -373,6 +373,14 @@ def test_bench_train_plan_units_match_oracle(gpu, bench_train):
             local[nid] = O.eval_node(n, [local[i] for i in n.inputs], params)
         got = get(u.output, rows)
         err = O.oracle_err(got, local[u.output])
+        if len(u.node_ids) == 3 and m.graph.find_node(u.node_ids[0]).op == "Conv2dBackX":
+            # fused dgrad + Add + ReluBack (fusion.fuse_dgrad_relu_back; bit-identical to the unfused
+            # plan): the sum of two gradients cancels, so one bf16 ulp of the rounded dgrad is
+            # measured against the operands' magnitude, not the (possibly tiny) sum's
+            add = m.graph.find_node(u.node_ids[1])
+            mag = np.abs(local[add.inputs[0]]) + np.abs(local[add.inputs[1]])
+            den = np.maximum(mag, max(0.01 * float(mag.max()), 1e-12))
+            err = float(np.max(np.abs(got - local[u.output]) / den))
         checked += 1
         if not np.all(np.isfinite(got)) or err > 2e-2:
             bad.append((u.output, ops, err))
