@@ -560,6 +560,9 @@ def main():
     ap.add_argument("--no-configs", dest="configs", action="store_false",
                     help="skip the other BASELINE configs (small CNN, ResNet-18 TF32, DenseNet-121, MobileNet-V2)")
     args = ap.parse_args()
+    if os.environ.get("SOL_BENCH_WATCHDOG"):  # diagnostics: dump every thread's stack if a run stalls
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["SOL_BENCH_WATCHDOG"]), repeat=False)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args)
     if args.impl == "reference":

@@ -305,7 +305,9 @@ constexpr uint32_t ws_tmem_cols() {
 // L2 -> shared-memory traffic for the narrow 3x3 convolutions, whose im2col A is L2-bound).
 constexpr int WS_RESB_MAX = 80 * 1024;
 
-template <typename T, typename TO, int BN, int MODE, bool RESB = false>
+// EPI = 1: training dgrad epilogues with a ReLU-output mask (IgemmArgs::res_mode / mask);
+// a separate instantiation so the inference residual epilogue keeps its register allocation
+template <typename T, typename TO, int BN, int MODE, bool RESB = false, int EPI = 0>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     igemm_ws_kernel(const IgemmArgs a, const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
@@ -381,7 +383,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             for (int kb = 0; kb < num_kb; ++kb)
                 tma_load_2d(smem_u32(bres_smem + kb * B_BYTES), &tmap_b, kb * BK, 0, smem_u32(bres));
         }
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        // With TMA operands only thread 0 produces. The other producer threads must not run the
+        // loop: nothing waits for them, so a thread that fell a full ring cycle behind saw the
+        // empty barrier's parity alias (phase p vs p + 2) and could wait for a completion that never
+        // comes once the pipeline drained -- the rare end-of-kernel stall (one CTA left with one
+        // producer warp in mbarrier.try_wait; found with cuda-gdb, scripts/diag/hang_hunt.sh)
+        const int t_first = (A_TMA && tid != 0) ? tiles : static_cast<int>(blockIdx.x);
+        for (int t = t_first; t < tiles; t += gridDim.x) {
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
             int rn[8], rh[8], rw[8];
@@ -533,8 +541,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const bool has_bias = a.bias != nullptr;
         const bool has_fold = a.ep_scale != nullptr;
         const bool has_res = a.residual != nullptr;
-        const bool res_mask = a.res_mode == 1;
-        const bool has_m2 = a.mask != nullptr;  // host guarantees one chunk per warp (SLOTS == 1)
+        const bool res_mask = EPI == 1 && a.res_mode == 1;
+        const bool has_m2 = EPI == 1 && a.mask != nullptr;  // host guarantees one chunk per warp (SLOTS == 1)
         const int act = a.relu ? 1 : a.act;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -782,15 +790,15 @@ CUtensorMap make_tmap_im2col(const IgemmArgs& a, int dtype, int rows = BM) {
     return m;
 }
 
-template <typename T, typename TO, int BN, int MODE, bool RESB = false>
+template <typename T, typename TO, int BN, int MODE, bool RESB = false, int EPI = 0>
 void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
     constexpr int STAGE_BYTES = RESB ? BM * ROWB : BM * ROWB + BN * ROWB;
-    constexpr int EPI = ws_epi_bytes<TO, BN>();
-    constexpr int STAGES = ws_stages<STAGE_BYTES, EPI + (RESB ? WS_RESB_MAX : 0)>();
-    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + EPI + (RESB ? WS_RESB_MAX : 0);
+    constexpr int EPI_BYTES = ws_epi_bytes<TO, BN>();
+    constexpr int STAGES = ws_stages<STAGE_BYTES, EPI_BYTES + (RESB ? WS_RESB_MAX : 0)>();
+    constexpr int SMEM = STAGES * STAGE_BYTES + 2048 + EPI_BYTES + (RESB ? WS_RESB_MAX : 0);
     static std::once_flag once;
     std::call_once(once, [] {
-        SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE, RESB>,
+        SOL_CUDA(cudaFuncSetAttribute(igemm_ws_kernel<T, TO, BN, MODE, RESB, EPI>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     });
     const int M = a.N * a.OH * a.OW;
@@ -823,13 +831,29 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
         if ((BN / CW + 1) / 2 > 1 || !a.residual) throw std::logic_error("igemm: epilogue mask needs one chunk per warp");
         tm = make_tmap_2d(a.mask, dto, a.Nout, static_cast<uint64_t>(M), a.ld_res, 32);
     }
-    igemm_ws_kernel<T, TO, BN, MODE, RESB><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2, tm);
+    igemm_ws_kernel<T, TO, BN, MODE, RESB, EPI><<<grid, WS_THREADS, SMEM, s>>>(a, tb, ta, tc, tr, ta2, tm);
     SOL_CUDA(cudaGetLastError());
 }
 
 template <typename T, typename TO, int MODE>
+void dispatch_ws_mask(const IgemmArgs& a, cudaStream_t s) {
+    // the add + mask form needs one epilogue chunk per warp: 128-wide tiles (bf16), 64 (f32)
+    constexpr int BNMAX = sizeof(TO) == 2 ? 128 : 64;
+    int bn = a.tile_n ? std::min(a.tile_n == 65 ? 64 : a.tile_n, BNMAX) : std::min(igemm_block_n(a.Nout), BNMAX);
+    if (bn < 64) bn = 64;
+    if constexpr (BNMAX == 128) {
+        if (bn == 128) return launch_ws_t<T, TO, 128, MODE, false, 1>(a, s);
+    }
+    launch_ws_t<T, TO, 64, MODE, false, 1>(a, s);
+}
+
+template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
-    if (a.tile_n && !(a.mask && a.tile_n > (sizeof(TO) == 2 ? 128 : 64))) {  // autotuned choice
+    if constexpr (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL || MODE == IG_FPROP) {
+        if (a.mask || a.res_mode) return dispatch_ws_mask<T, TO, MODE>(a, s);
+    }
+    if (a.mask || a.res_mode) throw std::invalid_argument("igemm: masked epilogues are fprop-path only");
+    if (a.tile_n) {  // autotuned choice
         if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
             if (a.tile_n == 65 && a.K_pad / 64 * 64 * ROWB <= WS_RESB_MAX) return launch_ws_t<T, TO, 64, MODE, true>(a, s);
         }
@@ -847,7 +871,6 @@ void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
             return launch_ws_t<T, TO, 64, MODE, true>(a, s);
     }
     int bn_sel = igemm_block_n(a.Nout);
-    if (a.mask) bn_sel = std::min(bn_sel, sizeof(TO) == 2 ? 128 : 64);  // one epilogue chunk per warp
     // small-M GEMMs (the classifier: M = batch): narrower N tiles put more SMs on the long K loop
     const int64_t m_tiles = ceil_div(static_cast<int64_t>(a.N) * a.OH * a.OW, BM);
     if (bn_sel > 64 && m_tiles * ceil_div(a.Nout, bn_sel) < num_sms() / 4) bn_sel = 64;

@@ -154,7 +154,8 @@ class DevicePlan:
             cg = run_pipeline(cg)
         self.graph = cg
         self.units: List[ExecUnit] = partition(cg)
-        if options.train and options.relu_mask_from_output and options.fuse_relu_back:
+        if (options.train and options.relu_mask_from_output and options.fuse_relu_back
+                and not os.environ.get("SOL_NO_FUSE_RELU_BACK")):
             from .fusion import fuse_dgrad_relu_back
             self.units = fuse_dgrad_relu_back(cg, self.units)
         if options.fuse_epilogue and not options.train:
