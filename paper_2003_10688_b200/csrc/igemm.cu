@@ -320,9 +320,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     constexpr int STAGE_BYTES = RESB ? A_BYTES : A_BYTES + B_BYTES;
     constexpr int EPI_BYTES = ws_epi_bytes<TO, BN>();
     constexpr int STAGES = ws_stages<STAGE_BYTES, EPI_BYTES + (RESB ? WS_RESB_MAX : 0)>();
-    // accumulator stages: 2 (epilogue overlaps the next mainloop); the dual GEMM at BN = 256 keeps
-    // one (half the TMEM) -- see the dispatch note
-    constexpr int NACC = (MODE == IG_DUAL && BN == 256) ? 1 : 2;
+    constexpr int NACC = 2;  // accumulator stages: the epilogue overlaps the next mainloop
     constexpr uint32_t TCOLS = NACC == 1 ? static_cast<uint32_t>(BN) : ws_tmem_cols<BN>();
     constexpr uint32_t IDESC = make_idesc(AbFmt<T>::v, BN, BM, 0, 0);
     constexpr int KSTEP_BYTES = 32;
@@ -892,13 +890,12 @@ void dispatch_mode(const IgemmArgs& a, cudaStream_t s) {
                         a.kh <= 8 && a.kw <= 8;
     if constexpr (sizeof(T) == 2 && sizeof(TO) == 2) {
         if (a.src2) {
-            // N tiles of at most 128 (TMEM 2 x 128 columns): with 256-wide tiles (the whole TMEM)
-            // the dual GEMM stalled intermittently (~1 in 10^3 full-size launches); at 128 it ran
-            // clean through 8k ResNet-50 steps and 80k single-block launches
-            // 256-wide single-accumulator tiles halve the A re-reads of the wide (N >= 1024)
-            // stride-2 tails (ResNet-50 l3.0 / l4.0: -8 us each); SOL_DUAL_BN256=0/1 forces off/on
+            // 256-wide tiles with two accumulator stages (the whole TMEM) halve the A re-reads of
+            // both sources: ResNet-50 l2.0 / l3.0 / l4.0 tails 107 / 91 / 84 -> 95 / 84 / 81 us.
+            // (The intermittent stall once blamed on this configuration was the idle-producer
+            // barrier aliasing fixed in igemm_ws_kernel.) SOL_DUAL_BN256=0/1 forces off/on
             static const char* bn256_env = std::getenv("SOL_DUAL_BN256");
-            const bool bn256 = a.tile_n ? a.tile_n == 256 : (bn256_env ? bn256_env[0] == '1' : a.Nout >= 1024);
+            const bool bn256 = a.tile_n ? a.tile_n == 256 : (bn256_env ? bn256_env[0] == '1' : true);
             if (a.Nout > 128 && bn256) return launch_ws_t<T, TO, 256, IG_DUAL>(a, s);
             if (a.Nout > 64) return launch_ws_t<T, TO, 128, IG_DUAL>(a, s);
             return dispatch_ws<T, TO, IG_DUAL>(a, s);
