@@ -16,5 +16,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python scripts/diag/one_train_step.py > gpurun_out/ncu_lt.log 2>&1; echo "ncu train rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:igemm_ws_kernel --launch-skip 20 -c 1 \
   -o gpurun_out/r02_conv_full -f python bench.py --steps 1 --warmup 1 --no-train --no-cpu-baseline --no-configs > gpurun_out/ncu_cf.log 2>&1; echo "ncu conv rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:wgrad_ws_kernel -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:wgrad_halo_kernel -c 1 \
   -o gpurun_out/r02_wgrad_full -f python scripts/wgrad_micro.py l1.conv2 --ncu > gpurun_out/ncu_wf.log 2>&1; echo "ncu wgrad rc=$?"
