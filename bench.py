@@ -402,7 +402,8 @@ def run_b200(args):
         xt = x[:Bt] if Bt <= B else rng.uniform(-1, 1, (Bt, 3, 224, 224)).astype(np.float32)
         tdev, te2e, th2d, td2h, tsync = bench_model(mt, {"x": xt, "t": t}, args.train_steps, args.warmup, ["loss"])
         troof, ttimes = roofline_of(mt, peaks, peaks_kind,
-                                    {"conv_fprop_tcgen05", "conv_dgrad_tcgen05", "conv_dgrad_fused_tcgen05", "conv_wgrad_tcgen05",
+                                    {"conv_fprop_tcgen05", "conv_fprop_bnstats_tcgen05", "conv_dgrad_tcgen05", "conv_dgrad_fused_tcgen05",
+                                     "conv_wgrad_tcgen05",
                                      "conv_stem_tcgen05", "conv_stem_wgrad_tcgen05"}, "tensor")
         tfam = {}
         for st, tt in zip(mt.steps, ttimes):

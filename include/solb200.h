@@ -246,6 +246,13 @@ int sol_b200_plan_set_lr(sol_b200_plan_t p, float lr, int32_t* n_steps);
 /* Median device time (us) of module step `step` run alone `reps` times (after one warm-up run),
    on the plan's buffers as they are: the measurement behind autotune (dnn.cpp:214-290). */
 int sol_b200_plan_time_step(sol_b200_plan_t p, int32_t step, int32_t reps, double* us);
+/* BatchNorm statistics from the producing convolution's GEMM epilogue (training plans): the conv
+ * step writes per-(M tile, row quarter) partial sums of (y - shift) and (y - shift)^2 of its stored
+ * bf16 output, shift = the BN's previous batch mean; the BN step then skips its statistics pass
+ * over y and finalises from those partials. bn_binding = the index of the conv output among the
+ * BN unit's bindings. SOL_E_UNSUPPORTED when the conv's kernel path cannot (halo / stem / fused
+ * epilogue / not bf16) or the unit has no training BN on that binding. */
+int sol_b200_plan_link_bn_stats(sol_b200_plan_t p, int32_t conv_step, int32_t bn_step, int32_t bn_binding);
 /* sol_b200_module_set_option on the module a plan step owns (the plan owns added modules). */
 int sol_b200_plan_step_set_option(sol_b200_plan_t p, int32_t step, int32_t key, int32_t value);
 

@@ -48,6 +48,7 @@ SYMBOLS = [
     "sol_b200_module_set_sibling_outputs", "sol_b200_plan_comm_info",
     "sol_b200_plan_copy_fence", "sol_b200_plan_copy_wait", "sol_b200_module_set_option",
     "sol_b200_plan_set_lr", "sol_b200_plan_time_step", "sol_b200_plan_step_set_option",
+    "sol_b200_plan_link_bn_stats",
 ]
 
 
@@ -171,6 +172,7 @@ def lib():
             "sol_b200_plan_copy_wait": [vp, u64],
             "sol_b200_module_set_sibling_outputs": [vp, i32],
             "sol_b200_module_set_option": [vp, i32, i32],
+            "sol_b200_plan_link_bn_stats": [vp, i32, i32, i32],
             "sol_b200_plan_set_lr": [vp, C.c_float, C.POINTER(i32)],
             "sol_b200_plan_time_step": [vp, i32, i32, C.POINTER(C.c_double)],
             "sol_b200_plan_step_set_option": [vp, i32, i32, i32],

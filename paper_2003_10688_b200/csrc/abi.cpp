@@ -376,6 +376,13 @@ int sol_b200_plan_step_set_option(sol_b200_plan_t p, int32_t step, int32_t key, 
     });
 }
 
+int sol_b200_plan_link_bn_stats(sol_b200_plan_t p, int32_t conv_step, int32_t bn_step, int32_t bn_binding) {
+    return guard([&] {
+        if (!p->p->link_bn_stats(conv_step, bn_step, bn_binding))
+            throw solb200::UnsupportedError("the conv cannot emit this BatchNorm's statistics");
+    });
+}
+
 int sol_b200_plan_comm_info(sol_b200_plan_t p, int32_t* nranks, int32_t* rank, int32_t* cuda_device) {
     return guard([&] {
         int n = 1, r = 0, d = 0;

@@ -344,6 +344,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     const int n_tiles = (a.Nout + BN - 1) / BN;
     const int tiles = m_tiles * n_tiles;
     const int num_kb = a.K_pad / BK;
+    // Work order: tile v = start + k * stride, mapped to t = m * n_tiles + n. EPI == 2 (BN statistics)
+    // pins every CTA to one N tile (the host sizes the grid as a multiple of n_tiles), so a warp's
+    // columns never change and its statistics accumulate in registers across all its tiles.
+    const int v_start = EPI == 2 ? static_cast<int>(blockIdx.x) / n_tiles : static_cast<int>(blockIdx.x);
+    const int v_stride = EPI == 2 ? static_cast<int>(gridDim.x) / n_tiles : static_cast<int>(gridDim.x);
+    const int v_end = EPI == 2 ? m_tiles : tiles;
+    const int n_pin = static_cast<int>(blockIdx.x) % n_tiles;
+    auto tile_of = [&](int v) { return EPI == 2 ? v * n_tiles + n_pin : v; };
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -386,8 +394,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // empty barrier's parity alias (phase p vs p + 2) and could wait for a completion that never
         // comes once the pipeline drained -- the rare end-of-kernel stall (one CTA left with one
         // producer warp in mbarrier.try_wait; found with cuda-gdb, scripts/diag/hang_hunt.sh)
-        const int t_first = (A_TMA && tid != 0) ? tiles : static_cast<int>(blockIdx.x);
-        for (int t = t_first; t < tiles; t += gridDim.x) {
+        const int v_first = (A_TMA && tid != 0) ? v_end : v_start;
+        for (int v = v_first; v < v_end; v += v_stride) {
+            const int t = tile_of(v);
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
             int rn[8], rh[8], rw[8];
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const uint64_t a_desc0 = sw128_desc(smem_u32(smem), 16, 1024);
         const uint64_t bres_desc0 = RESB ? sw128_desc(smem_u32(bres_smem), 16, 1024) : 0;
         const bool do_mma = !(a.dbg & 2);
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int v = v_start; v < v_end; v += v_stride) {
             mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
             tc_fence_after();
             const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -546,10 +555,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         uint32_t acc_phase = 0;
         int buf = 0;
         uint32_t rphase = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        constexpr int SLOTS = (BN / CW + 1) / 2 > 0 ? (BN / CW + 1) / 2 : 1;
+        // EPI == 2: this warp's running BN sums, per chunk slot and owned column pair
+        float st_s[SLOTS][2], st_q[SLOTS][2];
+#pragma unroll
+        for (int k = 0; k < SLOTS; ++k) st_s[k][0] = st_s[k][1] = st_q[k][0] = st_q[k][1] = 0.f;
+        for (int v = v_start; v < v_end; v += v_stride) {
+            const int t = tile_of(v);
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
-            constexpr int SLOTS = (BN / CW + 1) / 2 > 0 ? (BN / CW + 1) / 2 : 1;
             constexpr int LCOLS = BN < CW ? BN : CW;  // TMEM columns per chunk (never past the tile)
             // residual boxes for this warp's first two chunks are TMA-loaded into the two staging
             // buffers before waiting for the accumulator, so their latency hides behind the mainloop
@@ -732,6 +746,36 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                         : "memory");
                     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                 }
+                if constexpr (EPI == 2) {
+                    // BN statistics of the stored chunk, read back from the staging buffer (the
+                    // TMA store reads it concurrently): lane l owns columns n + 2l, n + 2l + 1;
+                    // rows past M (zero-filled A) are excluded; sums of (y - shift) accumulate
+                    // in registers until the CTA's last tile
+                    static_assert(sizeof(TO) == 2, "BN statistics epilogue is bf16");
+                    const int rv = min(32, M - (m0 + q * 32));
+                    const int c0 = n + 2 * lane;
+                    if (c0 < a.Nout && rv > 0) {
+                        const float h0 = __ldg(a.stat_shift + c0);
+                        const float h1 = c0 + 1 < a.Nout ? __ldg(a.stat_shift + c0 + 1) : 0.f;
+                        const uint32_t base = smem_u32(sb) + static_cast<uint32_t>((lane & 3) * 4);
+                        float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+                        for (int r = 0; r < rv; ++r) {
+                            uint32_t w;
+                            asm volatile("ld.shared.b32 %0, [%1];\n"
+                                         : "=r"(w)
+                                         : "r"(base + static_cast<uint32_t>(r * 128 + (((lane >> 2) ^ (r & 7)) << 4))));
+                            const float v0 = __uint_as_float(w << 16) - h0, v1 = __uint_as_float(w & 0xffff0000u) - h1;
+                            s0 += v0;
+                            q0 = fmaf(v0, v0, q0);
+                            s1 += v1;
+                            q1 = fmaf(v1, v1, q1);
+                        }
+                        st_s[s][0] += s0;
+                        st_q[s][0] += q0;
+                        st_s[s][1] += s1;
+                        st_q[s][1] += q1;
+                    }
+                }
                 buf ^= 1;
             }
             tc_fence_before();
@@ -743,6 +787,30 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
         __syncwarp();
+        if constexpr (EPI == 2) {
+            // one partial block per (CTA, lane quarter): stat_partial[(c * MAXB + b) * 2 + {sum, sum sq}]
+            // (MAXB = a.stat_blocks >= 4 * gridDim.x; CTA 0 zero-fills the blocks no CTA owns)
+            const int64_t nblk = a.stat_blocks;
+            const int64_t blk = static_cast<int64_t>(blockIdx.x) * 4 + q;
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s) {
+                const int cc = half * CW + s * 2 * CW;
+                if (cc >= BN) break;
+                const int c0 = n_pin * BN + cc + 2 * lane;
+                if (c0 < a.Nout) {
+                    *reinterpret_cast<double2*>(a.stat_partial + (c0 * nblk + blk) * 2) = make_double2(st_s[s][0], st_q[s][0]);
+                    if (c0 + 1 < a.Nout)
+                        *reinterpret_cast<double2*>(a.stat_partial + ((c0 + 1) * nblk + blk) * 2) =
+                            make_double2(st_s[s][1], st_q[s][1]);
+                }
+            }
+            // blocks past 4 x gridDim.x belong to no CTA: zeroed, channels spread over the CTAs
+            const int used = 4 * static_cast<int>(gridDim.x);
+            for (int c = blockIdx.x; c < a.Nout; c += gridDim.x)
+                for (int b = used + (tid - 128); b < static_cast<int>(nblk); b += 256)
+                    *reinterpret_cast<double2*>(a.stat_partial + (static_cast<int64_t>(c) * nblk + b) * 2) =
+                        make_double2(0.0, 0.0);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -819,7 +887,12 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
         }
     }
     const int tiles = static_cast<int>(ceil_div(M, BM) * ceil_div(a.Nout, BN));
-    const int grid = std::min(tiles, num_sms());
+    int grid = std::min(tiles, num_sms());
+    if constexpr (EPI == 2) {  // every CTA pinned to one N tile (see the kernel's work order)
+        const int nt = static_cast<int>(ceil_div(a.Nout, BN)), mt = static_cast<int>(ceil_div(M, BM));
+        if (nt > num_sms() || a.stat_blocks < 4 * num_sms()) throw std::invalid_argument("igemm: BN statistics layout");
+        grid = nt * std::max(1, std::min(mt, num_sms() / nt));
+    }
     const int dto = sizeof(TO) == 2 ? DT_BF16 : DT_F32;
     CUtensorMap tc = make_tmap_2d(a.out, dto, a.ldo, static_cast<uint64_t>(M), a.ldo, 32);
     CUtensorMap tr = tc, tm = tc;
@@ -846,7 +919,21 @@ void dispatch_ws_mask(const IgemmArgs& a, cudaStream_t s) {
 }
 
 template <typename T, typename TO, int MODE>
+void dispatch_ws_stats(const IgemmArgs& a, cudaStream_t s) {
+    if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
+        const int bn = a.tile_n ? (a.tile_n == 65 ? 64 : a.tile_n) : std::max(64, igemm_block_n(a.Nout));
+        switch (bn) {
+            case 64: return launch_ws_t<T, TO, 64, MODE, false, 2>(a, s);
+            case 128: return launch_ws_t<T, TO, 128, MODE, false, 2>(a, s);
+            default: return launch_ws_t<T, TO, 256, MODE, false, 2>(a, s);
+        }
+    }
+    throw std::invalid_argument("igemm: BN statistics epilogue needs a bf16 TMA / TMA-im2col conv");
+}
+
+template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
+    if (a.stat_partial) return dispatch_ws_stats<T, TO, MODE>(a, s);
     if constexpr (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL || MODE == IG_FPROP) {
         if (a.mask || a.res_mode) return dispatch_ws_mask<T, TO, MODE>(a, s);
     }
@@ -1216,6 +1303,17 @@ int igemm_block_n(int nout) {
     return 256;
 }
 
+bool igemm_stats_supported(const IgemmArgs& a) {
+    if (a.dtype != DT_BF16 || a.out_dtype != DT_BF16 || a.mode != IG_FPROP || a.src2) return false;
+    if (a.residual || a.mask || a.res_mode || a.ep_scale || a.act || a.relu) return false;
+    const bool plain = a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.K_pad == a.SC;
+    const bool im2col = !plain && a.SC % 64 == 0 && a.K_pad == a.kh * a.kw * a.SC && a.kh <= 8 && a.kw <= 8;
+    // the halo path (stride-1 3x3 on 64/128 channels) stores from registers: keep it, unfused
+    return (plain || im2col) && !halo_supported(a) && a.ldo % 8 == 0 && (a.Nout + 63) / 64 <= num_sms();
+}
+
+int igemm_stat_blocks(const IgemmArgs&) { return 4 * num_sms(); }
+
 void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
     // profiling only: SOL_CONV_DBG ORs debug flags into every plan conv (1 = skip stores, 2 = skip MMA)
     static const int env_dbg = std::getenv("SOL_CONV_DBG") ? std::atoi(std::getenv("SOL_CONV_DBG")) : 0;
@@ -1232,7 +1330,7 @@ void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.src2 && (a.SC % 64 || a.SC2 % 64 || a.K1 != a.SC || a.K_pad != a.SC + a.SC2 || a.mode != IG_FPROP))
         throw std::invalid_argument("igemm: dual GEMM needs two 1x1 convs over 128-byte channel blocks");
-    if (!a.src2 && !a.mask && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
+    if (!a.src2 && !a.mask && !a.stat_partial && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
         else dispatch_mode<__nv_bfloat16, float>(a, s);

@@ -49,6 +49,13 @@ struct IgemmArgs {
     // a dgrad epilogue; mask = the ReLU output, same layout as the residual; N tiles of one chunk
     // per epilogue warp so both boxes fit the warp's two staging buffers)
     const void* mask = nullptr;
+    // optional BatchNorm statistics of the stored (bf16) output, for a training BN that consumes it
+    // (sol_b200_plan_link_bn_stats): per channel c and block b = (CTA, 32-row lane quarter),
+    //   stat_partial[(c * stat_blocks + b) * 2 + {0, 1}] = sum over the block's rows of (y - shift[c])^{1,2}
+    // with shift = stat_shift (the previous step's batch mean); blocks no CTA owns are zeroed
+    double* stat_partial = nullptr;
+    const float* stat_shift = nullptr;
+    int stat_blocks = 0;  // partial blocks allocated (igemm_stat_blocks)
     // dual GEMM (inference bottleneck-block fusion): K = [0, K1) reads A from `src` as a 1x1
     // stride-1 conv, K = [K1, K_pad) reads a second 1x1 conv with stride s2 over src2
     // [N, SH2, SW2, SC2] on the same output grid; B packs both weight matrices side by side.
@@ -68,6 +75,9 @@ struct IgemmArgs {
 
 // Launches on `stream`. Throws on unsupported shapes (no fallback path exists).
 void igemm_launch(const IgemmArgs& a, cudaStream_t stream);
+// whether igemm_launch can emit BN statistics (IgemmArgs::stat_partial) for this conv
+bool igemm_stats_supported(const IgemmArgs& a);
+int igemm_stat_blocks(const IgemmArgs& a);  // one per (CTA, lane quarter): 4 x SM count
 
 // Few-channel stem convolution (stem.cu): bf16, input pixels of 8 channels holding Cin <= 4,
 // Cout = 64, kw <= 8, K packed (kh, kw in 8 slots, c in 4) to stem_kpad(kh) (pack_stem_weight).

@@ -506,6 +506,17 @@ public:
                                       : "linear_fused_tcgen05";
     }
 
+    int stat_blocks() const override {
+        if (op_ != SOL_OP_CONV2D || stem_ || pool_ || bn_g_ >= 0 || res_idx_ >= 0 || act_ != 0 || nchw_in_) return 0;
+        const IgemmArgs g = fprop_args(nullptr, nullptr);
+        return igemm_stats_supported(g) ? igemm_stat_blocks(g) : 0;
+    }
+    void set_stat_output(double* partial, const float* shift) override {
+        stat_partial_ = partial;
+        stat_shift_ = shift;
+        family = "conv_fprop_bnstats_tcgen05";
+    }
+
     IgemmArgs fprop_args(const void* src, void* out) const {
         IgemmArgs g;
         g.mode = IG_FPROP;
@@ -604,6 +615,9 @@ public:
                 }
                 g.act = act_;
                 g.tile_n = tile_n_;
+                g.stat_partial = stat_partial_;
+                g.stat_shift = stat_shift_;
+                g.stat_blocks = stat_partial_ ? igemm_stat_blocks(g) : 0;
                 if (stem_) stem_launch(g, s);
                 else igemm_launch(g, s);
                 break;
@@ -733,6 +747,8 @@ private:
     bool coef_valid_ = false;
     int bn_g_ = -1, bn_b_ = -1, bn_m_ = -1, bn_v_ = -1;
     float bn_eps_ = 1e-5f;
+    double* stat_partial_ = nullptr;  // BN statistics epilogue (link_bn_stats)
+    const float* stat_shift_ = nullptr;
     int res_idx_ = -1;
     int res_mode_ = 0;  // 1: the residual binding is a ReLU output used as a backward mask
     int mask_idx_ = -1;  // fused Add + ReluBack: the ReLU output binding (residual = the added gradient)
@@ -1102,6 +1118,23 @@ public:
 
 private:
     bool update_running_ = false;  // training BN: update running_mean / running_var in place
+
+public:
+    bool use_producer_stats(int binding, int blocks, double** partial, const float** shift) override {
+        for (auto& b : bn_) {
+            if (!b.training || b.x_binding != binding || blocks <= 0) continue;
+            if (b.ext_partial == nullptr || b.ext_blocks != blocks) {
+                b.ext_partial = static_cast<double*>(dev_alloc(static_cast<size_t>(b.C) * blocks * 2 * sizeof(double)));
+                b.ext_blocks = blocks;
+            }
+            *partial = b.ext_partial;
+            *shift = b.stats;  // the previous step's batch mean (zeros before the first step)
+            return true;
+        }
+        return false;
+    }
+
+private:
     struct SlotSrc {
         int binding;
     };
@@ -1118,6 +1151,8 @@ private:
         int64_t pixels;
         int x_ld;
         int xN, xH, xW;
+        double* ext_partial = nullptr;  // statistics written by the producing conv's epilogue
+        int ext_blocks = 0;
     };
     struct DwPrep {
         int w, bias;
@@ -1549,6 +1584,30 @@ void DfpModule::run(void* const* args, int nargs, void* scratch, cudaStream_t s,
                 bn_infer_coef(static_cast<const float*>(args[b.g]), static_cast<const float*>(args[b.b]),
                               static_cast<const float*>(args[b.m]), static_cast<const float*>(args[b.v]), b.eps,
                               b.coef, b.C, s);
+            continue;
+        }
+        if (b.ext_partial) {
+            // statistics from the producing conv's epilogue: sums of (y - previous mean) per
+            // (M tile, row quarter) block; the finalisation reads the shift before it overwrites
+            // the mean with this step's (same thread per channel)
+            FinalizeArgs f;
+            f.mode = FIN_BN_STATS;
+            f.C = b.C;
+            f.blocks = b.ext_blocks;
+            f.partial = b.ext_partial;
+            f.count = static_cast<double>(b.pixels);
+            f.eps = b.eps;
+            f.shift = b.stats;
+            f.gamma = static_cast<const float*>(args[b.g]);
+            f.beta = static_cast<const float*>(args[b.b]);
+            f.stats_out = b.stats;
+            f.coef = b.coef;
+            if (b.m >= 0 && b.v >= 0 && update_running_) {
+                f.running_mean = static_cast<float*>(args[b.m]);
+                f.running_var = static_cast<float*>(args[b.v]);
+                f.momentum = b.momentum;
+            }
+            dfp_finalize(f, s);
             continue;
         }
         double* partial = static_cast<double*>(scratch);

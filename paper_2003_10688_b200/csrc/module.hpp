@@ -34,6 +34,13 @@ public:
     // Weight packing of this run issued ahead of the plan's steps (inside a pack batch, pack.cuh);
     // false when the module packs nothing this run.
     virtual bool prepack(void* const* args, cudaStream_t s, bool frozen) { return false; }
+    // BatchNorm statistics from the producing conv's epilogue (sol_b200_module_link_bn_stats):
+    // a conv reports how many partial blocks its epilogue would write (0: cannot) and takes the
+    // buffers; a BN unit switches the BN whose input is `binding` to those partials and returns
+    // its partial buffer and shift array (nullptr: no such training BN).
+    virtual int stat_blocks() const { return 0; }
+    virtual void set_stat_output(double* partial, const float* shift) {}
+    virtual bool use_producer_stats(int binding, int blocks, double** partial, const float** shift) { return false; }
 
     std::string family;
     int n_args = 0;

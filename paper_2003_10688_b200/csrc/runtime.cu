@@ -773,6 +773,25 @@ bool Plan::step_set_option(int i, int key, int value) {
     return ok;
 }
 
+bool Plan::link_bn_stats(int conv_step, int bn_step, int bn_binding) {
+    const int n = static_cast<int>(steps_.size());
+    if (conv_step < 0 || conv_step >= n || bn_step <= conv_step || bn_step >= n || !steps_[conv_step].module ||
+        !steps_[bn_step].module)
+        throw std::invalid_argument("link_bn_stats: a conv step followed by a BN step");
+    Module* conv = steps_[conv_step].module.get();
+    const int blocks = conv->stat_blocks();
+    if (blocks <= 0) return false;
+    double* partial = nullptr;
+    const float* shift = nullptr;
+    if (!steps_[bn_step].module->use_producer_stats(bn_binding, blocks, &partial, &shift)) return false;
+    conv->set_stat_output(partial, shift);
+    if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+    }
+    return true;
+}
+
 void Plan::comm_info(int* nranks, int* rank, int* cuda_device) const {
     *nranks = 1;
     *rank = 0;

@@ -148,6 +148,8 @@ public:
     int set_lr(float lr);  // SgdUpdate steps' runtime learning rate; returns how many steps took it
     double time_step(int i, int reps);  // median device time (us) of step i run alone, eagerly
     bool step_set_option(int i, int key, int value);
+    // BN statistics from a conv step's epilogue for a later training-BN step (Module::use_producer_stats)
+    bool link_bn_stats(int conv_step, int bn_step, int bn_binding);
     void h2d(int id, const void* src, uint64_t bytes);
     void stage_h2d(int id, const void* src, uint64_t bytes);
     // host-side fences on the copy stream: a ticket taken after stage_h2d() calls is complete once

@@ -57,6 +57,8 @@ class OptimizeOptions:
     nccl_allreduce: bool = False   # test hook: run the NCCL gradient all-reduce even with one replica
     relu_mask_from_output: bool = True  # training: ReluBack masks read the ReLU output (passes.py), so
                                         # BN+ReLU fuse and the pre-activation is never stored
+    bn_stats_from_conv: bool = True  # training, bf16: a training BN's batch statistics come out of the
+                                     # producing conv's GEMM epilogue (no statistics pass over its output)
     fuse_relu_back: bool = True    # training: a stride-1 Conv2dBackX applies the following ReluBack
                                    # mask (read from the ReLU output) in its GEMM epilogue
     update_bn_stats: bool = True   # training: update BN running_mean / running_var on the device
@@ -250,6 +252,10 @@ class DevicePlan:
                 L.check(lib.sol_b200_plan_add_allreduce(self.plan, self.buf[gname], n, L.DT_F32, 1.0 / o.world_size))
                 self.steps.append(StepInfo("allreduce", "nccl_allreduce", gname, algo_bytes=4.0 * n))
 
+        link_stats = (o.train and o.bn_stats_from_conv and o.dtype == "bf16"
+                      and not os.environ.get("SOL_NO_BN_STATS_EPI"))
+        conv_step = {}  # output of a single-Conv2d unit -> its plan step
+        self.bn_stats_links = 0
         for ui, u in enumerate(self.units):
             out_buf(u.output)
             if u.output in absorbed:  # computed by its BatchNormBackX sibling's step
@@ -271,7 +277,21 @@ class DevicePlan:
                 L.check(lib.sol_b200_module_set_sibling_outputs(mod.handle, mask))
                 mod.n_args += bin(mask).count("1")
                 ids += [out_buf(x) for x in (gam, bet) if x]
+            step = len(self.steps)
             add_step(mod, ids, StepInfo("unit", "", u.output, node_ids=list(u.node_ids)))
+            if link_stats:
+                first = g.find_node(u.node_ids[0])
+                if u.kind == "dnn" and len(u.node_ids) == 1 and first.op == "Conv2d":
+                    conv_step[u.output] = step
+                elif (u.kind == "dfp" and first.op == "BatchNorm2d" and first.attrs.training
+                      and first.inputs[0] in conv_step and first.inputs[0] in u.inputs):
+                    rc = lib.sol_b200_plan_link_bn_stats(self.plan, conv_step[first.inputs[0]], step,
+                                                         u.inputs.index(first.inputs[0]))
+                    if rc == 0:
+                        self.bn_stats_links += 1
+                        self.steps[conv_step[first.inputs[0]]].family = "conv_fprop_bnstats_tcgen05"
+                    elif rc != L.SOL_E_UNSUPPORTED:
+                        L.check(rc)
             issue_bucket(self.ar_schedule.get(ui, ()))
         # graph outputs: canonical f32 copies for the host
         self.out_canon: Dict[str, int] = {}

@@ -174,3 +174,47 @@ def test_fused_dgrad_relu_back_is_exact(gpu, dtype):
     assert ga.keys() == gb.keys()
     for k in ga:
         assert np.array_equal(ga[k], gb[k]), k
+
+
+def test_bn_stats_from_conv_epilogue(gpu):
+    """bn_stats_from_conv: a training BatchNorm's batch statistics come out of the producing conv's
+    GEMM epilogue (partial sums of (y - previous batch mean) per M tile and row quarter) instead of
+    a pass over y. After several steps (the shift is then the previous step's mean), every linked
+    BN unit's output matches the oracle BN of the plan's own conv output, and the loss follows the
+    statistics-pass plan (bf16 rounding flips amplify through the network, hence the tolerance)."""
+    import torch
+    from paper_2003_10688_b200 import dfp, frontend, graph, models
+    from tests.gpu_util import from_device
+    g = models.resnet(50, hw=64, classes=16, width=16, train=True, seed=5)
+    ins = _inputs(graph.infer_shapes(g, 8), 8, seed=10)
+    a = frontend.optimize(g, _opts(train=True, lr=0.0, keep_all=True))
+    b = frontend.optimize(g, _opts(train=True, lr=0.0, bn_stats_from_conv=False))
+    pa = a._plan(True)
+    assert pa.bn_stats_links > 20 and b._plan(True).bn_stats_links == 0
+    assert any(st.family == "conv_fprop_bnstats_tcgen05" for st in pa.steps)
+    for _ in range(3):
+        la, lb = a.train_step(ins), b.train_step(ins)
+    np.testing.assert_allclose(la, lb, rtol=2e-2)
+
+    def get(nm):
+        raw = pa.read_tensor(nm)
+        f32 = dfp.is_f32_tensor(pa.graph, nm)
+        t = torch.from_numpy(raw.view(np.float32).copy() if f32 else raw.view(np.int16).copy())
+        return from_device(t if f32 else t.view(torch.bfloat16), pa.graph.meta_of(nm)).astype(np.float64)
+
+    linked = {pa.steps[i].output for i in range(len(pa.steps)) if pa.steps[i].family == "conv_fprop_bnstats_tcgen05"}
+    checked, bad = 0, []
+    for u in pa.units:
+        first = pa.graph.find_node(u.node_ids[0])
+        if u.kind != "dfp" or first.op != "BatchNorm2d" or first.inputs[0] not in linked:
+            continue
+        local = {nm: get(nm) for nm in u.inputs}
+        params = {k: np.asarray(v, np.float64) for k, v in pa.params.items()}
+        for nid in u.node_ids:
+            n = pa.graph.find_node(nid)
+            local[nid] = O.eval_node(n, [local[i] for i in n.inputs], params)
+        err = O.oracle_err(get(u.output), local[u.output])
+        checked += 1
+        if err > 2e-2:
+            bad.append((u.output, err))
+    assert checked > 20 and not bad, bad
