@@ -2482,7 +2482,11 @@ bool launch_maxpool_back_fast(const DfpArgs& a, cudaStream_t s) {
 // while it is still in L2 for the mask.
 constexpr int kBandSmemCap = 36 * 1024;
 
-template <typename T, bool ADD, bool MASK>
+// MXX: the ReluBack mask source is the pool's own input (the ReLU output, passes.relu_mask_from_output).
+// A pixel only receives gradient as the argmax of a window, whose max is then the pixel's value:
+// mask(p) = x[p] > 0 = (window max > 0), decided in phase 1, so phase 2 never reads the mask tensor
+// (bit-identical; one activation-sized read fewer).
+template <typename T, bool ADD, bool MASK, bool MXX = false>
 __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __grid_constant__ DfpArgs a,
                                                                     PoolBackSpec ps, int R) {
     constexpr int V = VEC<T>;
@@ -2538,7 +2542,7 @@ __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __g
         }
 #pragma unroll
         for (int e = 0; e < V; ++e)
-            if (!(best[e] > a.min_init)) bidx[e] = 255;
+            if (!(best[e] > a.min_init) || (MXX && !(best[e] > 0.f))) bidx[e] = 255;
         uint8_t* dst = am_s + (static_cast<int>(t) * a.C + c);
         if constexpr (V == 8) {
             uint2 r;
@@ -2648,7 +2652,11 @@ bool launch_maxpool_back_band(const DfpArgs& a, cudaStream_t s) {
     const int rmax = static_cast<int>(std::min<int64_t>(16, kBandSmemCap / row_bytes - 1));
     if (rmax < 1) return false;
     const bool add = ps.s1 >= 0, mask = ps.sm >= 0;
-    auto kern = add ? (mask ? maxpool_back_band_kernel<T, true, true> : maxpool_back_band_kernel<T, true, false>)
+    // mask read from the pool input itself: decided in phase 1 (MXX)
+    const bool mxx = mask && a.in[ps.sm] == a.in[a.pool_x] && a.in_ld[ps.sm] == a.in_ld[a.pool_x] &&
+                     std::getenv("SOL_NO_POOLBACK_MXX") == nullptr;
+    auto kern = mxx ? (add ? maxpool_back_band_kernel<T, true, false, true> : maxpool_back_band_kernel<T, false, false, true>)
+              : add ? (mask ? maxpool_back_band_kernel<T, true, true> : maxpool_back_band_kernel<T, true, false>)
                     : (mask ? maxpool_back_band_kernel<T, false, true> : maxpool_back_band_kernel<T, false, false>);
     // band height: minimise (waves of resident blocks) x (window rows per block) — with N*bands
     // just above a multiple of the resident count the last wave would run nearly empty
