@@ -908,10 +908,15 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
 
 template <typename T, typename TO, int MODE>
 void dispatch_ws_mask(const IgemmArgs& a, cudaStream_t s) {
-    // the add + mask form needs one epilogue chunk per warp: 128-wide tiles (bf16), 64 (f32)
+    // the add + mask form needs one epilogue chunk per warp: 128-wide tiles (bf16), 64 (f32); the
+    // mask-only form (ReluBack) takes any tile, 256 included (bf16)
     constexpr int BNMAX = sizeof(TO) == 2 ? 128 : 64;
-    int bn = a.tile_n ? std::min(a.tile_n == 65 ? 64 : a.tile_n, BNMAX) : std::min(igemm_block_n(a.Nout), BNMAX);
+    const int lim = (sizeof(TO) == 2 && !a.mask) ? 256 : BNMAX;
+    int bn = a.tile_n ? std::min(a.tile_n == 65 ? 64 : a.tile_n, lim) : std::min(igemm_block_n(a.Nout), lim);
     if (bn < 64) bn = 64;
+    if constexpr (sizeof(TO) == 2) {
+        if (bn == 256) return launch_ws_t<T, TO, 256, MODE, false, 1>(a, s);
+    }
     if constexpr (BNMAX == 128) {
         if (bn == 128) return launch_ws_t<T, TO, 128, MODE, false, 1>(a, s);
     }
