@@ -231,11 +231,8 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
 
 // split-K reduction straight into the canonical layout: canonical i = ((co*Cin + ci)*KH + kh)*KW + kw
 // reads packed j = co*KH*KW*ld + (kh*KW + kw)*ld + ci of every split
-// splits = partials per column group; column group g (packed columns [g * cpg, (g + 1) * cpg))
-// sums partials [g * splits, (g + 1) * splits) -- one group (cpg = all columns) except for the
-// halo wgrad, whose CTAs each own one filter row
 __global__ void wgrad_reduce_canon_kernel(const float* __restrict__ ws, float* __restrict__ w, int64_t n, int splits,
-                                          int Cout, int Cin, int KH, int KW, int ld, int cpg) {
+                                          int Cout, int Cin, int KH, int KW, int ld) {
     const int64_t total = static_cast<int64_t>(Cout) * Cin * KH * KW;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -245,30 +242,65 @@ __global__ void wgrad_reduce_canon_kernel(const float* __restrict__ ws, float* _
         const int co = static_cast<int>(i / (static_cast<int64_t>(KW) * KH * Cin));
         const int pcol = (kh * KW + kw) * ld + ci;
         const int64_t j = static_cast<int64_t>(co) * KH * KW * ld + pcol;
-        const int sp0 = pcol / cpg * splits;
         float acc = 0.f;
-        for (int sp = sp0; sp < sp0 + splits; ++sp) acc += __ldg(ws + sp * n + j);
+        for (int sp = 0; sp < splits; ++sp) acc += __ldg(ws + sp * n + j);
         w[i] = acc;
     }
 }
 
+// Halo wgrad partials (wgrad_halo.cu): group g's spg partials are compact [N co][tiles x 128];
+// each thread sums one partial position over the group's CTAs (contiguous, coalesced reads) and
+// scatters it to the packed dW [Cout][tap * sc + ci] or the canonical dW [co][ci][kh][kw].
+__global__ void wgrad_reduce_halo_kernel(const float* __restrict__ ws, float* __restrict__ dw_packed,
+                                         float* __restrict__ dw_canon, int canon_cin, int spg, int sc,
+                                         const WhPlan hp) {
+    const int cols = wh_cols(hp);
+    const int64_t pf = wh_partial_floats(hp);
+    const int64_t total = static_cast<int64_t>(hp.groups) * pf;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(e / pf);
+        const int64_t r = e - static_cast<int64_t>(g) * pf;
+        const int co_l = static_cast<int>(r / cols), cl = static_cast<int>(r - static_cast<int64_t>(co_l) * cols);
+        int co, tap, ci;
+        if (hp.pairs) {
+            co = co_l;
+            tap = cl / sc;
+            ci = cl - tap * sc;
+            if (tap >= 9) continue;
+        } else {
+            const int os = g % hp.n_co, cs = (g / hp.n_co) % hp.n_ci, tg = g / (hp.n_co * hp.n_ci);
+            tap = tg * hp.TT + cl / 128;
+            if (tap >= 9) continue;
+            ci = cs * 128 + (cl & 127);
+            co = os * hp.N + co_l;
+        }
+        const float* src = ws + static_cast<int64_t>(g) * spg * pf + r;
+        float acc = 0.f;
+        for (int sp = 0; sp < spg; ++sp) acc += __ldg(src + static_cast<int64_t>(sp) * pf);
+        if (dw_canon) {
+            if (ci < canon_cin) dw_canon[((static_cast<int64_t>(co) * canon_cin + ci) * 3 + tap / 3) * 3 + tap % 3] = acc;
+        } else {
+            dw_packed[static_cast<int64_t>(co) * 9 * sc + tap * sc + ci] = acc;
+        }
+    }
+}
+
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, float* __restrict__ dw, int64_t n,
-                                    int splits, int ncol, int cpg) {
+                                    int splits) {
     const int64_t i4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
     if (i4 >= n) return;
-    if (i4 + 4 <= n && ncol % 4 == 0 && cpg % 4 == 0) {
-        const int s0 = static_cast<int>(i4 % ncol) / cpg * splits;
+    if (i4 + 4 <= n) {
         float4 acc = make_float4(0, 0, 0, 0);
-        for (int s = s0; s < s0 + splits; ++s) {
+        for (int s = 0; s < splits; ++s) {
             float4 v = __ldg(reinterpret_cast<const float4*>(ws + s * n + i4));
             acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
         *reinterpret_cast<float4*>(dw + i4) = acc;
     } else {
-        for (int64_t i = i4; i < n && i < i4 + 4; ++i) {
-            const int s0 = static_cast<int>(i % ncol) / cpg * splits;
+        for (int64_t i = i4; i < n; ++i) {
             float acc = 0.f;
-            for (int s = s0; s < s0 + splits; ++s) acc += ws[s * n + i];
+            for (int s = 0; s < splits; ++s) acc += ws[s * n + i];
             dw[i] = acc;
         }
     }
@@ -1235,7 +1267,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 struct WgradPlan {
     int ncol, bn, splits, kb_per_split;
     bool fast = false, swap = false, halo = false;
-    int spg = 0, cpg = 0;  // reduction: partials per column group, columns per group (0: one group)
+    int spg = 0;           // reduction: partials per group (0: one group of all splits)
+    WhPlan hp{};           // halo wgrad grouping (hp.pairs = 1: a single group)
     int m_tiles = 1, n_tiles = 1;
 };
 
@@ -1246,7 +1279,8 @@ WgradPlan plan_wgrad(const WgradArgs& a) {
     if (wgrad_halo_supported(a)) {  // one partial per CTA (wgrad_halo.cu)
         p.halo = true;
         p.bn = 64;
-        p.splits = wgrad_halo_splits(a, &p.spg, &p.cpg);
+        p.splits = wgrad_halo_splits(a, &p.spg);
+        p.hp = wgrad_halo_plan(a);
         p.kb_per_split = 0;
         return p;
     }
@@ -1347,6 +1381,7 @@ void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
 
 size_t wgrad_workspace_floats(const WgradArgs& a) {
     WgradPlan p = plan_wgrad(a);
+    if (p.halo) return static_cast<size_t>(p.splits) * wh_partial_floats(p.hp);
     return p.splits > 1 ? static_cast<size_t>(p.splits) * a.Cout * p.ncol : 0;
 }
 
@@ -1356,7 +1391,7 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
     if (a.SC % vec != 0 || a.ld_dy % vec != 0)
         throw std::invalid_argument("wgrad: channel counts must be multiples of 16 bytes");
     WgradPlan p = plan_wgrad(a);
-    if (p.splits <= 1) a.workspace = nullptr;
+    if (p.splits <= 1 && !p.halo) a.workspace = nullptr;  // the halo path always reduces its partials
     else if (a.workspace == nullptr) throw std::invalid_argument("wgrad: workspace required");
     if (p.halo) {
         wgrad_halo_launch(a, s);
@@ -1387,18 +1422,23 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
             default: launch_wgrad_t<float, 128>(a, p.ncol, p.splits, p.kb_per_split, s); break;
         }
     }
-    if (p.splits > 1 && a.dw_canon) {
+    if (p.halo) {
+        const int64_t total = static_cast<int64_t>(p.hp.groups) * wh_partial_floats(p.hp);
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8L * num_sms())));
+        wgrad_reduce_halo_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw, a.dw_canon, a.canon_cin, p.spg, a.SC, p.hp);
+        SOL_CUDA(cudaGetLastError());
+    } else if (p.splits > 1 && a.dw_canon) {
         const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
         const int64_t total = static_cast<int64_t>(a.Cout) * a.canon_cin * a.kh * a.kw;
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8L * num_sms())));
-        wgrad_reduce_canon_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw_canon, n, p.spg ? p.spg : p.splits, a.Cout,
-                                                       a.canon_cin, a.kh, a.kw, a.SC, p.cpg ? p.cpg : p.ncol);
+        wgrad_reduce_canon_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw_canon, n, p.splits, a.Cout, a.canon_cin,
+                                                       a.kh, a.kw, a.SC);
         SOL_CUDA(cudaGetLastError());
     } else if (p.splits > 1) {
         const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
         const int threads = 256;
         wgrad_reduce_kernel<<<static_cast<unsigned>(ceil_div(ceil_div(n, 4), threads)), threads, 0, s>>>(
-            a.workspace, a.dw, n, p.spg ? p.spg : p.splits, p.ncol, p.cpg ? p.cpg : p.ncol);
+            a.workspace, a.dw, n, p.splits);
         SOL_CUDA(cudaGetLastError());
     } else if (a.dw_canon) {
         unpack_conv_grad(a.dw, a.dw_canon, a.Cout, a.canon_cin, a.kh, a.kw, a.SC, s);

@@ -117,9 +117,36 @@ struct WgradArgs {
     int canon_cin = 0;
 };
 void wgrad_launch(const WgradArgs& a, cudaStream_t stream);
-// halo weight gradient (wgrad_halo.cu): stride-1 3x3, 64 -> 64 or 128 -> 128 channels, bf16
+// halo weight gradient (wgrad_halo.cu): stride-1 3x3, bf16; 64 -> 64, 128 -> 128 and >= 256-channel
+// shapes. Work = (tap group, ci slice, co slice) x pixel units; every CTA writes one compact partial
+// [co slice][its tiles x 128] of its group's dW entries (wh_group_of maps an entry to its group and
+// offset).
+struct WhPlan {
+    int Wp, K, R, HX;          // row pitch (W + 2), pixel rows per unit (64 / 128), output rows, x rows
+    int pairs;                 // 64 input channels: five M tiles of two taps
+    int ncx, ncd, N;           // x / dy 64-channel blocks per unit, co slice width
+    int n_ci, n_co, TT;        // ci slices (128), co slices, taps per CTA
+    int tap_groups, groups;
+    int cb_bytes, dy_blk, stage_bytes;
+    int row_blocks, units;
+};
+WhPlan wgrad_halo_plan(const WgradArgs& a);
+// columns of one CTA's partial (its tiles x 128) and the partial's size in floats (co slice rows)
+__host__ __device__ inline int wh_cols(const WhPlan& g) { return (g.pairs ? 5 : g.TT) * 128; }
+__host__ __device__ inline int64_t wh_partial_floats(const WhPlan& g) { return static_cast<int64_t>(g.N) * wh_cols(g); }
+// group of dW entry (co, packed column = tap * sc + ci) and its offset inside a partial
+__host__ __device__ inline int wh_group_of(const WhPlan& g, int sc, int co, int col, int64_t* off) {
+    if (g.pairs) {
+        *off = static_cast<int64_t>(co) * wh_cols(g) + col;
+        return 0;
+    }
+    const int tap = col / sc, ci = col - tap * sc;
+    const int tg = tap / g.TT, cs = ci / 128, os = co / g.N;
+    *off = static_cast<int64_t>(co - os * g.N) * wh_cols(g) + (tap - tg * g.TT) * 128 + (ci - cs * 128);
+    return (tg * g.n_ci + cs) * g.n_co + os;
+}
 bool wgrad_halo_supported(const WgradArgs& a);
-int wgrad_halo_splits(const WgradArgs& a, int* splits_per_group = nullptr, int* cols_per_group = nullptr);
+int wgrad_halo_splits(const WgradArgs& a, int* splits_per_group = nullptr);
 void wgrad_halo_launch(const WgradArgs& a, cudaStream_t stream);
 size_t wgrad_workspace_floats(const WgradArgs& a);
 

@@ -28,6 +28,10 @@ CASES = [
     (2, 64, 13, 29, 64, 3, 1, 1),     # halo-tile kernel, ragged rows / junk columns
     (2, 128, 28, 28, 128, 3, 1, 1),   # ResNet-50 layer-2 shape: halo fprop, halo wgrad by filter row
     (3, 128, 11, 19, 128, 3, 1, 1),   # halo wgrad (128 channels), ragged rows / junk columns
+    (2, 256, 14, 14, 256, 3, 1, 1),   # ResNet-50 layer 3: halo wgrad by (tap pair, ci slice)
+    (2, 512, 7, 7, 512, 3, 1, 1),     # ResNet-50 layer 4: 64-row units, two co slices
+    (1, 256, 9, 11, 512, 3, 1, 1),    # wide halo wgrad, ragged
+    (1, 64, 5, 5, 64, 3, 1, 1),       # halo wgrad with a single unit (one partial, still reduced)
 ]
 
 
