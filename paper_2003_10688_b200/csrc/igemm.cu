@@ -745,6 +745,48 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                         if (act == 2) f[i] = fminf(f[i], 6.0f);
                     }
                 }
+                if constexpr (EPI == 3) {
+                    // sub-pixel dgrad class stored in place: this lane's row is one class-grid
+                    // pixel; its 128 bytes go to the strided output pixel (and zeros to the rest
+                    // of its stride cell when the other classes have no taps)
+                    static_assert(sizeof(TO) == 2, "in-place sub-pixel classes are bf16");
+                    const int m = m0 + q * 32 + lane;
+                    if (m < M && !(a.dbg & 1)) {
+                        const int ohw = a.OH * a.OW;
+                        const int img = m / ohw, rem = m - img * ohw;
+                        const int i = rem / a.OW, j = rem - i * a.OW;
+                        const int oy = a.sub_sh * i, ox = a.sub_sw * j;
+                        TO* base = static_cast<TO*>(a.out) + n;
+                        const bool full = n + CW <= a.ldo;
+                        uint4 pk[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            __nv_bfloat162 p0 = __floats2bfloat162_rn(f[8 * k], f[8 * k + 1]);
+                            __nv_bfloat162 p1 = __floats2bfloat162_rn(f[8 * k + 2], f[8 * k + 3]);
+                            __nv_bfloat162 p2 = __floats2bfloat162_rn(f[8 * k + 4], f[8 * k + 5]);
+                            __nv_bfloat162 p3 = __floats2bfloat162_rn(f[8 * k + 6], f[8 * k + 7]);
+                            pk[k] = make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                                               *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+                        }
+                        for (int da = 0; da < a.sub_sh; ++da) {
+                            for (int db = 0; db < a.sub_sw; ++db) {
+                                const bool mine = da == a.sub_a && db == a.sub_b;
+                                if (!mine && !a.sub_zero) continue;
+                                if (oy + da >= a.sub_H || ox + db >= a.sub_W) continue;
+                                TO* o = base + ((static_cast<int64_t>(img) * a.sub_H + oy + da) * a.sub_W + ox + db) * a.ldo;
+                                if (full) {
+#pragma unroll
+                                    for (int k = 0; k < 8; ++k)
+                                        *reinterpret_cast<uint4*>(o + 8 * k) = mine ? pk[k] : make_uint4(0, 0, 0, 0);
+                                } else {
+                                    for (int k = 0; k < CW && n + k < a.ldo; ++k)
+                                        o[k] = mine ? __float2bfloat16_rn(f[k]) : __float2bfloat16_rn(0.f);
+                                }
+                            }
+                        }
+                    }
+                    continue;
+                }
                 // the staging buffer is free once the TMA store issued two chunks ago has read it
                 // (with a residual, the buffer was drained before the residual load was issued)
                 if (!has_res) {
@@ -969,7 +1011,21 @@ void dispatch_ws_stats(const IgemmArgs& a, cudaStream_t s) {
 }
 
 template <typename T, typename TO, int MODE>
+void dispatch_ws_sub(const IgemmArgs& a, cudaStream_t s) {
+    if constexpr (sizeof(T) == 2 && sizeof(TO) == 2 && (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL)) {
+        const int bn = a.tile_n ? (a.tile_n == 65 ? 64 : a.tile_n) : std::max(64, igemm_block_n(a.Nout));
+        switch (bn) {
+            case 64: return launch_ws_t<T, TO, 64, MODE, false, 3>(a, s);
+            case 128: return launch_ws_t<T, TO, 128, MODE, false, 3>(a, s);
+            default: return launch_ws_t<T, TO, 256, MODE, false, 3>(a, s);
+        }
+    }
+    throw std::invalid_argument("igemm: in-place sub-pixel classes need a bf16 TMA / TMA-im2col conv");
+}
+
+template <typename T, typename TO, int MODE>
 void dispatch_ws(const IgemmArgs& a, cudaStream_t s) {
+    if (a.sub_sh) return dispatch_ws_sub<T, TO, MODE>(a, s);
     if (a.stat_partial) return dispatch_ws_stats<T, TO, MODE>(a, s);
     if constexpr (MODE == IG_FPROP_TMA || MODE == IG_FPROP_IM2COL || MODE == IG_FPROP) {
         if (a.mask || a.res_mode) return dispatch_ws_mask<T, TO, MODE>(a, s);
@@ -1353,6 +1409,15 @@ bool igemm_stats_supported(const IgemmArgs& a) {
 
 int igemm_stat_blocks(const IgemmArgs&) { return 4 * num_sms(); }
 
+bool igemm_sub_supported(const IgemmArgs& a) {
+    static const bool off = std::getenv("SOL_NO_SUBPIXEL_INPLACE") != nullptr;
+    if (off || a.dtype != DT_BF16 || a.out_dtype != DT_BF16 || a.mode != IG_FPROP || a.src2) return false;
+    if (a.residual || a.mask || a.res_mode || a.ep_scale || a.bias || a.act || a.relu || a.stat_partial) return false;
+    const bool plain = a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.K_pad == a.SC;
+    const bool im2col = !plain && a.SC % 64 == 0 && a.K_pad == a.kh * a.kw * a.SC && a.kh <= 8 && a.kw <= 8;
+    return (plain || im2col) && a.ldo % 8 == 0;
+}
+
 void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
     // profiling only: SOL_CONV_DBG ORs debug flags into every plan conv (1 = skip stores, 2 = skip MMA)
     static const int env_dbg = std::getenv("SOL_CONV_DBG") ? std::atoi(std::getenv("SOL_CONV_DBG")) : 0;
@@ -1369,7 +1434,7 @@ void igemm_launch(const IgemmArgs& a_in, cudaStream_t s) {
     if (a.N * a.OH * a.OW <= 0 || a.Nout <= 0) return;
     if (a.src2 && (a.SC % 64 || a.SC2 % 64 || a.K1 != a.SC || a.K_pad != a.SC + a.SC2 || a.mode != IG_FPROP))
         throw std::invalid_argument("igemm: dual GEMM needs two 1x1 convs over 128-byte channel blocks");
-    if (!a.src2 && !a.mask && !a.stat_partial && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
+    if (!a.src2 && !a.mask && !a.stat_partial && !a.sub_sh && a.tile_n == 0 && halo_supported(a)) return halo_launch(a, s);  // a forced tile: im2col path
     if (a.dtype == DT_BF16) {
         if (a.out_dtype == DT_BF16) dispatch_mode<__nv_bfloat16, __nv_bfloat16>(a, s);
         else dispatch_mode<__nv_bfloat16, float>(a, s);

@@ -56,6 +56,11 @@ struct IgemmArgs {
     double* stat_partial = nullptr;
     const float* stat_shift = nullptr;
     int stat_blocks = 0;  // partial blocks allocated (igemm_stat_blocks)
+    // strided dgrad by sub-pixel classes, stored in place: GEMM row (n, i, j) of the class grid
+    // (N, OH, OW) goes to pixel (n, sub_sh * i + sub_a, sub_sw * j + sub_b) of the [N, sub_H, sub_W]
+    // output with direct 16-byte stores; sub_zero: the class also zeroes the other positions of its
+    // sub_sh x sub_sw cell (the classes without taps). 0 = ordinary output.
+    int sub_sh = 0, sub_sw = 0, sub_a = 0, sub_b = 0, sub_H = 0, sub_W = 0, sub_zero = 0;
     // dual GEMM (inference bottleneck-block fusion): K = [0, K1) reads A from `src` as a 1x1
     // stride-1 conv, K = [K1, K_pad) reads a second 1x1 conv with stride s2 over src2
     // [N, SH2, SW2, SC2] on the same output grid; B packs both weight matrices side by side.
@@ -77,6 +82,8 @@ struct IgemmArgs {
 void igemm_launch(const IgemmArgs& a, cudaStream_t stream);
 // whether igemm_launch can emit BN statistics (IgemmArgs::stat_partial) for this conv
 bool igemm_stats_supported(const IgemmArgs& a);
+// whether igemm_launch can store a sub-pixel dgrad class in place (IgemmArgs::sub_*)
+bool igemm_sub_supported(const IgemmArgs& a);
 int igemm_stat_blocks(const IgemmArgs& a);  // one per (CTA, lane quarter): 4 x SM count
 
 // Few-channel stem convolution (stem.cu): bf16, input pixels of 8 channels holding Cin <= 4,

@@ -376,6 +376,15 @@ public:
     }
 
     void run_subpixel(void* const* args, void* out, void* scratch, cudaStream_t s, bool frozen) {
+        // in place: every class stores straight into its stride positions of dx (no scratch, no
+        // interleave pass) when all of them take the bf16 TMA paths and either every class has
+        // taps or only the first does (a 1x1 strided conv: that class zeroes the rest of each cell)
+        int with_taps = 0;
+        for (const auto& c : classes_) with_taps += c.th ? 1 : 0;
+        const bool only_first = with_taps == 1 && classes_[0].th;
+        bool inplace = with_taps == static_cast<int>(classes_.size()) || only_first;
+        for (size_t ci = 0; ci < classes_.size() && inplace; ++ci)
+            if (classes_[ci].th) inplace = igemm_sub_supported(class_args(classes_[ci], args, out));
         InterleaveArgs il;
         il.sh = sh_;
         il.sw = sw_;
@@ -395,28 +404,43 @@ public:
                 pack_dgrad_class(static_cast<const float*>(args[w_idx_]), c.packed, dtype_, static_cast<int>(cout_),
                                  static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), c.kpad, c.th, c.tw, c.kh0,
                                  c.kw0, sh_, sw_, s);
-            IgemmArgs g;
-            g.mode = IG_FPROP;
-            g.dtype = dtype_;
-            g.out_dtype = dtype_;
-            g.src = args[0];
-            g.wt = c.packed;
-            g.out = dst;
-            g.N = static_cast<int>(in_.N);
-            g.SH = static_cast<int>(in_.H);
-            g.SW = static_cast<int>(in_.W);
-            g.SC = static_cast<int>(in_.ld);
-            g.OH = c.OHc;
-            g.OW = c.OWc;
-            g.kh = c.th; g.kw = c.tw; g.sh = 1; g.sw = 1; g.ph = -c.offh; g.pw = -c.offw;
-            g.Nout = static_cast<int>(cin_);
-            g.K_pad = c.kpad;
-            g.ldo = static_cast<int>(out_.ld);
-            g.tile_n = tile_n_;
+            IgemmArgs g = class_args(c, args, inplace ? out : dst);
+            if (inplace) {
+                g.sub_sh = sh_;
+                g.sub_sw = sw_;
+                g.sub_a = static_cast<int>(ci) / sw_;
+                g.sub_b = static_cast<int>(ci) % sw_;
+                g.sub_H = static_cast<int>(out_.H);
+                g.sub_W = static_cast<int>(out_.W);
+                g.sub_zero = only_first ? 1 : 0;
+            }
             igemm_launch(g, s);
         }
         packed_valid_ = true;
-        subpixel_interleave(dtype_, il, s);
+        if (!inplace) subpixel_interleave(dtype_, il, s);
+    }
+
+    // the stride-1 forward conv computing one sub-pixel class of the strided dgrad
+    IgemmArgs class_args(const SubClass& c, void* const* args, void* dst) const {
+        IgemmArgs g;
+        g.mode = IG_FPROP;
+        g.dtype = dtype_;
+        g.out_dtype = dtype_;
+        g.src = args[0];
+        g.wt = c.packed;
+        g.out = dst;
+        g.N = static_cast<int>(in_.N);
+        g.SH = static_cast<int>(in_.H);
+        g.SW = static_cast<int>(in_.W);
+        g.SC = static_cast<int>(in_.ld);
+        g.OH = c.OHc;
+        g.OW = c.OWc;
+        g.kh = c.th; g.kw = c.tw; g.sh = 1; g.sw = 1; g.ph = -c.offh; g.pw = -c.offw;
+        g.Nout = static_cast<int>(cin_);
+        g.K_pad = c.kpad;
+        g.ldo = static_cast<int>(out_.ld);
+        g.tile_n = tile_n_;
+        return g;
     }
 
     // Fused epilogue chain after a Conv2d / Linear fprop (inference BatchNorm folding, the
