@@ -92,7 +92,9 @@ def test_train_step(gpu, name, hw, dtype):
                                for p, gn in tg.param_grads if g.params[p].ndim >= 2))
     print(f"{name} {dtype}: min grad cosine conv/linear {weights[0][0]:.4f} "
           f"(oracle self-consistency under operand rounding {floor:.4f}), all params {worst[0][0]:.4f}")
-    assert weights[0][0] >= min(0.95, 0.5 * floor), weights[:5]
+    # measured (B200): the plan is never below the floor (small CNN 0.994 vs 0.993, ResNet-18 bf16
+    # 0.923 vs 0.908, ResNet-50 f32 0.819 vs 0.694), so the bar sits at 90% of it (0.95 cap)
+    assert weights[0][0] >= min(0.95, 0.9 * floor), weights[:5]
     new = m.host_params()
     for p, _ in tg.param_grads[:8]:
         np.testing.assert_allclose(new[p], g.params[p] - np.float32(lr) * grads[p], rtol=1e-5, atol=1e-6)
