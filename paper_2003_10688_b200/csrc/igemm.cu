@@ -1348,8 +1348,12 @@ WgradPlan plan_wgrad(const WgradArgs& a) {
         p.m_tiles = static_cast<int>(ceil_div(Mt, 128));
         p.n_tiles = static_cast<int>(ceil_div(Nt, p.bn));
         const int tiles = p.m_tiles * p.n_tiles;
-        // ~2 work items per SM, each at least 4 k-blocks deep
-        static const int ips = std::getenv("SOL_WG_ITEMS_PER_SM") ? std::atoi(std::getenv("SOL_WG_ITEMS_PER_SM")) : 2;
+        // work items per SM, each at least 4 k-blocks deep: one for the few-tile (<= 4) layers with
+        // long pixel reductions (ResNet-50 layers 1-2 1x1: half the split-K partial traffic, 6-16 us
+        // faster each), two otherwise (the epilogue of one item overlaps the next item's mainloop);
+        // SOL_WG_ITEMS_PER_SM forces a count
+        static const int ips_env = std::getenv("SOL_WG_ITEMS_PER_SM") ? std::atoi(std::getenv("SOL_WG_ITEMS_PER_SM")) : 0;
+        const int ips = ips_env > 0 ? ips_env : (tiles <= 4 ? 1 : 2);
         int splits = std::max(1, std::min(std::max(1, total_kb / 4), (ips * num_sms() + tiles - 1) / tiles));
         p.kb_per_split = static_cast<int>(ceil_div(total_kb, splits));
         p.splits = static_cast<int>(ceil_div(total_kb, p.kb_per_split));
