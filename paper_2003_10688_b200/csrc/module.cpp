@@ -1088,10 +1088,15 @@ public:
         }
         // one pass over (dy, x) + the finalisation [+ the dx apply over each block's own rows], fused
         // in one cooperative launch when the grid is co-resident
-        // opt-in (SOL_BNBACK_FUSED_APPLY=1): measured slower on B200 (14.84 vs 14.30 ms per ResNet-50
-        // training step): the one-wave reduction grid applies at lower occupancy than the dedicated
-        // apply kernel, and the second grid barrier costs more than the saved launch
-        static const bool fuse_apply = std::getenv("SOL_BNBACK_FUSED_APPLY") != nullptr;
+        // Only for small tensors: the one-wave reduction grid applies at lower occupancy than the
+        // dedicated apply kernel (everywhere: 14.84 vs 14.30 ms per ResNet-50 training step), but when
+        // dy and x fit comfortably in L2 the re-read is cheap and the saved launch + finalize win
+        // (dy + x <= 60 MB: -90 us per step; 120 MB: worse)
+        // SOL_BNBACK_FUSED_APPLY=1/0 forces it on/off; SOL_BNBACK_FUSED_MB sets the size limit
+        static const char* fa_env = std::getenv("SOL_BNBACK_FUSED_APPLY");
+        static const double fa_mb = std::getenv("SOL_BNBACK_FUSED_MB") ? std::atof(std::getenv("SOL_BNBACK_FUSED_MB")) : 60.0;
+        const double pair_mb = 2.0 * static_cast<double>(delta_.pixels()) * C_ * elem_size(dtype_) / 1e6;
+        const bool fuse_apply = fa_env ? fa_env[0] == '1' : pair_mb <= fa_mb;
         void* apply_out = (op_ == SOL_OP_BATCHNORMBACKGAMMA || !fuse_apply) ? nullptr : out;
         const int fused = bn_back_reduce(dtype_, args[0], args[x_idx_], C_, delta_.pixels(), nullptr, partial, blocks_,
                                          s, &f, apply_out);
