@@ -928,13 +928,67 @@ __global__ void __launch_bounds__(THREADS) pool3s2_bulk_kernel(const __grid_cons
         geo(band, n, oh0, nr, h0, r_lo, r_hi);
         const T* tile = reinterpret_cast<const T*>(smem_raw + 128 + stage * stage_bytes);
         const int items = nr * a.OW * cv;
+        const bool cv_p2 = (cv & (cv - 1)) == 0;
+        const int cv_sh = __ffs(cv) - 1;
         for (int it = threadIdx.x; it < items; it += blockDim.x) {
-            const int cvec = it % cv;
-            const int rest = it / cv;
-            const int ow = rest % a.OW, r = rest / a.OW;
+            // no integer division on the common path (power-of-two channel vectors; r < R is small)
+            const int cvec = cv_p2 ? (it & (cv - 1)) : it % cv;
+            const int rest = cv_p2 ? (it >> cv_sh) : it / cv;
+            int ow = rest, r = 0;
+            while (ow >= a.OW) {
+                ow -= a.OW;
+                ++r;
+            }
             const int c = cvec * V;
             BnRegs<T> bn;
             if (BN0) bn.load(a.P, cs.bn0, c);
+            if constexpr (IS_MAX && sizeof(T) == 2) {
+                // The per-channel map act(fma(x, scale, shift)) is monotone in x (rounding is
+                // monotone; ReLU / ReLU6 are non-decreasing), so the window max of the mapped taps
+                // is the map of the raw max (scale >= 0) or of the raw min (scale < 0): reduce the
+                // raw bf16 taps with packed bf16x2 max / min (NaN taps ignored, as fmaxf does) and
+                // map once per output. Same result as mapping every tap; a third of the
+                // instructions (the f32 form of this kernel is issue-bound at IPC 3 on B200).
+                const uint32_t NEG_INF2 = 0xff80ff80u, POS_INF2 = 0x7f807f80u;
+                __nv_bfloat162 mx[4], mn[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    mx[j] = *reinterpret_cast<const __nv_bfloat162*>(&NEG_INF2);
+                    mn[j] = *reinterpret_cast<const __nv_bfloat162*>(&POS_INF2);
+                }
+                int taps = 0;
+#pragma unroll
+                for (int kr = 0; kr < 3; ++kr) {
+                    const int rr = 2 * r + kr;
+                    if (rr < r_lo || rr >= r_hi) continue;
+#pragma unroll
+                    for (int kc = 0; kc < 3; ++kc) {
+                        const int iw = ow * 2 - a.pw + kc;
+                        if (iw < 0 || iw >= a.W) continue;
+                        ++taps;
+                        const uint4 raw =
+                            *reinterpret_cast<const uint4*>(tile + rr * row_elems + static_cast<int64_t>(iw) * ldx + c);
+                        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            mx[j] = __hmax2(mx[j], h[j]);
+                            if (BN0) mn[j] = __hmin2(mn[j], h[j]);
+                        }
+                    }
+                }
+                float o[V], fx[V], fn[V];
+                unpack16(*reinterpret_cast<const uint4*>(mx), fx, static_cast<T*>(nullptr));
+                if (BN0) unpack16(*reinterpret_cast<const uint4*>(mn), fn, static_cast<T*>(nullptr));
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    float e = fx[q];
+                    if (BN0) e = fmaf(bn.k0[q] < 0.f ? fn[q] : fx[q], bn.k0[q], bn.k1[q]);
+                    if (ACT >= 1) e = fmaxf(e, 0.f);
+                    if (ACT == 2) e = fminf(e, 6.f);
+                    o[q] = fmaxf(taps ? e : -INFINITY, a.min_init);
+                }
+                store16(out + ((static_cast<int64_t>(n) * a.OH + oh0 + r) * a.OW + ow) * a.out_ld + c, o);
+            } else {
             float m[V];
 #pragma unroll
             for (int q = 0; q < V; ++q) m[q] = IS_MAX ? -INFINITY : 0.f;
@@ -967,6 +1021,7 @@ __global__ void __launch_bounds__(THREADS) pool3s2_bulk_kernel(const __grid_cons
                 else o[q] = m[q] / static_cast<float>(a.count_padding ? 9 : cnt);
             }
             store16(out + ((static_cast<int64_t>(n) * a.OH + oh0 + r) * a.OW + ow) * a.out_ld + c, o);
+            }
         }
         __syncthreads();  // every thread is done with this stage: refill it
         if (threadIdx.x == 0 && band + 2 * static_cast<int64_t>(gridDim.x) < total)
@@ -1080,13 +1135,13 @@ bool launch_pool_chain(const DfpArgs& a, cudaStream_t s, unsigned grid) {
     if (k3 && a.sh == 2 && a.sw == 2 && a.ph <= 1 && a.pw <= 1) {
         const bool bb = c.bn0 >= 0;
         // bands of input rows staged by bulk copies when R = 2 output rows fit 3 blocks per SM
-        static const int band_env = std::getenv("SOL_POOL_BAND") ? std::atoi(std::getenv("SOL_POOL_BAND")) : 1;
+        const int band_env = std::getenv("SOL_POOL_BAND") ? std::atoi(std::getenv("SOL_POOL_BAND")) : 1;  // per call (tests A/B it)
         // blocks per SM of the persistent 2-stage ring; 0 (default, measured fastest on B200: 126 vs
         // 150 us for the ResNet-50 stem pool) = one band per block, one stage, ~5 resident blocks
         static const int bps_env = std::getenv("SOL_POOL_BPS") ? std::atoi(std::getenv("SOL_POOL_BPS")) : 0;
         const int64_t row_bytes = static_cast<int64_t>(a.W) * a.in_ld[c.s0] * static_cast<int64_t>(sizeof(T));
         const int R = band_env;
-        const int64_t bands = static_cast<int64_t>(a.N) * ((a.OH + R - 1) / R);
+        const int64_t bands = R > 0 ? static_cast<int64_t>(a.N) * ((a.OH + R - 1) / R) : 0;  // SOL_POOL_BAND=0: row kernel
         const unsigned gb = static_cast<unsigned>(
             bps_env > 0 ? std::min<int64_t>(bands, static_cast<int64_t>(num_sms()) * bps_env) : bands);
         const size_t smem = 128 + (gb < bands ? 2 : 1) * static_cast<size_t>(2 * R + 1) * row_bytes;
@@ -2505,6 +2560,20 @@ bool launch_maxpool_back_fast(const DfpArgs& a, cudaStream_t s) {
     return true;
 }
 
+// (row, column) of a flat item index t over rows of `w` items without an integer division: a float
+// reciprocal estimate, corrected by one step (exact for t < 2^24)
+__device__ __forceinline__ void split_rc(int t, int w, float inv_w, int& row, int& col) {
+    row = __float2int_rz(static_cast<float>(t) * inv_w);
+    col = t - row * w;
+    if (col < 0) {
+        col += w;
+        --row;
+    } else if (col >= w) {
+        col -= w;
+        ++row;
+    }
+}
+
 // MaxPool2dBack for the 3x3 / stride 2 / pad 1 window (the ResNet stem pool) in ONE pass: a block
 // owns a band of 2R dx rows of one image; it first computes the first-max tap of the R+1 window
 // rows covering the band into shared memory (same scan order and min_init rule as
@@ -2527,15 +2596,19 @@ __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __g
     const int n = blockIdx.x / bands;
     const int oh0 = (blockIdx.x - n * bands) * R;
     const int nwr = min(R + 1, a.OH - oh0);
+    const bool cv_p2 = (cv & (cv - 1)) == 0;
+    const int cv_sh = __ffs(cv) - 1;
+    const float inv_ow = 1.f / static_cast<float>(a.OW);
     const T* x = static_cast<const T*>(a.in[a.pool_x]);
     const int ldx = a.in_ld[a.pool_x];
     // phase 1: first-max tap of windows (oh0 .. oh0+nwr-1, all ow)
     const int wins = nwr * a.OW * cv;
     for (int i = threadIdx.x; i < wins; i += THREADS) {
-        const int wv = i % cv;
-        const int t = i / cv;
-        const int ow = t % a.OW;
-        const int oh = oh0 + t / a.OW;
+        const int wv = cv_p2 ? (i & (cv - 1)) : i % cv;
+        const int t = cv_p2 ? (i >> cv_sh) : i / cv;
+        int ow, oh;
+        split_rc(t, a.OW, inv_ow, oh, ow);
+        oh += oh0;
         const int c = wv * V;
         // the 9 taps stay as raw 16-byte vectors (36 registers) until compared
         uint4 raw[9];
@@ -2552,6 +2625,44 @@ __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __g
                         x + ((static_cast<int64_t>(n) * a.H + hh) * a.W + ww) * ldx + c));
             }
         }
+        uint8_t* dst = am_s + (static_cast<int>(t) * a.C + c);
+        if constexpr (sizeof(T) == 2) {
+            // packed bf16x2: the window max (NaN taps ignored, like the strict '>' scan below),
+            // then the FIRST tap equal to it (scanning 8..0, the last write wins) -- the tap the
+            // scan's strict '>' keeps (+0 and -0 compare equal in both)
+            const uint32_t NEG_INF2 = 0xff80ff80u;
+            __nv_bfloat162 mx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mx[j] = *reinterpret_cast<const __nv_bfloat162*>(&NEG_INF2);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                if (!inb[k]) continue;
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) mx[j] = __hmax2(mx[j], h[j]);
+            }
+            uint32_t idx[4] = {0x00ff00ffu, 0x00ff00ffu, 0x00ff00ffu, 0x00ff00ffu};  // 16-bit lanes
+#pragma unroll
+            for (int k = 8; k >= 0; --k) {
+                if (!inb[k]) continue;
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[k]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t eq = __heq2_mask(h[j], mx[j]);
+                    idx[j] = (eq & (static_cast<uint32_t>(k) * 0x00010001u)) | (~eq & idx[j]);
+                }
+            }
+            float best[V];
+            unpack16(*reinterpret_cast<const uint4*>(mx), best, static_cast<T*>(nullptr));
+            uint32_t lo = __byte_perm(idx[0], idx[1], 0x6420), hi = __byte_perm(idx[2], idx[3], 0x6420);
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                if (!(best[e] > a.min_init) || (MXX && !(best[e] > 0.f))) {
+                    if (e < 4) lo |= 0xffu << (8 * e);
+                    else hi |= 0xffu << (8 * (e - 4));
+                }
+            *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
+        } else {
         float best[V];
         uint8_t bidx[V];
 #pragma unroll
@@ -2574,7 +2685,6 @@ __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __g
 #pragma unroll
         for (int e = 0; e < V; ++e)
             if (!(best[e] > a.min_init) || (MXX && !(best[e] > 0.f))) bidx[e] = 255;
-        uint8_t* dst = am_s + (static_cast<int>(t) * a.C + c);
         if constexpr (V == 8) {
             uint2 r;
             memcpy(&r, bidx, 8);
@@ -2583,6 +2693,7 @@ __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __g
             uint32_t r;
             memcpy(&r, bidx, 4);
             *reinterpret_cast<uint32_t*>(dst) = r;
+        }
         }
     }
     __syncthreads();
@@ -2598,10 +2709,11 @@ __global__ void __launch_bounds__(THREADS, 3) maxpool_back_band_kernel(const __g
     const int ld0 = a.in_ld[ps.s0], ld1 = ADD ? a.in_ld[ps.s1] : 0, ldm = MASK ? a.in_ld[ps.sm] : 0;
     T* out = static_cast<T*>(a.out);
     for (int i = threadIdx.x; i < items; i += THREADS) {
-        const int wv = i % cv;
-        const int t = i / cv;
-        const int qw = t % a.OW;
-        const int qh = oh0 + t / a.OW;
+        const int wv = cv_p2 ? (i & (cv - 1)) : i % cv;
+        const int t = cv_p2 ? (i >> cv_sh) : i / cv;
+        int qw, qh;
+        split_rc(t, a.OW, inv_ow, qh, qw);
+        qh += oh0;
         const int c = wv * V;
         const bool has_r = qw + 1 < a.OW, has_d = qh + 1 < a.OH;  // windows (., qw+1), (qh+1, .)
         const bool px_r = 2 * qw + 1 < a.W, px_d = 2 * qh + 1 < a.H;

@@ -203,3 +203,39 @@ def test_maxpool_back_band_stem_scale(gpu, monkeypatch, dtype):
     monkeypatch.setenv("SOL_NO_POOLBACK_BAND", "1")
     _, two_pass = run_unit(gp, u, env, dtype, gpu)
     assert np.array_equal(band, two_pass)
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_maxpool_bulk_stem_scale(gpu, monkeypatch, dtype):
+    """The ResNet stem's inference BatchNorm + MaxPool unit at 224x224 (112x112 -> 56x56, 3x3/2/1)
+    on the bulk band kernel: matches the oracle, and is bit-identical to the per-tap row kernel
+    (SOL_POOL_BAND=0). The bf16 band kernel reduces raw taps with packed max / min and maps the
+    BatchNorm once (monotone map): gammas of both signs and a zero, inputs on a coarse grid so
+    windows hold ties, so both the max and the min branch are exercised."""
+    from paper_2003_10688_b200 import models
+    from paper_2003_10688_b200 import graph, partition, passes
+    batch = 2
+    g = models.resnet(18, hw=224, classes=16, width=16)
+    gp = passes.run_pipeline(graph.infer_shapes(g, batch))
+    units = [u for u in partition.partition(gp)
+             if any(gp.find_node(nid).op == "MaxPool2d" for nid in u.node_ids)]
+    assert len(units) == 1
+    u = units[0]
+    rng = np.random.default_rng(11)
+    for pn in u.params:
+        c = gp.params[pn].shape[0]
+        if pn.endswith("gamma"):
+            gam = rng.uniform(0.25, 2.0, c) * np.where(rng.random(c) < 0.5, -1.0, 1.0)
+            gam[0] = 0.0
+            gp.params[pn] = gam.astype(np.float32)
+        elif pn.endswith("beta") or pn.endswith("running_mean"):
+            gp.params[pn] = rng.uniform(-1, 1, c).astype(np.float32)
+        elif pn.endswith("running_var"):
+            gp.params[pn] = rng.uniform(0.5, 2.0, c).astype(np.float32)
+    env = {nm: (rng.integers(-4, 5, gp.meta_of(nm).shape) / 4.0).astype(np.float32) for nm in u.inputs}
+    _check_units(gp, [u], env, dtype, gpu)
+    fam, bulk = run_unit(gp, u, env, dtype, gpu)
+    assert fam == "dfp_maxpool"
+    monkeypatch.setenv("SOL_POOL_BAND", "0")
+    _, rowk = run_unit(gp, u, env, dtype, gpu)
+    assert np.array_equal(bulk, rowk)
