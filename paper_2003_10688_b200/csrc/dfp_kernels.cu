@@ -956,18 +956,21 @@ __global__ void __launch_bounds__(THREADS) pool3s2_bulk_kernel(const __grid_cons
                     mx[j] = *reinterpret_cast<const __nv_bfloat162*>(&NEG_INF2);
                     mn[j] = *reinterpret_cast<const __nv_bfloat162*>(&POS_INF2);
                 }
-                int taps = 0;
+                // out-of-image taps are clamped onto an in-window tap (pad <= 1: the window's
+                // centre row / column is always inside): a duplicate never changes a max or min,
+                // and the loop has no branches
+                int rofs[3], cofs[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    rofs[k] = min(max(2 * r + k, r_lo), r_hi - 1);
+                    cofs[k] = min(max(ow * 2 - a.pw + k, 0), a.W - 1);
+                }
 #pragma unroll
                 for (int kr = 0; kr < 3; ++kr) {
-                    const int rr = 2 * r + kr;
-                    if (rr < r_lo || rr >= r_hi) continue;
 #pragma unroll
                     for (int kc = 0; kc < 3; ++kc) {
-                        const int iw = ow * 2 - a.pw + kc;
-                        if (iw < 0 || iw >= a.W) continue;
-                        ++taps;
-                        const uint4 raw =
-                            *reinterpret_cast<const uint4*>(tile + rr * row_elems + static_cast<int64_t>(iw) * ldx + c);
+                        const uint4 raw = *reinterpret_cast<const uint4*>(
+                            tile + rofs[kr] * row_elems + static_cast<int64_t>(cofs[kc]) * ldx + c);
                         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -985,7 +988,7 @@ __global__ void __launch_bounds__(THREADS) pool3s2_bulk_kernel(const __grid_cons
                     if (BN0) e = fmaf(bn.k0[q] < 0.f ? fn[q] : fx[q], bn.k0[q], bn.k1[q]);
                     if (ACT >= 1) e = fmaxf(e, 0.f);
                     if (ACT == 2) e = fminf(e, 6.f);
-                    o[q] = fmaxf(taps ? e : -INFINITY, a.min_init);
+                    o[q] = fmaxf(e, a.min_init);
                 }
                 store16(out + ((static_cast<int64_t>(n) * a.OH + oh0 + r) * a.OW + ow) * a.out_ld + c, o);
             } else {
