@@ -303,27 +303,35 @@ __global__ void __launch_bounds__(SR_THREADS, 1)
                     __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + (static_cast<int64_t>(n) * PH + py) * PW * a.ldo;
                     for (int item = et; item < PW * 8; item += 128) {
                         const int px = item >> 3, j = item & 7;
+                        // window taps clamped onto in-window ones (a duplicate never changes a max;
+                        // OH, OW even: only the top / left edges clip), all nine loads in flight,
+                        // packed bf16x2 max (NaN taps ignored, as fmaxf does), then min_init
+                        const uint8_t* rs[3];
+                        int cs[3];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            rs[k] = ring + (max(2 * py + k - 1, 0) % 3) * SR_ROW_BYTES;
+                            cs[k] = max(2 * px + k - 1, 0);
+                        }
+                        uint4 tv[9];
+#pragma unroll
+                        for (int kr = 0; kr < 3; ++kr)
+#pragma unroll
+                            for (int kc = 0; kc < 3; ++kc)
+                                tv[kr * 3 + kc] = *reinterpret_cast<const uint4*>(rs[kr] + cs[kc] * 128 + ((j ^ (cs[kc] & 7)) << 4));
+                        __nv_bfloat162 mx[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) mx[i] = reinterpret_cast<const __nv_bfloat162*>(&tv[0])[i];
+#pragma unroll
+                        for (int t = 1; t < 9; ++t)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) mx[i] = __hmax2(mx[i], reinterpret_cast<const __nv_bfloat162*>(&tv[t])[i]);
                         float m[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) m[i] = a.pool_min_init;
-#pragma unroll
-                        for (int dy = -1; dy <= 1; ++dy) {
-                            const int r = 2 * py + dy;
-                            if (r < 0) continue;
-                            const uint8_t* rs = ring + (r % 3) * SR_ROW_BYTES;
-#pragma unroll
-                            for (int dx = -1; dx <= 1; ++dx) {
-                                const int c = 2 * px + dx;
-                                if (c < 0) continue;
-                                const uint4 v = *reinterpret_cast<const uint4*>(rs + c * 128 + ((j ^ (c & 7)) << 4));
-                                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) {
-                                    const float2 t2 = __bfloat1622float2(h[i]);
-                                    m[2 * i] = fmaxf(m[2 * i], t2.x);
-                                    m[2 * i + 1] = fmaxf(m[2 * i + 1], t2.y);
-                                }
-                            }
+                        for (int i = 0; i < 4; ++i) {
+                            const float2 t2 = __bfloat1622float2(mx[i]);
+                            m[2 * i] = fmaxf(t2.x, a.pool_min_init);
+                            m[2 * i + 1] = fmaxf(t2.y, a.pool_min_init);
                         }
                         store16(orow + px * a.ldo + j * 8, m);
                     }
