@@ -166,8 +166,9 @@ class DevicePlan:
             # dual-GEMM bottleneck tails (kill switch SOL_NO_DUAL=1)
             if options.dtype == "bf16" and not os.environ.get("SOL_NO_DUAL"):
                 self.units = fuse_bottleneck_tails(cg, self.units)
-            # stem conv + BN + 3x3/2 max pool in one kernel: exact, but its 4 epilogue warps
-            # (BN + pooling) bound it at 416 us vs 182 + 150 us unfused (B200), so opt-in only
+            # stem conv + BN + 3x3/2 max pool in one kernel: exact, but still slower than the
+            # unfused pair (284 us vs 166 + 95 us on B200; 8 epilogue warps measured 298 us), so
+            # opt-in only
             if os.environ.get("SOL_STEM_POOL"):
                 from .fusion import fuse_stem_pool
                 self.units = fuse_stem_pool(cg, self.units, self._direct_stem_inputs())
