@@ -961,7 +961,7 @@ void launch_ws_t(const IgemmArgs& a, cudaStream_t s) {
         }
     }
     const int tiles = static_cast<int>(ceil_div(M, BM) * ceil_div(a.Nout, BN));
-    int grid = std::min(tiles, num_sms());
+    int grid = std::min(tiles, a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms());
     if constexpr (EPI == 2) {  // every CTA pinned to one N tile (see the kernel's work order)
         const int nt = static_cast<int>(ceil_div(a.Nout, BN)), mt = static_cast<int>(ceil_div(M, BM));
         if (nt > num_sms() || a.stat_blocks < 4 * num_sms()) throw std::invalid_argument("igemm: BN statistics layout");

@@ -34,6 +34,7 @@ struct IgemmArgs {
     int K_pad = 0;             // padded reduction extent of the packed operand
     int ldo = 0;
     int relu = 0;              // fused epilogue ReLU (unused by the reference path)
+    int max_ctas = 0;          // cap on the persistent grid (0 = one CTA per SM); concurrent launches share the SMs
     int dbg = 0;               // profiling knobs: 1 = skip output stores, 2 = skip MMA issue
     // fused epilogue (inference BN folding, beyond the reference pass set):
     //   y = act( (acc + bias) * ep_scale[c] + ep_shift[c] [+ residual[m, c]] )

@@ -373,7 +373,30 @@ public:
         sub_scratch_ = off + 256;
         launches = 1;
         for (auto& c : classes_) launches += c.th ? 2 : 0;
+        // the class GEMMs run concurrently on side streams (fork / join with events, so a captured
+        // plan gets parallel graph branches), each persistent over its share of the SMs
+        if (!std::getenv("SOL_SUBPIX_SERIAL")) {
+            int with_taps = 0;
+            for (const auto& c : classes_) with_taps += c.th ? 1 : 0;
+            if (with_taps > 1) {
+                side_.resize(classes_.size());
+                side_done_.resize(classes_.size());
+                for (size_t i = 0; i < classes_.size(); ++i) {
+                    SOL_CUDA(cudaStreamCreateWithFlags(&side_[i], cudaStreamNonBlocking));
+                    SOL_CUDA(cudaEventCreateWithFlags(&side_done_[i], cudaEventDisableTiming));
+                }
+                SOL_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+            }
+        }
     }
+    ~HeavyModule() override {
+        for (auto st : side_) cudaStreamDestroy(st);
+        for (auto ev : side_done_) cudaEventDestroy(ev);
+        if (fork_) cudaEventDestroy(fork_);
+    }
+    std::vector<cudaStream_t> side_;
+    std::vector<cudaEvent_t> side_done_;
+    cudaEvent_t fork_ = nullptr;
 
     void run_subpixel(void* const* args, void* out, void* scratch, cudaStream_t s, bool frozen) {
         // in place: every class stores straight into its stride positions of dx (no scratch, no
@@ -393,18 +416,37 @@ public:
         il.W = static_cast<int>(out_.W);
         il.ld = static_cast<int>(out_.ld);
         il.out = out;
+        // concurrent classes: SMs shared in proportion to each class's tile cost, its K blocks
+        // (taps x 128-byte channel blocks) plus ~4 K-block-equivalents of epilogue per tile
+        const bool par = !side_.empty();
+        const int64_t kb_tap = (static_cast<int64_t>(in_.ld) * static_cast<int64_t>(elem_size(dtype_)) + 127) / 128;
+        auto cost = [&](const SubClass& c) {
+            return (static_cast<int64_t>(c.th) * c.tw * kb_tap + 4) * c.OHc * c.OWc;
+        };
+        int64_t wsum = 0;
+        for (const auto& c : classes_) wsum += c.th ? cost(c) : 0;
+        if (par) SOL_CUDA(cudaEventRecord(fork_, s));
         for (size_t ci = 0; ci < classes_.size(); ++ci) {
             SubClass& c = classes_[ci];
             il.ch[ci] = c.OHc;
             il.cw[ci] = c.OWc;
             if (!c.th) continue;
+            cudaStream_t cs = s;
+            int ctas = 0;
+            if (par) {
+                cs = side_[ci];
+                SOL_CUDA(cudaStreamWaitEvent(cs, fork_, 0));
+                const int64_t w = cost(c);
+                ctas = static_cast<int>(std::max<int64_t>(1, (w * num_sms() + wsum / 2) / wsum));
+            }
             void* dst = static_cast<uint8_t*>(scratch) + c.scratch_off;
             il.cls[ci] = dst;
             if (!prepacked_ && !(frozen && packed_valid_))
                 pack_dgrad_class(static_cast<const float*>(args[w_idx_]), c.packed, dtype_, static_cast<int>(cout_),
                                  static_cast<int>(cin_), kh_, kw_, static_cast<int>(in_.ld), c.kpad, c.th, c.tw, c.kh0,
-                                 c.kw0, sh_, sw_, s);
+                                 c.kw0, sh_, sw_, cs);
             IgemmArgs g = class_args(c, args, inplace ? out : dst);
+            g.max_ctas = ctas;
             if (inplace) {
                 g.sub_sh = sh_;
                 g.sub_sw = sw_;
@@ -414,7 +456,11 @@ public:
                 g.sub_W = static_cast<int>(out_.W);
                 g.sub_zero = only_first ? 1 : 0;
             }
-            igemm_launch(g, s);
+            igemm_launch(g, cs);
+            if (par) {
+                SOL_CUDA(cudaEventRecord(side_done_[ci], cs));
+                SOL_CUDA(cudaStreamWaitEvent(s, side_done_[ci], 0));
+            }
         }
         packed_valid_ = true;
         if (!inplace) subpixel_interleave(dtype_, il, s);
