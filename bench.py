@@ -384,7 +384,8 @@ def run_b200(args):
     roof, times = roofline_of(m, peaks, peaks_kind, conv_fams, "tensor",
                               traffic=conv_traffic_profile("resnet50_infer_b256_bf16"))
     dfp_fams = {s.family for s in m.steps if s.family.startswith("dfp_")}
-    roof_dfp, _ = roofline_of(m, peaks, peaks_kind, dfp_fams, "hbm")
+    roof_dfp, _ = roofline_of(m, peaks, peaks_kind, dfp_fams, "hbm",
+                              traffic=conv_traffic_profile("resnet50_infer_b256_bf16_dfp"))
     fam_time = {}
     for st, t in zip(m.steps, times):
         fam_time[st.family] = fam_time.get(st.family, 0.0) + t
@@ -404,7 +405,8 @@ def run_b200(args):
         troof, ttimes = roofline_of(mt, peaks, peaks_kind,
                                     {"conv_fprop_tcgen05", "conv_fprop_bnstats_tcgen05", "conv_dgrad_tcgen05", "conv_dgrad_fused_tcgen05",
                                      "conv_wgrad_tcgen05",
-                                     "conv_stem_tcgen05", "conv_stem_wgrad_tcgen05"}, "tensor")
+                                     "conv_stem_tcgen05", "conv_stem_wgrad_tcgen05"}, "tensor",
+                                    traffic=conv_traffic_profile("resnet50_train_b128_bf16"))
         tfam = {}
         for st, tt in zip(mt.steps, ttimes):
             tfam[st.family] = tfam.get(st.family, 0.0) + tt
