@@ -417,11 +417,13 @@ public:
         il.ld = static_cast<int>(out_.ld);
         il.out = out;
         // concurrent classes: SMs shared in proportion to each class's tile cost, its K blocks
-        // (taps x 128-byte channel blocks) plus ~4 K-block-equivalents of epilogue per tile
+        // (taps x 128-byte channel blocks) plus ~11 K-block-equivalents of epilogue per tile (the
+        // in-place strided stores; fitted on ResNet-50 l2.0 / l3.0 class launches timed alone:
+        // t_tile = a + b * kb with a / b = 10.6-10.9)
         const bool par = !side_.empty();
         const int64_t kb_tap = (static_cast<int64_t>(in_.ld) * static_cast<int64_t>(elem_size(dtype_)) + 127) / 128;
         auto cost = [&](const SubClass& c) {
-            return (static_cast<int64_t>(c.th) * c.tw * kb_tap + 4) * c.OHc * c.OWc;
+            return (static_cast<int64_t>(c.th) * c.tw * kb_tap + 11) * c.OHc * c.OWc;
         };
         int64_t wsum = 0;
         for (const auto& c : classes_) wsum += c.th ? cost(c) : 0;
