@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         const bool res_mask = EPI == 1 && a.res_mode == 1;
         const bool has_m2 = EPI == 1 && a.mask != nullptr;  // host guarantees one chunk per warp (SLOTS == 1)
         const int act = a.relu ? 1 : a.act;
+        const bool no_sub_transpose = EPI == 3 && a.dbg & 4096;  // SOL_CONV_DBG=4096: scattered stores
         int acc = 0;
         uint32_t acc_phase = 0;
         int buf = 0;
@@ -751,6 +752,60 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
                     // of its stride cell when the other classes have no taps)
                     static_assert(sizeof(TO) == 2, "in-place sub-pixel classes are bf16");
                     const int m = m0 + q * 32 + lane;
+                    if (n + CW <= a.ldo && !(a.dbg & 1) && !no_sub_transpose) {
+                        // coalesced form: the warp's 32 rows go through the (idle) staging buffer,
+                        // then every store instruction writes 4 whole output pixels (4 x 128 B)
+                        // instead of 32 scattered 16-byte pieces. Per lane: its stride cell's
+                        // origin and a mask of the cell positions inside the image
+                        TO* cell = nullptr;
+                        uint32_t pos_ok = 0;
+                        if (m < M) {
+                            const int ohw = a.OH * a.OW;
+                            const int img = m / ohw, rem = m - img * ohw;
+                            const int i = rem / a.OW, j = rem - i * a.OW;
+                            const int oy = a.sub_sh * i, ox = a.sub_sw * j;
+                            cell = static_cast<TO*>(a.out) + n + ((static_cast<int64_t>(img) * a.sub_H + oy) * a.sub_W + ox) * a.ldo;
+                            for (int da = 0; da < a.sub_sh; ++da)
+                                for (int db = 0; db < a.sub_sw; ++db)
+                                    if (oy + da < a.sub_H && ox + db < a.sub_W) pos_ok |= 1u << (da * a.sub_sw + db);
+                        }
+                        uint8_t* sbuf = stage_buf;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            __nv_bfloat162 p0 = __floats2bfloat162_rn(f[8 * k], f[8 * k + 1]);
+                            __nv_bfloat162 p1 = __floats2bfloat162_rn(f[8 * k + 2], f[8 * k + 3]);
+                            __nv_bfloat162 p2 = __floats2bfloat162_rn(f[8 * k + 4], f[8 * k + 5]);
+                            __nv_bfloat162 p3 = __floats2bfloat162_rn(f[8 * k + 6], f[8 * k + 7]);
+                            *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                                make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                                           *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+                        }
+                        __syncwarp();
+                        const int k = lane & 7;
+                        const int mine_pos = a.sub_a * a.sub_sw + a.sub_b;
+#pragma unroll 2
+                        for (int it = 0; it < 8; ++it) {
+                            const int r = it * 4 + (lane >> 3);
+                            const uint4 val = *reinterpret_cast<const uint4*>(sbuf + r * 128 + ((k ^ (r & 7)) << 4));
+                            TO* cr = reinterpret_cast<TO*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(cell), r));
+                            const uint32_t ok = __shfl_sync(0xffffffffu, pos_ok, r);
+                            if (!a.sub_zero) {  // this class's own position only
+                                if ((ok >> mine_pos) & 1u)
+                                    *reinterpret_cast<uint4*>(cr + (static_cast<int64_t>(a.sub_a) * a.sub_W + a.sub_b) * a.ldo + 8 * k) = val;
+                                continue;
+                            }
+                            for (int da = 0; da < a.sub_sh; ++da)
+                                for (int db = 0; db < a.sub_sw; ++db) {
+                                    const int ps = da * a.sub_sw + db;
+                                    const bool mine = ps == mine_pos;
+                                    if ((!mine && !a.sub_zero) || !((ok >> ps) & 1u)) continue;
+                                    *reinterpret_cast<uint4*>(cr + (static_cast<int64_t>(da) * a.sub_W + db) * a.ldo + 8 * k) =
+                                        mine ? val : make_uint4(0, 0, 0, 0);
+                                }
+                        }
+                        __syncwarp();  // the rows are read before the next chunk rewrites the buffer
+                        continue;
+                    }
                     if (m < M && !(a.dbg & 1)) {
                         const int ohw = a.OH * a.OW;
                         const int img = m / ohw, rem = m - img * ohw;

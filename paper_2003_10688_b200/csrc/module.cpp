@@ -416,17 +416,40 @@ public:
         il.W = static_cast<int>(out_.W);
         il.ld = static_cast<int>(out_.ld);
         il.out = out;
-        // concurrent classes: SMs shared in proportion to each class's tile cost, its K blocks
-        // (taps x 128-byte channel blocks) plus ~11 K-block-equivalents of epilogue per tile (the
-        // in-place strided stores; fitted on ResNet-50 l2.0 / l3.0 class launches timed alone:
-        // t_tile = a + b * kb with a / b = 10.6-10.9)
+        // concurrent classes: each runs persistent over its own SM share. A tile of class c costs
+        // (its K blocks = taps x 128-byte channel blocks) + E K-block equivalents of epilogue; SMs
+        // go one at a time to the class with the latest finish ceil(tiles / SMs) x tile cost (wave
+        // quantisation included). E = 24 measured best on ResNet-50's l2.0 / l3.0 / l4.0 strided
+        // dgrads (SOL_SUBPIX_EPI_KB overrides)
         const bool par = !side_.empty();
         const int64_t kb_tap = (static_cast<int64_t>(in_.ld) * static_cast<int64_t>(elem_size(dtype_)) + 127) / 128;
-        auto cost = [&](const SubClass& c) {
-            return (static_cast<int64_t>(c.th) * c.tw * kb_tap + 11) * c.OHc * c.OWc;
-        };
-        int64_t wsum = 0;
-        for (const auto& c : classes_) wsum += c.th ? cost(c) : 0;
+        static const int64_t epi_kb = std::getenv("SOL_SUBPIX_EPI_KB") ? std::atoi(std::getenv("SOL_SUBPIX_EPI_KB")) : 24;
+        std::vector<int> share(classes_.size(), 0);
+        if (par) {
+            std::vector<int64_t> tiles(classes_.size(), 0), tcost(classes_.size(), 0);
+            int given = 0;
+            for (size_t ci = 0; ci < classes_.size(); ++ci) {
+                const SubClass& c = classes_[ci];
+                if (!c.th) continue;
+                tiles[ci] = ceil_div(static_cast<int64_t>(in_.N) * c.OHc * c.OWc, int64_t(128));
+                tcost[ci] = static_cast<int64_t>(c.th) * c.tw * kb_tap + epi_kb;
+                share[ci] = 1;
+                ++given;
+            }
+            for (; given < num_sms(); ++given) {
+                size_t worst = 0;
+                int64_t wt = -1;
+                for (size_t ci = 0; ci < classes_.size(); ++ci) {
+                    if (!share[ci]) continue;
+                    const int64_t t = ceil_div(tiles[ci], static_cast<int64_t>(share[ci])) * tcost[ci];
+                    if (t > wt) {
+                        wt = t;
+                        worst = ci;
+                    }
+                }
+                ++share[worst];
+            }
+        }
         if (par) SOL_CUDA(cudaEventRecord(fork_, s));
         for (size_t ci = 0; ci < classes_.size(); ++ci) {
             SubClass& c = classes_[ci];
@@ -438,8 +461,7 @@ public:
             if (par) {
                 cs = side_[ci];
                 SOL_CUDA(cudaStreamWaitEvent(cs, fork_, 0));
-                const int64_t w = cost(c);
-                ctas = static_cast<int>(std::max<int64_t>(1, (w * num_sms() + wsum / 2) / wsum));
+                ctas = share[ci];
             }
             void* dst = static_cast<uint8_t*>(scratch) + c.scratch_off;
             il.cls[ci] = dst;
