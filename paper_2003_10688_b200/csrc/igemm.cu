@@ -230,21 +230,36 @@ __global__ void __launch_bounds__(THREADS, 1) wgrad_kernel(WgradArgs a, int kb_p
 }
 
 // split-K reduction straight into the canonical layout: canonical i = ((co*Cin + ci)*KH + kh)*KW + kw
-// reads packed j = co*KH*KW*ld + (kh*KW + kw)*ld + ci of every split
+// reads packed j = co*KH*KW*ld + (kh*KW + kw)*ld + ci of every split. Threads walk the PACKED
+// index, so the `splits` partial reads are coalesced and only the one canonical write scatters
+// (for a 3x3 the canonical walk read each partial with a stride of ld floats); the split sums
+// keep their order (bit-identical), four partial loads in flight.
 __global__ void wgrad_reduce_canon_kernel(const float* __restrict__ ws, float* __restrict__ w, int64_t n, int splits,
                                           int Cout, int Cin, int KH, int KW, int ld) {
-    const int64_t total = static_cast<int64_t>(Cout) * Cin * KH * KW;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int kw = static_cast<int>(i % KW);
-        const int kh = static_cast<int>((i / KW) % KH);
-        const int ci = static_cast<int>((i / (KW * KH)) % Cin);
-        const int co = static_cast<int>(i / (static_cast<int64_t>(KW) * KH * Cin));
-        const int pcol = (kh * KW + kw) * ld + ci;
-        const int64_t j = static_cast<int64_t>(co) * KH * KW * ld + pcol;
+    const int64_t rowlen = static_cast<int64_t>(KH) * KW * ld;
+    const int64_t total = static_cast<int64_t>(Cout) * rowlen;
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < total;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int co = static_cast<int>(j / rowlen);
+        const int pcol = static_cast<int>(j - co * rowlen);
+        const int tap = pcol / ld;
+        const int ci = pcol - tap * ld;
+        if (ci >= Cin) continue;
+        const int kh = tap / KW, kw = tap - kh * KW;
         float acc = 0.f;
-        for (int sp = 0; sp < splits; ++sp) acc += __ldg(ws + sp * n + j);
-        w[i] = acc;
+        int sp = 0;
+        for (; sp + 4 <= splits; sp += 4) {
+            const float v0 = __ldg(ws + static_cast<int64_t>(sp) * n + j);
+            const float v1 = __ldg(ws + static_cast<int64_t>(sp + 1) * n + j);
+            const float v2 = __ldg(ws + static_cast<int64_t>(sp + 2) * n + j);
+            const float v3 = __ldg(ws + static_cast<int64_t>(sp + 3) * n + j);
+            acc += v0;
+            acc += v1;
+            acc += v2;
+            acc += v3;
+        }
+        for (; sp < splits; ++sp) acc += __ldg(ws + static_cast<int64_t>(sp) * n + j);
+        w[((static_cast<int64_t>(co) * Cin + ci) * KH + kh) * KW + kw] = acc;
     }
 }
 
@@ -1553,7 +1568,7 @@ void wgrad_launch(const WgradArgs& a_in, cudaStream_t s) {
         SOL_CUDA(cudaGetLastError());
     } else if (p.splits > 1 && a.dw_canon) {
         const int64_t n = static_cast<int64_t>(a.Cout) * p.ncol;
-        const int64_t total = static_cast<int64_t>(a.Cout) * a.canon_cin * a.kh * a.kw;
+        const int64_t total = static_cast<int64_t>(a.Cout) * a.kh * a.kw * a.SC;  // packed walk
         const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8L * num_sms())));
         wgrad_reduce_canon_kernel<<<grid, 256, 0, s>>>(a.workspace, a.dw_canon, n, p.splits, a.Cout, a.canon_cin,
                                                        a.kh, a.kw, a.SC);
