@@ -292,7 +292,18 @@ __global__ void wgrad_reduce_halo_kernel(const float* __restrict__ ws, float* __
         }
         const float* src = ws + static_cast<int64_t>(g) * spg * pf + r;
         float acc = 0.f;
-        for (int sp = 0; sp < spg; ++sp) acc += __ldg(src + static_cast<int64_t>(sp) * pf);
+        int sp = 0;
+        for (; sp + 4 <= spg; sp += 4) {  // four partial loads in flight, sums in split order
+            const float v0 = __ldg(src + static_cast<int64_t>(sp) * pf);
+            const float v1 = __ldg(src + static_cast<int64_t>(sp + 1) * pf);
+            const float v2 = __ldg(src + static_cast<int64_t>(sp + 2) * pf);
+            const float v3 = __ldg(src + static_cast<int64_t>(sp + 3) * pf);
+            acc += v0;
+            acc += v1;
+            acc += v2;
+            acc += v3;
+        }
+        for (; sp < spg; ++sp) acc += __ldg(src + static_cast<int64_t>(sp) * pf);
         if (dw_canon) {
             if (ci < canon_cin) dw_canon[((static_cast<int64_t>(co) * canon_cin + ci) * 3 + tap / 3) * 3 + tap % 3] = acc;
         } else {
