@@ -561,13 +561,16 @@ bool launch_chain(const DfpArgs& a, cudaStream_t s) {
 // recognised by symbolic evaluation of the program, whatever registers it uses.
 struct MaskSpec {
     int ok = 0, s0 = -1, s1 = -1, sm = -1, six = 0;
+    int scaled = 0;     // source = LD(s0) * scale (GlobalAvgPoolBack: an [N, C] gradient / (H*W))
+    float scale = 1.f;
 };
 
 MaskSpec match_mask(const Program& p) {
     // symbolic value of each register: LD(slot), ADD(LD, LD) or MASK(LD | ADD, LD)
     struct Sym {
-        int kind = 0;  // 0 unknown, 1 LD, 2 ADD, 3 MASK
+        int kind = 0;  // 0 unknown, 1 LD, 2 ADD, 3 MASK, 4 LD * imm
         int s0 = -1, s1 = -1, sm = -1, six = 0;
+        float scale = 1.f;
     };
     Sym reg[NREG];
     MaskSpec m;
@@ -584,6 +587,12 @@ MaskSpec match_mask(const Program& p) {
                 if (in.a >= NREG) return m;
                 r = reg[in.a];
                 break;
+            case PW_SCALE:  // r[dst] *= imm
+                if (reg[in.dst].kind != 1) return m;
+                r = reg[in.dst];
+                r.kind = 4;
+                r.scale = in.imm;
+                break;
             case PW_ADD: {
                 if (in.a >= NREG || in.b >= NREG) return m;
                 const Sym &x = reg[in.a], &y = reg[in.b];
@@ -597,12 +606,14 @@ MaskSpec match_mask(const Program& p) {
             case PW_MASK6: {
                 if (in.a >= NREG || in.b >= NREG) return m;
                 const Sym &x = reg[in.a], &y = reg[in.b];
-                if ((x.kind != 1 && x.kind != 2) || y.kind != 1) return m;
+                if ((x.kind != 1 && x.kind != 2 && x.kind != 4) || y.kind != 1) return m;
                 r.kind = 3;
                 r.s0 = x.s0;
                 r.s1 = x.kind == 2 ? x.s1 : -1;
                 r.sm = y.s0;
                 r.six = in.op == PW_MASK6;
+                r.scale = x.kind == 4 ? x.scale : 1.f;
+                r.kind = x.kind == 4 ? 5 : 3;  // 5: MASK of a scaled load
                 break;
             }
             default:
@@ -610,16 +621,18 @@ MaskSpec match_mask(const Program& p) {
         }
         reg[in.dst] = r;
     }
-    if (reg[0].kind != 3) return m;
+    if (reg[0].kind != 3 && reg[0].kind != 5) return m;
     m.ok = 1;
     m.s0 = reg[0].s0;
     m.s1 = reg[0].s1;
     m.sm = reg[0].sm;
     m.six = reg[0].six;
+    m.scaled = reg[0].kind == 5;
+    m.scale = reg[0].scale;
     return m;
 }
 
-template <typename T, bool ADD, bool SIX>
+template <typename T, bool ADD, bool SIX, bool NC = false>
 __global__ void __launch_bounds__(THREADS) mask_kernel(const __grid_constant__ DfpArgs a, MaskSpec ms) {
     constexpr int V = VEC<T>;
     constexpr int U = 4;
@@ -636,6 +649,7 @@ __global__ void __launch_bounds__(THREADS) mask_kernel(const __grid_constant__ D
     const T* xm = static_cast<const T*>(a.in[ms.sm]) + a.in_coff[ms.sm] + c;
     const int ld0 = a.in_ld[ms.s0], ld1 = ADD ? a.in_ld[ms.s1] : 0, ldm = a.in_ld[ms.sm];
     T* out = static_cast<T*>(a.out) + a.out_coff + c;
+    const int64_t hw = static_cast<int64_t>(a.OH) * a.OW;
     const int64_t step = static_cast<int64_t>(gridDim.x) * rows;
     for (int64_t p0 = static_cast<int64_t>(blockIdx.x) * rows + row; p0 < P; p0 += step * U) {
         uint4 r0[U], r1[U], rm[U];
@@ -643,7 +657,8 @@ __global__ void __launch_bounds__(THREADS) mask_kernel(const __grid_constant__ D
         for (int u = 0; u < U; ++u) {
             const int64_t p = p0 + u * step;
             if (p < P) {
-                r0[u] = __ldg(reinterpret_cast<const uint4*>(x0 + p * ld0));
+                // NC: the source is an [N, C] tensor broadcast over the image's pixels
+                r0[u] = __ldg(reinterpret_cast<const uint4*>(x0 + (NC ? p / hw : p) * ld0));
                 if (ADD) r1[u] = __ldg(reinterpret_cast<const uint4*>(x1 + p * ld1));
                 rm[u] = __ldg(reinterpret_cast<const uint4*>(xm + p * ldm));
             }
@@ -655,6 +670,10 @@ __global__ void __launch_bounds__(THREADS) mask_kernel(const __grid_constant__ D
             float v[V], m[V];
             unpack16(r0[u], v, static_cast<T*>(nullptr));
             unpack16(rm[u], m, static_cast<T*>(nullptr));
+            if (ms.scaled) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) v[i] *= ms.scale;  // PW_SCALE's f32 multiply
+            }
             if (ADD) {
                 float w[V];
                 unpack16(r1[u], w, static_cast<T*>(nullptr));
@@ -675,11 +694,17 @@ template <typename T>
 bool launch_mask(const DfpArgs& a, cudaStream_t s) {
     const MaskSpec m = match_mask(a.post);
     if (!m.ok) return false;
+    // the scaled source may be an [N, C] broadcast (GlobalAvgPoolBack + ReluBack)
+    const bool nc = m.scaled && m.s0 < a.n_in && a.in_kind[m.s0] == IN_NC && m.s1 < 0;
     for (int sl : {m.s0, m.s1, m.sm})
-        if (sl >= 0 && (sl >= a.n_in || a.in_kind[sl] != IN_PIX)) return false;
+        if (sl >= 0 && !(nc && sl == m.s0) && (sl >= a.n_in || a.in_kind[sl] != IN_PIX)) return false;
+    if (m.scaled && a.in_coff[m.s0] != 0) return false;
     const dim3 grid = row_geo(a.C, VEC<T>, static_cast<int64_t>(a.N) * a.OH * a.OW).grid;
     const bool add = m.s1 >= 0;
-    if (add) {
+    if (nc) {
+        if (m.six) mask_kernel<T, false, true, true><<<grid, THREADS, 0, s>>>(a, m);
+        else mask_kernel<T, false, false, true><<<grid, THREADS, 0, s>>>(a, m);
+    } else if (add) {
         if (m.six) mask_kernel<T, true, true><<<grid, THREADS, 0, s>>>(a, m);
         else mask_kernel<T, true, false><<<grid, THREADS, 0, s>>>(a, m);
     } else {
@@ -2908,7 +2933,7 @@ void dfp_launch_t(const DfpArgs& a, cudaStream_t s) {
         case FAM_POINTWISE: {
             if (launch_chain<T>(a, s)) break;
             if (a.out2) throw std::invalid_argument("dfp: activation sibling needs a straight-line chain unit");
-            if (launch_mask<T>(a, s)) break;
+            if (!std::getenv("SOL_NO_MASK_KERNEL") && launch_mask<T>(a, s)) break;  // switch read per call (tests)
             if (launch_pointwise_pre<T>(a, s)) break;
             const int64_t work = static_cast<int64_t>(a.N) * a.OH * a.OW * (a.C / V);
             pointwise_kernel<T><<<grid_for(work, THREADS), THREADS, 0, s>>>(a);

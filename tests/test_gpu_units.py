@@ -239,3 +239,28 @@ def test_maxpool_bulk_stem_scale(gpu, monkeypatch, dtype):
     monkeypatch.setenv("SOL_POOL_BAND", "0")
     _, rowk = run_unit(gp, u, env, dtype, gpu)
     assert np.array_equal(bulk, rowk)
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_gap_back_relu_back_mask_kernel(gpu, monkeypatch, dtype):
+    """ResNet-50's last training unit, GlobalAvgPoolBack + ReluBack (dx = relu_out > 0 ? g[n, c] /
+    (H*W) : 0), on the mask kernel with an [N, C] broadcast source: matches the oracle and is
+    bit-identical to the generic DFP interpreter (SOL_NO_MASK_KERNEL=1)."""
+    from paper_2003_10688_b200 import models
+    from paper_2003_10688_b200 import autodiff, graph, partition, passes
+    batch = 4
+    g = models.resnet(50, hw=64, classes=16, width=16, train=True)
+    gi = graph.infer_shapes(g, batch)
+    gi = graph.infer_shapes(autodiff.build_training_graph(gi).graph, batch)
+    gp = passes.run_pipeline(gi)
+    units = [u for u in partition.partition(gp)
+             if any(gp.find_node(nid).op == "GlobalAvgPoolBack" for nid in u.node_ids)]
+    assert len(units) == 1
+    u = units[0]
+    rng = np.random.default_rng(3)
+    env = {nm: rng.uniform(-1, 1, gp.meta_of(nm).shape).astype(np.float32) for nm in u.inputs}
+    _check_units(gp, [u], env, dtype, gpu)
+    fam, fast = run_unit(gp, u, env, dtype, gpu)
+    monkeypatch.setenv("SOL_NO_MASK_KERNEL", "1")
+    _, generic = run_unit(gp, u, env, dtype, gpu)
+    assert np.array_equal(fast, generic)
